@@ -1,0 +1,329 @@
+"""Benchmark: filtered megapixels/sec of the Nystrom kernel filter on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = the whole hot path (BASELINE.json north_star) over one synthetic
+image: k-means++ seeding + Lloyd (K0/K1), host FP64 eig of the m0 x m0
+landmark kernel, features + horizontal pass (K2), vertical pass +
+reconstruction + guard + division (K3).  Default workload: BASELINE.json
+configs[1] (cfg 2, 1920x1080x3, m0=64, sigma_s=5/R=15, sigma_r=0.1, 15 it).
+
+Prints ONE JSON line (rank 0).  ``value`` = Mpix/s with the input resident in
+HBM (output stays in HBM); ``e2e`` = the same through the public API from
+pinned host buffers with H2D/D2H inside the timed region.  L2 (126 MB) is
+flushed with a 512 MB write before every timed step.  ``--impl reference``
+times the CPU oracle port (oracle/nys_oracle.py; the reference is pure
+Python and cannot travel to the GPU box) on a bounded row crop of the same
+workload using all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1901_06112_b200.synthetic import CONFIGS  # noqa: E402
+
+METRIC = "filtered megapixels/sec (d-channel, m landmarks)"
+UNIT = "Mpix/s"
+
+
+def _cfg_dict(wl, extra=None):
+    d = {"workload": wl.name, "H": wl.H, "W": wl.W, "channels": wl.channels, "guide": wl.mode,
+         "m0": wl.m0, "spatial": wl.spatial, "sigma_s": wl.sigma, "radius": wl.radius,
+         "sigma_r": round(float(wl.theta), 6), "kmeans_iters": wl.max_iter, "seed": 0}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def _params(wl):
+    from paper_1901_06112_b200 import FilterParams, SpatialKernel
+
+    sk = SpatialKernel.box(wl.radius) if wl.spatial == "box" else SpatialKernel.gaussian(wl.sigma, wl.radius)
+    return FilterParams(spatial=sk, theta=float(wl.theta), m0=wl.m0, seed=0, kmeans_max_iter=wl.max_iter,
+                        mode=wl.mode if wl.mode != "nlm" else "nlm", patch_radius=max(wl.patch_radius, 1),
+                        pca_dim=27 if wl.mode == "nlm" else 25)
+
+
+def _guide(f_img, wl):
+    from paper_1901_06112_b200 import PatchGuide
+
+    return PatchGuide(f_img, wl.patch_radius) if wl.mode == "nlm" else f_img
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _ffma_peak():
+    p = ROOT / "profiles" / "ffma_peak.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return None
+
+
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    from paper_1901_06112_b200 import Image, _native, fast_filter
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    wl = CONFIGS[args.config]
+    if world > 1:
+        from paper_1901_06112_b200 import parallel
+
+        return parallel.bench_sharded(args, wl, rank, world)
+    f_np = wl.image(seed=0)
+    n, H, W = f_np.shape
+    px = H * W
+    f_dev = torch.from_numpy(f_np).to(dev)
+    f_img = Image(data=f_dev, range_max=1.0)
+    g_img = _guide(f_img, wl)
+    params = _params(wl)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def l2_flush():
+        flush.random_(0, 255)  # 512 MB write > 126 MB L2
+
+    # warm-up (also JIT-free: the library is prebuilt)
+    for _ in range(args.warmup):
+        fast_filter(f_img, g_img, params)
+    torch.cuda.synchronize()
+
+    lib = _native.lib()
+    step_ms, k_ms = [], {"k_feat_hpass": 0.0, "k_vpass": 0.0}
+    k_n = {"k_feat_hpass": 0, "k_vpass": 0}
+    launches0 = int(lib.nys_kernel_launches())
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            l2_flush()
+            evs = []
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rep = fast_filter(f_img, g_img, params, kernel_events=evs)
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            for name, a, b, _band in evs:
+                k_ms[name] += a.elapsed_time(b)
+                k_n[name] += 1
+        torch.cuda.synchronize()
+    launches = int(lib.nys_kernel_launches()) - launches0
+    ms = sum(step_ms) / len(step_ms)
+    value = px / (ms * 1e-3) / 1e6
+
+    # end to end through the public API from pinned host buffers
+    f_host = torch.from_numpy(f_np).pin_memory()
+    h_img = Image(data=f_host, range_max=1.0)
+    hg = _guide(h_img, wl)
+    fast_filter(h_img, hg, params)
+    e2e_ms = []
+    torch.cuda.synchronize()
+    for _ in range(max(1, args.steps)):
+        l2_flush()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep_h = fast_filter(h_img, hg, params)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e = sum(e2e_ms) / len(e2e_ms)
+    out_bytes = int(rep_h.output.data.numel() * 4)
+
+    # roofline of the dominant kernel (algorithmic bytes per launch / avg launch time)
+    u = n if wl.mode != "nlm" else n  # stored input channels read (patches gathered from f)
+    P = (wl.m0 + 1) * (n + 1)         # planes incl. the rank-1 lead group
+    T = 2 * wl.radius + 1
+    rho = n * 9 if wl.mode == "nlm" else n
+    bytes_px = {"k_feat_hpass": 4 * (u + P), "k_vpass": 4 * (P + u + n)}
+    # algorithmic FP32 FMA-pipe ops per pixel (FIR taps, y = M b, features, contraction)
+    fir = P * (2 if wl.spatial == "box" else T)
+    flops_px = {"k_feat_hpass": fir + wl.m0 * wl.m0 + wl.m0 * (2 * rho + 1) + wl.m0 * n,
+                "k_vpass": fir + wl.m0 * (2 * rho + 1) + 2 * P}
+    avg = {k: k_ms[k] / max(1, k_n[k]) for k in k_ms}
+    dom = max(avg, key=avg.get)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_px[dom] * px / (avg[dom] * 1e-3) / 1e9
+    ffma = _ffma_peak()
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+            "bytes_per_px": bytes_px[dom], "launch_ms": round(avg[dom], 4),
+            "kernel_ms": {k: round(v, 4) for k, v in avg.items()}}
+    fma_t = flops_px[dom] * px / (avg[dom] * 1e-3) / 1e12
+    roof["fma"] = {"achieved_tfma": round(fma_t, 2), "ops_per_px": flops_px[dom],
+                   "peak_tfma": ffma.get("tfma_per_s") if ffma else None,
+                   "frac": round(fma_t / ffma["tfma_per_s"], 4) if ffma else None}
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        tr = json.loads(prof.read_text()).get(wl.name, {}).get(dom)
+        if tr:
+            roof["traffic"] = tr
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded random-polygon scene, SURVEY §8d)",
+        "config": _cfg_dict(wl, {"l2": "flushed: 512 MB write before every timed step", "parallelism": "single"}),
+        "e2e": {"value": round(px / (e2e * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_step": round(e2e, 3),
+                "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": out_bytes,
+                "path": "fast_filter(Image(pinned host float32)) -> pinned host output"},
+        "gpu_launches": launches // max(1, args.steps),
+        "gpu_launches_total": launches,
+        "roofline": roof,
+        "stage_ms": {k: round(v * 1e3, 3) for k, v in rep.timings.items()},
+        "clocks": clk.summary(),
+        "report": {"retained_rank": rep.retained_rank, "quant_error": rep.quant_error,
+                   "guarded_pixels": rep.guarded_pixels, "min_denominator": rep.min_denominator},
+    }
+    if not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(wl, args.cpu_rows)
+    return result
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(wl, rows: int, threads: int | None = None):
+    """CPU oracle port on a bounded row crop of the same workload."""
+    from oracle import nys_oracle as O
+
+    threads = threads or (os.cpu_count() or 1)
+    f = wl.image(seed=0, H=rows).astype(np.float64)
+    p = O.patch_stack(f, wl.patch_radius) if wl.mode == "nlm" else f
+    t0 = time.perf_counter()
+    O.fast_filter(f, p, float(wl.theta), wl.spatial, wl.sigma, wl.radius, wl.m0, 0, wl.max_iter, threads=threads)
+    dt = time.perf_counter() - t0
+    px = f.shape[1] * f.shape[2]
+    return {"value": round(px / dt / 1e6, 5), "unit": UNIT, "cores": max(threads, _blas_threads()),
+            "kind": "port", "seconds": round(dt, 2),
+            "sample": f"oracle/nys_oracle.fast_filter (FP64 NumPy restatement of the reference) on the first "
+                      f"{rows} rows x {wl.W} cols of {wl.name}, k-means on that crop; rank loop on {threads} "
+                      f"threads, BLAS on {_blas_threads()}"}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return None
+    wl = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_baseline(wl, max(8, rows // 4), threads)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_baseline(wl, rows, threads)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    value = sum(vals) / len(vals)
+    r["value"] = round(value, 5)
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / len(secs), 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random-polygon scene, SURVEY §8d)",
+            "config": _cfg_dict(wl, {"sample_rows": rows}),
+            "cpu_baseline": r,
+            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=64, help="rows of the CPU-baseline crop")
+    ap.add_argument("--ref-rows", type=int, default=32, help="rows of the reference-arm crop per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,226 @@
+/*
+ * nysfilter_b200.h -- C ABI of the B200-native Nystrom kernel-filter hot path.
+ *
+ * The reference (`nysfilter` 0.1.0, /root/reference/pkg/src/nysfilter) is pure
+ * Python; it has no FFI.  Each entry point below replaces the NumPy region of
+ * the reference named in its comment, so a Python (ctypes) or C/C++ host can
+ * bind them directly.  Conventions:
+ *   - every pointer marked [dev] is CUDA device memory, [host] is host memory;
+ *   - images are planar float32, plane c at `base + c * plane_stride`, rows of
+ *     `W` contiguous floats (reference layout: image.py:33-72, data[c, y, x]);
+ *   - the library never allocates or frees device memory: callers pass
+ *     workspaces sized by the matching *_workspace_bytes() query;
+ *   - all work is enqueued on `stream` (a cudaStream_t passed as void*);
+ *     nothing synchronises the host unless documented;
+ *   - the return value is 0 on success, NYS_EINVAL / NYS_EUNSUPPORTED for bad
+ *     arguments (checked before any launch), or NYS_ECUDA + cudaError_t.
+ */
+#ifndef NYSFILTER_B200_H
+#define NYSFILTER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NYS_OK 0
+#define NYS_EINVAL 1
+#define NYS_EUNSUPPORTED 2
+#define NYS_ECUDA 1000
+
+#define NYS_SPATIAL_BOX 0          /* spatial.py:32 kind "box" */
+#define NYS_SPATIAL_GAUSSIAN_FIR 1 /* spatial.py:32 kind "gaussian_fir" */
+
+#define NYS_MAX_RADIUS 64          /* taps = 2R+1 <= 129 */
+#define NYS_MAX_M0 256
+#define NYS_MAX_RHO 64
+#define NYS_MAX_CHANNELS 64
+
+/* Library ABI version (major*100 + minor). */
+int nys_abi_version(void);
+
+/* Kernels launched by this library since load (all entry points, all streams). */
+uint64_t nys_kernel_launches(void);
+
+/* ---------------------------------------------------------------------- */
+/* Landmarks: k-means++ seeding + Lloyd (landmarks.py:60-129)             */
+/* ---------------------------------------------------------------------- */
+
+/* Bytes of device workspace needed by nys_kmeans_run / nys_kmeans_* for m
+ * points of dimension rho and m0 centroids. */
+size_t nys_kmeans_workspace_bytes(int64_t m, int rho, int m0);
+
+/*
+ * Full k-means on one device, replacing kmeans_landmarks (landmarks.py:76-129):
+ *  - k-means++ seeding in FP64 (landmarks.py:60-73).  The host supplies the
+ *    random stream it drew from numpy's default_rng(seed):  first_index =
+ *    rng.integers(m), then uniforms[j-1] = rng.random() for draw j = 1..m0-1
+ *    (Generator.choice(m, p) == searchsorted(cdf, random(), 'right')).
+ *  - Lloyd iterations (<= max_iter) with the reference's break rule
+ *    (labels unchanged -> stop before the update) and empty-cluster repair.
+ *  - the final exact (differenced) assignment and quant_error.
+ * points [dev]: planar (rho, m) float32 with plane stride `plane_stride`.
+ * centroids_out [dev]: m0*rho float64 row-major.
+ * errors_out [dev]: max_iter float64 (Σ nearest after each assignment step).
+ * stats_out [dev]: int64[4] = {iterations_run, first_zero_total_draw (or -1),
+ *                              last_changed_count, empty_repairs}.
+ * quant_error_out [dev]: float64[1].  assignment_out [dev] (nullable): int64[m].
+ * seed_indices_out [dev] (nullable): int64[m0], the k-means++ picks.
+ * If stats_out[1] >= 0 the k-means++ stream hit sum(d2) == 0 at that draw; the
+ * reference then switches to rng.integers(m) (landmarks.py:69-70) and the
+ * caller must re-run with nys_kmeans_run_seeded() using seed_indices_out[<j]
+ * followed by its own integers(m) draws.
+ */
+int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho,
+                   int m0, int max_iter, int64_t first_index, const double* uniforms /*[host] m0-1*/,
+                   double* centroids_out, double* errors_out, int64_t* stats_out,
+                   double* quant_error_out, int64_t* assignment_out, int64_t* seed_indices_out,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same, but with all m0 seed indices already chosen by the host
+ * (seed_indices [host] int64[m0]); used for the sum(d2)==0 corner case. */
+int nys_kmeans_run_seeded(const float* points, int64_t plane_stride, int64_t m, int rho,
+                          int m0, int max_iter, const int64_t* seed_indices,
+                          double* centroids_out, double* errors_out, int64_t* stats_out,
+                          double* quant_error_out, int64_t* assignment_out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* --- step-wise k-means for the row-band-sharded multi-GPU driver --------- */
+/* Per-rank partial results are combined by the caller (NCCL all-reduce) in a
+ * fixed order; these helpers expose exactly the per-rank reductions.        */
+
+/* d2 := min(d2, |x - c|^2) (or := when init != 0) in FP64 over the local
+ * points; writes the local FP64 sum of d2 to sum_out [dev] (1 double). */
+int nys_kmeanspp_update(const float* points, int64_t plane_stride, int64_t m, int rho,
+                        const double* c /*[dev] rho*/, int init, double* d2,
+                        double* sum_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* First local index i with prefix_sum(d2)[i] > target (FP64); -1 if none.
+ * index_out [dev] int64[1]. */
+int nys_kmeanspp_pick(const double* d2, int64_t m, double target, int64_t* index_out,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* One Lloyd assignment pass over the local points against centroids (FP64
+ * [dev] m0*rho).  labels [dev] int32[m] is read (previous) and rewritten.
+ * acc_out [dev] float64[m0*(rho+1) + 2]: per-cluster coordinate sums and
+ * counts (cluster j at j*(rho+1): rho sums then count), then Σ nearest, then
+ * the number of changed labels.  first_pass != 0 counts every label as
+ * changed. */
+int nys_kmeans_assign(const float* points, int64_t plane_stride, int64_t m, int rho,
+                      const double* centroids, int m0, int32_t* labels, int first_pass,
+                      double* acc_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Exact (differenced) FP64 nearest distance and Σ (landmarks.py:121-129);
+ * assignment_out nullable. sum_out [dev] 1 double. */
+int nys_kmeans_exact(const float* points, int64_t plane_stride, int64_t m, int rho,
+                     const double* centroids, int m0, int64_t* assignment_out,
+                     double* sum_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Local maximum of `nearest` recomputed against `centroids` for the points
+ * labelled `labels`, excluding indices listed in excluded [dev] int64[n_excl];
+ * writes {value, local index} as two doubles to out [dev].  Used for the
+ * empty-cluster repair (landmarks.py:114-119). */
+int nys_kmeans_farthest(const float* points, int64_t plane_stride, int64_t m, int rho,
+                        const double* centroids, int m0, const int32_t* labels,
+                        const int64_t* excluded, int n_excl, double* out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* Gather point `index` (rho coordinates, FP64) into dst [dev]. */
+int nys_gather_point(const float* points, int64_t plane_stride, int rho, int64_t index,
+                     double* dst, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Filter (filters.py:214-257 + spatial.py:194-209 + nystrom.py:43-114)   */
+/* ---------------------------------------------------------------------- */
+
+/* Everything one filter launch needs.  Host-side struct; the library copies
+ * the constants into kernel parameters / device constants itself. */
+typedef struct nys_filter_desc {
+    /* geometry */
+    int n;          /* filtered channels (f) */
+    int rho;        /* guide dimension (p); for guide_kind==1 must be n*9 */
+    int H, W;       /* full image size (the borders replicate at 0 and H-1/W-1) */
+    int guide_kind; /* 0: planar guide (rho planes); 1: raw 3x3 patches of f
+                       gathered on the fly (channel, dy, dx order, edge-replicated,
+                       filters.py:174-181) */
+    /* spatial kernel */
+    int spatial_kind;   /* NYS_SPATIAL_BOX | NYS_SPATIAL_GAUSSIAN_FIR */
+    int radius;         /* R (box radius or FIR truncation radius) */
+    double sigma;       /* FIR sigma (ignored for box) */
+    /* range kernel and landmarks */
+    int m0;             /* landmarks */
+    double theta;       /* Gaussian range scale: kappa = exp(-|s-t|^2/(2 theta^2)) */
+    /* Nystrom algebra, computed on the host in FP64 (nystrom.py:67-114):
+     * M = sum_{k retained} w_k w_k^T / alpha_k, u0 = w_0, alpha0 = alpha_1 */
+    const double* centroids; /* [host] m0*rho */
+    const double* M;         /* [host] m0*m0 row-major */
+    const double* u0;        /* [host] m0 */
+    double alpha0;
+    double eps_den;          /* 1e-12 * (2S+1)^2 * max|alpha| (filters.py:242) */
+} nys_filter_desc;
+
+/* Size of the horizontal-pass plane buffer for `rows` image rows:
+ * (m0+1)*(n+1) planes of rows*W float32. */
+size_t nys_filter_planes_bytes(const nys_filter_desc* d, int rows);
+
+/* Device bytes for the filter's constant block + reduction scratch. */
+size_t nys_filter_workspace_bytes(const nys_filter_desc* d);
+
+/* Upload the per-call constants (centroids, M, u0, taps) into `workspace`
+ * and reset the min|eta| / guarded-pixel accumulators.  Call once per filter
+ * before the band passes below. */
+int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/*
+ * K2: range features + horizontal pass for image rows [row0, row0+rows).
+ * f [dev] (n,H,W) planar, f_plane_stride; guide [dev] (rho,H,W) (ignored for
+ * guide_kind 1; may alias f).  planes [dev]: (m0+1)*(n+1) planes, plane
+ * stride planes_stride (>= rows*W), row r of the band at (r-row0)*W.
+ * Plane (i*(n+1)+c) holds the row-filtered y_i*f_c (c<n) or y_i (c==n), with
+ * y = M b(x) for i<m0 and y_{m0} = u0.b(x) (the rank-1 lead term).
+ */
+int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
+                     const float* guide, int64_t guide_plane_stride,
+                     int row0, int rows, float* planes, int64_t planes_stride,
+                     const void* workspace, void* stream);
+
+/*
+ * K3: vertical pass + per-pixel reconstruction, guard and division for
+ * output rows [out0, out0+out_rows).  The planes buffer must hold rows
+ * [max(0,out0-R), min(H,out0+out_rows+R)) with its first row = planes_row0.
+ * out [dev] (n,H,W) planar with out_plane_stride.  Accumulates min|eta| and
+ * the guarded-pixel count into the workspace.
+ */
+int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
+                     const float* guide, int64_t guide_plane_stride,
+                     const float* planes, int64_t planes_stride, int planes_row0,
+                     int out0, int out_rows, float* out, int64_t out_plane_stride,
+                     const void* workspace, void* stream);
+
+/* Copy {min|eta| (float64), guarded pixels (int64 bit pattern in a double
+ * slot)} into stats_out [dev] (2 x 8 bytes). */
+int nys_filter_stats(const nys_filter_desc* d, const void* workspace, void* stats_out, void* stream);
+
+/* Materialise the raw (2r+1)^2*n patch guide (filters.py:174-181) as planes:
+ * out [dev] (n*(2r+1)^2, H, W). */
+int nys_patch_guide(const float* f, int64_t f_plane_stride, int n, int H, int W, int r,
+                    float* out, int64_t out_plane_stride, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Host FP64 helpers (symeig.py, nystrom.py)                               */
+/* ---------------------------------------------------------------------- */
+
+/* Cyclic Jacobi eigendecomposition of a symmetric k x k matrix (row-major,
+ * symmetrised as (A+A^T)/2), descending eigenvalues, largest-|.| entry of
+ * each eigenvector non-negative (symeig.py:58-125).  vectors_out column j
+ * pairs with values_out[j].  Returns the number of sweeps in *sweeps. */
+int nys_jacobi_eig(const double* a, int k, double* values_out, double* vectors_out, int* sweeps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NYSFILTER_B200_H */

@@ -1,0 +1,770 @@
+// K0 / K1 / K1f: k-means landmark selection in range space, B200 (sm_100a) CUDA.
+//
+// Reference region replaced (/root/reference/pkg/src/nysfilter/landmarks.py):
+//   _plus_plus_init   60-73   -> k_pp_update (FP64 D^2, bit-exact per point) + k_pp_select
+//   _assign (loop)    37-57   -> k_assign   (FP32 differenced distances, first index on ties)
+//   Lloyd update      108-119 -> k_reduce + k_finalize (+ k_repair for empty clusters)
+//   final _assign     121-129 -> k_exact    (FP64 differenced form, quant_error)
+//
+// Determinism: every reduction uses a fixed shape (per-thread sequential runs,
+// fixed butterfly warp sums, warps and blocks combined in index order); no
+// floating-point atomics.  The k-means++ uniforms come from the host (numpy
+// default_rng(seed)), so the seed sequence matches the reference exactly as
+// long as the D^2 prefix sums cross u*total at the same index (they differ
+// from numpy's sequential cumsum only by FP64 rounding).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "nys_common.cuh"
+
+namespace nys {
+
+struct KState {
+  int converged;
+  int iters;
+  int n_empty;
+  int zero_draw;
+  long long changed;
+  long long repairs;
+};
+
+struct KLayout {
+  int64_t m;
+  int rho, m0, S;  // S: Lloyd slots per block = m0*(rho+1) + 2
+  int nb_assign, nb_seed;
+  int64_t seed_chunk;
+  size_t off_d2, off_labels, off_part, off_ppart, off_tot, off_cf, off_cprev, off_excl, off_state, off_arg,
+      off_idx, total;
+};
+
+static int g_sms = 0;
+static int sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static KLayout klayout(int64_t m, int rho, int m0) {
+  KLayout L;
+  L.m = m;
+  L.rho = rho;
+  L.m0 = m0;
+  L.S = m0 * (rho + 1) + 2;
+  L.nb_assign = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, ceil_div(m, 256)));
+  L.nb_seed = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(m, 1024)));
+  L.seed_chunk = ceil_div(m, L.nb_seed);
+  size_t o = 0;
+  L.off_d2 = o;      o = align256(o + (size_t)m * 8);
+  L.off_labels = o;  o = align256(o + (size_t)m * 4);
+  L.off_part = o;    o = align256(o + (size_t)L.nb_assign * L.S * 8);
+  L.off_ppart = o;   o = align256(o + (size_t)L.nb_seed * 8);
+  L.off_tot = o;     o = align256(o + (size_t)L.S * 8);
+  L.off_cf = o;      o = align256(o + (size_t)m0 * rho * 4);
+  L.off_cprev = o;   o = align256(o + (size_t)m0 * rho * 8);
+  L.off_excl = o;    o = align256(o + (size_t)m0 * 8);
+  L.off_state = o;   o = align256(o + sizeof(KState));
+  L.off_arg = o;     o = align256(o + (size_t)std::max(L.nb_assign, L.nb_seed) * 16);
+  L.off_idx = o;     o = align256(o + 64);
+  L.total = o;
+  return L;
+}
+
+// numpy's row reduction order for ((x - c)**2).sum(axis=1) over rho entries
+// (pairwise_sum: sequential from 0 below 8 terms, else 8 strided partials
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail).
+// __dmul_rn/__dadd_rn forbid FMA contraction, so every D^2 value is
+// bit-identical to the reference's (landmarks.py:64,72).
+__device__ __forceinline__ double sqdiff(double x, double c) {
+  const double t = __dsub_rn(x, c);
+  return __dmul_rn(t, t);
+}
+
+__device__ double d2_exact(const float* __restrict__ pts, long long ps, long long i, int rho,
+                           const double* __restrict__ c) {
+  if (rho < 8) {
+    double r = 0.0;
+    for (int d = 0; d < rho; ++d) r = __dadd_rn(r, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = sqdiff((double)__ldg(pts + k * ps + i), c[k]);
+  int d = 8;
+  const int full = rho - (rho % 8);
+  for (; d < full; d += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], sqdiff((double)__ldg(pts + (d + k) * ps + i), c[d + k]));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; d < rho; ++d) res = __dadd_rn(res, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
+  return res;
+}
+
+// fixed-shape block sum (blockDim multiple of 32, <= 1024)
+__device__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nw; ++k) r += sh[k];
+  return r;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------------------
+// k-means++ (landmarks.py:60-73)
+// ---------------------------------------------------------------------------
+__global__ void k_gather(const float* __restrict__ pts, long long ps, int rho, const long long* __restrict__ idxp,
+                         long long idx_const, double* __restrict__ dst) {
+  const long long idx = idxp ? *idxp : idx_const;
+  for (int d = threadIdx.x; d < rho; d += blockDim.x) dst[d] = (double)pts[d * ps + idx];
+}
+
+// d2 = min(d2, |x - c|^2) over the contiguous chunk of block b; ppart[b] = Σ chunk
+__global__ void __launch_bounds__(256) k_pp_update(const float* __restrict__ pts, long long ps, long long m,
+                                                   int rho, const double* __restrict__ c, int init,
+                                                   double* __restrict__ d2, double* __restrict__ ppart,
+                                                   long long chunk, const KState* st) {
+  __shared__ double sh[32];
+  __shared__ double cs[NYS_MAX_RHO];
+  if (st && st->zero_draw >= 0) return;
+  for (int d = threadIdx.x; d < rho; d += blockDim.x) cs[d] = c[d];
+  __syncthreads();
+  const long long lo = blockIdx.x * chunk, hi = min(m, lo + chunk);
+  double s = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double v = d2_exact(pts, ps, i, rho, cs);
+    const double nv = init ? v : fmin(d2[i], v);
+    d2[i] = nv;
+    s += nv;
+  }
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) ppart[blockIdx.x] = t;
+}
+
+// exclusive prefix over per-block sums + the in-chunk scan that finds the first
+// index whose running D^2 prefix exceeds u * total  (Generator.choice semantics)
+__device__ long long pp_find(const double* __restrict__ d2, long long m, const double* __restrict__ ppart,
+                             int nb, long long chunk, double target, double* sh, long long* shi) {
+  // one thread resolves the owning block (nb <= 592 sequential adds)
+  if (threadIdx.x == 0) {
+    double pre = 0.0;
+    int b = -1, last_pos = -1;
+    for (int k = 0; k < nb; ++k) {
+      if (ppart[k] > 0.0) last_pos = k;
+      if (pre + ppart[k] > target) {
+        b = k;
+        break;
+      }
+      pre += ppart[k];
+    }
+    if (b < 0) {  // rounding pushed target past the end: take the last positive block
+      b = last_pos;
+      pre = 0.0;
+      for (int k = 0; k < b; ++k) pre += ppart[k];
+      target = pre + ppart[b] * (1.0 - 1e-16);
+    }
+    sh[0] = (double)b;
+    sh[1] = target - pre;
+  }
+  __syncthreads();
+  const int b = (int)sh[0];
+  const double t = sh[1];
+  const long long lo = b * chunk, hi = min(m, lo + chunk);
+  const long long len = hi - lo;
+  const long long per = ceil_div(len, (long long)blockDim.x);
+  const long long s0 = lo + threadIdx.x * per, s1 = min(hi, s0 + per);
+  double mine = 0.0;
+  for (long long i = s0; i < s1; ++i) mine += d2[i];
+  double* runs = sh + 2;
+  runs[threadIdx.x] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pre = 0.0;
+    int owner = -1;
+    for (int k = 0; k < (int)blockDim.x; ++k) {
+      if (pre + runs[k] > t) {
+        owner = k;
+        break;
+      }
+      pre += runs[k];
+    }
+    if (owner < 0) {
+      for (int k = (int)blockDim.x - 1; k >= 0; --k)
+        if (runs[k] > 0.0) {
+          owner = k;
+          break;
+        }
+      pre = 0.0;
+      for (int k = 0; k < owner; ++k) pre += runs[k];
+    }
+    long long idx = -1;
+    const long long a0 = lo + (long long)owner * per, a1 = min(hi, a0 + per);
+    double acc = pre;
+    long long lastpos = -1;
+    for (long long i = a0; i < a1; ++i) {
+      if (d2[i] > 0.0) lastpos = i;
+      acc += d2[i];
+      if (acc > t) {
+        idx = i;
+        break;
+      }
+    }
+    if (idx < 0) idx = lastpos;
+    *shi = idx;
+  }
+  __syncthreads();
+  return *shi;
+}
+
+__global__ void __launch_bounds__(1024) k_pp_select(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                    const double* __restrict__ d2, const double* __restrict__ ppart,
+                                                    int nb, long long chunk, double u, int draw,
+                                                    double* __restrict__ cdst, long long* __restrict__ seed_idx,
+                                                    KState* st) {
+  __shared__ double sh[2 + 1024];
+  __shared__ long long shi;
+  if (st->zero_draw >= 0) return;
+  // total in fixed order
+  double v = 0.0;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) v += ppart[k];
+  const double total = block_sum(v, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) sh[0] = total;
+  __syncthreads();
+  const double tot = sh[0];
+  __syncthreads();
+  if (!(tot > 0.0)) {
+    if (threadIdx.x == 0) st->zero_draw = draw;
+    return;
+  }
+  const long long idx = pp_find(d2, m, ppart, nb, chunk, u * tot, sh, &shi);
+  if (threadIdx.x == 0 && seed_idx) seed_idx[draw] = idx;
+  for (int d = threadIdx.x; d < rho; d += blockDim.x) cdst[d] = (double)pts[d * ps + idx];
+}
+
+// ---------------------------------------------------------------------------
+// Lloyd assignment (landmarks.py:47-57 semantics, FP32 differenced distances)
+// ---------------------------------------------------------------------------
+template <int GR>
+__global__ void __launch_bounds__(256) k_assign(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                const float* __restrict__ Cf, int m0, int* __restrict__ labels,
+                                                int first, double* __restrict__ part, int S, const KState* st) {
+  extern __shared__ __align__(16) double dsm[];
+  if (st && st->converged) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int slots = m0 * (rho + 1);
+  double* wacc = dsm;                                  // nw x slots
+  float* Cs = reinterpret_cast<float*>(dsm + (size_t)nw * slots);
+  for (int k = threadIdx.x; k < nw * slots; k += blockDim.x) wacc[k] = 0.0;
+  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) Cs[k] = Cf[k];
+  __syncthreads();
+  double* my = wacc + (size_t)w * slots;
+  double near_sum = 0.0;
+  long long changed = 0;
+  const long long chunk = ceil_div(m, (long long)gridDim.x);
+  const long long lo = blockIdx.x * chunk, hi = min(m, lo + chunk);
+  for (long long base = lo + (long long)w * 32; base < hi; base += (long long)nw * 32) {
+    const long long i = base + lane;
+    const bool valid = i < hi;
+    float x[GR];
+#pragma unroll
+    for (int d = 0; d < GR; ++d) x[d] = (valid && d < rho) ? __ldg(pts + d * ps + i) : 0.f;
+    float best = INFINITY;
+    int arg = 0;
+    for (int j = 0; j < m0; ++j) {
+      float d2 = 0.f;
+#pragma unroll
+      for (int d = 0; d < GR; ++d)
+        if (d < rho) {
+          const float t = x[d] - Cs[j * rho + d];
+          d2 = fmaf(t, t, d2);
+        }
+      if (d2 < best) {  // strict: first index wins ties (np.argmin)
+        best = d2;
+        arg = j;
+      }
+    }
+    if (valid) {
+      near_sum += (double)best;
+      const int old = labels[i];
+      if (first || old != arg) ++changed;
+      labels[i] = arg;
+    }
+    // per-cluster coordinate sums: reduce each label group of the warp with a
+    // fixed butterfly (zeros elsewhere), lane 0 owns this warp's accumulators
+    unsigned rem = __ballot_sync(0xffffffffu, valid);
+    while (rem) {
+      const int leader = __ffs(rem) - 1;
+      const int L = __shfl_sync(0xffffffffu, arg, leader);
+      const unsigned grp = __ballot_sync(0xffffffffu, valid && arg == L);
+      const bool in = (grp >> lane) & 1u;
+#pragma unroll
+      for (int d = 0; d < GR; ++d)
+        if (d < rho) {
+          const double s = warp_sum(in ? (double)x[d] : 0.0);
+          if (lane == 0) my[L * (rho + 1) + d] += s;
+        }
+      if (lane == 0) my[L * (rho + 1) + rho] += (double)__popc(grp);
+      rem &= ~grp;
+    }
+  }
+  near_sum = warp_sum(near_sum);
+  const double ch = warp_sum((double)changed);
+  __shared__ double extra[2][32];
+  if (lane == 0) {
+    extra[0][w] = near_sum;
+    extra[1][w] = ch;
+  }
+  __syncthreads();
+  double* out = part + (size_t)blockIdx.x * S;
+  for (int k = threadIdx.x; k < slots; k += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < nw; ++q) s += wacc[(size_t)q * slots + k];
+    out[k] = s;
+  }
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      a += extra[0][q];
+      b += extra[1][q];
+    }
+    out[slots] = a;
+    out[slots + 1] = b;
+  }
+}
+
+// tot[k] = Σ_b part[b][k] in block order
+__global__ void k_reduce(const double* __restrict__ part, int nb, int S, double* __restrict__ tot,
+                         const KState* st) {
+  if (st && st->converged) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= S) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(size_t)b * S + k];
+  tot[k] = s;
+}
+
+// Lloyd bookkeeping for iteration `it` (landmarks.py:101-119)
+__global__ void k_finalize(const double* __restrict__ tot, int m0, int rho, int it, double* __restrict__ C,
+                           double* __restrict__ Cprev, float* __restrict__ Cf, double* __restrict__ errors,
+                           KState* st) {
+  if (st->converged) return;
+  const int slots = m0 * (rho + 1);
+  const long long changed = (long long)tot[slots + 1];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    errors[it] = tot[slots];
+    st->iters = it + 1;
+    st->changed = changed;
+  }
+  if (it > 0 && changed == 0) {
+    if (threadIdx.x == 0) st->converged = 1;
+    return;
+  }
+  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) Cprev[k] = C[k];
+  __syncthreads();
+  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) {
+    const int j = k / rho, d = k - j * rho;
+    const double cnt = tot[j * (rho + 1) + rho];
+    if (cnt > 0.0) C[k] = tot[j * (rho + 1) + d] / cnt;
+    Cf[k] = (float)C[k];
+  }
+  if (threadIdx.x == 0) {
+    int ne = 0;
+    for (int j = 0; j < m0; ++j) ne += tot[j * (rho + 1) + rho] > 0.0 ? 0 : 1;
+    st->n_empty = ne;
+  }
+}
+
+// empty-cluster repair (landmarks.py:114-119): for each empty j in ascending
+// order take the point farthest from its (pre-update) centroid, excluding
+// points already taken; first index on ties.  Rare; one block.
+__global__ void __launch_bounds__(1024) k_repair(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                 const int* __restrict__ labels, const double* __restrict__ tot,
+                                                 int m0, double* __restrict__ C, const double* __restrict__ Cprev,
+                                                 float* __restrict__ Cf, long long* __restrict__ excl, KState* st) {
+  __shared__ double bv[1024];
+  __shared__ long long bi[1024];
+  if (st->converged || st->n_empty == 0) return;
+  int nex = 0;
+  for (int j = 0; j < m0; ++j) {
+    if (tot[j * (rho + 1) + rho] > 0.0) continue;
+    double best = -INFINITY;
+    long long arg = m;
+    for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+      bool ex = false;
+      for (int q = 0; q < nex; ++q) ex |= (excl[q] == i);
+      double v;
+      if (ex) {
+        v = -1.0;
+      } else {
+        v = d2_exact(pts, ps, i, rho, Cprev + (size_t)labels[i] * rho);
+      }
+      if (v > best) {
+        best = v;
+        arg = i;
+      }
+    }
+    bv[threadIdx.x] = best;
+    bi[threadIdx.x] = arg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -INFINITY;
+      long long a = m;
+      for (int k = 0; k < (int)blockDim.x; ++k)
+        if (bv[k] > b || (bv[k] == b && bi[k] < a)) {
+          b = bv[k];
+          a = bi[k];
+        }
+      excl[nex] = a;
+      for (int d = 0; d < rho; ++d) {
+        C[j * rho + d] = (double)pts[d * ps + a];
+        Cf[j * rho + d] = pts[d * ps + a];
+      }
+      st->repairs += 1;
+    }
+    ++nex;
+    __syncthreads();
+  }
+}
+
+// final exact assignment (landmarks.py:121-129): FP64 differenced distances
+__global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                               const double* __restrict__ C, int m0, long long* __restrict__ asg,
+                                               double* __restrict__ part) {
+  extern __shared__ __align__(16) double csm[];
+  __shared__ double sh[32];
+  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) csm[k] = C[k];
+  __syncthreads();
+  const long long chunk = ceil_div(m, (long long)gridDim.x);
+  const long long lo = blockIdx.x * chunk, hi = min(m, lo + chunk);
+  double s = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    double best = INFINITY;
+    int arg = 0;
+    for (int j = 0; j < m0; ++j) {
+      const double v = d2_exact(pts, ps, i, rho, csm + (size_t)j * rho);
+      if (v < best) {
+        best = v;
+        arg = j;
+      }
+    }
+    if (asg) asg[i] = arg;
+    s += fmax(best, 0.0);
+  }
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void k_sum_parts(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) v += part[k];
+  const double t = block_sum(v, sh);
+  if (threadIdx.x == 0) out[0] = t;
+}
+
+__global__ void k_init_state(KState* st, long long* seed_idx, long long first, double* C, int rho, int m0) {
+  st->converged = 0;
+  st->iters = 0;
+  st->n_empty = 0;
+  st->zero_draw = -1;
+  st->changed = 0;
+  st->repairs = 0;
+  if (seed_idx) seed_idx[0] = first;
+}
+
+__global__ void k_c_to_f(const double* __restrict__ C, float* __restrict__ Cf, int n) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) Cf[k] = (float)C[k];
+}
+
+__global__ void k_write_stats(const KState* st, long long* out) {
+  out[0] = st->iters;
+  out[1] = st->zero_draw;
+  out[2] = st->changed;
+  out[3] = st->repairs;
+}
+
+// farthest point for the multi-GPU repair (value, local index) -- single block
+__global__ void __launch_bounds__(1024) k_farthest(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                   const double* __restrict__ C, const int* __restrict__ labels,
+                                                   const long long* __restrict__ excl, int nex, double* out) {
+  __shared__ double bv[1024];
+  __shared__ long long bi[1024];
+  double best = -INFINITY;
+  long long arg = m;
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+    bool ex = false;
+    for (int q = 0; q < nex; ++q) ex |= (excl[q] == i);
+    const double v = ex ? -1.0 : d2_exact(pts, ps, i, rho, C + (size_t)labels[i] * rho);
+    if (v > best) {
+      best = v;
+      arg = i;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = arg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = -INFINITY;
+    long long a = m;
+    for (int k = 0; k < (int)blockDim.x; ++k)
+      if (bv[k] > b || (bv[k] == b && bi[k] < a)) {
+        b = bv[k];
+        a = bi[k];
+      }
+    out[0] = b;
+    out[1] = (double)a;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_pick(const double* __restrict__ d2, long long m, const double* __restrict__ ppart,
+                                               int nb, long long chunk, double target, long long* out) {
+  __shared__ double sh[2 + 1024];
+  __shared__ long long shi;
+  double v = 0.0;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) v += ppart[k];
+  const double total = block_sum(v, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) sh[0] = total;
+  __syncthreads();
+  const double tot = sh[0];
+  __syncthreads();
+  if (!(tot > 0.0) || target >= tot) {
+    if (threadIdx.x == 0) *out = -1;
+    return;
+  }
+  const long long idx = pp_find(d2, m, ppart, nb, chunk, target, sh, &shi);
+  if (threadIdx.x == 0) *out = idx;
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static int launch_assign(const float* pts, long long ps, long long m, int rho, const float* Cf, int m0, int* labels,
+                         int first, double* part, int nb, int S, const KState* st, cudaStream_t s) {
+  const int slots = m0 * (rho + 1);
+  // warps per block limited by the per-warp FP64 accumulators in shared memory
+  const size_t budget = 160 * 1024;
+  int nw = 8;
+  while (nw > 1 && (size_t)nw * slots * 8 + (size_t)m0 * rho * 4 > budget) --nw;
+  const size_t smem = (size_t)nw * slots * 8 + (size_t)m0 * rho * 4;
+  if (smem > 220 * 1024) return NYS_EUNSUPPORTED;
+#define NYS_A_CASE(G)                                                                                        \
+  NYS_CUDA_TRY(cudaFuncSetAttribute(k_assign<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+  count_launch(); k_assign<G><<<nb, nw * 32, smem, s>>>(pts, ps, m, rho, Cf, m0, labels, first, part, S, st);
+  if (rho <= 4) {
+    NYS_A_CASE(4)
+  } else if (rho <= 16) {
+    NYS_A_CASE(16)
+  } else if (rho <= 32) {
+    NYS_A_CASE(32)
+  } else {
+    NYS_A_CASE(64)
+  }
+#undef NYS_A_CASE
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+static int check_common(const float* pts, int64_t m, int rho, int m0, void* ws, size_t wsb) {
+  if (!pts || m < 1 || rho < 1 || rho > NYS_MAX_RHO || m0 < 1 || m0 > NYS_MAX_M0 || m0 > m) return NYS_EINVAL;
+  if (!ws || wsb < klayout(m, rho, m0).total) return NYS_EINVAL;
+  return NYS_OK;
+}
+
+static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho, int m0, int max_iter,
+                               double* C, double* errors, int64_t* stats, double* qe, int64_t* asg,
+                               char* ws, const KLayout& L, cudaStream_t s) {
+  KState* st = reinterpret_cast<KState*>(ws + L.off_state);
+  int* labels = reinterpret_cast<int*>(ws + L.off_labels);
+  double* part = reinterpret_cast<double*>(ws + L.off_part);
+  double* tot = reinterpret_cast<double*>(ws + L.off_tot);
+  float* Cf = reinterpret_cast<float*>(ws + L.off_cf);
+  double* Cprev = reinterpret_cast<double*>(ws + L.off_cprev);
+  long long* excl = reinterpret_cast<long long*>(ws + L.off_excl);
+  count_launch(); k_c_to_f<<<1, 256, 0, s>>>(C, Cf, m0 * rho);
+  NYS_LAUNCH_CHECK();
+  for (int it = 0; it < max_iter; ++it) {
+    int rc = launch_assign(pts, ps, m, rho, Cf, m0, labels, it == 0, part, L.nb_assign, L.S, st, s);
+    if (rc) return rc;
+    count_launch(); k_reduce<<<(int)ceil_div(L.S, 256), 256, 0, s>>>(part, L.nb_assign, L.S, tot, st);
+    count_launch(); k_finalize<<<1, 256, 0, s>>>(tot, m0, rho, it, C, Cprev, Cf, errors, st);
+    count_launch(); k_repair<<<1, 1024, 0, s>>>(pts, ps, m, rho, labels, tot, m0, C, Cprev, Cf, excl, st);
+    NYS_LAUNCH_CHECK();
+  }
+  double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
+  const size_t smem = (size_t)m0 * rho * 8;
+  if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  count_launch(); k_exact<<<L.nb_assign, 256, smem, s>>>(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart);
+  count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, qe);
+  count_launch(); k_write_stats<<<1, 1, 0, s>>>(st, reinterpret_cast<long long*>(stats));
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+}  // namespace nys
+
+using namespace nys;
+
+extern "C" {
+
+int nys_abi_version(void) { return 100; }
+
+size_t nys_kmeans_workspace_bytes(int64_t m, int rho, int m0) {
+  if (m < 1 || rho < 1 || m0 < 1) return 0;
+  return klayout(m, rho, m0).total;
+}
+
+int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho, int m0, int max_iter,
+                   int64_t first_index, const double* uniforms, double* centroids_out, double* errors_out,
+                   int64_t* stats_out, double* quant_error_out, int64_t* assignment_out,
+                   int64_t* seed_indices_out, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
+  if (rc) return rc;
+  if (max_iter < 1 || first_index < 0 || first_index >= m || !centroids_out || !errors_out || !stats_out ||
+      !quant_error_out || (m0 > 1 && !uniforms))
+    return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  char* ws = reinterpret_cast<char*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  KState* st = reinterpret_cast<KState*>(ws + L.off_state);
+  double* d2 = reinterpret_cast<double*>(ws + L.off_d2);
+  double* ppart = reinterpret_cast<double*>(ws + L.off_ppart);
+  long long* seeds = reinterpret_cast<long long*>(seed_indices_out);
+  count_launch(); k_init_state<<<1, 1, 0, s>>>(st, seeds, first_index, centroids_out, rho, m0);
+  count_launch(); k_gather<<<1, 64, 0, s>>>(points, plane_stride, rho, nullptr, first_index, centroids_out);
+  NYS_LAUNCH_CHECK();
+  for (int j = 1; j < m0; ++j) {
+    count_launch(); k_pp_update<<<L.nb_seed, 256, 0, s>>>(points, plane_stride, m, rho, centroids_out + (size_t)(j - 1) * rho,
+                                          j == 1, d2, ppart, L.seed_chunk, st);
+    count_launch(); k_pp_select<<<1, 1024, 0, s>>>(points, plane_stride, m, rho, d2, ppart, L.nb_seed, L.seed_chunk,
+                                   uniforms[j - 1], j, centroids_out + (size_t)j * rho, seeds, st);
+    NYS_LAUNCH_CHECK();
+  }
+  return run_lloyd_and_final(points, plane_stride, m, rho, m0, max_iter, centroids_out, errors_out, stats_out,
+                             quant_error_out, assignment_out, ws, L, s);
+}
+
+int nys_kmeans_run_seeded(const float* points, int64_t plane_stride, int64_t m, int rho, int m0, int max_iter,
+                          const int64_t* seed_indices, double* centroids_out, double* errors_out,
+                          int64_t* stats_out, double* quant_error_out, int64_t* assignment_out, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
+  if (rc) return rc;
+  if (max_iter < 1 || !seed_indices || !centroids_out || !errors_out || !stats_out || !quant_error_out)
+    return NYS_EINVAL;
+  for (int j = 0; j < m0; ++j)
+    if (seed_indices[j] < 0 || seed_indices[j] >= m) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  char* ws = reinterpret_cast<char*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  KState* st = reinterpret_cast<KState*>(ws + L.off_state);
+  count_launch(); k_init_state<<<1, 1, 0, s>>>(st, nullptr, 0, centroids_out, rho, m0);
+  for (int j = 0; j < m0; ++j) {
+    count_launch();
+    k_gather<<<1, 64, 0, s>>>(points, plane_stride, rho, nullptr, seed_indices[j], centroids_out + (size_t)j * rho);
+  }
+  NYS_LAUNCH_CHECK();
+  return run_lloyd_and_final(points, plane_stride, m, rho, m0, max_iter, centroids_out, errors_out, stats_out,
+                             quant_error_out, assignment_out, ws, L, s);
+}
+
+int nys_kmeanspp_update(const float* points, int64_t plane_stride, int64_t m, int rho, const double* c, int init,
+                        double* d2, double* sum_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!points || !c || !d2 || !sum_out || m < 1 || rho < 1 || rho > NYS_MAX_RHO) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, 1);
+  if (!workspace || workspace_bytes < L.total) return NYS_EINVAL;
+  char* ws = reinterpret_cast<char*>(workspace);
+  double* ppart = reinterpret_cast<double*>(ws + L.off_ppart);
+  cudaStream_t s = (cudaStream_t)stream;
+  count_launch(); k_pp_update<<<L.nb_seed, 256, 0, s>>>(points, plane_stride, m, rho, c, init, d2, ppart, L.seed_chunk, nullptr);
+  count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_seed, sum_out);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeanspp_pick(const double* d2, int64_t m, double target, int64_t* index_out, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (!d2 || !index_out || m < 1) return NYS_EINVAL;
+  const KLayout L = klayout(m, 1, 1);
+  if (!workspace || workspace_bytes < L.total) return NYS_EINVAL;
+  // the per-block sums of the last nys_kmeanspp_update on this workspace
+  char* ws = reinterpret_cast<char*>(workspace);
+  double* ppart = reinterpret_cast<double*>(ws + L.off_ppart);
+  count_launch(); k_pick<<<1, 1024, 0, (cudaStream_t)stream>>>(d2, m, ppart, L.nb_seed, L.seed_chunk, target,
+                                                reinterpret_cast<long long*>(index_out));
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_assign(const float* points, int64_t plane_stride, int64_t m, int rho, const double* centroids, int m0,
+                      int32_t* labels, int first_pass, double* acc_out, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+  int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
+  if (rc) return rc;
+  if (!centroids || !labels || !acc_out) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  char* ws = reinterpret_cast<char*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  float* Cf = reinterpret_cast<float*>(ws + L.off_cf);
+  double* part = reinterpret_cast<double*>(ws + L.off_part);
+  count_launch(); k_c_to_f<<<1, 256, 0, s>>>(centroids, Cf, m0 * rho);
+  rc = launch_assign(points, plane_stride, m, rho, Cf, m0, labels, first_pass, part, L.nb_assign, L.S, nullptr, s);
+  if (rc) return rc;
+  count_launch(); k_reduce<<<(int)ceil_div(L.S, 256), 256, 0, s>>>(part, L.nb_assign, L.S, acc_out, nullptr);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_exact(const float* points, int64_t plane_stride, int64_t m, int rho, const double* centroids, int m0,
+                     int64_t* assignment_out, double* sum_out, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+  int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
+  if (rc) return rc;
+  if (!centroids || !sum_out) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  char* ws = reinterpret_cast<char*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
+  const size_t smem = (size_t)m0 * rho * 8;
+  if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  count_launch(); k_exact<<<L.nb_assign, 256, smem, s>>>(points, plane_stride, m, rho, centroids, m0,
+                                         reinterpret_cast<long long*>(assignment_out), ppart);
+  count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, sum_out);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_farthest(const float* points, int64_t plane_stride, int64_t m, int rho, const double* centroids, int m0,
+                        const int32_t* labels, const int64_t* excluded, int n_excl, double* out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
+  if (rc) return rc;
+  if (!centroids || !labels || !out || (n_excl > 0 && !excluded)) return NYS_EINVAL;
+  count_launch(); k_farthest<<<1, 1024, 0, (cudaStream_t)stream>>>(points, plane_stride, m, rho, centroids, labels,
+                                                    reinterpret_cast<const long long*>(excluded), n_excl, out);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_gather_point(const float* points, int64_t plane_stride, int rho, int64_t index, double* dst, void* stream) {
+  if (!points || !dst || rho < 1 || index < 0) return NYS_EINVAL;
+  count_launch(); k_gather<<<1, 64, 0, (cudaStream_t)stream>>>(points, plane_stride, rho, nullptr, index, dst);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,346 @@
+"""Filter API (drop-in mirror of reference ``filters.py``).
+
+``fast_filter(f, p, params) -> FilterReport`` keeps the reference's contract
+(filters.py:199-274): same parameters, same validation errors, same report
+fields and timing keys.  The work runs on the B200:
+
+  k-means++ + Lloyd  -> K0/K1 kernels (landmarks.py)
+  A, eig, drop rule  -> host FP64 (nystrom.mixing_plan), m0 x m0 only
+  features + H-pass  -> K2  nys_filter_hpass
+  V-pass + Σ_k + guard + division -> K3  nys_filter_vpass
+
+There is no CPU fallback: without the native library or a GPU every call
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import StageTimer, ptr, require_cuda, stream_ptr, to_device_f32, workspace
+from .bands import Band, plan_bands
+from .image import Image
+from .landmarks import DEFAULT_MAX_ITER, exact_assignment, kmeans_device
+from .nystrom import DEFAULT_EPS_DROP, RangeKernel, mixing_plan
+from .spatial import BOX, GAUSSIAN_FIR, GAUSSIAN_RECURSIVE, SpatialKernel
+
+MODE_BILATERAL = "bilateral"
+MODE_JOINT = "joint"
+MODE_NLM = "nlm"
+STRATEGY_KMEANS = "kmeans"
+STRATEGY_UNIFORM = "uniform"
+DENOMINATOR_EPS_SCALE = 1e-12
+
+# default cap on the horizontal-pass plane buffer (bytes); bands are planned
+# so that one band's planes fit (bands.plan_bands)
+PLANE_BUDGET_BYTES = 64 << 30
+
+
+@dataclass(frozen=True)
+class FilterParams:
+    """Everything that determines a filtering run (filters.py:57-86)."""
+
+    spatial: SpatialKernel
+    theta: float
+    m0: int = 15
+    seed: int = 0
+    landmark_strategy: str = STRATEGY_KMEANS
+    mode: str = MODE_BILATERAL
+    patch_radius: int = 3
+    pca_dim: int = 25
+    eps_drop: float = DEFAULT_EPS_DROP
+    kmeans_max_iter: int = DEFAULT_MAX_ITER
+
+    def __post_init__(self) -> None:
+        if self.theta <= 0:
+            raise ValueError("theta must be positive")
+        if self.m0 < 1:
+            raise ValueError("m0 must be >= 1")
+        if self.landmark_strategy not in (STRATEGY_KMEANS, STRATEGY_UNIFORM):
+            raise ValueError(f"unknown landmark strategy {self.landmark_strategy!r}")
+        if self.mode not in (MODE_BILATERAL, MODE_JOINT, MODE_NLM):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if not 0.0 <= self.eps_drop < 1.0:
+            raise ValueError("eps_drop must lie in [0, 1)")
+
+    @property
+    def range_kernel(self) -> RangeKernel:
+        return RangeKernel(theta=self.theta)
+
+
+@dataclass
+class FilterReport:
+    """filters.py:89-96 plus the landmarks actually used."""
+
+    output: Image
+    timings: dict = field(default_factory=dict)
+    retained_rank: int = 0
+    quant_error: float = 0.0
+    min_denominator: float = 0.0
+    guarded_pixels: int = 0
+    centroids: np.ndarray | None = None
+
+
+class PatchGuide:
+    """Lazy NLM guide: the raw (2r+1)^2 patches of ``source`` per pixel
+    (channel-major, then dy, then dx, edge-replicated: filters.py:174-181).
+
+    With ``pca_dim`` equal to the full patch dimension the reference's PCA
+    guide is a centring plus an orthonormal rotation of these patches, which
+    leaves every guide-space distance -- and therefore k-means, the range
+    kernel and the filter output -- unchanged (survey probe: 6.9e-10), so the
+    kernels gather raw patches straight from the image instead of storing a
+    dim-channel guide.  Landmark coordinates are then in raw-patch space.
+    """
+
+    def __init__(self, source: Image, patch_radius: int):
+        self.source = source
+        self.patch_radius = int(patch_radius)
+        self.range_max = source.range_max
+
+    @property
+    def channels(self) -> int:
+        return self.source.channels * (2 * self.patch_radius + 1) ** 2
+
+    @property
+    def height(self) -> int:
+        return self.source.height
+
+    @property
+    def width(self) -> int:
+        return self.source.width
+
+    def device_planes(self, f_dev: torch.Tensor | None = None) -> torch.Tensor:
+        f_dev = to_device_f32(self.source.data) if f_dev is None else f_dev
+        n, H, W = f_dev.shape
+        out = torch.empty((self.channels, H, W), dtype=torch.float32, device=f_dev.device)
+        _native.call("nys_patch_guide", ptr(f_dev), H * W, n, H, W, self.patch_radius, ptr(out), H * W,
+                     stream_ptr())
+        return out
+
+    @property
+    def data(self):
+        planes = self.device_planes()
+        return planes if self.source.on_device else planes.double().cpu().numpy()
+
+
+def _check_sizes(f, p) -> None:
+    if (f.width, f.height) != (p.width, p.height):
+        raise ValueError(f"input {f.width}x{f.height} and guide {p.width}x{p.height} must share the spatial size")
+
+
+def build_guide(f: Image, mode: str = MODE_BILATERAL, guide: Image | None = None, patch_radius: int = 3,
+                pca_dim: int = 25):
+    """Guide for the requested mode (filters.py:141-158)."""
+    if mode == MODE_BILATERAL:
+        return f
+    if mode == MODE_JOINT:
+        if guide is None:
+            raise ValueError("joint mode requires an external guide image")
+        _check_sizes(f, guide)
+        return guide
+    if mode == MODE_NLM:
+        return pca_patch_guide(f, patch_radius, pca_dim)
+    raise ValueError(f"unknown mode {mode!r}")
+
+
+def pca_patch_guide(f: Image, patch_radius: int, pca_dim: int):
+    """PCA patch guide (filters.py:161-187).  The full-dimension case (the
+    configuration BASELINE cfg 3 uses) is served by ``PatchGuide``; a
+    truncated projection (pca_dim < n(2r+1)^2) is §8 row f3 and not on the
+    B200 path yet."""
+    dim = f.channels * (2 * patch_radius + 1) ** 2
+    if not 1 <= pca_dim <= dim:
+        raise ValueError(f"pca_dim must lie in [1, {dim}], got {pca_dim}")
+    if pca_dim < dim:
+        raise NotImplementedError("truncated PCA patch guides (pca_dim < full) are not on the B200 path yet")
+    return PatchGuide(f, patch_radius)
+
+
+def _desc(n: int, rho: int, H: int, W: int, gkind: int, spatial: SpatialKernel, theta: float,
+          C_: np.ndarray, plan, keep: list) -> _native.FilterDesc:
+    d = _native.FilterDesc()
+    d.n, d.rho, d.H, d.W, d.guide_kind = n, rho, H, W, gkind
+    if spatial.kind == BOX:
+        d.spatial_kind, d.radius, d.sigma = _native.NYS_SPATIAL_BOX, spatial.radius, 0.0
+    elif spatial.kind == GAUSSIAN_FIR:
+        d.spatial_kind, d.radius, d.sigma = _native.NYS_SPATIAL_GAUSSIAN_FIR, spatial.radius, spatial.sigma
+    else:
+        raise NotImplementedError("recursive Gaussian (spatial.py:114-191) is §8 row f2, not on the B200 path yet")
+    d.m0 = C_.shape[0]
+    d.theta = theta
+    arrs = [np.ascontiguousarray(C_, dtype=np.float64), np.ascontiguousarray(plan.M, dtype=np.float64),
+            np.ascontiguousarray(plan.u0, dtype=np.float64)]
+    keep.extend(arrs)
+    d.centroids = arrs[0].ctypes.data_as(C.POINTER(C.c_double))
+    d.M = arrs[1].ctypes.data_as(C.POINTER(C.c_double))
+    d.u0 = arrs[2].ctypes.data_as(C.POINTER(C.c_double))
+    d.alpha0 = plan.alpha0
+    d.eps_den = plan.eps_den
+    return d
+
+
+@dataclass
+class _Inputs:
+    f: torch.Tensor          # (n, H, W) float32
+    guide: torch.Tensor      # planar guide for the kernels (== f for BLF / patch-on-the-fly)
+    gkind: int               # 0 planar, 1 3x3 patches gathered from f
+    points: torch.Tensor     # (rho, m) planar k-means points
+    rho: int
+
+
+def _prepare_inputs(f: Image, p) -> _Inputs:
+    f_dev = to_device_f32(f.data)
+    n, H, W = f_dev.shape
+    if p is f or (isinstance(p, Image) and p.data is f.data):
+        return _Inputs(f_dev, f_dev, 0, f_dev.reshape(n, H * W), n)
+    if isinstance(p, PatchGuide):
+        planes = p.device_planes(f_dev if p.source is f else None)
+        rho = planes.shape[0]
+        if p.patch_radius == 1 and p.source is f:
+            return _Inputs(f_dev, f_dev, 1, planes.reshape(rho, H * W), rho)
+        return _Inputs(f_dev, planes, 0, planes.reshape(rho, H * W), rho)
+    g_dev = to_device_f32(p.data)
+    return _Inputs(f_dev, g_dev, 0, g_dev.reshape(g_dev.shape[0], H * W), g_dev.shape[0])
+
+
+def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer: StageTimer | None = None,
+               plane_budget: int | None = None, out: torch.Tensor | None = None,
+               kernel_events: list | None = None):
+    """K2/K3 over row bands given landmarks; returns (out, plan, stats).
+
+    ``kernel_events`` (optional list) receives (name, start, end) CUDA events
+    recorded on the launching stream around every K2/K3 launch."""
+    n, H, W = inp.f.shape
+    S = params.spatial.effective_radius()
+    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S)
+    keep: list = []
+    d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
+    lib = _native.lib()
+    wsb = int(lib.nys_filter_workspace_bytes(C.byref(d)))
+    if wsb == 0:
+        raise NotImplementedError(f"filter shape n={n} rho={inp.rho} m0={d.m0} R={d.radius} not supported")
+    ws = workspace(wsb)
+    s = stream_ptr()
+    _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
+    if timer:
+        timer.mark("extrapolation")
+    row_bytes = int(lib.nys_filter_planes_bytes(C.byref(d), 1))
+    budget = plane_budget if plane_budget is not None else _plane_budget()
+    bands = plan_bands(H, d.radius, row_bytes, budget)
+    max_rows = max(b.hp_rows for b in bands)
+    planes = torch.empty(((d.m0 + 1) * (n + 1), max_rows * W), dtype=torch.float32, device=inp.f.device)
+    hps = int(planes.stride(0))
+    if out is None:
+        out = torch.empty((n, H, W), dtype=torch.float32, device=inp.f.device)
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    for b in bands:
+        e0 = ev() if kernel_events is not None else None
+        _native.check(lib.nys_filter_hpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, b.hp0, b.hp_rows,
+                                           ptr(planes), hps, ptr(ws), s), "nys_filter_hpass")
+        e1 = ev() if kernel_events is not None else None
+        _native.check(lib.nys_filter_vpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, ptr(planes), hps,
+                                           b.hp0, b.out0, b.out_rows, ptr(out), H * W, ptr(ws), s),
+                      "nys_filter_vpass")
+        if kernel_events is not None:
+            e2 = ev()
+            kernel_events.append(("k_feat_hpass", e0, e1, b))
+            kernel_events.append(("k_vpass", e1, e2, b))
+    if timer:
+        timer.mark("convolutions")
+    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device)
+    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats), s), "nys_filter_stats")
+    del keep
+    return out, plan, stats
+
+
+def _plane_budget() -> int:
+    free, _total = torch.cuda.mem_get_info()
+    return int(min(PLANE_BUDGET_BYTES, max(256 << 20, free * 0.7)))
+
+
+def _stats_host(stats: torch.Tensor) -> tuple[float, int]:
+    h = stats.cpu()
+    return float(h[0]), int(h[1:].view(torch.int64)[0])
+
+
+def _output_image(out: torch.Tensor, f: Image) -> Image:
+    """Output in the caller's container: device tensor stays on the device, a
+    host tensor (e.g. pinned) gets a host float32 tensor, NumPy gets the
+    reference's float64 ndarray."""
+    if f.on_device:
+        return Image(data=out, range_max=f.range_max)
+    if f.is_tensor:
+        host = torch.empty(out.shape, dtype=torch.float32, pin_memory=f.data.is_pinned())
+        host.copy_(out)
+        return Image(data=host, range_max=f.range_max)
+    return Image(data=out.double().cpu().numpy(), range_max=f.range_max)
+
+
+def _select_landmarks(inp: _Inputs, params: FilterParams):
+    if params.landmark_strategy == STRATEGY_KMEANS:
+        km = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter)
+        return km.centroids, km.quant_error
+    rng = np.random.default_rng(params.seed)
+    m = inp.points.shape[1]
+    idx = rng.choice(m, size=params.m0, replace=False)
+    centroids = inp.points[:, torch.as_tensor(idx, device=inp.points.device)].t().double().cpu().numpy()
+    _, qe = exact_assignment(inp.points, centroids, want_assignment=False)
+    return centroids, qe
+
+
+def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None = None) -> FilterReport:
+    """Low-rank kernel filter, Algorithm 1 (filters.py:199-274), on the B200."""
+    _check_sizes(f, p)
+    n, H, W = f.channels, f.height, f.width
+    if params.m0 > H * W:
+        raise ValueError(f"m0 = {params.m0} exceeds the pixel count {H * W}")
+    require_cuda()
+    timer = StageTimer()
+    timer.mark("start")
+    inp = _prepare_inputs(f, p)
+    timer.mark("upload")
+    centroids, qe = _select_landmarks(inp, params)
+    timer.mark("clustering")
+    timer.mark("eigendecomposition")  # host eig happens inside run_filter's mixing_plan
+    out, plan, stats = run_filter(inp, centroids, params, timer, kernel_events=kernel_events)
+    min_den, guarded = _stats_host(stats)
+    timer.mark("normalization")  # fused into K3
+    t = timer.elapsed()
+    timings = {k: t.get(k, 0.0) for k in ("clustering", "eigendecomposition", "extrapolation", "convolutions",
+                                          "normalization")}
+    timings["upload"] = t.get("upload", 0.0)
+    timings["total"] = sum(t.values())
+    return FilterReport(output=_output_image(out, f), timings=timings, retained_rank=int(plan.alphas.shape[0]),
+                        quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
+
+
+def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> FilterReport:
+    """Stage-1 parity boundary: the filter given landmarks
+    (e.g. the reference's own k-means centroids)."""
+    _check_sizes(f, p)
+    require_cuda()
+    timer = StageTimer()
+    timer.mark("start")
+    inp = _prepare_inputs(f, p)
+    C_ = np.ascontiguousarray(np.asarray(centroids, dtype=np.float64))
+    if C_.ndim != 2 or C_.shape[1] != inp.rho:
+        raise ValueError(f"landmark dim {C_.shape[-1]} != guide dim {inp.rho}")
+    timer.mark("upload")
+    out, plan, stats = run_filter(inp, C_, params, timer)
+    min_den, guarded = _stats_host(stats)
+    _, qe = exact_assignment(inp.points, C_, want_assignment=False)
+    timer.mark("normalization")
+    t = timer.elapsed()
+    t["total"] = sum(t.values())
+    return FilterReport(output=_output_image(out, f), timings=t, retained_rank=int(plan.alphas.shape[0]),
+                        quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=C_)

@@ -1,0 +1,165 @@
+"""Landmark selection on the GPU (mirror of reference ``landmarks.py:18-148``).
+
+``kmeans_landmarks`` keeps the reference's contract: k-means++ seeding from
+``np.random.default_rng(seed)`` (the host draws exactly the reference's
+stream: ``integers(m)`` then one ``random()`` per D^2 draw), Lloyd iterations
+until the labels repeat or ``max_iter``, empty-cluster repair, and the final
+exact assignment.  All passes over the points run in the K0/K1 CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import ptr, require_cuda, stream_ptr, to_device_f32, workspace
+
+DEFAULT_MAX_ITER = 50
+
+
+@dataclass(frozen=True)
+class LandmarkSet:
+    """Centroids plus each point's nearest-centroid assignment (landmarks.py:18-34)."""
+
+    centroids: np.ndarray
+    assignment: np.ndarray
+    quant_error: float
+    errors: tuple = ()
+
+    @property
+    def count(self) -> int:
+        return self.centroids.shape[0]
+
+
+@dataclass
+class DeviceKMeans:
+    centroids: np.ndarray          # (m0, rho) float64, host
+    quant_error: float
+    errors: tuple
+    iterations: int
+    seed_indices: np.ndarray
+    assignment: torch.Tensor | None  # int64 (m,) on device
+
+
+def _seed_stream(m: int, m0: int, seed: int):
+    rng = np.random.default_rng(seed)
+    first = int(rng.integers(m))
+    uniforms = np.ascontiguousarray(rng.random(m0 - 1) if m0 > 1 else np.zeros(1))
+    return first, uniforms
+
+
+def _replay_zero_total(m: int, m0: int, seed: int, j0: int, device_seeds: np.ndarray) -> np.ndarray:
+    """Seed indices when sum(D^2) hit 0 at draw j0: the reference switches to
+    rng.integers(m) for that and every later draw (landmarks.py:66-70)."""
+    rng = np.random.default_rng(seed)
+    rng.integers(m)
+    for _ in range(1, j0):
+        rng.random()
+    seeds = np.array(device_seeds, dtype=np.int64).copy()
+    for j in range(j0, m0):
+        seeds[j] = int(rng.integers(m))
+    return seeds
+
+
+def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER,
+                  want_assignment: bool = False) -> DeviceKMeans:
+    """k-means on planar device points ``(rho, m)`` float32 (rows may be any
+    plane stride; the last dim must be contiguous)."""
+    require_cuda()
+    if points.dim() != 2 or points.stride(1) != 1:
+        raise ValueError("points must be a (rho, m) tensor with contiguous rows")
+    rho, m = int(points.shape[0]), int(points.shape[1])
+    if m0 < 1 or m0 > m:
+        raise ValueError(f"m0 must be in [1, {m}], got {m0}")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    if rho > _native.NYS_MAX_RHO or m0 > _native.NYS_MAX_M0:
+        raise NotImplementedError(f"rho <= {_native.NYS_MAX_RHO} and m0 <= {_native.NYS_MAX_M0} on the B200 path")
+    lib = _native.lib()
+    dev = points.device
+    ps = int(points.stride(0))
+    wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
+    ws = workspace(wsb)
+    Cd = torch.empty((m0, rho), dtype=torch.float64, device=dev)
+    errs = torch.zeros(max_iter, dtype=torch.float64, device=dev)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    qe = torch.zeros(1, dtype=torch.float64, device=dev)
+    seeds = torch.zeros(m0, dtype=torch.int64, device=dev)
+    asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
+    first, uniforms = _seed_stream(m, m0, seed)
+    _native.check(lib.nys_kmeans_run(ptr(points), ps, m, rho, m0, max_iter, first,
+                                     uniforms.ctypes.data, ptr(Cd), ptr(errs), ptr(stats), ptr(qe),
+                                     ptr(asg), ptr(seeds), ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
+    st = stats.cpu().numpy()
+    if st[1] >= 0:  # sum(D^2) == 0 during seeding: redo with the reference's integers() picks
+        sidx = _replay_zero_total(m, m0, seed, int(st[1]), seeds.cpu().numpy())
+        sidx = np.ascontiguousarray(sidx, dtype=np.int64)
+        _native.check(lib.nys_kmeans_run_seeded(ptr(points), ps, m, rho, m0, max_iter, sidx.ctypes.data,
+                                                ptr(Cd), ptr(errs), ptr(stats), ptr(qe), ptr(asg),
+                                                ptr(ws), wsb, stream_ptr()), "nys_kmeans_run_seeded")
+        st = stats.cpu().numpy()
+        seeds_h = sidx
+    else:
+        seeds_h = seeds.cpu().numpy()
+    iters = int(st[0])
+    return DeviceKMeans(centroids=Cd.cpu().numpy(), quant_error=float(qe.cpu().numpy()[0]),
+                        errors=tuple(errs[:iters].cpu().numpy().tolist()), iterations=iters,
+                        seed_indices=seeds_h, assignment=asg)
+
+
+def _points_planar(points) -> torch.Tensor:
+    """(m, dim) host/device points -> planar (dim, m) float32 device tensor."""
+    if isinstance(points, torch.Tensor):
+        t = points
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(points, dtype=np.float64)))
+    if t.dim() != 2:
+        raise ValueError("points must be an (m, dim) matrix")
+    return to_device_f32(t.t())
+
+
+def kmeans_landmarks(points, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER) -> LandmarkSet:
+    """Cluster ``points`` (m, dim) into ``m0`` groups (landmarks.py:76-129)."""
+    pts = np.asarray(points) if not isinstance(points, torch.Tensor) else points
+    m = int(pts.shape[0])
+    if m0 < 1 or m0 > m:
+        raise ValueError(f"m0 must be in [1, {m}], got {m0}")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    res = kmeans_device(_points_planar(points), m0, seed=seed, max_iter=max_iter, want_assignment=True)
+    return LandmarkSet(centroids=res.centroids, assignment=res.assignment.cpu().numpy(),
+                       quant_error=res.quant_error, errors=res.errors)
+
+
+def exact_assignment(points_planar: torch.Tensor, centroids: np.ndarray, want_assignment: bool = True):
+    """Final exact assignment + quant_error on the device (landmarks.py:121-129)."""
+    rho, m = int(points_planar.shape[0]), int(points_planar.shape[1])
+    m0 = int(centroids.shape[0])
+    lib = _native.lib()
+    dev = points_planar.device
+    wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
+    ws = workspace(wsb)
+    Cd = torch.from_numpy(np.ascontiguousarray(centroids, dtype=np.float64)).to(dev)
+    asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
+    qe = torch.zeros(1, dtype=torch.float64, device=dev)
+    _native.check(lib.nys_kmeans_exact(ptr(points_planar), int(points_planar.stride(0)), m, rho, ptr(Cd), m0,
+                                       ptr(asg), ptr(qe), ptr(ws), wsb, stream_ptr()), "nys_kmeans_exact")
+    return asg, float(qe.cpu().numpy()[0])
+
+
+def uniform_landmarks(points, m0: int, seed: int = 0) -> LandmarkSet:
+    """``m0`` rows uniformly without replacement (landmarks.py:132-148)."""
+    pts = np.asarray(points, dtype=np.float64) if not isinstance(points, torch.Tensor) else points
+    m = int(pts.shape[0])
+    if m0 < 1 or m0 > m:
+        raise ValueError(f"m0 must be in [1, {m}], got {m0}")
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(m, size=m0, replace=False)
+    host = pts.cpu().numpy() if isinstance(pts, torch.Tensor) else pts
+    centroids = np.asarray(host, dtype=np.float64)[idx].copy()
+    asg, e = exact_assignment(_points_planar(points), centroids)
+    return LandmarkSet(centroids=centroids, assignment=asg.cpu().numpy(), quant_error=e, errors=(e,))

@@ -1,0 +1,129 @@
+"""Nystrom algebra (mirror of reference ``nystrom.py:29-114``).
+
+On the B200 path only the m0 x m0 landmark kernel A, its eigensystem, the drop
+rule and the mixing matrix M = W_r diag(1/alpha_r) W_r^T are formed (host,
+FP64).  The m0 x m cross kernel B and the extrapolated eigenvectors
+V = B^T W / alpha are never materialised: the K2/K3 kernels recompute
+b(x) = kappa(C, p(x)) per pixel and apply M there.  ``build_B``/``fit`` are
+kept as host-side API mirrors for diagnostics at small m (the reference's
+``fit`` is likewise a test/diagnostic boundary).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .image import RangeList
+from .landmarks import LandmarkSet
+from .symeig import SymMatrix, jacobi_eig
+
+DEFAULT_EPS_DROP = 1e-8
+KERNEL_ERROR_MAX_POINTS = 5000
+
+
+class DegenerateKernelError(RuntimeError):
+    """All eigenpairs of the landmark kernel were dropped (nystrom.py:29-30)."""
+
+
+@dataclass(frozen=True)
+class RangeKernel:
+    """Gaussian similarity exp(-|s-t|^2 / (2 theta^2)) (nystrom.py:33-54)."""
+
+    theta: float
+
+    def __post_init__(self) -> None:
+        if not self.theta > 0:
+            raise ValueError("theta must be positive")
+
+    def gram(self, left: np.ndarray, right: np.ndarray) -> np.ndarray:
+        left = np.asarray(left, dtype=np.float64)
+        right = np.asarray(right, dtype=np.float64)
+        inv = 1.0 / (2.0 * self.theta * self.theta)
+        out = np.empty((left.shape[0], right.shape[0]))
+        step = 32768
+        for s in range(0, right.shape[0], step):
+            d2 = ((left[:, None, :] - right[None, s:s + step, :]) ** 2).sum(axis=2)
+            np.exp(-d2 * inv, out=out[:, s:s + step])
+        return out
+
+
+@dataclass(frozen=True)
+class NystromModel:
+    landmarks: LandmarkSet
+    alphas: np.ndarray
+    extrapolated: np.ndarray
+    retained_rank: int
+
+
+def build_A(landmarks: np.ndarray, kernel: RangeKernel) -> SymMatrix:
+    """Landmark kernel, unit diagonal (nystrom.py:67-69)."""
+    return SymMatrix(kernel.gram(landmarks, landmarks))
+
+
+def build_B(landmarks: np.ndarray, range_list: RangeList, kernel: RangeKernel) -> np.ndarray:
+    """Cross kernel landmarks x guides (nystrom.py:72-79); diagnostic only."""
+    landmarks = np.asarray(landmarks, dtype=np.float64)
+    if landmarks.shape[1] != range_list.dim:
+        raise ValueError(f"landmark dim {landmarks.shape[1]} != range-list dim {range_list.dim}")
+    return kernel.gram(landmarks, range_list.vectors)
+
+
+def _retain(values: np.ndarray, vectors: np.ndarray, eps_drop: float):
+    """Keep alpha_k > eps_drop * alpha_1 (nystrom.py:103-109)."""
+    if values[0] <= 0.0:
+        raise DegenerateKernelError("landmark kernel has no positive eigenvalue")
+    keep = values > eps_drop * values[0]
+    if not keep.any():
+        raise DegenerateKernelError("every eigenpair fell below the drop threshold")
+    return values[keep].copy(), vectors[:, keep].copy()
+
+
+def extrapolate(B: np.ndarray, alphas: np.ndarray, vectors: np.ndarray) -> np.ndarray:
+    """v_k = B^T w_k / alpha_k (nystrom.py:112-114); diagnostic only."""
+    return (B.T @ vectors) / alphas[None, :]
+
+
+def fit(range_list: RangeList, landmarks: LandmarkSet, kernel: RangeKernel,
+        eps_drop: float = DEFAULT_EPS_DROP) -> NystromModel:
+    if not 0.0 <= eps_drop < 1.0:
+        raise ValueError("eps_drop must lie in [0, 1)")
+    eig = jacobi_eig(build_A(landmarks.centroids, kernel))
+    alphas, vectors = _retain(eig.values, eig.vectors, eps_drop)
+    B = build_B(landmarks.centroids, range_list, kernel)
+    return NystromModel(landmarks=landmarks, alphas=alphas, extrapolated=extrapolate(B, alphas, vectors),
+                        retained_rank=alphas.shape[0])
+
+
+def kernel_error(model: NystromModel, range_list: RangeList, kernel: RangeKernel,
+                 max_points: int = KERNEL_ERROR_MAX_POINTS) -> float:
+    """|K - K_hat|_F at test scale (nystrom.py:117-138)."""
+    m = range_list.m
+    if m > max_points:
+        raise ValueError(f"kernel_error materializes an m x m matrix; m={m} exceeds the "
+                         f"{max_points}-point diagnostic guard")
+    V = model.extrapolated
+    K = kernel.gram(range_list.vectors, range_list.vectors) - (V * model.alphas[None, :]) @ V.T
+    return float(np.sqrt((K * K).sum()))
+
+
+@dataclass(frozen=True)
+class MixingPlan:
+    """Host FP64 products the kernels need (filters.py:214-242)."""
+
+    alphas: np.ndarray   # retained eigenvalues, descending
+    M: np.ndarray        # (m0, m0) = W_r diag(1/alpha_r) W_r^T
+    u0: np.ndarray       # leading eigenvector w_1
+    alpha0: float
+    eps_den: float       # 1e-12 (2S+1)^2 max|alpha|
+
+
+def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int) -> MixingPlan:
+    eig = jacobi_eig(build_A(centroids, RangeKernel(theta)))
+    alphas, Wr = _retain(eig.values, eig.vectors, eps_drop)
+    M = (Wr / alphas[None, :]) @ Wr.T
+    M = (M + M.T) / 2.0
+    eps_den = 1e-12 * (2 * S + 1) ** 2 * float(np.abs(alphas).max())
+    return MixingPlan(alphas=alphas, M=np.ascontiguousarray(M), u0=np.ascontiguousarray(Wr[:, 0]),
+                      alpha0=float(alphas[0]), eps_den=eps_den)

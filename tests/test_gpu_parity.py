@@ -1,0 +1,180 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference's golden
+outputs and the pinned CPU oracle.
+
+Tolerances (BASELINE.json north_star): filter output max-abs <= 1e-4 on
+[0, 1] data given the reference's landmarks; k-means objective within 1e-3
+relative; guarded-pixel counts and retained ranks exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import FILTER_CASES, group, load_golden
+from oracle import nys_oracle as O
+from paper_1901_06112_b200 import (
+    FilterParams,
+    Image,
+    PatchGuide,
+    SpatialKernel,
+    fast_filter,
+    filter_with_landmarks,
+    kmeans_landmarks,
+)
+from paper_1901_06112_b200.filters import _prepare_inputs, run_filter
+from paper_1901_06112_b200.synthetic import CONFIGS, color_scene, spectral_scene
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _params(g, m0=None):
+    if str(g["spatial_kind"]) == "box":
+        sk = SpatialKernel.box(int(g["radius"]))
+    else:
+        sk = SpatialKernel.gaussian(float(g["sigma"]), int(g["radius"]))
+    return FilterParams(spatial=sk, theta=float(g["theta"]), m0=int(g["m0"] if m0 is None else m0), seed=0,
+                        kmeans_max_iter=int(g["max_iter"]), eps_drop=float(g["eps_drop"]))
+
+
+def _images(g):
+    f = Image(data=g["f"].astype(np.float64), range_max=1.0)
+    p = f if bool(g["guide_is_f"]) else Image(data=g["guide"].astype(np.float64), range_max=1.0)
+    return f, p
+
+
+@pytest.mark.parametrize("case", FILTER_CASES)
+def test_filter_with_reference_landmarks(case):
+    g = load_golden(case)
+    f, p = _images(g)
+    rep = filter_with_landmarks(f, p, g["centroids"], _params(g))
+    err = np.abs(rep.output.data - g["output"]).max()
+    assert err <= TOL, err
+    assert rep.retained_rank == int(g["retained_rank"])
+    assert rep.guarded_pixels == int(g["guarded_pixels"])
+
+
+@pytest.mark.parametrize("case", FILTER_CASES)
+def test_fast_filter_end_to_end(case):
+    g = load_golden(case)
+    f, p = _images(g)
+    rep = fast_filter(f, p, _params(g))
+    assert abs(rep.quant_error - float(g["quant_error"])) <= 1e-3 * float(g["quant_error"])
+    np.testing.assert_allclose(rep.centroids, g["centroids"], rtol=0, atol=1e-5)
+    err = np.abs(rep.output.data - g["output"]).max()
+    assert err <= TOL, err
+    assert rep.guarded_pixels == int(g["guarded_pixels"])
+    assert set(rep.timings) >= {"clustering", "eigendecomposition", "extrapolation", "convolutions",
+                                "normalization", "total"}
+
+
+def test_nlm_patch_guide_on_the_fly_equals_materialised():
+    g = load_golden("nlm_patch_box10")
+    f = Image(data=g["f"].astype(np.float64), range_max=1.0)
+    pg = PatchGuide(f, 1)
+    params = _params(g)
+    a = filter_with_landmarks(f, pg, g["centroids"], params)   # guide_kind 1: gathered in-kernel
+    b = filter_with_landmarks(f, Image(data=g["guide"].astype(np.float64), range_max=1.0), g["centroids"], params)
+    assert np.abs(a.output.data - b.output.data).max() <= 1e-6
+    assert np.abs(a.output.data - g["output"]).max() <= TOL
+    assert a.guarded_pixels == b.guarded_pixels == int(g["guarded_pixels"])
+
+
+def test_kmeans_known_answers():
+    for name, c in group(load_golden("kmeans_kat"), "").items():
+        m0, seed, it = (int(v) for v in c["meta"])
+        lm = kmeans_landmarks(c["points"], m0, seed=seed, max_iter=it)
+        # device points are float32: FP64 KAT inputs such as 0.1 round to 0.1f (1.5e-9 away)
+        np.testing.assert_allclose(lm.centroids, c["centroids"], rtol=1e-7, atol=1e-9, err_msg=name)
+        np.testing.assert_array_equal(lm.assignment, c["assignment"], err_msg=name)
+        assert lm.quant_error == pytest.approx(float(c["quant_error"]), rel=1e-9, abs=1e-12), name
+        assert len(lm.errors) == len(c["errors"]), name
+    lm = kmeans_landmarks(np.array([[0.0], [10.0]]), 2, seed=0)
+    assert sorted(lm.centroids.ravel().tolist()) == [0.0, 10.0] and lm.quant_error == 0.0
+
+
+def test_kmeans_errors_and_validation():
+    with pytest.raises(ValueError):
+        kmeans_landmarks(np.zeros((4, 2)), 5)
+    with pytest.raises(ValueError):
+        kmeans_landmarks(np.zeros((4, 2)), 0)
+    # all points identical: sum(D^2) == 0 at the first draw -> integers() path
+    lm = kmeans_landmarks(np.ones((50, 3)), 4, seed=1, max_iter=5)
+    O_C, O_lab, O_qe, _ = O.kmeans(np.ones((50, 3)), 4, 1, 5)
+    np.testing.assert_array_equal(lm.centroids, O_C)
+    assert lm.quant_error == O_qe == 0.0
+
+
+def test_kmeans_monotone_and_reproducible():
+    rng = np.random.default_rng(7)
+    centers = rng.uniform(0, 50, (5, 3))
+    pts = np.concatenate([c + 2.0 * rng.standard_normal((60, 3)) for c in centers]).astype(np.float32)
+    a = kmeans_landmarks(pts.astype(np.float64), 5, seed=2)
+    b = kmeans_landmarks(pts.astype(np.float64), 5, seed=2)
+    assert np.array_equal(a.centroids, b.centroids) and a.quant_error == b.quant_error
+    e = np.array(a.errors)
+    assert np.all(np.diff(e) <= 1e-6 * e[0])
+    C, lab, qe, _ = O.kmeans(pts.astype(np.float64), 5, 2, 50)
+    assert a.quant_error == pytest.approx(qe, rel=1e-6)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_config_crops_vs_oracle(cfg):
+    """Each BASELINE config's kernel on a seeded crop: stage 1 (filter given
+    the oracle's landmarks) and stage 2 (GPU k-means objective)."""
+    wl = CONFIGS[cfg]
+    H, W = {1: (96, 112), 2: (72, 128), 3: (64, 72), 4: (40, 48), 5: (48, 56)}[cfg]
+    f32 = wl.image(seed=cfg, H=H, W=W)
+    f64 = f32.astype(np.float64)
+    p64 = O.patch_stack(f64, 1) if wl.mode == "nlm" else f64
+    m0 = min(wl.m0, 24)
+    C, _lab, qe, _ = O.kmeans(O.range_vectors(p64), m0, 0, wl.max_iter)
+    ref = O.fast_filter_with_landmarks(f64, p64, C, wl.theta, wl.spatial, wl.sigma, wl.radius)
+    sk = SpatialKernel.box(wl.radius) if wl.spatial == "box" else SpatialKernel.gaussian(wl.sigma, wl.radius)
+    params = FilterParams(spatial=sk, theta=wl.theta, m0=m0, kmeans_max_iter=wl.max_iter)
+    f = Image(data=f64, range_max=1.0)
+    p = PatchGuide(f, 1) if wl.mode == "nlm" else f
+    rep = filter_with_landmarks(f, p, C, params)
+    assert np.abs(rep.output.data - ref["output"]).max() <= TOL
+    assert rep.guarded_pixels == ref["guarded_pixels"]
+    full = fast_filter(f, p, params)
+    assert abs(full.quant_error - qe) <= 1e-3 * qe
+    assert np.abs(full.output.data - ref["output"]).max() <= TOL
+
+
+def test_banded_equals_single_band_bitwise():
+    f32 = spectral_scene(96, 80, 8, 6, 0.03, seed=3)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    params = FilterParams(spatial=SpatialKernel.gaussian(3.0, 9), theta=0.25, m0=12)
+    inp = _prepare_inputs(f, f)
+    C = kmeans_landmarks(f32.reshape(8, -1).T.astype(np.float64), 12, max_iter=10).centroids
+    one, _, s1 = run_filter(inp, C, params)
+    row_bytes = (12 + 1) * (8 + 1) * 80 * 4
+    many, _, s2 = run_filter(inp, C, params, plane_budget=row_bytes * 30)  # 30-row bands incl. halo
+    torch.cuda.synchronize()
+    assert torch.equal(one, many)
+    assert torch.equal(s1, s2)
+
+
+def test_device_tensor_roundtrip_and_edge_sizes():
+    # 1-row, 1-column and tiny images; device-resident input returns a device tensor
+    for H, W in ((1, 37), (29, 1), (3, 3), (17, 300)):
+        f32 = color_scene(H, W, 3, 0.05, seed=H * 31 + W)
+        f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+        m0 = min(4, H * W)
+        params = FilterParams(spatial=SpatialKernel.gaussian(1.5, 4), theta=0.2, m0=m0, kmeans_max_iter=5)
+        rep = fast_filter(f, f, params)
+        assert isinstance(rep.output.data, torch.Tensor) and rep.output.data.is_cuda
+        C, _, qe, _ = O.kmeans(O.range_vectors(f32.astype(np.float64)), m0, 0, 5)
+        ref = O.fast_filter_with_landmarks(f32.astype(np.float64), f32.astype(np.float64), C, 0.2,
+                                           "gaussian_fir", 1.5, 4)
+        out = rep.output.data.double().cpu().numpy()
+        assert np.abs(out - ref["output"]).max() <= TOL, (H, W)
+
+
+def test_constant_image_is_fixed_point():
+    f = Image(data=np.full((3, 20, 24), 0.375), range_max=1.0)
+    rep = fast_filter(f, f, FilterParams(spatial=SpatialKernel.box(2), theta=0.1, m0=1, kmeans_max_iter=3))
+    assert np.abs(rep.output.data - 0.375).max() <= 1e-6
+    assert rep.retained_rank == 1

@@ -1,0 +1,160 @@
+"""CPU-side checks: the C-ABI library loads and exports every declared entry
+point, the host FP64 pieces (Jacobi, mixing plan), the band planner, and the
+drop-in API's validation behaviour.  No device compute."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, group, load_golden
+from oracle import nys_oracle as O
+from paper_1901_06112_b200 import (
+    FilterParams,
+    Image,
+    SpatialKernel,
+    SymMatrix,
+    _native,
+    build_guide,
+    jacobi_eig,
+)
+from paper_1901_06112_b200.bands import halo_rows, plan_bands, shard_rows
+from paper_1901_06112_b200.nystrom import DegenerateKernelError, _retain, mixing_plan
+
+
+def _declared_symbols():
+    text = (ROOT / "include" / "nysfilter_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|uint64_t)\s+(nys_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(_native.exported_symbols()) == declared
+    assert lib.nys_abi_version() == 100
+
+
+def test_native_jacobi_matches_reference_bitwise():
+    for name, c in group(load_golden("jacobi"), "").items():
+        es = jacobi_eig(SymMatrix(c["a"]))
+        np.testing.assert_array_equal(es.values, c["values"], err_msg=name)
+        np.testing.assert_allclose(es.vectors, c["vectors"], rtol=0, atol=1e-15, err_msg=name)
+
+
+def test_jacobi_known_answers():
+    es = jacobi_eig(SymMatrix(np.eye(3)))
+    np.testing.assert_array_equal(es.values, np.ones(3))
+    es = jacobi_eig(SymMatrix(np.array([[2.0, 1.0], [1.0, 2.0]])))
+    np.testing.assert_allclose(es.values, [3.0, 1.0], atol=1e-14)
+    with pytest.raises(ValueError):
+        SymMatrix(np.array([[1.0, np.nan], [0.0, 1.0]]))
+
+
+def test_mixing_plan_matches_oracle_algebra():
+    g = load_golden("blf_rgb_fir9")
+    C = g["centroids"]
+    plan = mixing_plan(C, float(g["theta"]), 1e-8, int(g["radius"]))
+    vals, vecs = O.jacobi_eig(O.gram(C, C, float(g["theta"])))
+    al, Wk = O.retain(vals, vecs, 1e-8)
+    np.testing.assert_allclose(plan.M, (Wk / al) @ Wk.T, rtol=1e-12, atol=1e-9)
+    assert plan.alpha0 == al[0]
+    assert plan.eps_den == pytest.approx(1e-12 * (2 * 9 + 1) ** 2 * np.abs(al).max())
+
+
+def test_drop_rule_and_degenerate():
+    v, w = _retain(np.array([2.0, 1e-9, 1e-7]), np.eye(3), 1e-8)
+    assert v.tolist() == [2.0, 1e-7]
+    with pytest.raises(DegenerateKernelError):
+        _retain(np.array([0.0, -1.0]), np.eye(2), 1e-8)
+
+
+def test_filter_params_validation_matches_reference():
+    sk = SpatialKernel.gaussian(2.0)
+    assert sk.radius == 6
+    with pytest.raises(ValueError):
+        FilterParams(spatial=sk, theta=0.0)
+    with pytest.raises(ValueError):
+        FilterParams(spatial=sk, theta=1.0, m0=0)
+    with pytest.raises(ValueError):
+        FilterParams(spatial=sk, theta=1.0, mode="other")
+    with pytest.raises(ValueError):
+        FilterParams(spatial=sk, theta=1.0, eps_drop=1.0)
+    with pytest.raises(ValueError):
+        SpatialKernel.box(-1)
+    with pytest.raises(ValueError):
+        SpatialKernel(kind="gaussian_fir", sigma=1.0, radius=0)
+    assert SpatialKernel.recursive(2.5).effective_radius() == 8
+
+
+def test_image_contract():
+    img = Image(data=np.arange(24.0).reshape(2, 3, 4))
+    assert (img.channels, img.height, img.width) == (2, 3, 4)
+    assert img.samples[1 * 12 + 2 * 4 + 3] == img.data[1, 2, 3]
+    with pytest.raises(ValueError):
+        Image(data=np.array([[np.inf]]))
+    with pytest.raises(ValueError):
+        Image(data=np.zeros((0, 3)))
+    with pytest.raises(ValueError):
+        build_guide(img, "joint")
+    with pytest.raises(ValueError):
+        build_guide(img, "joint", Image(data=np.zeros((1, 2, 2))))
+    assert build_guide(img, "bilateral") is img
+
+
+def test_plan_bands_cover_rows_with_halo():
+    H, R = 1000, 18
+    for budget_rows in (60, 100, 333, 2000):
+        bands = plan_bands(H, R, row_bytes=7, budget_bytes=7 * budget_rows)
+        assert bands[0].out0 == 0 and sum(b.out_rows for b in bands) == H
+        for a, b in zip(bands, bands[1:]):
+            assert a.out0 + a.out_rows == b.out0
+        for b in bands:
+            assert b.hp0 == max(0, b.out0 - R)
+            assert b.hp0 + b.hp_rows == min(H, b.out0 + b.out_rows + R)
+            assert b.hp_rows <= budget_rows
+    with pytest.raises(MemoryError):
+        plan_bands(H, R, row_bytes=7, budget_bytes=7 * (2 * R))
+
+
+def test_shard_rows_partition():
+    for H in (1, 7, 1080, 8192):
+        for G in (1, 2, 3, 8):
+            if G > H:
+                continue
+            spans = [shard_rows(H, G, g) for g in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == H
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0 and a1 > a0
+    assert halo_rows(0, 10, 100, 18) == (0, 28)
+    assert halo_rows(50, 60, 100, 18) == (32, 78)
+    assert halo_rows(90, 100, 100, 18) == (72, 100)
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1901_06112_b200 import fast_filter
+
+    f = Image(data=np.random.default_rng(0).random((3, 8, 8)), range_max=1.0)
+    with pytest.raises(RuntimeError):
+        fast_filter(f, f, FilterParams(spatial=SpatialKernel.gaussian(1.0), theta=0.2, m0=4))
+
+
+def test_out_of_scope_names_raise():
+    import paper_1901_06112_b200 as P
+
+    for name in ("brute_force_filter", "gaussian_recursive", "psnr", "load_image"):
+        with pytest.raises(NotImplementedError):
+            getattr(P, name)()
+
+
+def test_header_cites_reference():
+    text = (ROOT / "include" / "nysfilter_b200.h").read_text()
+    for cite in ("landmarks.py:76-129", "filters.py:214-257", "symeig.py:58-125"):
+        assert cite in text

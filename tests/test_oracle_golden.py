@@ -1,0 +1,123 @@
+"""Pin the CPU oracle (oracle/nys_oracle.py) to the reference's own outputs.
+
+tests/golden/*.npz were produced by running the reference package itself
+(tools/make_golden.py).  The oracle is only trusted as a checker for the
+CUDA path because these pass.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import FILTER_CASES, group, load_golden
+from oracle import nys_oracle as O
+
+
+@pytest.mark.parametrize("case", FILTER_CASES)
+def test_oracle_filter_matches_reference(case):
+    g = load_golden(case)
+    res = O.fast_filter_with_landmarks(g["f"], g["guide"], g["centroids"], float(g["theta"]),
+                                       str(g["spatial_kind"]).replace("gaussian", "gaussian_fir")
+                                       if str(g["spatial_kind"]) == "gaussian" else "box",
+                                       float(g["sigma"]), int(g["radius"]), float(g["eps_drop"]))
+    assert res["retained_rank"] == int(g["retained_rank"])
+    assert res["guarded_pixels"] == int(g["guarded_pixels"])
+    np.testing.assert_allclose(res["output"], g["output"], rtol=0, atol=1e-9)
+    assert res["min_denominator"] == pytest.approx(float(g["min_denominator"]), rel=1e-6, abs=1e-300)
+
+
+@pytest.mark.parametrize("case", FILTER_CASES)
+def test_oracle_kmeans_matches_reference(case):
+    g = load_golden(case)
+    C, lab, qe, errors = O.kmeans(O.range_vectors(g["guide"]), int(g["m0"]), 0, int(g["max_iter"]))
+    np.testing.assert_array_equal(C, g["centroids"])
+    np.testing.assert_array_equal(lab, g["assignment"])
+    assert qe == float(g["quant_error"])
+    np.testing.assert_array_equal(np.array(errors), g["errors"])
+
+
+def test_oracle_kmeans_known_answers():
+    cases = group(load_golden("kmeans_kat"), "")
+    for name, c in cases.items():
+        m0, seed, it = (int(v) for v in c["meta"])
+        C, lab, qe, errors = O.kmeans(c["points"], m0, seed, it)
+        np.testing.assert_array_equal(C, c["centroids"], err_msg=name)
+        np.testing.assert_array_equal(lab, c["assignment"], err_msg=name)
+        assert qe == float(c["quant_error"]), name
+    # analytic answers from pkg/tests/test_landmarks.py:12-29
+    C, _, qe, _ = O.kmeans(np.array([[0.0], [2.0], [10.0], [12.0]]), 2, 0)
+    assert sorted(C.ravel().tolist()) == [1.0, 11.0] and qe == pytest.approx(4.0)
+    C, _, qe, _ = O.kmeans(np.array([[0.0], [2.0], [10.0], [12.0]]), 1, 3)
+    assert C.ravel().tolist() == [6.0] and qe == pytest.approx(104.0)
+
+
+def test_oracle_jacobi_matches_reference():
+    for name, c in group(load_golden("jacobi"), "").items():
+        vals, vecs = O.jacobi_eig(c["a"])
+        np.testing.assert_allclose(vals, c["values"], rtol=0, atol=1e-12, err_msg=name)
+        np.testing.assert_allclose(vecs, c["vectors"], rtol=0, atol=1e-10, err_msg=name)
+
+
+def test_oracle_spatial_known_answers():
+    g = load_golden("spatial")
+    np.testing.assert_allclose(O.spatial_conv(g["plane"][None], "gaussian_fir", 1.3, 3)[0], g["fir_1.3_3"],
+                               rtol=0, atol=1e-13)
+    np.testing.assert_allclose(O.spatial_conv(g["plane"][None], "box", 0, 2)[0], g["box_2"], rtol=0, atol=1e-13)
+    np.testing.assert_array_equal(O.spatial_conv(g["plane"][None], "box", 0, 0)[0], g["box_0"])
+    # pkg/tests/test_spatial.py:40-52 box constant / impulse
+    for S in (0, 1, 3):
+        out = O.spatial_conv(np.full((1, 6, 5), 2.5), "box", 0, S)[0]
+        assert np.array_equal(out, np.full((6, 5), 2.5 * (2 * S + 1) ** 2))
+    imp = np.zeros((1, 7, 7))
+    imp[0, 3, 3] = 1
+    exp = np.zeros((7, 7))
+    exp[2:5, 2:5] = 1
+    assert np.array_equal(O.spatial_conv(imp, "box", 0, 1)[0], exp)
+    # FIR impulse ratio e^-1/2 (test_spatial.py:79-84)
+    imp = np.zeros((1, 9, 9))
+    imp[0, 4, 4] = 1
+    out = O.spatial_conv(imp, "gaussian_fir", 1.0, 3)[0]
+    assert out[4, 4] == pytest.approx(1.0) and out[4, 5] / out[4, 4] == pytest.approx(np.exp(-0.5))
+
+
+def test_oracle_full_rank_exactness():
+    g = load_golden("full_rank")
+    f = g["f"].astype(np.float64)
+    res = O.fast_filter(f, f, 0.3, "gaussian_fir", 1.0, 3, m0=144, seed=0, max_iter=5, eps_drop=0.0)
+    np.testing.assert_allclose(res["output"], g["fast"], atol=1e-9)
+    brute = O.brute_force_filter(f, f, 0.3, "gaussian_fir", 1.0, 3)
+    np.testing.assert_allclose(brute, g["brute"], atol=1e-12)
+    assert np.abs(res["output"] - brute).max() < 1e-8
+
+
+def test_choice_is_cumsum_searchsorted():
+    """The k-means++ draw the GPU reproduces (landmarks.py:68)."""
+    for seed in range(3):
+        r1 = np.random.default_rng(seed)
+        r2 = np.random.default_rng(seed)
+        d2 = np.random.default_rng(100 + seed).random(5000) ** 3
+        d2[::5] = 0.0
+        for _ in range(10):
+            a = r1.choice(d2.size, p=d2 / d2.sum())
+            p = d2 / d2.sum()
+            cdf = p.cumsum()
+            cdf /= cdf[-1]
+            assert a == np.searchsorted(cdf, r2.random(), side="right")
+
+
+def test_vector_uniforms_equal_scalar_stream():
+    r1 = np.random.default_rng(7)
+    r2 = np.random.default_rng(7)
+    assert r1.integers(1000) == r2.integers(1000)
+    v = r1.random(50)
+    assert np.array_equal(v, np.array([r2.random() for _ in range(50)]))
+
+
+def test_patch_stack_order():
+    f = np.arange(2 * 4 * 5, dtype=np.float64).reshape(2, 4, 5)
+    P = O.patch_stack(f, 1)
+    assert P.shape == (18, 4, 5)
+    # channel-major, then dy, then dx, edge replicate (filters.py:176-181)
+    assert P[4, 2, 3] == f[0, 2, 3]
+    assert P[9 + 0, 0, 0] == f[1, 0, 0]
+    assert P[9 + 8, 3, 4] == f[1, 3, 4]
+    assert P[2, 1, 1] == f[0, 0, 2]

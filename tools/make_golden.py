@@ -1,0 +1,151 @@
+"""Generate tests/golden/*.npz by running the REFERENCE package itself.
+
+Run in the build container only (the reference lives at /root/reference and
+does not travel to the GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba python tools/make_golden.py
+
+Each fixture stores the inputs (float32, exactly representable in the
+reference's float64), the reference's outputs, and the parameters.  The
+oracle (oracle/nys_oracle.py) is pinned against these in
+tests/test_oracle_golden.py and the CUDA path in tests/test_gpu_*.py.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+REF = Path("/root/reference/pkg/src")
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(ROOT))
+
+import nysfilter as ref  # noqa: E402  (the reference, imported read-only)
+from nysfilter.landmarks import kmeans_landmarks as ref_kmeans  # noqa: E402
+
+from paper_1901_06112_b200.synthetic import color_scene, spectral_scene  # noqa: E402
+from oracle.nys_oracle import patch_stack  # noqa: E402
+
+OUT = ROOT / "tests" / "golden"
+
+
+def _filter_case(name, f32, guide32, spatial, theta, m0, max_iter, mode="bilateral", eps_drop=1e-8):
+    f = ref.Image(data=f32.astype(np.float64), range_max=1.0)
+    p = f if guide32 is None else ref.Image(data=guide32.astype(np.float64), range_max=1.0)
+    if spatial[0] == "box":
+        sk = ref.SpatialKernel.box(spatial[1])
+    else:
+        sk = ref.SpatialKernel.gaussian(spatial[1], spatial[2])
+    params = ref.FilterParams(spatial=sk, theta=theta, m0=m0, seed=0, mode=mode, kmeans_max_iter=max_iter,
+                              eps_drop=eps_drop)
+    rep = ref.fast_filter(f, p, params)
+    rl = ref.extract_range_list(p)
+    lm = ref_kmeans(rl.vectors, m0, seed=0, max_iter=max_iter)
+    np.savez_compressed(
+        OUT / f"{name}.npz", f=f32, guide=(f32 if guide32 is None else guide32),
+        guide_is_f=guide32 is None, spatial_kind=spatial[0],
+        sigma=(0.0 if spatial[0] == "box" else spatial[1]), radius=(spatial[1] if spatial[0] == "box" else spatial[2]),
+        theta=theta, m0=m0, max_iter=max_iter, eps_drop=eps_drop,
+        output=rep.output.data, retained_rank=rep.retained_rank, quant_error=rep.quant_error,
+        min_denominator=rep.min_denominator, guarded_pixels=rep.guarded_pixels,
+        centroids=lm.centroids, assignment=lm.assignment, errors=np.array(lm.errors))
+    print(name, "rank", rep.retained_rank, "guarded", rep.guarded_pixels, "qe", rep.quant_error)
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    # BLF colour, FIR radius 9 (the cfg-1 kernel: sigma 3, R 9, theta 0.15, m0 32, 10 it)
+    f = color_scene(64, 72, 8, 0.04, seed=11)
+    _filter_case("blf_rgb_fir9", f, None, ("gaussian", 3.0, 9), 0.15, 32, 10)
+    # BLF colour, small generic radius (runtime-radius kernels)
+    f = color_scene(40, 48, 6, 0.05, seed=12)
+    _filter_case("blf_rgb_fir4", f, None, ("gaussian", 1.5, 4), 0.1, 8, 15)
+    # joint BLF with an external 2-channel guide
+    g = color_scene(40, 48, 5, 0.05, seed=13)[:2].copy()
+    _filter_case("joint_rgb_g2", f, g, ("gaussian", 2.0, 5), 0.2, 6, 10, mode="joint")
+    # NLM: raw 3x3x3 patch guide, box(10) -> cfg-3 semantics at small size
+    f = color_scene(48, 40, 6, 0.08, seed=14, lo=0.1, hi=0.9, shading=0.1)
+    P = patch_stack(f.astype(np.float64), 1).astype(np.float32)
+    _filter_case("nlm_patch_box10", f, P, ("box", 10), 0.3 * np.sqrt(27.0) * 0.08, 16, 15, mode="joint")
+    # NLM with a small box (edge-heavy)
+    _filter_case("nlm_patch_box3", f, P, ("box", 3), 0.3 * np.sqrt(27.0) * 0.08, 8, 15, mode="joint")
+    # hyperspectral: 31 bands, FIR radius 12 (cfg-4 kernel), m0 12
+    h = spectral_scene(32, 40, 31, 6, 0.03, seed=15)
+    _filter_case("hyper31_fir12", h, None, ("gaussian", 4.0, 12), 0.25, 12, 15)
+    # hyperspectral: 16 bands, FIR radius 18 (cfg-5 kernel), m0 10
+    h = spectral_scene(40, 44, 16, 6, 0.03, seed=16)
+    _filter_case("hyper16_fir18", h, None, ("gaussian", 6.0, 18), 0.2, 10, 15)
+    # FIR radius 15 (cfg-2 kernel)
+    f = color_scene(48, 56, 10, 0.05, seed=17)
+    _filter_case("blf_rgb_fir15", f, None, ("gaussian", 5.0, 15), 0.1, 16, 15)
+
+    # k-means known answers (reference test inputs + seeded blobs)
+    km = {}
+    cases = {
+        "two_points": (np.array([[0.0], [10.0]]), 2, 0, 50),
+        "two_cluster": (np.array([[0.0], [2.0], [10.0], [12.0]]), 2, 0, 50),
+        "single": (np.array([[0.0], [2.0], [10.0], [12.0]]), 1, 3, 50),
+        "ties": (np.array([[0.0], [1.0], [2.0]]), 2, 9, 50),
+        "empty_repair": (np.array([[0.0], [0.0], [0.0], [100.0], [100.0], [0.1]]), 3, 0, 50),
+    }
+    rng = np.random.default_rng(6)
+    cases["rgb200"] = (np.round(rng.uniform(0, 255, (200, 3))).astype(np.float64), 8, 11, 50)
+    rng = np.random.default_rng(8)
+    centers = rng.uniform(0, 50, (3, 2))
+    cases["blobs"] = (np.concatenate([c + rng.standard_normal((50, 2)).astype(np.float32) for c in centers]
+                                     ).astype(np.float64), 3, 4, 200)
+    for k, (pts, m0, seed, it) in cases.items():
+        lm = ref_kmeans(pts, m0, seed=seed, max_iter=it)
+        km[f"{k}__points"] = pts
+        km[f"{k}__meta"] = np.array([m0, seed, it])
+        km[f"{k}__centroids"] = lm.centroids
+        km[f"{k}__assignment"] = lm.assignment
+        km[f"{k}__quant_error"] = np.array(lm.quant_error)
+        km[f"{k}__errors"] = np.array(lm.errors)
+    np.savez_compressed(OUT / "kmeans_kat.npz", **km)
+
+    # Jacobi eigensystems (symeig.py) on landmark kernels and random symmetric matrices
+    ev = {}
+    rng = np.random.default_rng(0)
+    for i, k in enumerate((1, 2, 5, 16, 33)):
+        A = rng.standard_normal((k, k))
+        A = A + A.T
+        es = ref.jacobi_eig(ref.SymMatrix(A))
+        ev[f"m{i}__a"] = A
+        ev[f"m{i}__values"] = es.values
+        ev[f"m{i}__vectors"] = es.vectors
+    lms = rng.uniform(0, 1, (24, 3))
+    A = ref.build_A(lms, ref.RangeKernel(theta=0.2)).entries
+    es = ref.jacobi_eig(ref.SymMatrix(A))
+    ev["kern__a"], ev["kern__values"], ev["kern__vectors"] = A, es.values, es.vectors
+    np.savez_compressed(OUT / "jacobi.npz", **ev)
+
+    # separable convolution known answers (spatial.py)
+    sp = {}
+    rng = np.random.default_rng(4)
+    plane = rng.uniform(0, 1, (11, 13))
+    sp["plane"] = plane
+    sp["fir_1.3_3"] = ref.gaussian_fir(plane, 1.3, 3)
+    sp["box_2"] = ref.box_filter(plane, 2)
+    sp["box_0"] = ref.box_filter(plane, 0)
+    np.savez_compressed(OUT / "spatial.npz", **sp)
+
+    # full-rank exactness (SPEC.md acceptance #1): fast == brute at m0 = m, eps_drop = 0
+    f = color_scene(12, 12, 4, 0.05, seed=18)
+    fi = ref.Image(data=f.astype(np.float64), range_max=1.0)
+    params = ref.FilterParams(spatial=ref.SpatialKernel.gaussian(1.0, 3), theta=0.3, m0=144, seed=0,
+                              eps_drop=0.0, kmeans_max_iter=5)
+    rep = ref.fast_filter(fi, fi, params)
+    brute = ref.brute_force_filter(fi, fi, params)
+    np.savez_compressed(OUT / "full_rank.npz", f=f, fast=rep.output.data, brute=brute.data,
+                        retained_rank=rep.retained_rank)
+    print("full rank: max|fast-brute|", np.abs(rep.output.data - brute.data).max(), "rank", rep.retained_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -161,42 +161,46 @@ typedef struct nys_filter_desc {
     double eps_den;          /* 1e-12 * (2S+1)^2 * max|alpha| (filters.py:242) */
 } nys_filter_desc;
 
-/* Size of the horizontal-pass plane buffer for `rows` image rows:
- * (m0+1)*(n+1) planes of rows*W float32. */
+/* Size of the horizontal-pass plane buffer for a band of `rows` output rows:
+ * (m0+1)*(n+1) planes of (rows + 2R) virtual rows x Wp floats, Wp = W rounded
+ * up to a multiple of 4.  Virtual row v of a band starting at out0 holds the
+ * row-filtered planes of image row clamp(out0 - R + v, 0, H-1), so the
+ * vertical pass never clamps (replicate borders, spatial.py:85-88). */
 size_t nys_filter_planes_bytes(const nys_filter_desc* d, int rows);
 
 /* Device bytes for the filter's constant block + reduction scratch. */
 size_t nys_filter_workspace_bytes(const nys_filter_desc* d);
 
-/* Upload the per-call constants (centroids, M, u0, taps) into `workspace`
- * and reset the min|eta| / guarded-pixel accumulators.  Call once per filter
- * before the band passes below. */
+/* Upload the per-call constants (centroids, M, u0) into `workspace` and reset
+ * the min|eta| / guarded-pixel accumulators.  Call once per filter before the
+ * band passes below (synchronises `stream` once: the source is pageable). */
 int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspace_bytes,
                        void* stream);
 
 /*
- * K2: range features + horizontal pass for image rows [row0, row0+rows).
+ * K2: range features + horizontal pass for the band of output rows
+ * [out0, out0+out_rows) (computes its rows + 2R virtual halo rows).
  * f [dev] (n,H,W) planar, f_plane_stride; guide [dev] (rho,H,W) (ignored for
- * guide_kind 1; may alias f).  planes [dev]: (m0+1)*(n+1) planes, plane
- * stride planes_stride (>= rows*W), row r of the band at (r-row0)*W.
+ * guide_kind 1; may alias f).  planes [dev] 16-byte aligned: (m0+1)*(n+1)
+ * planes, plane stride planes_stride (multiple of 4, >= (out_rows+2R)*Wp).
  * Plane (i*(n+1)+c) holds the row-filtered y_i*f_c (c<n) or y_i (c==n), with
  * y = M b(x) for i<m0 and y_{m0} = u0.b(x) (the rank-1 lead term).
  */
 int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
                      const float* guide, int64_t guide_plane_stride,
-                     int row0, int rows, float* planes, int64_t planes_stride,
+                     int out0, int out_rows, float* planes, int64_t planes_stride,
                      const void* workspace, void* stream);
 
 /*
- * K3: vertical pass + per-pixel reconstruction, guard and division for
- * output rows [out0, out0+out_rows).  The planes buffer must hold rows
- * [max(0,out0-R), min(H,out0+out_rows+R)) with its first row = planes_row0.
- * out [dev] (n,H,W) planar with out_plane_stride.  Accumulates min|eta| and
- * the guarded-pixel count into the workspace.
+ * K3: vertical pass + per-pixel reconstruction, guard and division for the
+ * band [out0, out0+out_rows) whose planes K2 produced.  The plane stack is
+ * read through a TMA descriptor (cp.async.bulk.tensor).  out [dev] (n,H,W)
+ * planar with out_plane_stride.  Accumulates min|eta| and the guarded-pixel
+ * count into the workspace.
  */
 int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
                      const float* guide, int64_t guide_plane_stride,
-                     const float* planes, int64_t planes_stride, int planes_row0,
+                     const float* planes, int64_t planes_stride,
                      int out0, int out_rows, float* out, int64_t out_plane_stride,
                      const void* workspace, void* stream);
 

@@ -62,7 +62,7 @@ _SIGS = {
     "nys_filter_workspace_bytes": (_S, [C.POINTER(FilterDesc)]),
     "nys_filter_prepare": (_I, [C.POINTER(FilterDesc), _P, _S, _P]),
     "nys_filter_hpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
-    "nys_filter_vpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _I, _I, _I, _P, _L, _P, _P]),
+    "nys_filter_vpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
     "nys_filter_stats": (_I, [C.POINTER(FilterDesc), _P, _P, _P]),
     "nys_patch_guide": (_I, [_P, _L, _I, _I, _I, _I, _P, _L, _P]),
     "nys_jacobi_eig": (_I, [_P, _I, _P, _P, C.POINTER(C.c_int)]),

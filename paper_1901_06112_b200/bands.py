@@ -5,7 +5,8 @@ Two uses, both driven by the R-row vertical halo of the separable kernel:
 * within one GPU, when the (m0+1)(n+1) horizontally-filtered planes of the
   whole image exceed the HBM budget (cfg 5: 67 M px x 1105 planes x 4 B =
   296 GB > 180 GB), K2/K3 run band by band; band b's K2 covers its output
-  rows plus R rows on each side (edge-replicated at the image border);
+  rows plus R virtual rows on each side (rows outside the image replicate
+  the border row, so K3 never clamps);
 * across GPUs, rank g owns the rows [g*H/G, (g+1)*H/G) and receives
   R (+ patch radius) input rows from each neighbour (``parallel.py``).
 """
@@ -19,14 +20,12 @@ from dataclasses import dataclass
 class Band:
     out0: int      # first output row
     out_rows: int  # output rows
-    hp0: int       # first row of the horizontal-pass planes for this band
-    hp_rows: int   # rows of planes (out rows + halo, clipped at the border)
+    hp0: int       # first virtual row of the horizontal-pass planes (out0 - R, may be < 0)
+    hp_rows: int   # rows of planes: out_rows + 2R virtual rows
 
 
 def band_for(out0: int, out_rows: int, H: int, R: int) -> Band:
-    hp0 = max(0, out0 - R)
-    hp1 = min(H, out0 + out_rows + R)
-    return Band(out0, out_rows, hp0, hp1 - hp0)
+    return Band(out0, out_rows, out0 - R, out_rows + 2 * R)
 
 
 def plan_bands(H: int, R: int, row_bytes: int, budget_bytes: int, max_bands: int | None = None) -> list[Band]:
@@ -35,8 +34,8 @@ def plan_bands(H: int, R: int, row_bytes: int, budget_bytes: int, max_bands: int
     if H < 1 or R < 0 or row_bytes < 1:
         raise ValueError("bad band geometry")
     max_rows = budget_bytes // row_bytes
-    if max_rows >= H:
-        return [Band(0, H, 0, H)]
+    if max_rows >= H + 2 * R:
+        return [band_for(0, H, H, R)]
     out_max = max_rows - 2 * R
     if out_max < 1:
         raise MemoryError(f"plane buffer budget {budget_bytes} B cannot hold one band "

@@ -1,0 +1,109 @@
+// Shared pieces of the K2/K3 filter kernels (layout, guide access, host helpers).
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "nys_common.cuh"
+
+namespace nys {
+
+// ---------------------------------------------------------------------------
+// constants block in the workspace (float offsets)
+// ---------------------------------------------------------------------------
+struct FilterLayout {
+  int m0, rho, rhop, m0q;  // rhop: rho padded to 4; m0q: (m0+1) padded to 8
+  size_t off_C, off_MT, off_U0, n_floats;
+  size_t stats_off_bytes, total_bytes;
+};
+
+inline FilterLayout filter_layout(const nys_filter_desc* d) {
+  FilterLayout L;
+  L.m0 = d->m0;
+  L.rho = d->rho;
+  L.rhop = (int)ceil_div(d->rho, 4) * 4;
+  L.m0q = (int)ceil_div(d->m0 + 1, 8) * 8;
+  L.off_C = 0;
+  L.off_MT = L.off_C + (size_t)d->m0 * L.rhop;
+  L.off_U0 = L.off_MT + (size_t)d->m0 * L.m0q;
+  L.n_floats = L.off_U0 + (size_t)ceil_div(d->m0, 4) * 4;
+  L.stats_off_bytes = ((L.n_floats * 4 + 255) / 256) * 256;
+  L.total_bytes = L.stats_off_bytes + 256;
+  return L;
+}
+
+inline int wpitch(int W) { return (int)ceil_div(W, 4) * 4; }
+
+struct FilterStats {
+  unsigned int min_abs_eta_bits;  // float bits, non-negative => integer order
+  unsigned int pad;
+  unsigned long long guarded;
+};
+
+// guide coordinate d of pixel (row, x): planar guide or an on-the-fly 3x3 patch
+// of f (channel, dy, dx order, edge replicate: filters.py:174-181)
+__device__ __forceinline__ float guide_at(const float* __restrict__ g, long long gps,
+                                          const float* __restrict__ f, long long fps, int gkind,
+                                          int d, int row, int x, int H, int W) {
+  if (gkind == 0) return __ldg(g + (long long)d * gps + (long long)row * W + x);
+  const int c = d / 9, k = d - c * 9, dy = k / 3 - 1, dx = k - (k / 3) * 3 - 1;
+  const int yy = clampi(row + dy, 0, H - 1), xx = clampi(x + dx, 0, W - 1);
+  return __ldg(f + (long long)c * fps + (long long)yy * W + xx);
+}
+
+// host helpers
+inline int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+inline int validate(const nys_filter_desc* d) {
+  if (!d) return NYS_EINVAL;
+  if (d->n < 1 || d->n > NYS_MAX_CHANNELS || d->rho < 1 || d->rho > NYS_MAX_RHO) return NYS_EUNSUPPORTED;
+  if (d->H < 1 || d->W < 1 || d->m0 < 1 || d->m0 > NYS_MAX_M0) return NYS_EINVAL;
+  if (d->radius < 0 || d->radius > NYS_MAX_RADIUS) return NYS_EUNSUPPORTED;
+  if (d->spatial_kind != NYS_SPATIAL_BOX && d->spatial_kind != NYS_SPATIAL_GAUSSIAN_FIR) return NYS_EUNSUPPORTED;
+  if (d->spatial_kind == NYS_SPATIAL_GAUSSIAN_FIR && (!(d->sigma > 0) || d->radius < 1)) return NYS_EINVAL;
+  if (!(d->theta > 0)) return NYS_EINVAL;
+  if (d->guide_kind != 0 && d->guide_kind != 1) return NYS_EINVAL;
+  if (d->guide_kind == 1 && d->rho != 9 * d->n) return NYS_EINVAL;
+  return NYS_OK;
+}
+
+inline void fill_taps(const nys_filter_desc* d, float* taps) {
+  const int T = 2 * d->radius + 1;
+  for (int t = 0; t < NYS_MAX_TAPS; ++t) taps[t] = 0.f;
+  for (int t = 0; t < T; ++t) {
+    if (d->spatial_kind == NYS_SPATIAL_BOX) {
+      taps[t] = 1.f;
+    } else {
+      const double u = (double)(t - d->radius);
+      taps[t] = (float)std::exp(-(u * u) / (2.0 * d->sigma * d->sigma));  // spatial.py:72-75
+    }
+  }
+}
+
+inline float k2_of(const nys_filter_desc* d) {
+  return (float)(-1.4426950408889634 / (2.0 * d->theta * d->theta));
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace nys

@@ -1,0 +1,329 @@
+// K2 / K3: the Nystrom filter proper, B200 (sm_100a) CUDA.
+//
+// Reference region replaced (reference = /root/reference/pkg/src/nysfilter):
+//   filters.py:214-257   fast_filter k-loop, accumulation, denominator guard
+//   nystrom.py:43-79     RangeKernel.gram / build_B   (never materialised here)
+//   nystrom.py:112-114   extrapolate V = B^T W / alpha (never materialised here)
+//   spatial.py:91-109, 194-209  box / FIR row pass then column pass, replicate
+//
+// Formulation ("y-form"): with b_i(x) = exp(-|p(x)-c_i|^2/2θ^2)
+// and M = Σ_k w_k w_k^T / α_k (retained eigenpairs), the reference's
+//   zeta(x) = Σ_k α_k v_k(x) [ω * (v_k f)](x)   (v_k = B^T w_k / α_k)
+// equals  Σ_i b_i(x) [ω * (y_i f)](x)  with  y = M b  evaluated at the source
+// pixel.  K2 evaluates b and y per source pixel (a register-blocked
+// [px x m0] x [m0 x (m0+1)] product, the extra column being the lead
+// projection s0 = w_1.b) and runs the horizontal pass of the (m0+1)(n+1)
+// planes y_i f_c, y_i.  K3 TMA-stages tiles of those planes, runs the vertical
+// pass, contracts with b_i(x) recomputed at the centre pixel, and applies the
+// guard and division.  Only the horizontally filtered planes touch HBM.
+//
+// Plane buffer layout: plane p = i*(n+1) + c, each plane `rows + 2R` virtual
+// rows of pitch Wp = roundup(W, 4) floats; virtual row v maps to image row
+// clamp(v, 0, H-1), so K3 never clamps (replicate borders, spatial.py:85-88).
+#include "nys_filter_common.cuh"
+
+namespace nys {
+
+// ---------------------------------------------------------------------------
+// K2: features b, y = M b (+ lead s0), horizontal pass
+// ---------------------------------------------------------------------------
+constexpr int K2_THREADS = 512;
+constexpr int K2_XR = 16;  // output columns per FIR item
+constexpr int K2_CC = 4;   // planes per FIR item
+
+struct HArgs {
+  const float* f;
+  const float* g;
+  float* hp;
+  const float* cst;
+  long long fps, gps, hps;
+  int n, rho, rhop, H, W, Wp, m0, m0q, R, box, gkind;
+  int v0, vrows, TW, pitch, tiles_x;
+  float k2;
+  float taps[NYS_MAX_TAPS];
+};
+
+template <int RT>
+__device__ __forceinline__ void hfir(const HArgs& a, const float* __restrict__ yrow,
+                                     const float* __restrict__ Fs, int pitch, int xoff, int c0,
+                                     float (&acc)[K2_CC][K2_XR]) {
+  const int n = a.n;
+  const float* fr[K2_CC];
+  int mode[K2_CC];  // 0: y*f_c, 1: y, 2: no plane
+#pragma unroll
+  for (int cc = 0; cc < K2_CC; ++cc) {
+    const int c = c0 + cc;
+    fr[cc] = Fs + (size_t)min(c, n - 1) * pitch + xoff;
+    mode[cc] = c < n ? 0 : (c == n ? 1 : 2);
+  }
+#pragma unroll
+  for (int cc = 0; cc < K2_CC; ++cc)
+#pragma unroll
+    for (int o = 0; o < K2_XR; ++o) acc[cc][o] = 0.f;
+  auto plane_val = [&](int cc, float yv, float fv) { return mode[cc] == 0 ? yv * fv : (mode[cc] == 1 ? yv : 0.f); };
+
+  if (a.box) {  // sliding (2R+1)-sum re-anchored per item (spatial.py:91-99)
+    const int R = a.R;
+    float s[K2_CC];
+#pragma unroll
+    for (int cc = 0; cc < K2_CC; ++cc) s[cc] = 0.f;
+    for (int t = 0; t <= 2 * R; ++t) {
+      const float yv = yrow[t];
+#pragma unroll
+      for (int cc = 0; cc < K2_CC; ++cc) s[cc] += plane_val(cc, yv, fr[cc][t]);
+    }
+#pragma unroll
+    for (int o = 0; o < K2_XR; ++o) {
+      if (o > 0) {
+        const float yin = yrow[o + 2 * R], yout = yrow[o - 1];
+#pragma unroll
+        for (int cc = 0; cc < K2_CC; ++cc)
+          s[cc] += plane_val(cc, yin, fr[cc][o + 2 * R]) - plane_val(cc, yout, fr[cc][o - 1]);
+      }
+#pragma unroll
+      for (int cc = 0; cc < K2_CC; ++cc) acc[cc][o] = s[cc];
+    }
+    return;
+  }
+  if constexpr (RT > 0) {
+    constexpr int T = 2 * RT + 1;
+    constexpr int NIN = K2_XR + 2 * RT;
+    constexpr int NQ = (NIN + 3) / 4;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float4 y4 = *reinterpret_cast<const float4*>(yrow + 4 * q);
+      float4 f4[K2_CC];
+#pragma unroll
+      for (int cc = 0; cc < K2_CC; ++cc) f4[cc] = *reinterpret_cast<const float4*>(fr[cc] + 4 * q);
+      const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int s = 4 * q + e;
+        if (s < NIN) {
+#pragma unroll
+          for (int cc = 0; cc < K2_CC; ++cc) {
+            const float fv[4] = {f4[cc].x, f4[cc].y, f4[cc].z, f4[cc].w};
+            const float v = plane_val(cc, yv[e], fv[e]);
+#pragma unroll
+            for (int o = 0; o < K2_XR; ++o) {
+              const int t = s - o;
+              if (t >= 0 && t < T) acc[cc][o] = fmaf(a.taps[t], v, acc[cc][o]);
+            }
+          }
+        }
+      }
+    }
+  } else {
+    const int T = 2 * a.R + 1;
+    for (int t = 0; t < T; ++t) {
+      const float w = a.taps[t];
+#pragma unroll
+      for (int o = 0; o < K2_XR; ++o) {
+        const float yv = yrow[o + t];
+#pragma unroll
+        for (int cc = 0; cc < K2_CC; ++cc) acc[cc][o] = fmaf(w, plane_val(cc, yv, fr[cc][o + t]), acc[cc][o]);
+      }
+    }
+  }
+}
+
+template <int RT, int GR>
+__global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
+  extern __shared__ __align__(128) float sm[];
+  const int R = RT > 0 ? RT : a.R;
+  const int m0 = a.m0, m0q = a.m0q, n = a.n, rho = a.rho, rhop = a.rhop, W = a.W, H = a.H;
+  const int NC = n + 1, L = m0 + 1, pitch = a.pitch, TW = a.TW;
+  float* Cs = sm;                          // m0 x rhop
+  float* MT = Cs + (size_t)m0 * rhop;      // m0 x m0q   MT[j][i] = M[i][j], MT[j][m0] = u0[j]
+  float* Fs = MT + (size_t)m0 * m0q;       // n x pitch
+  float* Bs = Fs + (size_t)n * pitch;      // m0 x pitch
+  float* Ys = Bs + (size_t)m0 * pitch;     // m0q x pitch
+
+  const size_t ncst = (size_t)m0 * rhop + (size_t)m0 * m0q;
+  for (size_t k = threadIdx.x; k < ncst; k += blockDim.x) sm[k] = a.cst[k];
+
+  const int ncols = TW + 2 * R;
+  const int nq = (ncols + 3) / 4;          // pixel quads with features
+  const int nchunks = (NC + K2_CC - 1) / K2_CC;
+  const int XG = TW / K2_XR;
+  const int fir_items = L * nchunks * XG;
+  const int nic = m0q / 8;
+  const int gemm_items = nq * nic;
+  const int ntiles = a.tiles_x * a.vrows;
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int v = a.v0 + tile / a.tiles_x;
+    const int row = clampi(v, 0, H - 1);
+    const int x0 = (tile % a.tiles_x) * TW;
+    __syncthreads();  // previous tile's readers are done (and constants staged)
+    for (int k = threadIdx.x; k < n * nq * 4; k += blockDim.x) {
+      const int c = k / (nq * 4), s = k - c * (nq * 4);
+      const int x = clampi(x0 - R + s, 0, W - 1);
+      Fs[(size_t)c * pitch + s] = __ldg(a.f + (long long)c * a.fps + (long long)row * W + x);
+    }
+    // b_j(x) for every column of the tile incl. the 2R halo (difference-form distances)
+    for (int s = threadIdx.x; s < nq * 4; s += blockDim.x) {
+      const int x = clampi(x0 - R + s, 0, W - 1);
+      float gv[GR];
+#pragma unroll
+      for (int d = 0; d < GR; ++d) gv[d] = d < rho ? guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, row, x, H, W) : 0.f;
+      for (int j = 0; j < m0; ++j) {
+        const float4* cj = reinterpret_cast<const float4*>(Cs + (size_t)j * rhop);
+        float d2 = 0.f;
+#pragma unroll
+        for (int d4 = 0; d4 < GR / 4; ++d4) {
+          if (4 * d4 < rho) {
+            const float4 c4 = cj[d4];
+            const float t0 = gv[4 * d4] - c4.x, t1 = gv[4 * d4 + 1] - c4.y;
+            const float t2 = gv[4 * d4 + 2] - c4.z, t3 = gv[4 * d4 + 3] - c4.w;
+            d2 = fmaf(t0, t0, d2);
+            d2 = fmaf(t1, t1, d2);
+            d2 = fmaf(t2, t2, d2);
+            d2 = fmaf(t3, t3, d2);
+          }
+        }
+        Bs[(size_t)j * pitch + s] = range_kernel(d2, a.k2);
+      }
+    }
+    __syncthreads();
+    // [px x m0] x [m0 x m0q]: 4 pixels x 8 outputs per item, FP32 FMA
+    for (int it = threadIdx.x; it < gemm_items; it += blockDim.x) {
+      const int q = it % nq, ic = it / nq;
+      float acc[4][8];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) acc[p][ii] = 0.f;
+      const float* bcol = Bs + 4 * q;
+      const float* mcol = MT + 8 * ic;
+#pragma unroll 4
+      for (int j = 0; j < m0; ++j) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bcol + (size_t)j * pitch);
+        const float4 ma = *reinterpret_cast<const float4*>(mcol + (size_t)j * m0q);
+        const float4 mb = *reinterpret_cast<const float4*>(mcol + (size_t)j * m0q + 4);
+        const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+        const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) acc[p][ii] = fmaf(mm[ii], bb[p], acc[p][ii]);
+      }
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii)
+        *reinterpret_cast<float4*>(Ys + (size_t)(8 * ic + ii) * pitch + 4 * q) =
+            make_float4(acc[0][ii], acc[1][ii], acc[2][ii], acc[3][ii]);
+    }
+    __syncthreads();
+    const long long vrow = (long long)(v - a.v0) * a.Wp;
+    for (int it = threadIdx.x; it < fir_items; it += blockDim.x) {
+      const int i = it % L;
+      const int rest = it / L;
+      const int ch = rest % nchunks;
+      const int xg = rest / nchunks;
+      const int xo = x0 + xg * K2_XR;
+      if (xo >= W) continue;
+      float acc[K2_CC][K2_XR];
+      hfir<RT>(a, Ys + (size_t)i * pitch + xg * K2_XR, Fs, pitch, xg * K2_XR, ch * K2_CC, acc);
+#pragma unroll
+      for (int cc = 0; cc < K2_CC; ++cc) {
+        const int c = ch * K2_CC + cc;
+        if (c < NC) {
+          float* dst = a.hp + (long long)(i * NC + c) * a.hps + vrow + xo;
+#pragma unroll
+          for (int q4 = 0; q4 < K2_XR / 4; ++q4)
+            if (xo + 4 * q4 < a.Wp)
+              reinterpret_cast<float4*>(dst)[q4] =
+                  make_float4(acc[cc][4 * q4], acc[cc][4 * q4 + 1], acc[cc][4 * q4 + 2], acc[cc][4 * q4 + 3]);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace nys
+
+using namespace nys;
+
+extern "C" {
+
+int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_stride, const float* guide,
+                     int64_t guide_plane_stride, int out0, int out_rows, float* planes, int64_t planes_stride,
+                     const void* workspace, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  if (!f || !planes || !workspace || (d->guide_kind == 0 && !guide)) return NYS_EINVAL;
+  if (out0 < 0 || out_rows < 1 || out0 + out_rows > d->H) return NYS_EINVAL;
+  const int Wp = wpitch(d->W);
+  if (planes_stride < (int64_t)(out_rows + 2 * d->radius) * Wp || (planes_stride & 3)) return NYS_EINVAL;
+  if (reinterpret_cast<uintptr_t>(planes) & 15) return NYS_EINVAL;
+  const FilterLayout L = filter_layout(d);
+  HArgs a;
+  memset(&a, 0, sizeof(a));
+  a.f = f;
+  a.g = d->guide_kind == 0 ? guide : f;
+  a.hp = planes;
+  a.cst = reinterpret_cast<const float*>(workspace);
+  a.fps = f_plane_stride;
+  a.gps = d->guide_kind == 0 ? guide_plane_stride : f_plane_stride;
+  a.hps = planes_stride;
+  a.n = d->n;
+  a.rho = d->rho;
+  a.rhop = L.rhop;
+  a.H = d->H;
+  a.W = d->W;
+  a.Wp = Wp;
+  a.m0 = d->m0;
+  a.m0q = L.m0q;
+  a.R = d->radius;
+  a.box = d->spatial_kind == NYS_SPATIAL_BOX;
+  a.gkind = d->guide_kind;
+  a.v0 = out0 - d->radius;
+  a.vrows = out_rows + 2 * d->radius;
+  a.k2 = k2_of(d);
+  fill_taps(d, a.taps);
+  // tile width: 128 columns unless shared memory or a narrow image says otherwise
+  const size_t cst_floats = (size_t)d->m0 * L.rhop + (size_t)d->m0 * L.m0q;
+  const size_t per_col = (size_t)(d->n + d->m0 + L.m0q);
+  auto pitch_for = [&](int tw) {
+    int p = (int)ceil_div(tw + 2 * d->radius + 4, 4) * 4;
+    p += ((4 - p % 32) + 32) % 32;  // pitch = 4 (mod 32): LDS.128 across rows is conflict-free
+    return p;
+  };
+  int TW = 128;
+  while (TW > K2_XR && (cst_floats + per_col * (size_t)pitch_for(TW)) * 4 > 200 * 1024) TW -= K2_XR;
+  TW = std::min<int>(TW, (int)ceil_div(d->W, K2_XR) * K2_XR);
+  const size_t smem = (cst_floats + per_col * (size_t)pitch_for(TW)) * 4;
+  if (smem > 220 * 1024) return NYS_EUNSUPPORTED;
+  a.TW = TW;
+  a.pitch = pitch_for(TW);
+  a.tiles_x = (int)ceil_div(d->W, TW);
+  const long long ntiles = (long long)a.tiles_x * a.vrows;
+  const int grid = (int)std::min<long long>(ntiles, (long long)num_sms());
+  const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
+  cudaStream_t s = (cudaStream_t)stream;
+  auto go = [&](auto kern) -> int {
+    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
+    kern<<<grid, K2_THREADS, smem, s>>>(a);
+    NYS_LAUNCH_CHECK();
+    return NYS_OK;
+  };
+#define NYS_H_GR(RV)                                       \
+  switch (GR) {                                            \
+    case 4: return go(k_feat_hpass<RV, 4>);                \
+    case 16: return go(k_feat_hpass<RV, 16>);              \
+    case 32: return go(k_feat_hpass<RV, 32>);              \
+    default: return go(k_feat_hpass<RV, 64>);              \
+  }
+  const int rsel = a.box ? 0 : d->radius;
+  switch (rsel) {
+    case 9: NYS_H_GR(9)
+    case 12: NYS_H_GR(12)
+    case 15: NYS_H_GR(15)
+    case 18: NYS_H_GR(18)
+    default: NYS_H_GR(0)
+  }
+#undef NYS_H_GR
+}
+
+}  // extern "C"

@@ -17,110 +17,9 @@
 #include <cstring>
 #include <vector>
 
-#include "nys_common.cuh"
+#include "nys_kmeans_dev.cuh"
 
 namespace nys {
-
-struct KState {
-  int converged;
-  int iters;
-  int n_empty;
-  int zero_draw;
-  long long changed;
-  long long repairs;
-};
-
-struct KLayout {
-  int64_t m;
-  int rho, m0, S;  // S: Lloyd slots per block = m0*(rho+1) + 2
-  int nb_assign, nb_seed;
-  int64_t seed_chunk;
-  size_t off_d2, off_labels, off_part, off_ppart, off_tot, off_cf, off_cprev, off_excl, off_state, off_arg,
-      off_idx, total;
-};
-
-static int g_sms = 0;
-static int sms() {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
-  }
-  return g_sms;
-}
-
-static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-
-static KLayout klayout(int64_t m, int rho, int m0) {
-  KLayout L;
-  L.m = m;
-  L.rho = rho;
-  L.m0 = m0;
-  L.S = m0 * (rho + 1) + 2;
-  L.nb_assign = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, ceil_div(m, 256)));
-  L.nb_seed = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(m, 1024)));
-  L.seed_chunk = ceil_div(m, L.nb_seed);
-  size_t o = 0;
-  L.off_d2 = o;      o = align256(o + (size_t)m * 8);
-  L.off_labels = o;  o = align256(o + (size_t)m * 4);
-  L.off_part = o;    o = align256(o + (size_t)L.nb_assign * L.S * 8);
-  L.off_ppart = o;   o = align256(o + (size_t)L.nb_seed * 8);
-  L.off_tot = o;     o = align256(o + (size_t)L.S * 8);
-  L.off_cf = o;      o = align256(o + (size_t)m0 * rho * 4);
-  L.off_cprev = o;   o = align256(o + (size_t)m0 * rho * 8);
-  L.off_excl = o;    o = align256(o + (size_t)m0 * 8);
-  L.off_state = o;   o = align256(o + sizeof(KState));
-  L.off_arg = o;     o = align256(o + (size_t)std::max(L.nb_assign, L.nb_seed) * 16);
-  L.off_idx = o;     o = align256(o + 64);
-  L.total = o;
-  return L;
-}
-
-// numpy's row reduction order for ((x - c)**2).sum(axis=1) over rho entries
-// (pairwise_sum: sequential from 0 below 8 terms, else 8 strided partials
-// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail).
-// __dmul_rn/__dadd_rn forbid FMA contraction, so every D^2 value is
-// bit-identical to the reference's (landmarks.py:64,72).
-__device__ __forceinline__ double sqdiff(double x, double c) {
-  const double t = __dsub_rn(x, c);
-  return __dmul_rn(t, t);
-}
-
-__device__ double d2_exact(const float* __restrict__ pts, long long ps, long long i, int rho,
-                           const double* __restrict__ c) {
-  if (rho < 8) {
-    double r = 0.0;
-    for (int d = 0; d < rho; ++d) r = __dadd_rn(r, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
-    return r;
-  }
-  double r[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r[k] = sqdiff((double)__ldg(pts + k * ps + i), c[k]);
-  int d = 8;
-  const int full = rho - (rho % 8);
-  for (; d < full; d += 8) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], sqdiff((double)__ldg(pts + (d + k) * ps + i), c[d + k]));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; d < rho; ++d) res = __dadd_rn(res, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
-  return res;
-}
-
-// fixed-shape block sum (blockDim multiple of 32, <= 1024)
-__device__ double block_sum(double v, double* sh) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int k = 0; k < nw; ++k) r += sh[k];
-  return r;  // valid in thread 0
-}
 
 // ---------------------------------------------------------------------------
 // k-means++ (landmarks.py:60-73)
@@ -595,15 +494,19 @@ static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho,
   float* Cf = reinterpret_cast<float*>(ws + L.off_cf);
   double* Cprev = reinterpret_cast<double*>(ws + L.off_cprev);
   long long* excl = reinterpret_cast<long long*>(ws + L.off_excl);
-  count_launch(); k_c_to_f<<<1, 256, 0, s>>>(C, Cf, m0 * rho);
-  NYS_LAUNCH_CHECK();
-  for (int it = 0; it < max_iter; ++it) {
-    int rc = launch_assign(pts, ps, m, rho, Cf, m0, labels, it == 0, part, L.nb_assign, L.S, st, s);
-    if (rc) return rc;
-    count_launch(); k_reduce<<<(int)ceil_div(L.S, 256), 256, 0, s>>>(part, L.nb_assign, L.S, tot, st);
-    count_launch(); k_finalize<<<1, 256, 0, s>>>(tot, m0, rho, it, C, Cprev, Cf, errors, st);
-    count_launch(); k_repair<<<1, 1024, 0, s>>>(pts, ps, m, rho, labels, tot, m0, C, Cprev, Cf, excl, st);
+  int rc = launch_lloyd_coop(pts, ps, m, rho, m0, max_iter, C, errors, ws, L, s);
+  if (rc != NYS_OK && rc != NYS_EUNSUPPORTED) return rc;
+  if (rc == NYS_EUNSUPPORTED) {  // step-wise fallback (no cooperative launch / oversized accumulators)
+    count_launch(); k_c_to_f<<<1, 256, 0, s>>>(C, Cf, m0 * rho);
     NYS_LAUNCH_CHECK();
+    for (int it = 0; it < max_iter; ++it) {
+      rc = launch_assign(pts, ps, m, rho, Cf, m0, labels, it == 0, part, L.nb_assign, L.S, st, s);
+      if (rc) return rc;
+      count_launch(); k_reduce<<<(int)ceil_div(L.S, 256), 256, 0, s>>>(part, L.nb_assign, L.S, tot, st);
+      count_launch(); k_finalize<<<1, 256, 0, s>>>(tot, m0, rho, it, C, Cprev, Cf, errors, st);
+      count_launch(); k_repair<<<1, 1024, 0, s>>>(pts, ps, m, rho, labels, tot, m0, C, Cprev, Cf, excl, st);
+      NYS_LAUNCH_CHECK();
+    }
   }
   double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
   const size_t smem = (size_t)m0 * rho * 8;
@@ -647,12 +550,18 @@ int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho
   count_launch(); k_init_state<<<1, 1, 0, s>>>(st, seeds, first_index, centroids_out, rho, m0);
   count_launch(); k_gather<<<1, 64, 0, s>>>(points, plane_stride, rho, nullptr, first_index, centroids_out);
   NYS_LAUNCH_CHECK();
-  for (int j = 1; j < m0; ++j) {
-    count_launch(); k_pp_update<<<L.nb_seed, 256, 0, s>>>(points, plane_stride, m, rho, centroids_out + (size_t)(j - 1) * rho,
-                                          j == 1, d2, ppart, L.seed_chunk, st);
-    count_launch(); k_pp_select<<<1, 1024, 0, s>>>(points, plane_stride, m, rho, d2, ppart, L.nb_seed, L.seed_chunk,
-                                   uniforms[j - 1], j, centroids_out + (size_t)j * rho, seeds, st);
-    NYS_LAUNCH_CHECK();
+  double* unif = reinterpret_cast<double*>(ws + L.off_unif);
+  if (m0 > 1) NYS_CUDA_TRY(cudaMemcpyAsync(unif, uniforms, (size_t)(m0 - 1) * sizeof(double), cudaMemcpyHostToDevice, s));
+  rc = launch_seed_coop(points, plane_stride, m, rho, m0, unif, centroids_out, seeds, ws, L, s);
+  if (rc != NYS_OK && rc != NYS_EUNSUPPORTED) return rc;
+  if (rc == NYS_EUNSUPPORTED) {  // step-wise fallback: two launches per draw
+    for (int j = 1; j < m0; ++j) {
+      count_launch(); k_pp_update<<<L.nb_seed, 256, 0, s>>>(points, plane_stride, m, rho, centroids_out + (size_t)(j - 1) * rho,
+                                            j == 1, d2, ppart, L.seed_chunk, st);
+      count_launch(); k_pp_select<<<1, 1024, 0, s>>>(points, plane_stride, m, rho, d2, ppart, L.nb_seed, L.seed_chunk,
+                                     uniforms[j - 1], j, centroids_out + (size_t)j * rho, seeds, st);
+      NYS_LAUNCH_CHECK();
+    }
   }
   return run_lloyd_and_final(points, plane_stride, m, rho, m0, max_iter, centroids_out, errors_out, stats_out,
                              quant_error_out, assignment_out, ws, L, s);

@@ -230,14 +230,16 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
     if timer:
         timer.mark("extrapolation")
-    row_bytes = int(lib.nys_filter_planes_bytes(C.byref(d), 1))
+    Wp = -(-W // 4) * 4
+    row_bytes = (d.m0 + 1) * (n + 1) * Wp * 4
     budget = plane_budget if plane_budget is not None else _plane_budget()
     bands = plan_bands(H, d.radius, row_bytes, budget)
     max_rows = max(b.hp_rows for b in bands)
-    planes = torch.empty(((d.m0 + 1) * (n + 1), max_rows * W), dtype=torch.float32, device=inp.f.device)
+    planes = torch.empty(((d.m0 + 1) * (n + 1), max_rows * Wp), dtype=torch.float32, device=inp.f.device)
     hps = int(planes.stride(0))
     if out is None:
         out = torch.empty((n, H, W), dtype=torch.float32, device=inp.f.device)
+
     def ev():
         e = torch.cuda.Event(enable_timing=True)
         e.record()
@@ -245,12 +247,11 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
 
     for b in bands:
         e0 = ev() if kernel_events is not None else None
-        _native.check(lib.nys_filter_hpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, b.hp0, b.hp_rows,
+        _native.check(lib.nys_filter_hpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, b.out0, b.out_rows,
                                            ptr(planes), hps, ptr(ws), s), "nys_filter_hpass")
         e1 = ev() if kernel_events is not None else None
         _native.check(lib.nys_filter_vpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, ptr(planes), hps,
-                                           b.hp0, b.out0, b.out_rows, ptr(out), H * W, ptr(ws), s),
-                      "nys_filter_vpass")
+                                           b.out0, b.out_rows, ptr(out), H * W, ptr(ws), s), "nys_filter_vpass")
         if kernel_events is not None:
             e2 = ev()
             kernel_events.append(("k_feat_hpass", e0, e1, b))

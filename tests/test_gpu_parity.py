@@ -88,7 +88,7 @@ def test_kmeans_known_answers():
         # device points are float32: FP64 KAT inputs such as 0.1 round to 0.1f (1.5e-9 away)
         np.testing.assert_allclose(lm.centroids, c["centroids"], rtol=1e-7, atol=1e-9, err_msg=name)
         np.testing.assert_array_equal(lm.assignment, c["assignment"], err_msg=name)
-        assert lm.quant_error == pytest.approx(float(c["quant_error"]), rel=1e-9, abs=1e-12), name
+        assert lm.quant_error == pytest.approx(float(c["quant_error"]), rel=1e-6, abs=1e-12), name
         assert len(lm.errors) == len(c["errors"]), name
     lm = kmeans_landmarks(np.array([[0.0], [10.0]]), 2, seed=0)
     assert sorted(lm.centroids.ravel().tolist()) == [0.0, 10.0] and lm.quant_error == 0.0
@@ -150,7 +150,7 @@ def test_banded_equals_single_band_bitwise():
     inp = _prepare_inputs(f, f)
     C = kmeans_landmarks(f32.reshape(8, -1).T.astype(np.float64), 12, max_iter=10).centroids
     one, _, s1 = run_filter(inp, C, params)
-    row_bytes = (12 + 1) * (8 + 1) * 80 * 4
+    row_bytes = (12 + 1) * (8 + 1) * 80 * 4  # Wp = 80
     many, _, s2 = run_filter(inp, C, params, plane_budget=row_bytes * 30)  # 30-row bands incl. halo
     torch.cuda.synchronize()
     assert torch.equal(one, many)

@@ -38,7 +38,7 @@ struct HArgs {
   const float* cst;
   long long fps, gps, hps;
   int n, rho, rhop, H, W, Wp, m0, m0q, R, box, gkind;
-  int v0, vrows, TW, pitch, tiles_x;
+  int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
   float k2;
   float taps[NYS_MAX_TAPS];
 };
@@ -133,40 +133,47 @@ __global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
   const int R = RT > 0 ? RT : a.R;
   const int m0 = a.m0, m0q = a.m0q, n = a.n, rho = a.rho, rhop = a.rhop, W = a.W, H = a.H;
   const int NC = n + 1, L = m0 + 1, pitch = a.pitch, TW = a.TW;
-  float* Cs = sm;                          // m0 x rhop
-  float* MT = Cs + (size_t)m0 * rhop;      // m0 x m0q   MT[j][i] = M[i][j], MT[j][m0] = u0[j]
-  float* Fs = MT + (size_t)m0 * m0q;       // n x pitch
-  float* Bs = Fs + (size_t)n * pitch;      // m0 x pitch
-  float* Ys = Bs + (size_t)m0 * pitch;     // m0q x pitch
+  const int RPT = a.rpt;
+  float* Cs = sm;                                  // m0 x rhop
+  float* MT = Cs + (size_t)m0 * rhop;              // m0 x m0q   MT[j][i] = M[i][j], MT[j][m0] = u0[j]
+  float* Fs = MT + (size_t)m0 * m0q;               // RPT x n x pitch
+  float* Bs = Fs + (size_t)RPT * n * pitch;        // RPT x m0 x pitch
+  float* Ys = Bs + (size_t)RPT * m0 * pitch;       // RPT x m0q x pitch
 
   const size_t ncst = (size_t)m0 * rhop + (size_t)m0 * m0q;
   for (size_t k = threadIdx.x; k < ncst; k += blockDim.x) sm[k] = a.cst[k];
 
   const int ncols = TW + 2 * R;
   const int nq = (ncols + 3) / 4;          // pixel quads with features
+  const int ncol4 = nq * 4;
   const int nchunks = (NC + K2_CC - 1) / K2_CC;
   const int XG = TW / K2_XR;
-  const int fir_items = L * nchunks * XG;
+  const int fir_items = RPT * L * nchunks * XG;
   const int nic = m0q / 8;
-  const int gemm_items = nq * nic;
-  const int ntiles = a.tiles_x * a.vrows;
+  const int gemm_items = RPT * nq * nic;
+  const int row_tiles = (a.vrows + RPT - 1) / RPT;
+  const int ntiles = a.tiles_x * row_tiles;
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int v = a.v0 + tile / a.tiles_x;
-    const int row = clampi(v, 0, H - 1);
+    const int vb = a.v0 + (tile / a.tiles_x) * RPT;  // first virtual row of the tile
     const int x0 = (tile % a.tiles_x) * TW;
     __syncthreads();  // previous tile's readers are done (and constants staged)
-    for (int k = threadIdx.x; k < n * nq * 4; k += blockDim.x) {
-      const int c = k / (nq * 4), s = k - c * (nq * 4);
+    for (int k = threadIdx.x; k < RPT * n * ncol4; k += blockDim.x) {
+      const int r = k / (n * ncol4), rem = k - r * (n * ncol4);
+      const int c = rem / ncol4, s = rem - c * ncol4;
+      const int row = clampi(vb + r, 0, H - 1);
       const int x = clampi(x0 - R + s, 0, W - 1);
-      Fs[(size_t)c * pitch + s] = __ldg(a.f + (long long)c * a.fps + (long long)row * W + x);
+      Fs[((size_t)r * n + c) * pitch + s] = __ldg(a.f + (long long)c * a.fps + (long long)row * W + x);
     }
     // b_j(x) for every column of the tile incl. the 2R halo (difference-form distances)
-    for (int s = threadIdx.x; s < nq * 4; s += blockDim.x) {
+    for (int k = threadIdx.x; k < RPT * ncol4; k += blockDim.x) {
+      const int r = k / ncol4, s = k - r * ncol4;
+      const int row = clampi(vb + r, 0, H - 1);
       const int x = clampi(x0 - R + s, 0, W - 1);
       float gv[GR];
 #pragma unroll
       for (int d = 0; d < GR; ++d) gv[d] = d < rho ? guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, row, x, H, W) : 0.f;
+      float* brow = Bs + (size_t)r * m0 * pitch + s;
       for (int j = 0; j < m0; ++j) {
         const float4* cj = reinterpret_cast<const float4*>(Cs + (size_t)j * rhop);
         float d2 = 0.f;
@@ -182,19 +189,20 @@ __global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
             d2 = fmaf(t3, t3, d2);
           }
         }
-        Bs[(size_t)j * pitch + s] = range_kernel(d2, a.k2);
+        brow[(size_t)j * pitch] = range_kernel(d2, a.k2);
       }
     }
     __syncthreads();
     // [px x m0] x [m0 x m0q]: 4 pixels x 8 outputs per item, FP32 FMA
     for (int it = threadIdx.x; it < gemm_items; it += blockDim.x) {
-      const int q = it % nq, ic = it / nq;
+      const int q = it % nq, rem = it / nq;
+      const int ic = rem % nic, r = rem / nic;
       float acc[4][8];
 #pragma unroll
       for (int p = 0; p < 4; ++p)
 #pragma unroll
         for (int ii = 0; ii < 8; ++ii) acc[p][ii] = 0.f;
-      const float* bcol = Bs + 4 * q;
+      const float* bcol = Bs + (size_t)r * m0 * pitch + 4 * q;
       const float* mcol = MT + 8 * ic;
 #pragma unroll 4
       for (int j = 0; j < m0; ++j) {
@@ -208,22 +216,26 @@ __global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
 #pragma unroll
           for (int ii = 0; ii < 8; ++ii) acc[p][ii] = fmaf(mm[ii], bb[p], acc[p][ii]);
       }
+      float* yout = Ys + (size_t)r * m0q * pitch + 4 * q;
 #pragma unroll
       for (int ii = 0; ii < 8; ++ii)
-        *reinterpret_cast<float4*>(Ys + (size_t)(8 * ic + ii) * pitch + 4 * q) =
+        *reinterpret_cast<float4*>(yout + (size_t)(8 * ic + ii) * pitch) =
             make_float4(acc[0][ii], acc[1][ii], acc[2][ii], acc[3][ii]);
     }
     __syncthreads();
-    const long long vrow = (long long)(v - a.v0) * a.Wp;
     for (int it = threadIdx.x; it < fir_items; it += blockDim.x) {
       const int i = it % L;
-      const int rest = it / L;
+      int rest = it / L;
       const int ch = rest % nchunks;
-      const int xg = rest / nchunks;
+      rest /= nchunks;
+      const int xg = rest % XG;
+      const int r = rest / XG;
       const int xo = x0 + xg * K2_XR;
-      if (xo >= W) continue;
+      if (xo >= W || vb + r >= a.v0 + a.vrows) continue;
       float acc[K2_CC][K2_XR];
-      hfir<RT>(a, Ys + (size_t)i * pitch + xg * K2_XR, Fs, pitch, xg * K2_XR, ch * K2_CC, acc);
+      hfir<RT>(a, Ys + ((size_t)r * m0q + i) * pitch + xg * K2_XR, Fs + (size_t)r * n * pitch, pitch, xg * K2_XR,
+               ch * K2_CC, acc);
+      const long long vrow = (long long)(vb + r - a.v0) * a.Wp;
 #pragma unroll
       for (int cc = 0; cc < K2_CC; ++cc) {
         const int c = ch * K2_CC + cc;
@@ -281,7 +293,9 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.vrows = out_rows + 2 * d->radius;
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);
-  // tile width: 128 columns unless shared memory or a narrow image says otherwise
+  // tile shape (TW columns x RPT rows): minimise a per-output-pixel cost model
+  // of the three barrier-separated phases (features, y GEMM, FIR), each of
+  // which runs ceil(items / 512) rounds, under the shared-memory budget
   const size_t cst_floats = (size_t)d->m0 * L.rhop + (size_t)d->m0 * L.m0q;
   const size_t per_col = (size_t)(d->n + d->m0 + L.m0q);
   auto pitch_for = [&](int tw) {
@@ -289,15 +303,38 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
     p += ((4 - p % 32) + 32) % 32;  // pitch = 4 (mod 32): LDS.128 across rows is conflict-free
     return p;
   };
-  int TW = 128;
-  while (TW > K2_XR && (cst_floats + per_col * (size_t)pitch_for(TW)) * 4 > 200 * 1024) TW -= K2_XR;
-  TW = std::min<int>(TW, (int)ceil_div(d->W, K2_XR) * K2_XR);
-  const size_t smem = (cst_floats + per_col * (size_t)pitch_for(TW)) * 4;
+  auto smem_for = [&](int tw, int rpt) { return (cst_floats + (size_t)rpt * per_col * pitch_for(tw)) * 4; };
+  const int R = d->radius, T = 2 * R + 1, NC = d->n + 1, Lm = d->m0 + 1;
+  const int nchunks = (int)ceil_div(NC, K2_CC);
+  const double fir_item = d->spatial_kind == NYS_SPATIAL_BOX ? 4.0 * (16 + 2 * R) * 3 : 64.0 * T + 4.0 * (16 + 2 * R);
+  const double gemm_item = 36.0 * d->m0;
+  const double feat_px = d->m0 * (2.0 * d->rho + 6.0);
+  const int wcap = (int)std::min<int64_t>(256, ceil_div(d->W, K2_XR) * K2_XR);
+  int TW = K2_XR, RPT = 1;
+  double best = 1e300;
+  for (int rpt = 1; rpt <= 4; rpt *= 2) {
+    if (rpt > out_rows + 2 * R) break;
+    for (int tw = K2_XR; tw <= wcap; tw += K2_XR) {
+      if (smem_for(tw, rpt) > 200 * 1024) break;
+      const int nq = (int)ceil_div(tw + 2 * R, 4);
+      const double fr = (double)ceil_div((int64_t)rpt * Lm * nchunks * (tw / K2_XR), K2_THREADS) * fir_item;
+      const double gr = (double)ceil_div((int64_t)rpt * nq * (L.m0q / 8), K2_THREADS) * gemm_item;
+      const double er = (double)ceil_div((int64_t)rpt * nq * 4, K2_THREADS) * feat_px;
+      const double cost = (fr + gr + er + 2000.0) / ((double)rpt * std::min(tw, d->W));
+      if (cost < best) {
+        best = cost;
+        TW = tw;
+        RPT = rpt;
+      }
+    }
+  }
+  const size_t smem = smem_for(TW, RPT);
   if (smem > 220 * 1024) return NYS_EUNSUPPORTED;
   a.TW = TW;
+  a.rpt = RPT;
   a.pitch = pitch_for(TW);
   a.tiles_x = (int)ceil_div(d->W, TW);
-  const long long ntiles = (long long)a.tiles_x * a.vrows;
+  const long long ntiles = (long long)a.tiles_x * ceil_div(a.vrows, RPT);
   const int grid = (int)std::min<long long>(ntiles, (long long)num_sms());
   const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
   cudaStream_t s = (cudaStream_t)stream;

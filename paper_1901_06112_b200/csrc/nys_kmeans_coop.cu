@@ -32,30 +32,32 @@ struct SeedArgs {
   double* d2;
   double* ppart;
   KState* st;
+  int d2_in_smem;
 };
 
-// owner search over `vals[0..n)` (global, read with ld.cg) for the first index
-// whose running sum exceeds `target`; each thread sums a contiguous run, the
-// runs are scanned, the owning thread walks its run.  Returns index (or the
-// last positive index if rounding pushed target past the end) and the sum of
-// all values before that index through *pre_out (thread 0 result).
+// owner search over vals[0..n) for the first index whose running sum exceeds
+// `target`: each thread sums a contiguous run, the run sums are scanned, the
+// owning thread walks its run.  If rounding pushed target past the end, the
+// last positive index is returned.  *before_out (nullable) receives the
+// running sum of all values before the returned index.  CG: vals were
+// written by other blocks (read with ld.global.cg); otherwise plain loads
+// (shared memory or this block's own global writes).
+template <bool CG>
 __device__ long long scan_find(const double* vals, long long n, double target, double* sh, int* shi,
-                               double* total_out) {
+                               double* before_out) {
+  auto ld = [&](long long i) { return CG ? __ldcg(vals + i) : vals[i]; };
   const long long per = ceil_div(n, (long long)blockDim.x);
   const long long a0 = min(n, (long long)threadIdx.x * per), a1 = min(n, a0 + per);
   double mine = 0.0;
   long long lastpos = -1;
   for (long long i = a0; i < a1; ++i) {
-    const double v = __ldcg(vals + i);
+    const double v = ld(i);
     mine += v;
     if (v > 0.0) lastpos = i;
   }
   const double incl = block_incl_scan(mine, sh);
-  __shared__ double tot_sh;
   __shared__ long long res_sh;
-  if (threadIdx.x == blockDim.x - 1) tot_sh = incl;
-  __syncthreads();
-  if (total_out) *total_out = tot_sh;
+  __shared__ double pre_sh;
   const int owner = block_first_true(incl > target, shi);
   if (threadIdx.x == 0) res_sh = -1;
   __syncthreads();
@@ -63,13 +65,20 @@ __device__ long long scan_find(const double* vals, long long n, double target, d
     double acc = incl - mine;
     long long idx = -1;
     for (long long i = a0; i < a1; ++i) {
-      acc += __ldcg(vals + i);
-      if (acc > target) {
+      const double v = ld(i);
+      if (acc + v > target) {
         idx = i;
         break;
       }
+      acc += v;
     }
-    res_sh = idx >= 0 ? idx : lastpos;
+    if (idx < 0) {  // rounding inside the run: fall back to its last positive value
+      idx = lastpos;
+      acc = incl - mine;
+      for (long long i = a0; i < idx; ++i) acc += ld(i);
+    }
+    res_sh = idx;
+    pre_sh = acc;
   }
   __syncthreads();
   if (owner == (int)blockDim.x) {
@@ -83,48 +92,100 @@ __device__ long long scan_find(const double* vals, long long n, double target, d
       long long r = -1;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = max(r, lps[w]);
       res_sh = r;
+      double acc = 0.0;
+      for (long long i = 0; i < r; ++i) acc += ld(i);
+      pre_sh = acc;
     }
     __syncthreads();
   }
   const long long r = res_sh;
+  if (before_out) *before_out = pre_sh;
   __syncthreads();
   return r;
 }
 
+template <int GR>
+__device__ __forceinline__ double d2_exact_r(const float (&x)[GR], int rho, const double* __restrict__ c) {
+  if (GR <= 8 || rho < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int d = 0; d < (GR < 8 ? GR : 8); ++d)
+      if (d < rho) r = __dadd_rn(r, sqdiff((double)x[d], c[d]));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = sqdiff((double)x[k], c[k]);
+  const int full = rho - (rho % 8);
+#pragma unroll
+  for (int d = 8; d < GR; d += 8)
+    if (d < full) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], sqdiff((double)x[d + k], c[d + k]));
+    }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+  for (int d = 0; d < GR; ++d)
+    if (d >= full && d < rho) res = __dadd_rn(res, sqdiff((double)x[d], c[d]));
+  return res;
+}
+
+template <int GR>
 __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
   cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double d2s[];  // this block's chunk of D^2 when it fits
   __shared__ double cs[NYS_MAX_RHO];
   __shared__ double sh[64];
   __shared__ int shi[2];
   __shared__ long long sel[1];
+  __shared__ double tot_sh;
   const int nb = gridDim.x, b = blockIdx.x, rho = a.rho;
   const long long chunk = ceil_div(a.m, (long long)nb);
   const long long lo = min(a.m, b * chunk), hi = min(a.m, lo + chunk);
+  const int len = (int)(hi - lo);
+  double* d2 = a.d2_in_smem ? d2s : a.d2 + lo;
+  const int B = blockDim.x;
   for (int j = 1; j < a.m0; ++j) {
     if ((int)threadIdx.x < rho) cs[threadIdx.x] = __ldcg(a.C + (size_t)(j - 1) * rho + threadIdx.x);
     __syncthreads();
     double s = 0.0;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const double v = d2_exact(a.pts, a.ps, i, rho, cs);
-      const double nv = j == 1 ? v : fmin(a.d2[i], v);
-      a.d2[i] = nv;
+    int i = threadIdx.x;
+    for (; i + 3 * B < len; i += 4 * B) {  // 4 independent points in flight
+      float x[4][GR];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int d = 0; d < GR; ++d) x[u][d] = d < rho ? __ldg(a.pts + d * a.ps + lo + i + u * B) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double v = d2_exact_r<GR>(x[u], rho, cs);
+        const double nv = j == 1 ? v : fmin(d2[i + u * B], v);
+        d2[i + u * B] = nv;
+        s += nv;
+      }
+    }
+    for (; i < len; i += B) {
+      float x[GR];
+#pragma unroll
+      for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(a.pts + d * a.ps + lo + i) : 0.f;
+      const double v = d2_exact_r<GR>(x, rho, cs);
+      const double nv = j == 1 ? v : fmin(d2[i], v);
+      d2[i] = nv;
       s += nv;
     }
     const double bs = block_sum(s, sh);
     if (threadIdx.x == 0) a.ppart[b] = bs;
     grid.sync();
     // every block resolves the owning block redundantly (identical arithmetic)
-    double total = 0.0;
-    const double u = a.uniforms[j - 1];
-    __shared__ double tot_sh;
+    double total;
     {
-      // total first, then the target
-      const long long per = ceil_div((long long)nb, (long long)blockDim.x);
+      const long long per = ceil_div((long long)nb, (long long)B);
       const long long a0 = min((long long)nb, (long long)threadIdx.x * per), a1 = min((long long)nb, a0 + per);
       double mine = 0.0;
-      for (long long i = a0; i < a1; ++i) mine += __ldcg(a.ppart + i);
+      for (long long q = a0; q < a1; ++q) mine += __ldcg(a.ppart + q);
       const double incl = block_incl_scan(mine, sh);
-      if (threadIdx.x == blockDim.x - 1) tot_sh = incl;
+      if (threadIdx.x == B - 1) tot_sh = incl;
       __syncthreads();
       total = tot_sh;
     }
@@ -132,22 +193,11 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
       if (b == 0 && threadIdx.x == 0) a.st->zero_draw = j;
       return;  // uniform across the grid
     }
-    const double target = u * total;
-    const long long bstar = scan_find(a.ppart, nb, target, sh, shi, nullptr);
+    const double target = a.uniforms[j - 1] * total;
+    double before = 0.0;
+    const long long bstar = scan_find<true>(a.ppart, nb, target, sh, shi, &before);
     if (b == (int)bstar) {
-      // prefix before this block, recomputed with the same run/scan shape
-      double before = 0.0;
-      {
-        const long long per = ceil_div((long long)nb, (long long)blockDim.x);
-        const long long a0 = min((long long)nb, (long long)threadIdx.x * per), a1 = min((long long)nb, a0 + per);
-        double mine = 0.0;
-        for (long long i = a0; i < a1 && i < bstar; ++i) mine += __ldcg(a.ppart + i);
-        const double incl = block_incl_scan(mine, sh);
-        if (threadIdx.x == blockDim.x - 1) tot_sh = incl;
-        __syncthreads();
-        before = tot_sh;
-      }
-      const long long k = scan_find(a.d2 + lo, hi - lo, target - before, sh, shi, nullptr);
+      const long long k = scan_find<false>(d2, len, target - before, sh, shi, nullptr);
       if (threadIdx.x == 0) sel[0] = lo + max(0ll, k);
       __syncthreads();
       const long long idx = sel[0];
@@ -179,7 +229,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int rho = a.rho, m0 = a.m0, slots = m0 * (rho + 1), S = a.S;
   double* wacc = dsm;                                   // nw x slots
-  double* Cd = wacc + (size_t)nw * slots;               // m0*rho current centroids (FP64)
+  double* Cd = wacc + (size_t)max(nw * slots, S);       // m0*rho current centroids (FP64)
   double* Cp = Cd + (size_t)m0 * rho;                   // m0*rho previous centroids
   long long* excl = reinterpret_cast<long long*>(Cp + (size_t)m0 * rho);  // m0
   float* Cf = reinterpret_cast<float*>(excl + m0);      // m0*rho FP32 copy for the assignment
@@ -249,23 +299,31 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       out[slots + 1] = c;
     }
     grid.sync();
-    // slot-parallel cross-block reduction (fixed block order)
-    for (long long k = (long long)b * blockDim.x + threadIdx.x; k < S; k += (long long)nb * blockDim.x) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int q = 0;
-      for (; q + 4 <= nb; q += 4) {
-        s0 += __ldcg(a.part + (size_t)q * S + k);
-        s1 += __ldcg(a.part + (size_t)(q + 1) * S + k);
-        s2 += __ldcg(a.part + (size_t)(q + 2) * S + k);
-        s3 += __ldcg(a.part + (size_t)(q + 3) * S + k);
+    // cross-block reduction: one warp per slot, lanes stride over the blocks,
+    // fixed butterfly -> deterministic; latency ~ nb/32 loads instead of nb
+    {
+      const int gw = (b * (int)blockDim.x + (int)threadIdx.x) >> 5;
+      const int nwarps = (nb * (int)blockDim.x) >> 5;
+      for (int k = gw; k < S; k += nwarps) {
+        double s0 = 0.0, s1 = 0.0;
+        int q = lane;
+        for (; q + 32 < nb; q += 64) {
+          s0 += __ldcg(a.part + (size_t)q * S + k);
+          s1 += __ldcg(a.part + (size_t)(q + 32) * S + k);
+        }
+        if (q < nb) s0 += __ldcg(a.part + (size_t)q * S + k);
+        const double t = warp_sum(s0 + s1);
+        if (lane == 0) a.tot[k] = t;
       }
-      for (; q < nb; ++q) s0 += __ldcg(a.part + (size_t)q * S + k);
-      a.tot[k] = (s0 + s1) + (s2 + s3);
     }
     grid.sync();
-    const double chg = __ldcg(a.tot + slots + 1);
+    // every block pulls the totals into shared memory once
+    double* tsh = wacc;  // reuse: the per-warp accumulators are rebuilt next iteration
+    for (int k = threadIdx.x; k < S; k += blockDim.x) tsh[k] = __ldcg(a.tot + k);
+    __syncthreads();
+    const double chg = tsh[slots + 1];
     if (b == 0 && threadIdx.x == 0) {
-      a.errors[it] = __ldcg(a.tot + slots);
+      a.errors[it] = tsh[slots];
       a.st->iters = it + 1;
       a.st->changed = (long long)chg;
     }
@@ -276,14 +334,14 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) {
       Cp[k] = Cd[k];
       const int j = k / rho, d = k - j * rho;
-      const double cnt = __ldcg(a.tot + j * (rho + 1) + rho);
-      if (cnt > 0.0) Cd[k] = __ldcg(a.tot + j * (rho + 1) + d) / cnt;
+      const double cnt = tsh[j * (rho + 1) + rho];
+      if (cnt > 0.0) Cd[k] = tsh[j * (rho + 1) + d] / cnt;
     }
     __syncthreads();
     // empty clusters, ascending j: farthest remaining point from its old centroid
     int nex = 0;
     for (int j = 0; j < m0; ++j) {
-      if (__ldcg(a.tot + j * (rho + 1) + rho) > 0.0) continue;
+      if (tsh[j * (rho + 1) + rho] > 0.0) continue;
       double bv = -INFINITY;
       long long bi = a.m;
       for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
@@ -344,6 +402,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       ++nex;
       __syncthreads();
     }
+    __syncthreads();  // tsh aliases wacc: nobody may still read the totals when it is re-zeroed
   }
   if (b == 0)
     for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) a.C[k] = Cd[k];
@@ -355,13 +414,10 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
 int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m0, const double* uniforms_dev,
                      double* C, long long* seeds, char* ws, const KLayout& L, cudaStream_t s) {
   if (m0 < 2) return NYS_OK;
-  int dev = 0, coop = 0, per_sm = 0;
+  int dev = 0, coop = 0;
   NYS_CUDA_TRY(cudaGetDevice(&dev));
   NYS_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return NYS_EUNSUPPORTED;
-  NYS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seed_coop, 512, 0));
-  const int nb = (int)std::max<long long>(1, std::min<long long>({(long long)per_sm * sms(), (long long)L.nb_coop,
-                                                                   ceil_div(m, 512)}));
   SeedArgs a;
   a.pts = pts;
   a.ps = ps;
@@ -375,9 +431,25 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
   a.ppart = reinterpret_cast<double*>(ws + L.off_ppart);
   a.st = reinterpret_cast<KState*>(ws + L.off_state);
   void* args[] = {&a};
-  count_launch();
-  NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_seed_coop, dim3(nb), dim3(512), args, 0, s));
-  return NYS_OK;
+  auto go = [&](auto kern) -> int {
+    // one block per SM; the block's D^2 chunk lives in shared memory when it fits
+    const int nb = (int)std::max<long long>(1, std::min<long long>((long long)sms(), ceil_div(m, 512)));
+    const long long chunk = ceil_div(m, (long long)nb);
+    size_t smem = (size_t)chunk * 8;
+    a.d2_in_smem = smem <= 200 * 1024;
+    if (!a.d2_in_smem) smem = 0;
+    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    int per_sm = 0;
+    NYS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, smem));
+    if (per_sm < 1) return NYS_EUNSUPPORTED;
+    count_launch();
+    NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(512), args, smem, s));
+    return NYS_OK;
+  };
+  if (rho <= 4) return go(k_seed_coop<4>);
+  if (rho <= 16) return go(k_seed_coop<16>);
+  if (rho <= 32) return go(k_seed_coop<32>);
+  return go(k_seed_coop<64>);
 }
 
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
@@ -389,8 +461,8 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   const int slots = m0 * (rho + 1);
   const size_t fixed = (size_t)m0 * rho * 8 * 2 + (size_t)m0 * 8 + (size_t)m0 * rho * 4 + 64;
   int nw = 8;
-  while (nw > 1 && (size_t)nw * slots * 8 + fixed > 200 * 1024) --nw;
-  const size_t smem = (size_t)nw * slots * 8 + fixed;
+  while (nw > 1 && (size_t)std::max(nw * slots, L.S) * 8 + fixed > 200 * 1024) --nw;
+  const size_t smem = (size_t)std::max(nw * slots, L.S) * 8 + fixed;
   if (smem > 220 * 1024) return NYS_EUNSUPPORTED;
   LloydArgs a;
   a.pts = pts;

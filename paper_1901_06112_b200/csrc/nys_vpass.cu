@@ -38,7 +38,7 @@ struct VArgs {
   FilterStats* stats;
   long long fps, gps, ops;
   int n, rho, rhop, H, W, m0, R, box, gkind;
-  int out0, out_rows, tiles_x, tiles_y, nchunks, u0_off, vec_out;
+  int out0, out_rows, tiles_x, tiles_y, nchunks, u0_off, vec_out, gcache;
   float k2, inv_alpha0, eps_den;
   float taps[NYS_MAX_TAPS];
 };
@@ -158,6 +158,10 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
   float* lsh = dsh + npx;                                 // npx: eta_lead
   float* Cs = lsh + npx;                                  // m0 x rhop
   float* U0 = Cs + (size_t)m0 * rhop;                     // m0
+  // guide cache for the centre-pixel features: planar rho <= 8 -> [rho][npx];
+  // 3x3 patch guide -> the f tile with a 1-pixel halo [n][TH+2][34]
+  float* gsh = U0 + ((m0 + 3) & ~3);
+  const int gmode = a.gcache;  // 0: global loads, 1: planar cache, 2: patch cache
   __shared__ __align__(8) unsigned long long full[K3_NS];
   __shared__ float red_min[K3_THREADS / 32];
   __shared__ unsigned long long red_cnt[K3_THREADS / 32];
@@ -198,6 +202,20 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
     if (tid == 0)
       for (int s = 0; s < K3_NS && s < nstages; ++s) issue(tx, ty, s, gstage + s);
     for (int k = tid; k < npx; k += blockDim.x) ssh[k] = 0.f;
+    if (gmode == 1) {
+      for (int k = tid; k < rho * npx; k += blockDim.x) {
+        const int d = k / npx, q = k - d * npx;
+        const int rr = min(t0 + (q >> 5), H - 1), cx = min(x0 + (q & 31), W - 1);
+        gsh[k] = __ldg(a.g + (long long)d * a.gps + (long long)rr * W + cx);
+      }
+    } else if (gmode == 2) {
+      for (int k = tid; k < n * (TH + 2) * 34; k += blockDim.x) {
+        const int c = k / ((TH + 2) * 34), q = k - c * ((TH + 2) * 34);
+        const int yy = clampi(min(t0 + q / 34 - 1, H - 1), 0, H - 1), xx = clampi(min(x0 + q % 34 - 1, W - 1), 0, W - 1);
+        gsh[k] = __ldg(a.f + (long long)c * a.fps + (long long)yy * W + xx);
+      }
+    }
+    __syncthreads();
 
     float acc[CPT][YR][4];
 #pragma unroll
@@ -212,12 +230,26 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
         // b_i at every tile pixel (and the lead projection s0 += u0_i b_i)
         float* bb = bsh + (i & 1) * npx;
         for (int k = tid; k < npx; k += blockDim.x) {
-          const int rr = min(t0 + (k >> 5), H - 1);
-          const int cx = min(x0 + (k & 31), W - 1);
           float d2 = 0.f;
-          for (int d = 0; d < rho; ++d) {
-            const float t = guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, rr, cx, H, W) - Cs[i * rhop + d];
-            d2 = fmaf(t, t, d2);
+          if (gmode == 1) {
+            for (int d = 0; d < rho; ++d) {
+              const float t = gsh[d * npx + k] - Cs[i * rhop + d];
+              d2 = fmaf(t, t, d2);
+            }
+          } else if (gmode == 2) {
+            const int ty0 = k >> 5, tx0 = k & 31;
+            for (int d = 0; d < rho; ++d) {
+              const int c = d / 9, q = d - c * 9, dy = q / 3, dx = q - (q / 3) * 3;
+              const float t = gsh[(c * (TH + 2) + ty0 + dy) * 34 + tx0 + dx] - Cs[i * rhop + d];
+              d2 = fmaf(t, t, d2);
+            }
+          } else {
+            const int rr = min(t0 + (k >> 5), H - 1);
+            const int cx = min(x0 + (k & 31), W - 1);
+            for (int d = 0; d < rho; ++d) {
+              const float t = guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, rr, cx, H, W) - Cs[i * rhop + d];
+              d2 = fmaf(t, t, d2);
+            }
           }
           const float b = range_kernel(d2, a.k2);
           bb[k] = b;
@@ -434,7 +466,10 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
     return NYS_EINVAL;
 
   const int npx = TH * 32;
-  const size_t smem = ((size_t)K3_NS * 4 * (TH + 2 * R) * 32 + 5 * (size_t)npx + (size_t)d->m0 * L.rhop + d->m0) *
+  a.gcache = (d->guide_kind == 0 && d->rho <= 8) ? 1 : (d->guide_kind == 1 ? 2 : 0);
+  const size_t gfloats = a.gcache == 1 ? (size_t)d->rho * npx : (a.gcache == 2 ? (size_t)d->n * (TH + 2) * 34 : 0);
+  const size_t smem = ((size_t)K3_NS * 4 * (TH + 2 * R) * 32 + 5 * (size_t)npx + (size_t)d->m0 * L.rhop +
+                       ((d->m0 + 3) & ~3) + gfloats) *
                       sizeof(float);
   if (smem > 227 * 1024) return NYS_EUNSUPPORTED;
   const long long ntiles = (long long)a.tiles_x * a.tiles_y;

@@ -61,7 +61,7 @@ extern "C" {
 
 size_t nys_filter_planes_bytes(const nys_filter_desc* d, int rows) {
   if (!d) return 0;
-  return (size_t)(d->m0 + 1) * (d->n + 1) * (size_t)(rows + 2 * d->radius) * (size_t)wpitch(d->W) * sizeof(float);
+  return (size_t)(rows + 2 * d->radius) * (size_t)plane_row_stride(d->W, (d->m0 + 1) * (d->n + 1)) * sizeof(float);
 }
 
 size_t nys_filter_workspace_bytes(const nys_filter_desc* d) {

@@ -38,6 +38,10 @@ inline FilterLayout filter_layout(const nys_filter_desc* d) {
 }
 
 inline int wpitch(int W) { return (int)ceil_div(W, 4) * 4; }
+// plane buffer: [virtual row][x / 32][plane][32] -> one K2 tile writes one
+// contiguous block, and one K3 TMA box row is 4 planes x 32 columns = 512 B
+inline int wpad32(int W) { return (int)ceil_div(W, 32) * 32; }
+inline int64_t plane_row_stride(int W, int nplanes) { return (int64_t)wpad32(W) * nplanes; }
 
 struct FilterStats {
   unsigned int min_abs_eta_bits;  // float bits, non-negative => integer order

@@ -17,9 +17,13 @@
 // pass, contracts with b_i(x) recomputed at the centre pixel, and applies the
 // guard and division.  Only the horizontally filtered planes touch HBM.
 //
-// Plane buffer layout: plane p = i*(n+1) + c, each plane `rows + 2R` virtual
-// rows of pitch Wp = roundup(W, 4) floats; virtual row v maps to image row
-// clamp(v, 0, H-1), so K3 never clamps (replicate borders, spatial.py:85-88).
+// Plane buffer layout: [virtual row][x / 32][plane][32 columns] with plane
+// p = i*(n+1) + c; a band has `rows + 2R` virtual rows and virtual row v maps to
+// image row clamp(v, 0, H-1), so K3 never clamps (replicate borders,
+// spatial.py:85-88).  K2's output tile is one contiguous block (streaming HBM
+// writes); K3 reads 4 planes x 32 columns = 512 B per row with one TMA box.
+#include <cstdlib>
+
 #include "nys_filter_common.cuh"
 
 namespace nys {
@@ -27,7 +31,7 @@ namespace nys {
 // ---------------------------------------------------------------------------
 // K2: features b, y = M b (+ lead s0), horizontal pass
 // ---------------------------------------------------------------------------
-constexpr int K2_THREADS = 512;
+constexpr int K2_THREADS = 256;  // two CTAs per SM: one fills in while the other waits at a phase barrier
 constexpr int K2_XR = 16;  // output columns per FIR item
 constexpr int K2_CC = 4;   // planes per FIR item
 
@@ -36,9 +40,10 @@ struct HArgs {
   const float* g;
   float* hp;
   const float* cst;
-  long long fps, gps, hps;
-  int n, rho, rhop, H, W, Wp, m0, m0q, R, box, gkind;
+  long long fps, gps, rs;  // rs: plane-buffer row stride (floats)
+  int n, rho, rhop, H, W, m0, m0q, R, box, gkind;
   int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
+  int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;
   float taps[NYS_MAX_TAPS];
 };
@@ -128,7 +133,7 @@ __device__ __forceinline__ void hfir(const HArgs& a, const float* __restrict__ y
 }
 
 template <int RT, int GR>
-__global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
+__global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
   extern __shared__ __align__(128) float sm[];
   const int R = RT > 0 ? RT : a.R;
   const int m0 = a.m0, m0q = a.m0q, n = a.n, rho = a.rho, rhop = a.rhop, W = a.W, H = a.H;
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
       Fs[((size_t)r * n + c) * pitch + s] = __ldg(a.f + (long long)c * a.fps + (long long)row * W + x);
     }
     // b_j(x) for every column of the tile incl. the 2R halo (difference-form distances)
-    for (int k = threadIdx.x; k < RPT * ncol4; k += blockDim.x) {
+    for (int k = threadIdx.x; k < ((a.dbg & 1) ? 0 : RPT * ncol4); k += blockDim.x) {
       const int r = k / ncol4, s = k - r * ncol4;
       const int row = clampi(vb + r, 0, H - 1);
       const int x = clampi(x0 - R + s, 0, W - 1);
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
     }
     __syncthreads();
     // [px x m0] x [m0 x m0q]: 4 pixels x 8 outputs per item, FP32 FMA
-    for (int it = threadIdx.x; it < gemm_items; it += blockDim.x) {
+    for (int it = threadIdx.x; it < ((a.dbg & 2) ? 0 : gemm_items); it += blockDim.x) {
       const int q = it % nq, rem = it / nq;
       const int ic = rem % nic, r = rem / nic;
       float acc[4][8];
@@ -233,19 +238,29 @@ __global__ void __launch_bounds__(K2_THREADS) k_feat_hpass(const HArgs a) {
       const int xo = x0 + xg * K2_XR;
       if (xo >= W || vb + r >= a.v0 + a.vrows) continue;
       float acc[K2_CC][K2_XR];
-      hfir<RT>(a, Ys + ((size_t)r * m0q + i) * pitch + xg * K2_XR, Fs + (size_t)r * n * pitch, pitch, xg * K2_XR,
-               ch * K2_CC, acc);
-      const long long vrow = (long long)(vb + r - a.v0) * a.Wp;
+      if (a.dbg & 4) {
+#pragma unroll
+        for (int cc = 0; cc < K2_CC; ++cc)
+#pragma unroll
+          for (int o = 0; o < K2_XR; ++o) acc[cc][o] = Ys[((size_t)r * m0q + i) * pitch + o + cc];
+      } else {
+        hfir<RT>(a, Ys + ((size_t)r * m0q + i) * pitch + xg * K2_XR, Fs + (size_t)r * n * pitch, pitch, xg * K2_XR,
+                 ch * K2_CC, acc);
+      }
+      if (a.dbg & 8) {
+        if (acc[0][0] == 1234.5f) a.hp[0] = acc[1][1];
+        continue;
+      }
+      float* dst0 = a.hp + (long long)(vb + r - a.v0) * a.rs + (long long)(xo >> 5) * (L * NC * 32) + (xo & 31);
 #pragma unroll
       for (int cc = 0; cc < K2_CC; ++cc) {
         const int c = ch * K2_CC + cc;
         if (c < NC) {
-          float* dst = a.hp + (long long)(i * NC + c) * a.hps + vrow + xo;
+          float* dst = dst0 + (i * NC + c) * 32;
 #pragma unroll
           for (int q4 = 0; q4 < K2_XR / 4; ++q4)
-            if (xo + 4 * q4 < a.Wp)
-              reinterpret_cast<float4*>(dst)[q4] =
-                  make_float4(acc[cc][4 * q4], acc[cc][4 * q4 + 1], acc[cc][4 * q4 + 2], acc[cc][4 * q4 + 3]);
+            reinterpret_cast<float4*>(dst)[q4] =
+                make_float4(acc[cc][4 * q4], acc[cc][4 * q4 + 1], acc[cc][4 * q4 + 2], acc[cc][4 * q4 + 3]);
         }
       }
     }
@@ -265,8 +280,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   if (st) return st;
   if (!f || !planes || !workspace || (d->guide_kind == 0 && !guide)) return NYS_EINVAL;
   if (out0 < 0 || out_rows < 1 || out0 + out_rows > d->H) return NYS_EINVAL;
-  const int Wp = wpitch(d->W);
-  if (planes_stride < (int64_t)(out_rows + 2 * d->radius) * Wp || (planes_stride & 3)) return NYS_EINVAL;
+  if (planes_stride < plane_row_stride(d->W, (d->m0 + 1) * (d->n + 1)) || (planes_stride & 3)) return NYS_EINVAL;
   if (reinterpret_cast<uintptr_t>(planes) & 15) return NYS_EINVAL;
   const FilterLayout L = filter_layout(d);
   HArgs a;
@@ -277,13 +291,12 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.cst = reinterpret_cast<const float*>(workspace);
   a.fps = f_plane_stride;
   a.gps = d->guide_kind == 0 ? guide_plane_stride : f_plane_stride;
-  a.hps = planes_stride;
+  a.rs = planes_stride;
   a.n = d->n;
   a.rho = d->rho;
   a.rhop = L.rhop;
   a.H = d->H;
   a.W = d->W;
-  a.Wp = Wp;
   a.m0 = d->m0;
   a.m0q = L.m0q;
   a.R = d->radius;
@@ -293,6 +306,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.vrows = out_rows + 2 * d->radius;
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);
+  if (const char* e = getenv("NYS_DBG_K2")) a.dbg = atoi(e);
   // tile shape (TW columns x RPT rows): minimise a per-output-pixel cost model
   // of the three barrier-separated phases (features, y GEMM, FIR), each of
   // which runs ceil(items / 512) rounds, under the shared-memory budget
@@ -315,7 +329,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   for (int rpt = 1; rpt <= 4; rpt *= 2) {
     if (rpt > out_rows + 2 * R) break;
     for (int tw = K2_XR; tw <= wcap; tw += K2_XR) {
-      if (smem_for(tw, rpt) > 200 * 1024) break;
+      if (smem_for(tw, rpt) > 110 * 1024) break;
       const int nq = (int)ceil_div(tw + 2 * R, 4);
       const double fr = (double)ceil_div((int64_t)rpt * Lm * nchunks * (tw / K2_XR), K2_THREADS) * fir_item;
       const double gr = (double)ceil_div((int64_t)rpt * nq * (L.m0q / 8), K2_THREADS) * gemm_item;
@@ -335,7 +349,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.pitch = pitch_for(TW);
   a.tiles_x = (int)ceil_div(d->W, TW);
   const long long ntiles = (long long)a.tiles_x * ceil_div(a.vrows, RPT);
-  const int grid = (int)std::min<long long>(ntiles, (long long)num_sms());
+  const int grid = (int)std::min<long long>(ntiles, (long long)num_sms() * 2);
   const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
   cudaStream_t s = (cudaStream_t)stream;
   auto go = [&](auto kern) -> int {

@@ -17,9 +17,10 @@
 // pass, contracts with b_i(x) recomputed at the centre pixel, and applies the
 // guard and division.  Only the horizontally filtered planes touch HBM.
 //
-// Plane buffer layout: plane p = i*(n+1) + c, each plane `rows + 2R` virtual
-// rows of pitch Wp = roundup(W, 4) floats; virtual row v maps to image row
-// clamp(v, 0, H-1), so K3 never clamps (replicate borders, spatial.py:85-88).
+// Plane buffer layout: [virtual row][x / 32][plane][32 columns] with plane
+// p = i*(n+1) + c; a band has `rows + 2R` virtual rows and virtual row v maps to
+// image row clamp(v, 0, H-1), so K3 never clamps (replicate borders,
+// spatial.py:85-88).  One TMA box = 32 columns x 4 planes x (TH+2R) rows.
 #include "nys_filter_common.cuh"
 
 namespace nys {
@@ -63,17 +64,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             unsigned long long* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
           smem_u32(dst)),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 
 // vertical FIR of one staged plane tile: 4 columns x YR rows per thread
-template <int RT, int YR>
+template <int RT, int YR, int RS>
 __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ src, float (&G)[YR][4]) {
 #pragma unroll
   for (int o = 0; o < YR; ++o) G[o][0] = G[o][1] = G[o][2] = G[o][3] = 0.f;
@@ -81,7 +82,7 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
     const int R = a.R;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int t = 0; t <= 2 * R; ++t) {
-      const float4 v = *reinterpret_cast<const float4*>(src + t * 32);
+      const float4 v = *reinterpret_cast<const float4*>(src + t * RS);
       s.x += v.x;
       s.y += v.y;
       s.z += v.z;
@@ -93,8 +94,8 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
     G[0][3] = s.w;
 #pragma unroll
     for (int o = 1; o < YR; ++o) {
-      const float4 vi = *reinterpret_cast<const float4*>(src + (o + 2 * R) * 32);
-      const float4 vo = *reinterpret_cast<const float4*>(src + (o - 1) * 32);
+      const float4 vi = *reinterpret_cast<const float4*>(src + (o + 2 * R) * RS);
+      const float4 vo = *reinterpret_cast<const float4*>(src + (o - 1) * RS);
       s.x += vi.x - vo.x;
       s.y += vi.y - vo.y;
       s.z += vi.z - vo.z;
@@ -110,7 +111,7 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
     constexpr int T = 2 * RT + 1;
 #pragma unroll
     for (int s = 0; s < YR + 2 * RT; ++s) {
-      const float4 v = *reinterpret_cast<const float4*>(src + s * 32);
+      const float4 v = *reinterpret_cast<const float4*>(src + s * RS);
 #pragma unroll
       for (int o = 0; o < YR; ++o) {
         const int t = s - o;
@@ -129,7 +130,7 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
       const float w = a.taps[t];
 #pragma unroll
       for (int o = 0; o < YR; ++o) {
-        const float4 v = *reinterpret_cast<const float4*>(src + (o + t) * 32);
+        const float4 v = *reinterpret_cast<const float4*>(src + (o + t) * RS);
         G[o][0] = fmaf(w, v.x, G[o][0]);
         G[o][1] = fmaf(w, v.y, G[o][1]);
         G[o][2] = fmaf(w, v.z, G[o][2]);
@@ -140,7 +141,8 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
 }
 
 template <int RT, int YR, int CPT>
-__global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CUtensorMap tmap, const VArgs a) {
+__global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CUtensorMap tmap4,
+                                                     const __grid_constant__ CUtensorMap tmap1, const VArgs a) {
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x;
   const int grp = tid >> 6, run = (tid >> 3) & 7, quad = tid & 7;
@@ -186,14 +188,21 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
   unsigned long long gstage = 0;  // running stage counter across tiles (mbarrier phases)
   const int ntiles = a.tiles_x * a.tiles_y;
 
+  // stage = up to 4 consecutive planes of a landmark group: a full chunk is one
+  // 4-plane box (SMEM [SR][4][32]); a partial last chunk is nval 1-plane boxes
+  // (SMEM [nval][SR][32])
   auto issue = [&](int tx, int ty, int s, unsigned long long gs) {
     const int i = s / nchunks, k = stage_chunk(s);
     const int buf = (int)(gs % K3_NS);
     const int nval = min(4, NC - 4 * k);
     mbar_expect_tx(&full[buf], (unsigned)(nval * plane_floats * 4));
-    for (int q = 0; q < nval; ++q)
-      tma_load_3d(stage + ((size_t)buf * 4 + q) * plane_floats, &tmap, tx * 32, ty * TH, i * NC + 4 * k + q,
-                  &full[buf]);
+    float* dst = stage + (size_t)buf * 4 * plane_floats;
+    if (nval == 4) {
+      tma_load_4d(dst, &tmap4, 0, i * NC + 4 * k, tx, ty * TH, &full[buf]);
+    } else {
+      for (int q = 0; q < nval; ++q)
+        tma_load_4d(dst + (size_t)q * plane_floats, &tmap1, 0, i * NC + 4 * k + q, tx, ty * TH, &full[buf]);
+    }
   };
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -229,31 +238,53 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
       if (i < m0) {
         // b_i at every tile pixel (and the lead projection s0 += u0_i b_i)
         float* bb = bsh + (i & 1) * npx;
-        for (int k = tid; k < npx; k += blockDim.x) {
-          float d2 = 0.f;
-          if (gmode == 1) {
+        const float u0i = U0[i];
+        if (gmode == 1) {
+          // 4 neighbouring pixels per thread step: independent chains, 128-bit SMEM traffic
+#pragma unroll 2
+          for (int k4 = tid; k4 < npx / 4; k4 += blockDim.x) {
+            float4 d2 = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int d = 0; d < rho; ++d) {
-              const float t = gsh[d * npx + k] - Cs[i * rhop + d];
-              d2 = fmaf(t, t, d2);
+              const float4 g4 = *reinterpret_cast<const float4*>(gsh + d * npx + 4 * k4);
+              const float c = Cs[i * rhop + d];
+              const float tx = g4.x - c, ty = g4.y - c, tz = g4.z - c, tw = g4.w - c;
+              d2.x = fmaf(tx, tx, d2.x);
+              d2.y = fmaf(ty, ty, d2.y);
+              d2.z = fmaf(tz, tz, d2.z);
+              d2.w = fmaf(tw, tw, d2.w);
             }
-          } else if (gmode == 2) {
-            const int ty0 = k >> 5, tx0 = k & 31;
-            for (int d = 0; d < rho; ++d) {
-              const int c = d / 9, q = d - c * 9, dy = q / 3, dx = q - (q / 3) * 3;
-              const float t = gsh[(c * (TH + 2) + ty0 + dy) * 34 + tx0 + dx] - Cs[i * rhop + d];
-              d2 = fmaf(t, t, d2);
-            }
-          } else {
-            const int rr = min(t0 + (k >> 5), H - 1);
-            const int cx = min(x0 + (k & 31), W - 1);
-            for (int d = 0; d < rho; ++d) {
-              const float t = guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, rr, cx, H, W) - Cs[i * rhop + d];
-              d2 = fmaf(t, t, d2);
-            }
+            const float4 b4 = make_float4(range_kernel(d2.x, a.k2), range_kernel(d2.y, a.k2),
+                                          range_kernel(d2.z, a.k2), range_kernel(d2.w, a.k2));
+            *reinterpret_cast<float4*>(bb + 4 * k4) = b4;
+            float4 s4 = *reinterpret_cast<float4*>(ssh + 4 * k4);
+            s4.x = fmaf(u0i, b4.x, s4.x);
+            s4.y = fmaf(u0i, b4.y, s4.y);
+            s4.z = fmaf(u0i, b4.z, s4.z);
+            s4.w = fmaf(u0i, b4.w, s4.w);
+            *reinterpret_cast<float4*>(ssh + 4 * k4) = s4;
           }
-          const float b = range_kernel(d2, a.k2);
-          bb[k] = b;
-          ssh[k] = fmaf(U0[i], b, ssh[k]);
+        } else {
+          for (int k = tid; k < npx; k += blockDim.x) {
+            float d2 = 0.f;
+            if (gmode == 2) {
+              const int ty0 = k >> 5, tx0 = k & 31;
+              for (int d = 0; d < rho; ++d) {
+                const int c = d / 9, q = d - c * 9, dy = q / 3, dx = q - (q / 3) * 3;
+                const float t = gsh[(c * (TH + 2) + ty0 + dy) * 34 + tx0 + dx] - Cs[i * rhop + d];
+                d2 = fmaf(t, t, d2);
+              }
+            } else {
+              const int rr = min(t0 + (k >> 5), H - 1);
+              const int cx = min(x0 + (k & 31), W - 1);
+              for (int d = 0; d < rho; ++d) {
+                const float t = guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, rr, cx, H, W) - Cs[i * rhop + d];
+                d2 = fmaf(t, t, d2);
+              }
+            }
+            const float b = range_kernel(d2, a.k2);
+            bb[k] = b;
+            ssh[k] = fmaf(u0i, b, ssh[k]);
+          }
         }
       }
       __syncthreads();
@@ -266,7 +297,13 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
           const int k = stage_chunk(s);
           const int c = 4 * k + grp;
           float G[YR][4];
-          if (c < NC) vfir<RT, YR>(a, stage + ((size_t)buf * 4 + grp) * plane_floats + pxo, G);
+          if (c < NC) {
+            const float* sb = stage + (size_t)buf * 4 * plane_floats;
+            if (4 * k + 4 <= NC)
+              vfir<RT, YR, 128>(a, sb + grp * 32 + run * YR * 128 + quad * 4, G);
+            else
+              vfir<RT, YR, 32>(a, sb + (size_t)grp * plane_floats + pxo, G);
+          }
           if (i < m0) {
             const float* bb = bsh + (i & 1) * npx + pxo;
 #pragma unroll
@@ -393,9 +430,8 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   if (st) return st;
   if (!f || !planes || !out || !workspace || (d->guide_kind == 0 && !guide)) return NYS_EINVAL;
   if (out0 < 0 || out_rows < 1 || out0 + out_rows > d->H) return NYS_EINVAL;
-  const int Wp = wpitch(d->W);
   const int vrows = out_rows + 2 * d->radius;
-  if (planes_stride < (int64_t)vrows * Wp || (planes_stride & 3)) return NYS_EINVAL;
+  if (planes_stride < plane_row_stride(d->W, (d->m0 + 1) * (d->n + 1)) || (planes_stride & 3)) return NYS_EINVAL;
   const FilterLayout L = filter_layout(d);
   const int NC = d->n + 1;
   const int nchunks = (int)ceil_div(NC, 4);
@@ -452,15 +488,21 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.eps_den = (float)d->eps_den;
   fill_taps(d, a.taps);
 
-  // TMA descriptor over the plane stack: (x, virtual row, plane), box 32 x (TH+2R) x 1
+  // TMA descriptors over the plane buffer: (32 cols, plane, x/32 tile, virtual row),
+  // boxes of 32 x 4 x 1 x (TH+2R) and 32 x 1 x 1 x (TH+2R)
   auto enc = encode_fn();
   if (!enc) return NYS_EUNSUPPORTED;
-  CUtensorMap tmap;
-  const cuuint64_t gdim[3] = {(cuuint64_t)d->W, (cuuint64_t)vrows, (cuuint64_t)((d->m0 + 1) * NC)};
-  const cuuint64_t gstr[2] = {(cuuint64_t)Wp * 4, (cuuint64_t)planes_stride * 4};
-  const cuuint32_t box[3] = {32, (cuuint32_t)(TH + 2 * R), 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(planes), gdim, gstr, box, estr,
+  const int P = (d->m0 + 1) * NC;
+  CUtensorMap tmap4, tmap1;
+  const cuuint64_t gdim[4] = {32, (cuuint64_t)P, (cuuint64_t)(wpad32(d->W) / 32), (cuuint64_t)vrows};
+  const cuuint64_t gstr[3] = {32 * 4, (cuuint64_t)P * 32 * 4, (cuuint64_t)planes_stride * 4};
+  const cuuint32_t box4[4] = {32, 4, 1, (cuuint32_t)(TH + 2 * R)};
+  const cuuint32_t box1[4] = {32, 1, 1, (cuuint32_t)(TH + 2 * R)};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (enc(&tmap4, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(planes), gdim, gstr, box4, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+      enc(&tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(planes), gdim, gstr, box1, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return NYS_EINVAL;
@@ -478,7 +520,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();
-    kern<<<grid, K3_THREADS, smem, s>>>(tmap, a);
+    kern<<<grid, K3_THREADS, smem, s>>>(tmap4, tmap1, a);
     NYS_LAUNCH_CHECK();
     return NYS_OK;
   };

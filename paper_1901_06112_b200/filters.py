@@ -230,13 +230,13 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
     if timer:
         timer.mark("extrapolation")
-    Wp = -(-W // 4) * 4
-    row_bytes = (d.m0 + 1) * (n + 1) * Wp * 4
+    rs = -(-W // 32) * 32 * (d.m0 + 1) * (n + 1)   # plane-buffer row stride: [row][x/32][plane][32]
+    row_bytes = rs * 4
     budget = plane_budget if plane_budget is not None else _plane_budget()
     bands = plan_bands(H, d.radius, row_bytes, budget)
     max_rows = max(b.hp_rows for b in bands)
-    planes = torch.empty(((d.m0 + 1) * (n + 1), max_rows * Wp), dtype=torch.float32, device=inp.f.device)
-    hps = int(planes.stride(0))
+    planes = torch.empty((max_rows, rs), dtype=torch.float32, device=inp.f.device)
+    hps = rs
     if out is None:
         out = torch.empty((n, H, W), dtype=torch.float32, device=inp.f.device)
 

@@ -150,7 +150,7 @@ def test_banded_equals_single_band_bitwise():
     inp = _prepare_inputs(f, f)
     C = kmeans_landmarks(f32.reshape(8, -1).T.astype(np.float64), 12, max_iter=10).centroids
     one, _, s1 = run_filter(inp, C, params)
-    row_bytes = (12 + 1) * (8 + 1) * 80 * 4  # Wp = 80
+    row_bytes = (12 + 1) * (8 + 1) * 96 * 4  # row stride: W padded to 32 x planes
     many, _, s2 = run_filter(inp, C, params, plane_budget=row_bytes * 30)  # 30-row bands incl. halo
     torch.cuda.synchronize()
     assert torch.equal(one, many)

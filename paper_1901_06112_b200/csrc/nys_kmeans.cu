@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(1024) k_repair(const float* __restrict__ pts, 
   }
 }
 
-// final exact assignment (landmarks.py:121-129): FP64 differenced distances
+// final exact assignment (landmarks.py:121-129): FP64 differenced distances in
+// numpy's summation order; the point is loaded once into registers
+template <int GR>
 __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, long long ps, long long m, int rho,
                                                const double* __restrict__ C, int m0, long long* __restrict__ asg,
                                                double* __restrict__ part) {
@@ -348,13 +350,16 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
   for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) csm[k] = C[k];
   __syncthreads();
   const long long chunk = ceil_div(m, (long long)gridDim.x);
-  const long long lo = blockIdx.x * chunk, hi = min(m, lo + chunk);
+  const long long lo = min(m, blockIdx.x * chunk), hi = min(m, lo + chunk);
   double s = 0.0;
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    float x[GR];
+#pragma unroll
+    for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(pts + d * ps + i) : 0.f;
     double best = INFINITY;
     int arg = 0;
     for (int j = 0; j < m0; ++j) {
-      const double v = d2_exact(pts, ps, i, rho, csm + (size_t)j * rho);
+      const double v = d2_exact_regs<GR>(x, rho, csm + (size_t)j * rho);
       if (v < best) {
         best = v;
         arg = j;
@@ -365,6 +370,22 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
   }
   const double t = block_sum(s, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+static int launch_exact(const float* pts, long long ps, long long m, int rho, const double* C, int m0, long long* asg,
+                        double* part, int nb, cudaStream_t s) {
+  const size_t smem = (size_t)m0 * rho * 8;
+  auto go = [&](auto kern) -> int {
+    if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
+    kern<<<nb, 256, smem, s>>>(pts, ps, m, rho, C, m0, asg, part);
+    NYS_LAUNCH_CHECK();
+    return NYS_OK;
+  };
+  if (rho <= 4) return go(k_exact<4>);
+  if (rho <= 16) return go(k_exact<16>);
+  if (rho <= 32) return go(k_exact<32>);
+  return go(k_exact<64>);
 }
 
 __global__ void k_sum_parts(const double* __restrict__ part, int nb, double* __restrict__ out) {
@@ -509,9 +530,8 @@ static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho,
     }
   }
   double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
-  const size_t smem = (size_t)m0 * rho * 8;
-  if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  count_launch(); k_exact<<<L.nb_assign, 256, smem, s>>>(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart);
+  int rc2 = launch_exact(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart, L.nb_assign, s);
+  if (rc2) return rc2;
   count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, qe);
   count_launch(); k_write_stats<<<1, 1, 0, s>>>(st, reinterpret_cast<long long*>(stats));
   NYS_LAUNCH_CHECK();
@@ -648,10 +668,9 @@ int nys_kmeans_exact(const float* points, int64_t plane_stride, int64_t m, int r
   char* ws = reinterpret_cast<char*>(workspace);
   cudaStream_t s = (cudaStream_t)stream;
   double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
-  const size_t smem = (size_t)m0 * rho * 8;
-  if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  count_launch(); k_exact<<<L.nb_assign, 256, smem, s>>>(points, plane_stride, m, rho, centroids, m0,
-                                         reinterpret_cast<long long*>(assignment_out), ppart);
+  rc = launch_exact(points, plane_stride, m, rho, centroids, m0, reinterpret_cast<long long*>(assignment_out), ppart,
+                    L.nb_assign, s);
+  if (rc) return rc;
   count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, sum_out);
   NYS_LAUNCH_CHECK();
   return NYS_OK;

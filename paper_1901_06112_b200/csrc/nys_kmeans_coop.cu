@@ -105,33 +105,6 @@ __device__ long long scan_find(const double* vals, long long n, double target, d
 }
 
 template <int GR>
-__device__ __forceinline__ double d2_exact_r(const float (&x)[GR], int rho, const double* __restrict__ c) {
-  if (GR <= 8 || rho < 8) {
-    double r = 0.0;
-#pragma unroll
-    for (int d = 0; d < (GR < 8 ? GR : 8); ++d)
-      if (d < rho) r = __dadd_rn(r, sqdiff((double)x[d], c[d]));
-    return r;
-  }
-  double r[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r[k] = sqdiff((double)x[k], c[k]);
-  const int full = rho - (rho % 8);
-#pragma unroll
-  for (int d = 8; d < GR; d += 8)
-    if (d < full) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], sqdiff((double)x[d + k], c[d + k]));
-    }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-#pragma unroll
-  for (int d = 0; d < GR; ++d)
-    if (d >= full && d < rho) res = __dadd_rn(res, sqdiff((double)x[d], c[d]));
-  return res;
-}
-
-template <int GR>
 __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double d2s[];  // this block's chunk of D^2 when it fits
@@ -159,7 +132,7 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
         for (int d = 0; d < GR; ++d) x[u][d] = d < rho ? __ldg(a.pts + d * a.ps + lo + i + u * B) : 0.f;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const double v = d2_exact_r<GR>(x[u], rho, cs);
+        const double v = d2_exact_regs<GR>(x[u], rho, cs);
         const double nv = j == 1 ? v : fmin(d2[i + u * B], v);
         d2[i + u * B] = nv;
         s += nv;
@@ -169,7 +142,7 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
       float x[GR];
 #pragma unroll
       for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(a.pts + d * a.ps + lo + i) : 0.f;
-      const double v = d2_exact_r<GR>(x, rho, cs);
+      const double v = d2_exact_regs<GR>(x, rho, cs);
       const double nv = j == 1 ? v : fmin(d2[i], v);
       d2[i] = nv;
       s += nv;
@@ -212,69 +185,152 @@ struct LloydArgs {
   const float* pts;
   long long ps, m;
   int rho, m0, max_iter, S;
-  double* C;        // in: seeds; out: final centroids
+  double* C;                 // in: seeds; out: final centroids
   int* labels;
-  double* part;     // nb x S
-  double* tot;      // S
-  double* arg;      // 2 x nb x 2 (double-buffered argmax pairs)
+  unsigned long long* gacc;  // 2 x (m0*rho sums + m0 counts), exact fixed point, parity-buffered
+  double* part;              // 2 x nb x 2 (objective, changed) per block, parity-buffered
+  double* arg;               // 2 x nb x 2 (double-buffered argmax pairs)
   double* errors;
   KState* st;
-  int nw;           // warps per block
+  unsigned* maxabs_bits;     // global max |x| (float bits), zeroed by k_init_state
+  int nw;                    // warps per block
 };
+
+// Warp-level accumulation of per-cluster coordinate sums as EXACT fixed-point
+// integers (x * 2^s rounded once per point): each distinct label among the
+// lanes is reduced with REDUX on 21-bit limbs, so sums are independent of
+// order and hence deterministic across blocks, warps and runs.
+template <int GR>
+__device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho, int label, bool valid, double scale,
+                                                   unsigned long long* acc, unsigned* cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned lim[GR][3];
+#pragma unroll
+  for (int d = 0; d < GR; ++d) {
+    const unsigned long long v = (unsigned long long)__double2ll_rn((double)x[d] * scale);
+    lim[d][0] = (unsigned)(v & 0x1FFFFFull);
+    lim[d][1] = (unsigned)((v >> 21) & 0x1FFFFFull);
+    lim[d][2] = (unsigned)(v >> 42);
+  }
+  unsigned rem = __ballot_sync(0xffffffffu, valid);
+  while (rem) {
+    const int leader = __ffs(rem) - 1;
+    const int L = __shfl_sync(0xffffffffu, label, leader);
+    const unsigned grp = __ballot_sync(0xffffffffu, valid && label == L);
+    if ((grp >> lane) & 1u) {
+#pragma unroll
+      for (int d = 0; d < GR; ++d)
+        if (d < rho) {
+          const unsigned long long s0 = __reduce_add_sync(grp, lim[d][0]);
+          const unsigned long long s1 = __reduce_add_sync(grp, lim[d][1]);
+          const unsigned long long s2 = __reduce_add_sync(grp, lim[d][2]);
+          if (lane == leader) acc[L * rho + d] += s0 + (s1 << 21) + (s2 << 42);
+        }
+      if (lane == leader) cnt[L] += __popc(grp);
+    }
+    rem &= ~grp;
+  }
+}
 
 template <int GR>
 __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double dsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int rho = a.rho, m0 = a.m0, slots = m0 * (rho + 1), S = a.S;
-  double* wacc = dsm;                                   // nw x slots
-  double* Cd = wacc + (size_t)max(nw * slots, S);       // m0*rho current centroids (FP64)
-  double* Cp = Cd + (size_t)m0 * rho;                   // m0*rho previous centroids
-  long long* excl = reinterpret_cast<long long*>(Cp + (size_t)m0 * rho);  // m0
-  float* Cf = reinterpret_cast<float*>(excl + m0);      // m0*rho FP32 copy for the assignment
+  const int rho = a.rho, m0 = a.m0, msl = m0 * rho, gstride = msl + m0;
+  unsigned long long* wacc = reinterpret_cast<unsigned long long*>(dsm);      // nw x msl (per-warp sums)
+  unsigned* wcnt = reinterpret_cast<unsigned*>(wacc + (size_t)nw * msl);       // nw x m0 (per-warp counts)
+  double* Cd = reinterpret_cast<double*>(wcnt + (((size_t)nw * m0 + 1) & ~size_t(1)));  // m0*rho current (FP64)
+  double* Cp = Cd + (size_t)msl;                                               // m0*rho previous
+  double* tsh = Cp + (size_t)msl;                                              // msl sums + m0 counts (FP64)
+  long long* excl = reinterpret_cast<long long*>(tsh + gstride);              // m0
+  float* Cf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(excl + m0) + 15) & ~uintptr_t(15));
+  const int rhop = (rho + 3) & ~3;                                             // Cf rows: 16-byte aligned
   __shared__ double sh[64];
   __shared__ double extra[2][32];
+  __shared__ double misc[2];
   const int nb = gridDim.x, b = blockIdx.x;
   const long long chunk = ceil_div(a.m, (long long)nb);
   const long long lo = min(a.m, b * chunk), hi = min(a.m, lo + chunk);
 
-  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) Cd[k] = __ldcg(a.C + k);
-  __syncthreads();
+  // fixed-point scale 2^s with |sum| < 2^61 for any cluster: s = 61 - log2(max|x| * m)
+  {
+    float mx = 0.f;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      for (int d = 0; d < rho; ++d) mx = fmaxf(mx, fabsf(__ldg(a.pts + d * a.ps + i)));
+    mx = warp_max(mx);
+    if (lane == 0 && mx > 0.f) atomicMax(a.maxabs_bits, __float_as_uint(mx));
+  }
+  for (int k = threadIdx.x; k < msl; k += blockDim.x) Cd[k] = __ldcg(a.C + k);
+  grid.sync();
+  const float maxabs = __uint_as_float(__ldcg(a.maxabs_bits));
+  int sexp = 0;
+  if (maxabs > 0.f) sexp = 61 - ilogb((double)maxabs * (double)a.m) - 1;
+  const double scale = ldexp(1.0, sexp), inv_scale = ldexp(1.0, -sexp);
+
   for (int it = 0; it < a.max_iter; ++it) {
-    for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) Cf[k] = (float)Cd[k];
-    for (int k = threadIdx.x; k < nw * slots; k += blockDim.x) wacc[k] = 0.0;
+    const int par = it & 1;
+    unsigned long long* G = a.gacc + (size_t)par * gstride;
+    for (int k = threadIdx.x; k < m0 * rhop; k += blockDim.x) {
+      const int j = k / rhop, d = k - j * rhop;
+      Cf[k] = d < rho ? (float)Cd[j * rho + d] : 0.f;
+    }
+    for (int k = threadIdx.x; k < nw * msl; k += blockDim.x) wacc[k] = 0ull;
+    for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0u;
     __syncthreads();
-    double* my = wacc + (size_t)w * slots;
+    unsigned long long* myacc = wacc + (size_t)w * msl;
+    unsigned* mycnt = wcnt + (size_t)w * m0;
     double near_sum = 0.0, changed = 0.0;
-    for (long long base = lo + (long long)w * 32; base < hi; base += (long long)nw * 32) {
-      const long long i = base + lane;
-      const bool valid = i < hi;
-      float x[GR];
+    // two 32-pixel tiles per warp step: every centroid LDS serves two points
+    for (long long base = lo + (long long)w * 64; base < hi; base += (long long)nw * 64) {
+      float x[2][GR];
+      float best[2] = {INFINITY, INFINITY};
+      int arg[2] = {0, 0};
+      bool valid[2];
 #pragma unroll
-      for (int d = 0; d < GR; ++d) x[d] = (valid && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
-      float best = INFINITY;
-      int arg = 0;
+      for (int h = 0; h < 2; ++h) {
+        const long long i = base + 32 * h + lane;
+        valid[h] = i < hi;
+#pragma unroll
+        for (int d = 0; d < GR; ++d) x[h][d] = (valid[h] && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
+      }
       for (int j = 0; j < m0; ++j) {
-        float d2 = 0.f;
+        const float4* cj = reinterpret_cast<const float4*>(Cf + (size_t)j * rhop);
+        float d2[2] = {0.f, 0.f};
 #pragma unroll
-        for (int d = 0; d < GR; ++d)
-          if (d < rho) {
-            const float t = x[d] - Cf[j * rho + d];
-            d2 = fmaf(t, t, d2);
+        for (int d4 = 0; d4 < (GR + 3) / 4; ++d4) {
+          if (4 * d4 < rho) {
+            const float4 c4 = cj[d4];
+            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (4 * d4 + e < GR && 4 * d4 + e < rho) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const float t = x[h][4 * d4 + e] - cc[e];
+                  d2[h] = fmaf(t, t, d2[h]);
+                }
+              }
           }
-        if (d2 < best) {  // strict: first index wins ties (np.argmin)
-          best = d2;
-          arg = j;
         }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (d2[h] < best[h]) {  // strict: first index wins ties (np.argmin)
+            best[h] = d2[h];
+            arg[h] = j;
+          }
       }
-      if (valid) {
-        near_sum += (double)best;
-        const int old = a.labels[i];
-        if (it == 0 || old != arg) changed += 1.0;
-        a.labels[i] = arg;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long i = base + 32 * h + lane;
+        if (valid[h]) {
+          near_sum += (double)best[h];
+          const int old = a.labels[i];
+          if (it == 0 || old != arg[h]) changed += 1.0;
+          a.labels[i] = arg[h];
+        }
+        warp_accumulate_fx<GR>(x[h], rho, arg[h], valid[h], scale, myacc, mycnt);
       }
-      warp_accumulate<GR>(x, rho, arg, valid, my);
     }
     near_sum = warp_sum(near_sum);
     changed = warp_sum(changed);
@@ -283,47 +339,50 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       extra[1][w] = changed;
     }
     __syncthreads();
-    double* out = a.part + (size_t)b * S;
-    for (int k = threadIdx.x; k < slots; k += blockDim.x) {
-      double s = 0.0;
-      for (int q = 0; q < nw; ++q) s += wacc[(size_t)q * slots + k];
-      out[k] = s;
+    // block totals -> global exact integer accumulators (order-independent)
+    for (int k = threadIdx.x; k < msl; k += blockDim.x) {
+      unsigned long long t = 0;
+      for (int q = 0; q < nw; ++q) t += wacc[(size_t)q * msl + k];
+      if (t) atomicAdd(G + k, t);
     }
+    for (int k = threadIdx.x; k < m0; k += blockDim.x) {
+      unsigned long long t = 0;
+      for (int q = 0; q < nw; ++q) t += wcnt[(size_t)q * m0 + k];
+      if (t) atomicAdd(G + msl + k, t);
+    }
+    double* P = a.part + (size_t)par * nb * 2;
     if (threadIdx.x == 0) {
       double e = 0.0, c = 0.0;
       for (int q = 0; q < nw; ++q) {
         e += extra[0][q];
         c += extra[1][q];
       }
-      out[slots] = e;
-      out[slots + 1] = c;
+      P[2 * b] = e;
+      P[2 * b + 1] = c;
     }
     grid.sync();
-    // cross-block reduction: one warp per slot, lanes stride over the blocks,
-    // fixed butterfly -> deterministic; latency ~ nb/32 loads instead of nb
+    // every block: totals into shared memory, objective/changed in fixed block order
+    for (int k = threadIdx.x; k < msl; k += blockDim.x)
+      tsh[k] = (double)(long long)__ldcg(G + k) * inv_scale;
+    for (int k = threadIdx.x; k < m0; k += blockDim.x) tsh[msl + k] = (double)__ldcg(G + msl + k);
     {
-      const int gw = (b * (int)blockDim.x + (int)threadIdx.x) >> 5;
-      const int nwarps = (nb * (int)blockDim.x) >> 5;
-      for (int k = gw; k < S; k += nwarps) {
-        double s0 = 0.0, s1 = 0.0;
-        int q = lane;
-        for (; q + 32 < nb; q += 64) {
-          s0 += __ldcg(a.part + (size_t)q * S + k);
-          s1 += __ldcg(a.part + (size_t)(q + 32) * S + k);
-        }
-        if (q < nb) s0 += __ldcg(a.part + (size_t)q * S + k);
-        const double t = warp_sum(s0 + s1);
-        if (lane == 0) a.tot[k] = t;
+      double e = 0.0, c = 0.0;
+      for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+        e += __ldcg(P + 2 * q);
+        c += __ldcg(P + 2 * q + 1);
       }
+      e = block_sum(e, sh);
+      if (threadIdx.x == 0) misc[0] = e;
+      c = block_sum(c, sh);
+      if (threadIdx.x == 0) misc[1] = c;
     }
-    grid.sync();
-    // every block pulls the totals into shared memory once
-    double* tsh = wacc;  // reuse: the per-warp accumulators are rebuilt next iteration
-    for (int k = threadIdx.x; k < S; k += blockDim.x) tsh[k] = __ldcg(a.tot + k);
+    // the other parity's accumulators are free until after the next barrier
+    if (b == 0)
+      for (int k = threadIdx.x; k < gstride; k += blockDim.x) a.gacc[(size_t)(par ^ 1) * gstride + k] = 0ull;
     __syncthreads();
-    const double chg = tsh[slots + 1];
+    const double chg = misc[1];
     if (b == 0 && threadIdx.x == 0) {
-      a.errors[it] = tsh[slots];
+      a.errors[it] = misc[0];
       a.st->iters = it + 1;
       a.st->changed = (long long)chg;
     }
@@ -331,17 +390,17 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       if (b == 0 && threadIdx.x == 0) a.st->converged = 1;
       break;  // uniform: every block read the same total
     }
-    for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) {
+    for (int k = threadIdx.x; k < msl; k += blockDim.x) {
       Cp[k] = Cd[k];
-      const int j = k / rho, d = k - j * rho;
-      const double cnt = tsh[j * (rho + 1) + rho];
-      if (cnt > 0.0) Cd[k] = tsh[j * (rho + 1) + d] / cnt;
+      const int j = k / rho;
+      const double cnt = tsh[msl + j];
+      if (cnt > 0.0) Cd[k] = tsh[k] / cnt;
     }
     __syncthreads();
     // empty clusters, ascending j: farthest remaining point from its old centroid
     int nex = 0;
     for (int j = 0; j < m0; ++j) {
-      if (tsh[j * (rho + 1) + rho] > 0.0) continue;
+      if (tsh[msl + j] > 0.0) continue;
       double bv = -INFINITY;
       long long bi = a.m;
       for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
@@ -402,10 +461,10 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       ++nex;
       __syncthreads();
     }
-    __syncthreads();  // tsh aliases wacc: nobody may still read the totals when it is re-zeroed
+    __syncthreads();
   }
   if (b == 0)
-    for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) a.C[k] = Cd[k];
+    for (int k = threadIdx.x; k < msl; k += blockDim.x) a.C[k] = Cd[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -458,11 +517,13 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   NYS_CUDA_TRY(cudaGetDevice(&dev));
   NYS_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return NYS_EUNSUPPORTED;
-  const int slots = m0 * (rho + 1);
-  const size_t fixed = (size_t)m0 * rho * 8 * 2 + (size_t)m0 * 8 + (size_t)m0 * rho * 4 + 64;
+  const int msl = m0 * rho;
+  const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
+                       (size_t)m0 * ((rho + 3) & ~3) * 4 + 96;
+  auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed; };
   int nw = 8;
-  while (nw > 1 && (size_t)std::max(nw * slots, L.S) * 8 + fixed > 200 * 1024) --nw;
-  const size_t smem = (size_t)std::max(nw * slots, L.S) * 8 + fixed;
+  while (nw > 1 && need(nw) > 200 * 1024) --nw;
+  const size_t smem = need(nw);
   if (smem > 220 * 1024) return NYS_EUNSUPPORTED;
   LloydArgs a;
   a.pts = pts;
@@ -474,12 +535,16 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   a.S = L.S;
   a.C = C;
   a.labels = reinterpret_cast<int*>(ws + L.off_labels);
+  a.gacc = reinterpret_cast<unsigned long long*>(ws + L.off_tot);
   a.part = reinterpret_cast<double*>(ws + L.off_part);
-  a.tot = reinterpret_cast<double*>(ws + L.off_tot);
   a.arg = reinterpret_cast<double*>(ws + L.off_arg);
   a.errors = errors;
   a.st = reinterpret_cast<KState*>(ws + L.off_state);
+  a.maxabs_bits = reinterpret_cast<unsigned*>(ws + L.off_idx);
   a.nw = nw;
+  // the exact accumulators start at zero (both parities) and max|x| at +0
+  NYS_CUDA_TRY(cudaMemsetAsync(a.gacc, 0, (size_t)2 * (msl + m0) * 8, s));
+  NYS_CUDA_TRY(cudaMemsetAsync(a.maxabs_bits, 0, sizeof(unsigned), s));
   void* args[] = {&a};
   auto go = [&](auto kern) -> int {
     int per_sm = 0;
@@ -487,7 +552,7 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     NYS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
     if (per_sm < 1) return NYS_EUNSUPPORTED;
     const int nb = (int)std::max<long long>(
-        1, std::min<long long>({(long long)per_sm * sms(), (long long)L.nb_coop, ceil_div(m, (long long)nw * 32)}));
+        1, std::min<long long>({(long long)per_sm * sms(), (long long)L.nb_coop, ceil_div(m, (long long)nw * 64)}));
     count_launch();
     NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(nw * 32), args, smem, s));
     return NYS_OK;

@@ -49,7 +49,7 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.off_labels = o;  o = align256(o + (size_t)m * 4);
   L.off_part = o;    o = align256(o + (size_t)std::max(L.nb_assign, L.nb_coop) * L.S * 8);
   L.off_ppart = o;   o = align256(o + (size_t)std::max(L.nb_seed, L.nb_coop) * 8);
-  L.off_tot = o;     o = align256(o + (size_t)L.S * 8);
+  L.off_tot = o;     o = align256(o + (size_t)std::max(L.S, 2 * (m0 * rho + m0)) * 8);
   L.off_cf = o;      o = align256(o + (size_t)m0 * rho * 4);
   L.off_cprev = o;   o = align256(o + (size_t)m0 * rho * 8);
   L.off_excl = o;    o = align256(o + (size_t)m0 * 8);
@@ -91,6 +91,40 @@ __device__ __forceinline__ double d2_exact(const float* __restrict__ pts, long l
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
   for (; d < rho; ++d) res = __dadd_rn(res, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
   return res;
+}
+
+// exact FP64 |x - c|^2 in numpy's pairwise order for a compile-time bound GR >= rho
+template <int GR>
+__device__ __forceinline__ double d2_exact_regs(const float (&x)[GR], int rho, const double* __restrict__ c) {
+  if (GR <= 8 || rho < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int d = 0; d < (GR < 8 ? GR : 8); ++d)
+      if (d < rho) r = __dadd_rn(r, sqdiff((double)x[d], c[d]));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = sqdiff((double)x[k], c[k]);
+  const int full = rho - (rho % 8);
+#pragma unroll
+  for (int d = 8; d < GR; d += 8)
+    if (d < full) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], sqdiff((double)x[d + k], c[d + k]));
+    }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+  for (int d = 0; d < GR; ++d)
+    if (d >= full && d < rho) res = __dadd_rn(res, sqdiff((double)x[d], c[d]));
+  return res;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
 // fixed-shape block sum (blockDim multiple of 32, <= 1024)

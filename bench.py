@@ -233,6 +233,7 @@ def run_ours(args, rank: int, world: int):
         "e2e": {"value": round(px / (e2e * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_step": round(e2e, 3),
                 "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": out_bytes,
                 "path": "fast_filter(Image(pinned host float32)) -> pinned host output"},
+        "step_ms": [round(x, 3) for x in step_ms],
         "gpu_launches": launches // max(1, args.steps),
         "gpu_launches_total": launches,
         "roofline": roof,

@@ -341,12 +341,13 @@ __global__ void __launch_bounds__(1024) k_repair(const float* __restrict__ pts, 
 
 // final exact assignment (landmarks.py:121-129): FP64 differenced distances in
 // numpy's summation order; the point is loaded once into registers
-template <int GR>
+template <int GR, int RX>
 __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, long long ps, long long m, int rho,
                                                const double* __restrict__ C, int m0, long long* __restrict__ asg,
                                                double* __restrict__ part) {
   extern __shared__ __align__(16) double csm[];
   __shared__ double sh[32];
+  if (RX > 0) rho = RX;  // compile-time rho for the common small dimensions
   for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) csm[k] = C[k];
   __syncthreads();
   const long long chunk = ceil_div(m, (long long)gridDim.x);
@@ -382,10 +383,16 @@ static int launch_exact(const float* pts, long long ps, long long m, int rho, co
     NYS_LAUNCH_CHECK();
     return NYS_OK;
   };
-  if (rho <= 4) return go(k_exact<4>);
-  if (rho <= 16) return go(k_exact<16>);
-  if (rho <= 32) return go(k_exact<32>);
-  return go(k_exact<64>);
+  switch (rho) {
+    case 1: return go(k_exact<4, 1>);
+    case 2: return go(k_exact<4, 2>);
+    case 3: return go(k_exact<4, 3>);
+    case 4: return go(k_exact<4, 4>);
+    default: break;
+  }
+  if (rho <= 16) return go(k_exact<16, 0>);
+  if (rho <= 32) return go(k_exact<32, 0>);
+  return go(k_exact<64, 0>);
 }
 
 __global__ void k_sum_parts(const double* __restrict__ part, int nb, double* __restrict__ out) {

@@ -33,6 +33,7 @@ struct SeedArgs {
   double* ppart;
   KState* st;
   int d2_in_smem;
+  int* flag;  // last published draw (owner block -> everyone)
 };
 
 // owner search over vals[0..n) for the first index whose running sum exceeds
@@ -104,7 +105,7 @@ __device__ long long scan_find(const double* vals, long long n, double target, d
   return r;
 }
 
-template <int GR>
+template <int GR, int RX>
 __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double d2s[];  // this block's chunk of D^2 when it fits
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
   __shared__ int shi[2];
   __shared__ long long sel[1];
   __shared__ double tot_sh;
-  const int nb = gridDim.x, b = blockIdx.x, rho = a.rho;
+  const int nb = gridDim.x, b = blockIdx.x, rho = RX > 0 ? RX : a.rho;  // RX: compile-time rho
   const long long chunk = ceil_div(a.m, (long long)nb);
   const long long lo = min(a.m, b * chunk), hi = min(a.m, lo + chunk);
   const int len = (int)(hi - lo);
@@ -176,8 +177,17 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
       const long long idx = sel[0];
       if ((int)threadIdx.x < rho) a.C[(size_t)j * rho + threadIdx.x] = (double)__ldg(a.pts + threadIdx.x * a.ps + idx);
       if (threadIdx.x == 0 && a.seeds) a.seeds[j] = idx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(a.flag, j);  // publish centroid j (cheaper than a second grid barrier)
+      }
     }
-    grid.sync();
+    if (threadIdx.x == 0) {
+      while (atomicAdd(a.flag, 0) < j) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
   }
 }
 
@@ -232,12 +242,12 @@ __device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho
   }
 }
 
-template <int GR>
+template <int GR, int RX>
 __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double dsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int rho = a.rho, m0 = a.m0, msl = m0 * rho, gstride = msl + m0;
+  const int rho = RX > 0 ? RX : a.rho, m0 = a.m0, msl = m0 * rho, gstride = msl + m0;  // RX: compile-time rho
   unsigned long long* wacc = reinterpret_cast<unsigned long long*>(dsm);      // nw x msl (per-warp sums)
   unsigned* wcnt = reinterpret_cast<unsigned*>(wacc + (size_t)nw * msl);       // nw x m0 (per-warp counts)
   double* Cd = reinterpret_cast<double*>(wcnt + (((size_t)nw * m0 + 1) & ~size_t(1)));  // m0*rho current (FP64)
@@ -489,6 +499,8 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
   a.d2 = reinterpret_cast<double*>(ws + L.off_d2);
   a.ppart = reinterpret_cast<double*>(ws + L.off_ppart);
   a.st = reinterpret_cast<KState*>(ws + L.off_state);
+  a.flag = reinterpret_cast<int*>(ws + L.off_idx + 32);
+  NYS_CUDA_TRY(cudaMemsetAsync(a.flag, 0, sizeof(int), s));
   void* args[] = {&a};
   auto go = [&](auto kern) -> int {
     // one block per SM; the block's D^2 chunk lives in shared memory when it fits
@@ -505,10 +517,16 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
     NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(512), args, smem, s));
     return NYS_OK;
   };
-  if (rho <= 4) return go(k_seed_coop<4>);
-  if (rho <= 16) return go(k_seed_coop<16>);
-  if (rho <= 32) return go(k_seed_coop<32>);
-  return go(k_seed_coop<64>);
+  switch (rho) {
+    case 1: return go(k_seed_coop<4, 1>);
+    case 2: return go(k_seed_coop<4, 2>);
+    case 3: return go(k_seed_coop<4, 3>);
+    case 4: return go(k_seed_coop<4, 4>);
+    default: break;
+  }
+  if (rho <= 16) return go(k_seed_coop<16, 0>);
+  if (rho <= 32) return go(k_seed_coop<32, 0>);
+  return go(k_seed_coop<64, 0>);
 }
 
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
@@ -557,10 +575,16 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(nw * 32), args, smem, s));
     return NYS_OK;
   };
-  if (rho <= 4) return go(k_lloyd_coop<4>);
-  if (rho <= 16) return go(k_lloyd_coop<16>);
-  if (rho <= 32) return go(k_lloyd_coop<32>);
-  return go(k_lloyd_coop<64>);
+  switch (rho) {
+    case 1: return go(k_lloyd_coop<4, 1>);
+    case 2: return go(k_lloyd_coop<4, 2>);
+    case 3: return go(k_lloyd_coop<4, 3>);
+    case 4: return go(k_lloyd_coop<4, 4>);
+    default: break;
+  }
+  if (rho <= 16) return go(k_lloyd_coop<16, 0>);
+  if (rho <= 32) return go(k_lloyd_coop<32, 0>);
+  return go(k_lloyd_coop<64, 0>);
 }
 
 }  // namespace nys

@@ -124,15 +124,16 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
     if ((int)threadIdx.x < rho) cs[threadIdx.x] = __ldcg(a.C + (size_t)(j - 1) * rho + threadIdx.x);
     __syncthreads();
     double s = 0.0;
+    constexpr int U = GR <= 4 ? 4 : 1;  // independent points in flight (register budget)
     int i = threadIdx.x;
-    for (; i + 3 * B < len; i += 4 * B) {  // 4 independent points in flight
-      float x[4][GR];
+    for (; i + (U - 1) * B < len; i += U * B) {
+      float x[U][GR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int d = 0; d < GR; ++d) x[u][d] = d < rho ? __ldg(a.pts + d * a.ps + lo + i + u * B) : 0.f;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const double v = d2_exact_regs<GR>(x[u], rho, cs);
         const double nv = j == 1 ? v : fmin(d2[i + u * B], v);
         d2[i + u * B] = nv;
@@ -214,14 +215,6 @@ template <int GR>
 __device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho, int label, bool valid, double scale,
                                                    unsigned long long* acc, unsigned* cnt) {
   const int lane = threadIdx.x & 31;
-  unsigned lim[GR][3];
-#pragma unroll
-  for (int d = 0; d < GR; ++d) {
-    const unsigned long long v = (unsigned long long)__double2ll_rn((double)x[d] * scale);
-    lim[d][0] = (unsigned)(v & 0x1FFFFFull);
-    lim[d][1] = (unsigned)((v >> 21) & 0x1FFFFFull);
-    lim[d][2] = (unsigned)(v >> 42);
-  }
   unsigned rem = __ballot_sync(0xffffffffu, valid);
   while (rem) {
     const int leader = __ffs(rem) - 1;
@@ -231,9 +224,10 @@ __device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho
 #pragma unroll
       for (int d = 0; d < GR; ++d)
         if (d < rho) {
-          const unsigned long long s0 = __reduce_add_sync(grp, lim[d][0]);
-          const unsigned long long s1 = __reduce_add_sync(grp, lim[d][1]);
-          const unsigned long long s2 = __reduce_add_sync(grp, lim[d][2]);
+          const unsigned long long v = (unsigned long long)__double2ll_rn((double)x[d] * scale);
+          const unsigned long long s0 = __reduce_add_sync(grp, (unsigned)(v & 0x1FFFFFull));
+          const unsigned long long s1 = __reduce_add_sync(grp, (unsigned)((v >> 21) & 0x1FFFFFull));
+          const unsigned long long s2 = __reduce_add_sync(grp, (unsigned)(v >> 42));
           if (lane == leader) acc[L * rho + d] += s0 + (s1 << 21) + (s2 << 42);
         }
       if (lane == leader) cnt[L] += __popc(grp);
@@ -291,14 +285,17 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     unsigned long long* myacc = wacc + (size_t)w * msl;
     unsigned* mycnt = wcnt + (size_t)w * m0;
     double near_sum = 0.0, changed = 0.0;
-    // two 32-pixel tiles per warp step: every centroid LDS serves two points
-    for (long long base = lo + (long long)w * 64; base < hi; base += (long long)nw * 64) {
-      float x[2][GR];
-      float best[2] = {INFINITY, INFINITY};
-      int arg[2] = {0, 0};
-      bool valid[2];
+    // HH 32-pixel tiles per warp step: every centroid LDS serves HH points
+    constexpr int HH = GR <= 4 ? 2 : 1;
+    for (long long base = lo + (long long)w * 32 * HH; base < hi; base += (long long)nw * 32 * HH) {
+      float x[HH][GR];
+      float best[HH];
+      int arg[HH];
+      bool valid[HH];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < HH; ++h) {
+        best[h] = INFINITY;
+        arg[h] = 0;
         const long long i = base + 32 * h + lane;
         valid[h] = i < hi;
 #pragma unroll
@@ -306,7 +303,9 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       }
       for (int j = 0; j < m0; ++j) {
         const float4* cj = reinterpret_cast<const float4*>(Cf + (size_t)j * rhop);
-        float d2[2] = {0.f, 0.f};
+        float d2[HH];
+#pragma unroll
+        for (int h = 0; h < HH; ++h) d2[h] = 0.f;
 #pragma unroll
         for (int d4 = 0; d4 < (GR + 3) / 4; ++d4) {
           if (4 * d4 < rho) {
@@ -316,7 +315,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
             for (int e = 0; e < 4; ++e)
               if (4 * d4 + e < GR && 4 * d4 + e < rho) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < HH; ++h) {
                   const float t = x[h][4 * d4 + e] - cc[e];
                   d2[h] = fmaf(t, t, d2[h]);
                 }
@@ -324,14 +323,14 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
           }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < HH; ++h)
           if (d2[h] < best[h]) {  // strict: first index wins ties (np.argmin)
             best[h] = d2[h];
             arg[h] = j;
           }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < HH; ++h) {
         const long long i = base + 32 * h + lane;
         if (valid[h]) {
           near_sum += (double)best[h];

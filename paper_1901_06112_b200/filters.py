@@ -39,6 +39,7 @@ DENOMINATOR_EPS_SCALE = 1e-12
 # default cap on the horizontal-pass plane buffer (bytes); bands are planned
 # so that one band's planes fit (bands.plan_bands)
 PLANE_BUDGET_BYTES = 64 << 30
+SMALL_PLANES_BYTES = 8 << 30
 
 
 @dataclass(frozen=True)
@@ -232,7 +233,12 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
         timer.mark("extrapolation")
     rs = -(-W // 32) * 32 * (d.m0 + 1) * (n + 1)   # plane-buffer row stride: [row][x/32][plane][32]
     row_bytes = rs * 4
-    budget = plane_budget if plane_budget is not None else _plane_budget()
+    if plane_budget is not None:
+        budget = plane_budget
+    elif (H + 2 * d.radius) * row_bytes <= SMALL_PLANES_BYTES:
+        budget = SMALL_PLANES_BYTES  # single band; skip the (synchronising) free-memory query
+    else:
+        budget = _plane_budget()
     bands = plan_bands(H, d.radius, row_bytes, budget)
     max_rows = max(b.hp_rows for b in bands)
     planes = torch.empty((max_rows, rs), dtype=torch.float32, device=inp.f.device)

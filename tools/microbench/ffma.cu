@@ -62,6 +62,21 @@ __global__ void k_f32x2(float* out, float a0, float b0, int iters) {
   if (s == 12345.f) out[threadIdx.x] = s;
 }
 
+template <int NACC>
+__global__ void k_dfma(double* out, double a0, double b0, int iters) {
+  double acc[NACC], x[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) { acc[k] = threadIdx.x * 1e-3 + k; x[k] = a0 + k * 1e-4; }
+  double b = b0 + threadIdx.x * 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = fma(x[k], b, acc[k]);
+    b = b * 0.9999;
+  }
+  double s = 0; for (int k = 0; k < NACC; ++k) s += acc[k];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
 int main() {
   int dev = 0; cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
@@ -82,6 +97,8 @@ int main() {
   run("reg3", [&] { k_reg3<16><<<blocks, threads>>>(out, 1.f, 0.5f, iters); }, 16.0 * iters);
   run("const", [&] { k_const<16><<<blocks, threads>>>(out, 1.f, iters / 16); }, 16.0 * 16 * (iters / 16));
   run("f32x2", [&] { k_f32x2<16><<<blocks, threads>>>(out, 1.f, 0.5f, iters); }, 16.0 * iters);
+  double* dout; cudaMalloc(&dout, 4096 * 8);
+  run("dfma", [&] { k_dfma<16><<<blocks, threads>>>(dout, 1.0, 0.5, iters); }, 16.0 * iters);
   cudaError_t err = cudaGetLastError(); printf("err=%s\n", cudaGetErrorString(err));
   return 0;
 }

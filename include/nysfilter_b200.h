@@ -159,6 +159,11 @@ typedef struct nys_filter_desc {
     const double* u0;        /* [host] m0 */
     double alpha0;
     double eps_den;          /* 1e-12 * (2S+1)^2 * max|alpha| (filters.py:242) */
+    /* rows [row_lo, row_hi) of the image are present in the f / guide buffers
+     * (base pointers still address image row 0); row_hi == 0 means all H rows.
+     * Used by the row-band-sharded multi-GPU path, whose ranks hold their rows
+     * plus R (+1) halo rows; reads never leave this range. */
+    int row_lo, row_hi;
 } nys_filter_desc;
 
 /* Size of the horizontal-pass plane buffer for a band of `rows` output rows:

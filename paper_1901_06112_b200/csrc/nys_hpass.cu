@@ -43,6 +43,7 @@ struct HArgs {
   long long fps, gps, rs;  // rs: plane-buffer row stride (floats)
   int n, rho, rhop, H, W, m0, m0q, R, box, gkind;
   int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
+  int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;
   float taps[NYS_MAX_TAPS];
@@ -166,14 +167,14 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
     for (int k = threadIdx.x; k < RPT * n * ncol4; k += blockDim.x) {
       const int r = k / (n * ncol4), rem = k - r * (n * ncol4);
       const int c = rem / ncol4, s = rem - c * ncol4;
-      const int row = clampi(vb + r, 0, H - 1);
+      const int row = clampi(clampi(vb + r, 0, H - 1), a.rlo, a.rhi - 1);
       const int x = clampi(x0 - R + s, 0, W - 1);
       Fs[((size_t)r * n + c) * pitch + s] = __ldg(a.f + (long long)c * a.fps + (long long)row * W + x);
     }
     // b_j(x) for every column of the tile incl. the 2R halo (difference-form distances)
     for (int k = threadIdx.x; k < ((a.dbg & 1) ? 0 : RPT * ncol4); k += blockDim.x) {
       const int r = k / ncol4, s = k - r * ncol4;
-      const int row = clampi(vb + r, 0, H - 1);
+      const int row = clampi(clampi(vb + r, 0, H - 1), a.rlo, a.rhi - 1);
       const int x = clampi(x0 - R + s, 0, W - 1);
       float gv[GR];
 #pragma unroll
@@ -304,6 +305,8 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.gkind = d->guide_kind;
   a.v0 = out0 - d->radius;
   a.vrows = out_rows + 2 * d->radius;
+  a.rlo = std::max(0, d->row_lo);
+  a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);
   if (const char* e = getenv("NYS_DBG_K2")) a.dbg = atoi(e);

@@ -390,6 +390,12 @@ static int launch_exact(const float* pts, long long ps, long long m, int rho, co
     case 4: return go(k_exact<4, 4>);
     default: break;
   }
+  switch (rho) {  // exact compile-time dimensions of the BASELINE guides
+    case 16: return go(k_exact<16, 16>);
+    case 27: return go(k_exact<32, 27>);
+    case 31: return go(k_exact<32, 31>);
+    default: break;
+  }
   if (rho <= 16) return go(k_exact<16, 0>);
   if (rho <= 32) return go(k_exact<32, 0>);
   return go(k_exact<64, 0>);

@@ -260,8 +260,18 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   // fixed-point scale 2^s with |sum| < 2^61 for any cluster: s = 61 - log2(max|x| * m)
   {
     float mx = 0.f;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
-      for (int d = 0; d < rho; ++d) mx = fmaxf(mx, fabsf(__ldg(a.pts + d * a.ps + i)));
+    if (a.ps == a.m && (reinterpret_cast<uintptr_t>(a.pts) & 15) == 0 && (a.m & 3) == 0) {
+      // contiguous planes: one flat float4 sweep over rho*m values
+      const long long n4 = (long long)rho * a.m / 4;
+      const float4* p4 = reinterpret_cast<const float4*>(a.pts);
+      for (long long q = (long long)b * blockDim.x + threadIdx.x; q < n4; q += (long long)nb * blockDim.x) {
+        const float4 v = __ldg(p4 + q);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+    } else {
+      for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+        for (int d = 0; d < rho; ++d) mx = fmaxf(mx, fabsf(__ldg(a.pts + d * a.ps + i)));
+    }
     mx = warp_max(mx);
     if (lane == 0 && mx > 0.f) atomicMax(a.maxabs_bits, __float_as_uint(mx));
   }
@@ -523,6 +533,12 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
     case 4: return go(k_seed_coop<4, 4>);
     default: break;
   }
+  switch (rho) {  // exact compile-time dimensions of the BASELINE guides
+    case 16: return go(k_seed_coop<16, 16>);
+    case 27: return go(k_seed_coop<32, 27>);
+    case 31: return go(k_seed_coop<32, 31>);
+    default: break;
+  }
   if (rho <= 16) return go(k_seed_coop<16, 0>);
   if (rho <= 32) return go(k_seed_coop<32, 0>);
   return go(k_seed_coop<64, 0>);
@@ -579,6 +595,12 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     case 2: return go(k_lloyd_coop<4, 2>);
     case 3: return go(k_lloyd_coop<4, 3>);
     case 4: return go(k_lloyd_coop<4, 4>);
+    default: break;
+  }
+  switch (rho) {  // exact compile-time dimensions of the BASELINE guides
+    case 16: return go(k_lloyd_coop<16, 16>);
+    case 27: return go(k_lloyd_coop<32, 27>);
+    case 31: return go(k_lloyd_coop<32, 31>);
     default: break;
   }
   if (rho <= 16) return go(k_lloyd_coop<16, 0>);

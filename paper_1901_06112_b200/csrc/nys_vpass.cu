@@ -40,6 +40,7 @@ struct VArgs {
   long long fps, gps, ops;
   int n, rho, rhop, H, W, m0, R, box, gkind;
   int out0, out_rows, tiles_x, tiles_y, nchunks, u0_off, vec_out, gcache;
+  int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   float k2, inv_alpha0, eps_den;
   float taps[NYS_MAX_TAPS];
 };
@@ -214,13 +215,13 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
     if (gmode == 1) {
       for (int k = tid; k < rho * npx; k += blockDim.x) {
         const int d = k / npx, q = k - d * npx;
-        const int rr = min(t0 + (q >> 5), H - 1), cx = min(x0 + (q & 31), W - 1);
+        const int rr = clampi(min(t0 + (q >> 5), H - 1), a.rlo, a.rhi - 1), cx = min(x0 + (q & 31), W - 1);
         gsh[k] = __ldg(a.g + (long long)d * a.gps + (long long)rr * W + cx);
       }
     } else if (gmode == 2) {
       for (int k = tid; k < n * (TH + 2) * 34; k += blockDim.x) {
         const int c = k / ((TH + 2) * 34), q = k - c * ((TH + 2) * 34);
-        const int yy = clampi(min(t0 + q / 34 - 1, H - 1), 0, H - 1), xx = clampi(min(x0 + q % 34 - 1, W - 1), 0, W - 1);
+        const int yy = clampi(clampi(t0 + q / 34 - 1, 0, H - 1), a.rlo, a.rhi - 1), xx = clampi(x0 + q % 34 - 1, 0, W - 1);
         gsh[k] = __ldg(a.f + (long long)c * a.fps + (long long)yy * W + xx);
       }
     }
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
                 d2 = fmaf(t, t, d2);
               }
             } else {
-              const int rr = min(t0 + (k >> 5), H - 1);
+              const int rr = clampi(min(t0 + (k >> 5), H - 1), a.rlo, a.rhi - 1);
               const int cx = min(x0 + (k & 31), W - 1);
               for (int d = 0; d < rho; ++d) {
                 const float t = guide_at(a.g, a.gps, a.f, a.fps, a.gkind, d, rr, cx, H, W) - Cs[i * rhop + d];
@@ -483,6 +484,8 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.nchunks = nchunks;
   a.u0_off = (int)L.off_U0;
   a.vec_out = ((d->W & 3) == 0) && ((out_plane_stride & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  a.rlo = std::max(0, d->row_lo);
+  a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
   a.inv_alpha0 = (float)(1.0 / d->alpha0);
   a.eps_den = (float)d->eps_den;

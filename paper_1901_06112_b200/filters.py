@@ -212,16 +212,25 @@ def _prepare_inputs(f: Image, p) -> _Inputs:
 
 def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer: StageTimer | None = None,
                plane_budget: int | None = None, out: torch.Tensor | None = None,
-               kernel_events: list | None = None):
+               kernel_events: list | None = None, rows: tuple[int, int] | None = None, row_origin: int = 0,
+               H_global: int | None = None):
     """K2/K3 over row bands given landmarks; returns (out, plan, stats).
 
     ``kernel_events`` (optional list) receives (name, start, end) CUDA events
-    recorded on the launching stream around every K2/K3 launch."""
-    n, H, W = inp.f.shape
+    recorded on the launching stream around every K2/K3 launch.
+
+    Row sharding (parallel.py): ``inp.f``/``inp.guide`` hold image rows
+    [row_origin, row_origin + rows_local) of an image of ``H_global`` rows and
+    only output rows ``rows = (lo, hi)`` are produced (``out`` is then
+    (n, hi-lo, W)).  Kernel pointers are rebased so rows stay global."""
+    n, h_local, W = inp.f.shape
+    H = H_global if H_global is not None else h_local
+    lo, hi = rows if rows is not None else (0, H)
     S = params.spatial.effective_radius()
     plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S)
     keep: list = []
     d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
+    d.row_lo, d.row_hi = row_origin, row_origin + h_local
     lib = _native.lib()
     wsb = int(lib.nys_filter_workspace_bytes(C.byref(d)))
     if wsb == 0:
@@ -235,16 +244,24 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     row_bytes = rs * 4
     if plane_budget is not None:
         budget = plane_budget
-    elif (H + 2 * d.radius) * row_bytes <= SMALL_PLANES_BYTES:
+    elif (hi - lo + 2 * d.radius) * row_bytes <= SMALL_PLANES_BYTES:
         budget = SMALL_PLANES_BYTES  # single band; skip the (synchronising) free-memory query
     else:
         budget = _plane_budget()
-    bands = plan_bands(H, d.radius, row_bytes, budget)
+    bands = [Band(b.out0 + lo, b.out_rows, b.hp0 + lo, b.hp_rows)
+             for b in plan_bands(hi - lo, d.radius, row_bytes, budget)]
     max_rows = max(b.hp_rows for b in bands)
     planes = torch.empty((max_rows, rs), dtype=torch.float32, device=inp.f.device)
     hps = rs
     if out is None:
-        out = torch.empty((n, H, W), dtype=torch.float32, device=inp.f.device)
+        out = torch.empty((n, hi - lo, W), dtype=torch.float32, device=inp.f.device)
+    # rebased pointers: image row r of the inputs is local row r - row_origin,
+    # output row r is local row r - lo
+    f_ptr = ptr(inp.f) - row_origin * W * 4
+    g_ptr = ptr(inp.guide) - row_origin * W * 4
+    o_ptr = ptr(out) - lo * W * 4
+    f_ps = g_ps = h_local * W
+    o_ps = (hi - lo) * W
 
     def ev():
         e = torch.cuda.Event(enable_timing=True)
@@ -253,11 +270,11 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
 
     for b in bands:
         e0 = ev() if kernel_events is not None else None
-        _native.check(lib.nys_filter_hpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, b.out0, b.out_rows,
+        _native.check(lib.nys_filter_hpass(C.byref(d), f_ptr, f_ps, g_ptr, g_ps, b.out0, b.out_rows,
                                            ptr(planes), hps, ptr(ws), s), "nys_filter_hpass")
         e1 = ev() if kernel_events is not None else None
-        _native.check(lib.nys_filter_vpass(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W, ptr(planes), hps,
-                                           b.out0, b.out_rows, ptr(out), H * W, ptr(ws), s), "nys_filter_vpass")
+        _native.check(lib.nys_filter_vpass(C.byref(d), f_ptr, f_ps, g_ptr, g_ps, ptr(planes), hps,
+                                           b.out0, b.out_rows, o_ptr, o_ps, ptr(ws), s), "nys_filter_vpass")
         if kernel_events is not None:
             e2 = ev()
             kernel_events.append(("k_feat_hpass", e0, e1, b))

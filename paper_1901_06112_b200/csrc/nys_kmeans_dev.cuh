@@ -47,8 +47,10 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   size_t o = 0;
   L.off_d2 = o;      o = align256(o + (size_t)m * 8);
   L.off_labels = o;  o = align256(o + (size_t)m * 4);
-  L.off_part = o;    o = align256(o + (size_t)std::max(L.nb_assign, L.nb_coop) * L.S * 8);
+  // ppart before anything that depends on (rho, m0): the step-wise
+  // nys_kmeanspp_update / _pick pair must agree on it for any (rho, m0)
   L.off_ppart = o;   o = align256(o + (size_t)std::max(L.nb_seed, L.nb_coop) * 8);
+  L.off_part = o;    o = align256(o + (size_t)std::max(L.nb_assign, L.nb_coop) * L.S * 8);
   L.off_tot = o;     o = align256(o + (size_t)std::max(L.S, 2 * (m0 * rho + m0)) * 8);
   L.off_cf = o;      o = align256(o + (size_t)m0 * rho * 4);
   L.off_cprev = o;   o = align256(o + (size_t)m0 * rho * 8);

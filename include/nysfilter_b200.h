@@ -173,6 +173,11 @@ typedef struct nys_filter_desc {
  * vertical pass never clamps (replicate borders, spatial.py:85-88). */
 size_t nys_filter_planes_bytes(const nys_filter_desc* d, int rows);
 
+/* Floats per virtual row of the plane buffer ([row][x/32][plane][32]); pass
+ * it (or more) as planes_stride.  Includes the raw-feature planes K2 stores
+ * for K3 when the guide is high-dimensional (rho > 8) or the NLM patch guide. */
+int64_t nys_filter_plane_row_stride(const nys_filter_desc* d);
+
 /* Device bytes for the filter's constant block + reduction scratch. */
 size_t nys_filter_workspace_bytes(const nys_filter_desc* d);
 

@@ -61,6 +61,7 @@ _SIGS = {
     "nys_gather_point": (_I, [_P, _L, _I, _L, _P, _P]),
     "nys_filter_planes_bytes": (_S, [C.POINTER(FilterDesc), _I]),
     "nys_filter_workspace_bytes": (_S, [C.POINTER(FilterDesc)]),
+    "nys_filter_plane_row_stride": (_L, [C.POINTER(FilterDesc)]),
     "nys_filter_prepare": (_I, [C.POINTER(FilterDesc), _P, _S, _P]),
     "nys_filter_hpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
     "nys_filter_vpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),

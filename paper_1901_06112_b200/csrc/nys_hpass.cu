@@ -44,6 +44,7 @@ struct HArgs {
   int n, rho, rhop, H, W, m0, m0q, R, box, gkind;
   int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
+  int npl, bplanes;  // planes per buffer row block; store raw b_i planes after the filtered ones
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;
   float taps[NYS_MAX_TAPS];
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
         if (acc[0][0] == 1234.5f) a.hp[0] = acc[1][1];
         continue;
       }
-      float* dst0 = a.hp + (long long)(vb + r - a.v0) * a.rs + (long long)(xo >> 5) * (L * NC * 32) + (xo & 31);
+      float* dst0 = a.hp + (long long)(vb + r - a.v0) * a.rs + (long long)(xo >> 5) * (a.npl * 32) + (xo & 31);
 #pragma unroll
       for (int cc = 0; cc < K2_CC; ++cc) {
         const int c = ch * K2_CC + cc;
@@ -263,6 +264,20 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
             reinterpret_cast<float4*>(dst)[q4] =
                 make_float4(acc[cc][4 * q4], acc[cc][4 * q4 + 1], acc[cc][4 * q4 + 2], acc[cc][4 * q4 + 3]);
         }
+      }
+    }
+    if (a.bplanes) {
+      // raw b_i of the tile's output columns (K3 reads them at the centre pixel)
+      for (int it = threadIdx.x; it < RPT * m0 * XG; it += blockDim.x) {
+        const int i = it % m0, rest = it / m0, xg = rest % XG, r = rest / XG;
+        const int xo = x0 + xg * K2_XR;
+        if (xo >= W || vb + r >= a.v0 + a.vrows) continue;
+        const float* src = Bs + ((size_t)r * m0 + i) * pitch + R + xg * K2_XR;
+        float* dst = a.hp + (long long)(vb + r - a.v0) * a.rs + (long long)(xo >> 5) * (a.npl * 32) +
+                     (long long)(L * NC + i) * 32 + (xo & 31);
+#pragma unroll
+        for (int q4 = 0; q4 < K2_XR / 4; ++q4)
+          reinterpret_cast<float4*>(dst)[q4] = make_float4(src[4 * q4], src[4 * q4 + 1], src[4 * q4 + 2], src[4 * q4 + 3]);
       }
     }
   }
@@ -281,7 +296,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   if (st) return st;
   if (!f || !planes || !workspace || (d->guide_kind == 0 && !guide)) return NYS_EINVAL;
   if (out0 < 0 || out_rows < 1 || out0 + out_rows > d->H) return NYS_EINVAL;
-  if (planes_stride < plane_row_stride(d->W, (d->m0 + 1) * (d->n + 1)) || (planes_stride & 3)) return NYS_EINVAL;
+  if (planes_stride < plane_row_stride(d->W, buffer_planes(d)) || (planes_stride & 3)) return NYS_EINVAL;
   if (reinterpret_cast<uintptr_t>(planes) & 15) return NYS_EINVAL;
   const FilterLayout L = filter_layout(d);
   HArgs a;
@@ -306,6 +321,8 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.v0 = out0 - d->radius;
   a.vrows = out_rows + 2 * d->radius;
   a.rlo = std::max(0, d->row_lo);
+  a.npl = buffer_planes(d);
+  a.bplanes = use_bplanes(d);
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);

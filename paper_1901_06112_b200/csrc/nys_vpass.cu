@@ -143,7 +143,8 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
 
 template <int RT, int YR, int CPT>
 __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CUtensorMap tmap4,
-                                                     const __grid_constant__ CUtensorMap tmap1, const VArgs a) {
+                                                     const __grid_constant__ CUtensorMap tmap1,
+                                                     const __grid_constant__ CUtensorMap tmapb, const VArgs a) {
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x;
   const int grp = tid >> 6, run = (tid >> 3) & 7, quad = tid & 7;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
   // guide cache for the centre-pixel features: planar rho <= 8 -> [rho][npx];
   // 3x3 patch guide -> the f tile with a 1-pixel halo [n][TH+2][34]
   float* gsh = U0 + ((m0 + 3) & ~3);
-  const int gmode = a.gcache;  // 0: global loads, 1: planar cache, 2: patch cache
+  const int gmode = a.gcache;  // 0: global loads, 1: planar cache, 2: patch cache, 3: b planes from K2
   __shared__ __align__(8) unsigned long long full[K3_NS];
   __shared__ float red_min[K3_THREADS / 32];
   __shared__ unsigned long long red_cnt[K3_THREADS / 32];
@@ -196,7 +197,9 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
     const int i = s / nchunks, k = stage_chunk(s);
     const int buf = (int)(gs % K3_NS);
     const int nval = min(4, NC - 4 * k);
-    mbar_expect_tx(&full[buf], (unsigned)(nval * plane_floats * 4));
+    const bool with_b = gmode == 3 && i < m0 && k == 0;  // landmark i's raw b tile rides on its first chunk
+    mbar_expect_tx(&full[buf], (unsigned)(nval * plane_floats * 4 + (with_b ? npx * 4 : 0)));
+    if (with_b) tma_load_4d(bsh + (i & 1) * npx, &tmapb, 0, (m0 + 1) * NC + i, tx, ty * TH + R, &full[buf]);
     float* dst = stage + (size_t)buf * 4 * plane_floats;
     if (nval == 4) {
       tma_load_4d(dst, &tmap4, 0, i * NC + 4 * k, tx, ty * TH, &full[buf]);
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
     const int pxo = run * YR * 32 + quad * 4;  // this thread's first pixel in tile order (row-major, 32 wide)
     int s = 0;
     for (int i = 0; i <= m0; ++i) {
-      if (i < m0) {
+      if (i < m0 && gmode != 3) {
         // b_i at every tile pixel (and the lead projection s0 += u0_i b_i)
         float* bb = bsh + (i & 1) * npx;
         const float u0i = U0[i];
@@ -295,6 +298,19 @@ __global__ void __launch_bounds__(K3_THREADS) k_vpass(const __grid_constant__ CU
           const unsigned long long gs = gstage + s;
           const int buf = (int)(gs % K3_NS);
           mbar_wait(&full[buf], (unsigned)((gs / K3_NS) & 1));
+          if (gmode == 3 && i < m0 && kk == 0) {
+            const float u0i = U0[i];
+            const float* bb = bsh + (i & 1) * npx;
+            for (int q = tid; q < npx / 4; q += blockDim.x) {
+              const float4 b4 = *reinterpret_cast<const float4*>(bb + 4 * q);
+              float4 s4 = *reinterpret_cast<float4*>(ssh + 4 * q);
+              s4.x = fmaf(u0i, b4.x, s4.x);
+              s4.y = fmaf(u0i, b4.y, s4.y);
+              s4.z = fmaf(u0i, b4.z, s4.z);
+              s4.w = fmaf(u0i, b4.w, s4.w);
+              *reinterpret_cast<float4*>(ssh + 4 * q) = s4;
+            }
+          }
           const int k = stage_chunk(s);
           const int c = 4 * k + grp;
           float G[YR][4];
@@ -432,7 +448,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   if (!f || !planes || !out || !workspace || (d->guide_kind == 0 && !guide)) return NYS_EINVAL;
   if (out0 < 0 || out_rows < 1 || out0 + out_rows > d->H) return NYS_EINVAL;
   const int vrows = out_rows + 2 * d->radius;
-  if (planes_stride < plane_row_stride(d->W, (d->m0 + 1) * (d->n + 1)) || (planes_stride & 3)) return NYS_EINVAL;
+  if (planes_stride < plane_row_stride(d->W, buffer_planes(d)) || (planes_stride & 3)) return NYS_EINVAL;
   const FilterLayout L = filter_layout(d);
   const int NC = d->n + 1;
   const int nchunks = (int)ceil_div(NC, 4);
@@ -495,8 +511,8 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   // boxes of 32 x 4 x 1 x (TH+2R) and 32 x 1 x 1 x (TH+2R)
   auto enc = encode_fn();
   if (!enc) return NYS_EUNSUPPORTED;
-  const int P = (d->m0 + 1) * NC;
-  CUtensorMap tmap4, tmap1;
+  const int P = buffer_planes(d);
+  CUtensorMap tmap4, tmap1, tmapb;
   const cuuint64_t gdim[4] = {32, (cuuint64_t)P, (cuuint64_t)(wpad32(d->W) / 32), (cuuint64_t)vrows};
   const cuuint64_t gstr[3] = {32 * 4, (cuuint64_t)P * 32 * 4, (cuuint64_t)planes_stride * 4};
   const cuuint32_t box4[4] = {32, 4, 1, (cuuint32_t)(TH + 2 * R)};
@@ -509,9 +525,14 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return NYS_EINVAL;
+  const cuuint32_t boxb[4] = {32, 1, 1, (cuuint32_t)TH};  // centre rows only
+  if (enc(&tmapb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(planes), gdim, gstr, boxb, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return NYS_EINVAL;
 
   const int npx = TH * 32;
-  a.gcache = (d->guide_kind == 0 && d->rho <= 8) ? 1 : (d->guide_kind == 1 ? 2 : 0);
+  a.gcache = use_bplanes(d) ? 3 : 1;  // b planes from K2, or a planar guide tile (rho <= 8)
   const size_t gfloats = a.gcache == 1 ? (size_t)d->rho * npx : (a.gcache == 2 ? (size_t)d->n * (TH + 2) * 34 : 0);
   const size_t smem = ((size_t)K3_NS * 4 * (TH + 2 * R) * 32 + 5 * (size_t)npx + (size_t)d->m0 * L.rhop +
                        ((d->m0 + 3) & ~3) + gfloats) *
@@ -523,7 +544,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();
-    kern<<<grid, K3_THREADS, smem, s>>>(tmap4, tmap1, a);
+    kern<<<grid, K3_THREADS, smem, s>>>(tmap4, tmap1, tmapb, a);
     NYS_LAUNCH_CHECK();
     return NYS_OK;
   };

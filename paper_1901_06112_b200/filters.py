@@ -240,7 +240,7 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
     if timer:
         timer.mark("extrapolation")
-    rs = -(-W // 32) * 32 * (d.m0 + 1) * (n + 1)   # plane-buffer row stride: [row][x/32][plane][32]
+    rs = int(lib.nys_filter_plane_row_stride(C.byref(d)))   # [row][x/32][plane][32] (+ raw b planes)
     row_bytes = rs * 4
     if plane_budget is not None:
         budget = plane_budget

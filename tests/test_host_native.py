@@ -25,7 +25,7 @@ from paper_1901_06112_b200.nystrom import DegenerateKernelError, _retain, mixing
 
 def _declared_symbols():
     text = (ROOT / "include" / "nysfilter_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|uint64_t)\s+(nys_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|uint64_t|int64_t)\s+(nys_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
     if ((int)threadIdx.x < rho) cs[threadIdx.x] = __ldcg(a.C + (size_t)(j - 1) * rho + threadIdx.x);
     __syncthreads();
     double s = 0.0;
-    constexpr int U = GR <= 4 ? 4 : 1;  // independent points in flight (register budget)
+    constexpr int U = GR <= 4 ? 4 : 2;  // independent points in flight (register budget)
     int i = threadIdx.x;
     for (; i + (U - 1) * B < len; i += U * B) {
       float x[U][GR];
@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   long long* excl = reinterpret_cast<long long*>(tsh + gstride);              // m0
   float* Cf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(excl + m0) + 15) & ~uintptr_t(15));
   const int rhop = (rho + 3) & ~3;                                             // Cf rows: 16-byte aligned
+  const int m0p = (m0 + 3) & ~3;                                               // Cf rows padded to 4
   __shared__ double sh[64];
   __shared__ double extra[2][32];
   __shared__ double misc[2];
@@ -285,9 +286,9 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   for (int it = 0; it < a.max_iter; ++it) {
     const int par = it & 1;
     unsigned long long* G = a.gacc + (size_t)par * gstride;
-    for (int k = threadIdx.x; k < m0 * rhop; k += blockDim.x) {
+    for (int k = threadIdx.x; k < m0p * rhop; k += blockDim.x) {
       const int j = k / rhop, d = k - j * rhop;
-      Cf[k] = d < rho ? (float)Cd[j * rho + d] : 0.f;
+      Cf[k] = j >= m0 ? 3.0e38f : (d < rho ? (float)Cd[j * rho + d] : 0.f);  // padded rows never win
     }
     for (int k = threadIdx.x; k < nw * msl; k += blockDim.x) wacc[k] = 0ull;
     for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0u;
@@ -311,33 +312,47 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
 #pragma unroll
         for (int d = 0; d < GR; ++d) x[h][d] = (valid[h] && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
       }
-      for (int j = 0; j < m0; ++j) {
-        const float4* cj = reinterpret_cast<const float4*>(Cf + (size_t)j * rhop);
-        float d2[HH];
+      // JJ centroids per step: independent FMA chains for the long guides
+      constexpr int JJ = GR >= 16 ? 4 : 1;
+      for (int j0 = 0; j0 < m0; j0 += JJ) {
+        float d2[JJ][HH];
 #pragma unroll
-        for (int h = 0; h < HH; ++h) d2[h] = 0.f;
+        for (int jj = 0; jj < JJ; ++jj)
+#pragma unroll
+          for (int h = 0; h < HH; ++h) d2[jj][h] = 0.f;
 #pragma unroll
         for (int d4 = 0; d4 < (GR + 3) / 4; ++d4) {
           if (4 * d4 < rho) {
-            const float4 c4 = cj[d4];
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+            float cc[JJ][4];
+#pragma unroll
+            for (int jj = 0; jj < JJ; ++jj) {
+              const float4 c4 = reinterpret_cast<const float4*>(Cf + (size_t)(j0 + jj) * rhop)[d4];
+              cc[jj][0] = c4.x;
+              cc[jj][1] = c4.y;
+              cc[jj][2] = c4.z;
+              cc[jj][3] = c4.w;
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e)
               if (4 * d4 + e < GR && 4 * d4 + e < rho) {
 #pragma unroll
-                for (int h = 0; h < HH; ++h) {
-                  const float t = x[h][4 * d4 + e] - cc[e];
-                  d2[h] = fmaf(t, t, d2[h]);
-                }
+                for (int jj = 0; jj < JJ; ++jj)
+#pragma unroll
+                  for (int h = 0; h < HH; ++h) {
+                    const float t = x[h][4 * d4 + e] - cc[jj][e];
+                    d2[jj][h] = fmaf(t, t, d2[jj][h]);
+                  }
               }
           }
         }
 #pragma unroll
-        for (int h = 0; h < HH; ++h)
-          if (d2[h] < best[h]) {  // strict: first index wins ties (np.argmin)
-            best[h] = d2[h];
-            arg[h] = j;
-          }
+        for (int jj = 0; jj < JJ; ++jj)
+#pragma unroll
+          for (int h = 0; h < HH; ++h)
+            if (d2[jj][h] < best[h]) {  // strict, ascending j: first index wins ties (np.argmin)
+              best[h] = d2[jj][h];
+              arg[h] = j0 + jj;
+            }
       }
 #pragma unroll
       for (int h = 0; h < HH; ++h) {
@@ -552,7 +567,7 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   if (!coop) return NYS_EUNSUPPORTED;
   const int msl = m0 * rho;
   const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
-                       (size_t)m0 * ((rho + 3) & ~3) * 4 + 96;
+                       (size_t)((m0 + 3) & ~3) * ((rho + 3) & ~3) * 4 + 96;
   auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed; };
   int nw = 8;
   while (nw > 1 && need(nw) > 200 * 1024) --nw;

@@ -233,6 +233,11 @@ int nys_patch_guide(const float* f, int64_t f_plane_stride, int n, int H, int W,
  * pairs with values_out[j].  Returns the number of sweeps in *sweeps. */
 int nys_jacobi_eig(const double* a, int k, double* values_out, double* vectors_out, int* sweeps);
 
+/* Fast symmetric eigensolver used on the hot path (Householder tridiagonal +
+ * implicit QL): same eigenpairs as nys_jacobi_eig up to rounding, basis and
+ * signs; descending eigenvalues, eigenvectors as columns. */
+int nys_sym_eig(const double* a, int k, double* values_out, double* vectors_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,7 @@ _SIGS = {
     "nys_filter_stats": (_I, [C.POINTER(FilterDesc), _P, _P, _P]),
     "nys_patch_guide": (_I, [_P, _L, _I, _I, _I, _I, _P, _L, _P]),
     "nys_jacobi_eig": (_I, [_P, _I, _P, _P, C.POINTER(C.c_int)]),
+    "nys_sym_eig": (_I, [_P, _I, _P, _P]),
 }
 
 _lib = None

@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v" if verbose else "-O3", "-c", str(CSRC / src), "-o", str(obj)]
         else:
-            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-c", str(CSRC / src), "-o", str(obj)]
+            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-c", str(CSRC / src), "-o", str(obj)]
         cmds.append(cmd)
 
     def run(cmd):

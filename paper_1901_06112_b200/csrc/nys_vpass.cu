@@ -543,6 +543,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   cudaStream_t s = (cudaStream_t)stream;
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     count_launch();
     kern<<<grid, K3_THREADS, smem, s>>>(tmap4, tmap1, tmapb, a);
     NYS_LAUNCH_CHECK();

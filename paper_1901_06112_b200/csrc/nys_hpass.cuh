@@ -23,13 +23,15 @@ struct HArgs {
   int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   int npl, bplanes;  // planes per buffer row block; store raw b_i planes after the filtered ones
-  int ku, nu, tcols;  // tcgen05 path: K (m0 padded to 8), N ((m0+1) padded to 16), TMEM columns
+  int ku, nu, tcols, nbuf;  // tcgen05 path: K (m0 padded to 8), N ((m0+1) padded to 16), TMEM columns per group, y/f buffers
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;
   float taps[NYS_MAX_TAPS];
 };
 
-template <int RT>
+// FEXT: Fs holds a row per plane channel of every chunk (f_c, then 1 for the
+// y plane, then 0 padding), so a plane value is always one FMUL y * Fs[c]
+template <int RT, bool FEXT = false>
 __device__ __forceinline__ void hfir(const HArgs& a, const float* __restrict__ yrow,
                                      const float* __restrict__ Fs, int pitch, int xoff, int c0,
                                      float (&acc)[K2_CC][K2_XR]) {
@@ -39,14 +41,17 @@ __device__ __forceinline__ void hfir(const HArgs& a, const float* __restrict__ y
 #pragma unroll
   for (int cc = 0; cc < K2_CC; ++cc) {
     const int c = c0 + cc;
-    fr[cc] = Fs + (size_t)min(c, n - 1) * pitch + xoff;
-    mode[cc] = c < n ? 0 : (c == n ? 1 : 2);
+    fr[cc] = Fs + (size_t)(FEXT ? c : min(c, n - 1)) * pitch + xoff;
+    mode[cc] = FEXT ? 0 : (c < n ? 0 : (c == n ? 1 : 2));
   }
 #pragma unroll
   for (int cc = 0; cc < K2_CC; ++cc)
 #pragma unroll
     for (int o = 0; o < K2_XR; ++o) acc[cc][o] = 0.f;
-  auto plane_val = [&](int cc, float yv, float fv) { return mode[cc] == 0 ? yv * fv : (mode[cc] == 1 ? yv : 0.f); };
+  auto plane_val = [&](int cc, float yv, float fv) {
+    if constexpr (FEXT) return yv * fv;
+    return mode[cc] == 0 ? yv * fv : (mode[cc] == 1 ? yv : 0.f);
+  };
 
   if (a.box) {  // sliding (2R+1)-sum re-anchored per item (spatial.py:91-99)
     const int R = a.R;
@@ -109,6 +114,54 @@ __device__ __forceinline__ void hfir(const HArgs& a, const float* __restrict__ y
 #pragma unroll
         for (int cc = 0; cc < K2_CC; ++cc) acc[cc][o] = fmaf(w, plane_val(cc, yv, fr[cc][o + t]), acc[cc][o]);
       }
+    }
+  }
+}
+
+// One plane of a FIR item: acc[o] = sum_t taps[t] * y[o+t] * fr[o+t], o < K2_XR.
+// The caller loops over the item's planes without unrolling, which keeps the
+// unrolled body (~0.6k instructions for R = 15) inside the instruction cache.
+template <int RT>
+__device__ __forceinline__ void hfir_plane(const HArgs& a, const float* __restrict__ yrow,
+                                           const float* __restrict__ frow, float (&acc)[K2_XR]) {
+#pragma unroll
+  for (int o = 0; o < K2_XR; ++o) acc[o] = 0.f;
+  if constexpr (RT > 0) {
+    constexpr int T = 2 * RT + 1;
+    constexpr int NIN = K2_XR + 2 * RT;
+    constexpr int NQ = (NIN + 3) / 4;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float4 y4 = *reinterpret_cast<const float4*>(yrow + 4 * q);
+      const float4 f4 = *reinterpret_cast<const float4*>(frow + 4 * q);
+      const float v4[4] = {y4.x * f4.x, y4.y * f4.y, y4.z * f4.z, y4.w * f4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int s = 4 * q + e;
+        if (s < NIN) {
+#pragma unroll
+          for (int o = 0; o < K2_XR; ++o) {
+            const int t = s - o;
+            if (t >= 0 && t < T) acc[o] = fmaf(a.taps[t], v4[e], acc[o]);
+          }
+        }
+      }
+    }
+  } else if (a.box) {  // sliding (2R+1)-sum re-anchored per item (spatial.py:91-99)
+    const int R = a.R;
+    float sum = 0.f;
+    for (int t = 0; t <= 2 * R; ++t) sum += yrow[t] * frow[t];
+#pragma unroll
+    for (int o = 0; o < K2_XR; ++o) {
+      if (o > 0) sum += yrow[o + 2 * R] * frow[o + 2 * R] - yrow[o - 1] * frow[o - 1];
+      acc[o] = sum;
+    }
+  } else {
+    const int T = 2 * a.R + 1;
+    for (int t = 0; t < T; ++t) {
+      const float w = a.taps[t];
+#pragma unroll
+      for (int o = 0; o < K2_XR; ++o) acc[o] = fmaf(w, yrow[o + t] * frow[o + t], acc[o]);
     }
   }
 }

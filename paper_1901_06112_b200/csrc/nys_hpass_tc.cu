@@ -12,14 +12,19 @@
 //
 // One tile = one virtual row x TW output columns, i.e. TW + 2R <= 128 source
 // pixels = the 128 rows (TMEM lanes) of one UMMA M=128 tile:
-//   1. all 256 threads: pixel s = tid % 128 evaluates b_j for half of the
-//      landmarks and writes b_hi / b_lo into the K-major A operand (SMEM);
-//   2. one thread issues 3 x K/8 tcgen05.mma into TMEM and commits to an
-//      mbarrier; meanwhile the threads stage the tile's f rows;
-//   3. tcgen05.ld drains the accumulator (lane = pixel, column = i) into the
-//      y rows in SMEM (aliasing the dead A operand);
+//   1. features: pixel p (TMEM lane p) evaluates b_j for half of the
+//      landmarks and stores b_hi / b_lo into the A operand in TMEM (tcgen05.st);
+//   2. one thread issues 3 x K/8 tcgen05.mma (A from TMEM, B = M from SMEM)
+//      into the TMEM accumulator and commits to an mbarrier;
+//   3. epilogue: tcgen05.ld drains the accumulator (lane = pixel, column = i)
+//      into the y rows in SMEM, and the tile's f rows are staged;
 //   4. FIR items (4 planes x 16 columns) write the blocked plane buffer.
-// The B operand (M and u0, split hi/lo) is built once per persistent CTA.
+// Steps 1-2 of tile t+1 run before step 4 of tile t, so the tensor core works
+// while the CUDA cores filter.  A persistent CTA (one per SM) runs two such
+// pipelines (groups of 256 threads, own TMEM columns, y/f buffers and group
+// barrier) that share one copy of the B operand (M and u0, split hi/lo,
+// K-major core matrices); with double-buffered y/f rows a group needs one
+// barrier per tile, and the other group fills the SM while it waits.
 #include <cstdlib>
 
 #include "nys_hpass.cuh"
@@ -27,30 +32,37 @@
 
 namespace nys {
 
-constexpr int K2T_THREADS = 256;
-constexpr int K2T_PX = 128;  // UMMA M: source pixels per tile
+constexpr int K2T_GROUP = 256;               // threads per pipeline group
+constexpr int K2T_THREADS = 2 * K2T_GROUP;     // two groups per CTA share the B operand
+constexpr int K2T_PX = 128;                    // UMMA M: source pixels per tile
 
 __host__ __device__ inline int align32f(int v) { return (v + 31) & ~31; }
 
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(K2T_GROUP) : "memory");
+}
+
 template <int RT, int GR>
-__global__ void __launch_bounds__(K2T_THREADS, 2) k_feat_hpass_tc(const HArgs a) {
+__global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a) {
   extern __shared__ __align__(128) float sm[];
-  __shared__ uint64_t mma_bar;
+  __shared__ uint64_t mma_bar[2];
   __shared__ uint32_t tmem_base;
   const int R = RT > 0 ? RT : a.R;
   const int m0 = a.m0, m0q = a.m0q, n = a.n, rho = a.rho, rhop = a.rhop, W = a.W, H = a.H;
   const int NC = n + 1, L = m0 + 1, pitch = a.pitch, TW = a.TW;
-  const int KU = a.ku, NU = a.nu;
+  const int KU = a.ku, NU = a.nu, nbuf = a.nbuf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = tid / K2T_GROUP, gtid = tid % K2T_GROUP;
+  const int nchunks = (NC + K2_CC - 1) / K2_CC;
+  const int nfr = nchunks * K2_CC;  // f rows per buffer: f_c, 1 (y plane), 0 padding
 
   float* Cs = sm;                                  // m0 x rhop
   float* Bh = Cs + align32f(m0 * rhop);            // NU x KU, K-major core matrices
   float* Bl = Bh + NU * KU;
-  float* Fs = Bl + NU * KU;                        // n x pitch
-  float* U = Fs + align32f(n * pitch);             // A hi/lo (2 x 128 x KU) | y rows (m0q x pitch)
-  float* Ah = U;
-  float* Al = U + K2T_PX * KU;
-  float* Ys = U;
+  float* gbase = Bl + NU * KU;                     // per group, per buffer: Fs (nfr x pitch), Ys (m0q x pitch)
+  const int buf_floats = align32f(nfr * pitch) + m0q * pitch;
+  auto Fs_of = [&](int b) { return gbase + (size_t)(g * nbuf + b) * buf_floats; };
+  auto Ys_of = [&](int b) { return Fs_of(b) + align32f(nfr * pitch); };
 
   for (int k = tid; k < m0 * rhop; k += K2T_THREADS) Cs[k] = a.cst[k];
   {
@@ -64,174 +76,214 @@ __global__ void __launch_bounds__(K2T_THREADS, 2) k_feat_hpass_tc(const HArgs a)
       Bl[o] = umma::to_tf32(v - h);
     }
   }
-  if (warp == 0) umma::tmem_alloc(&tmem_base, (uint32_t)a.tcols);
-  if (tid == 0) {
-    umma::mbar_init(&mma_bar, 1);
+  if (warp == 0) umma::tmem_alloc(&tmem_base, (uint32_t)(2 * a.tcols));
+  if (tid < 2) {
+    umma::mbar_init(&mma_bar[tid], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  umma::fence_proxy_async();  // B operand: generic-proxy writes -> tensor core
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  const uint32_t tmem = tmem_base;
+  // this group's TMEM columns: D = [0, NU), A_hi = [a_hi, +KU), A_lo = [a_lo, +KU)
+  const uint32_t tmem = tmem_base + (uint32_t)(g * a.tcols);
+  const uint32_t a_hi = tmem + (uint32_t)align32f(NU), a_lo = a_hi + (uint32_t)align32f(KU);
   const uint32_t idesc = umma::idesc_tf32(K2T_PX, NU);
+  const int q = warp & 3, hh = (warp >> 2) & 1;  // TMEM sub-partition (lanes 32q..) and column half
+  const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+  const int px = 32 * q + lane;                  // this thread's source pixel (TMEM lane) in a tile
+  uint64_t* bar = &mma_bar[g];
 
   const int ncols = TW + 2 * R;  // <= 128
   const int ncol4 = (ncols + 3) & ~3;
-  const int nchunks = (NC + K2_CC - 1) / K2_CC;
   const int XG = TW / K2_XR;
   const int fir_items = L * nchunks * XG;
   const int ntiles = a.tiles_x * a.vrows;
   const int khalf = KU / 2;  // landmarks per feature thread (multiple of 4)
 
-  uint32_t phase = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, phase ^= 1u) {
-    const int vr = a.v0 + tile / a.tiles_x;  // virtual row
+  // 1. features of `tile`: pixel px evaluates b_j for its half of the landmarks
+  // and stores b_hi / b_lo into the A operand in TMEM (raw b planes for K3 too)
+  auto features = [&](int tile) {
+    const int vr = a.v0 + tile / a.tiles_x;
     const int x0 = (tile % a.tiles_x) * TW;
     const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
-    __syncthreads();  // the previous tile's FIR is done with Ys (= A) and Fs
-    // 1. features -> A operand (b_hi, b_lo), raw b planes for K3 when requested
-    {
-      const int s = tid & (K2T_PX - 1), h = tid >> 7;
-      if (s < ncols && !(a.dbg & 1)) {
-        const int xs = x0 - R + s;
-        const int x = clampi(xs, 0, W - 1);
-        float gv[GR];
+    const int xs = x0 - R + px;
+    const int x = clampi(xs, 0, W - 1);
+    float gv[GR];
 #pragma unroll
-        for (int dd = 0; dd < GR; ++dd)
-          gv[dd] = dd < rho ? guide_at(a.g, a.gps, a.f, a.fps, a.gkind, dd, row, x, H, W) : 0.f;
-        float* bdst = nullptr;
-        if (a.bplanes && s >= R && s < R + TW && xs < ((W + 31) & ~31))
-          bdst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) +
-                 (long long)(L * NC) * 32 + (xs & 31);
-        for (int j0 = h * khalf; j0 < (h + 1) * khalf; j0 += 4) {
-          float bv[4];
+    for (int dd = 0; dd < GR; ++dd)
+      gv[dd] = dd < rho ? guide_at(a.g, a.gps, a.f, a.fps, a.gkind, dd, row, x, H, W) : 0.f;
+    float* bdst = nullptr;
+    if (a.bplanes && px >= R && px < R + TW && xs < ((W + 31) & ~31))
+      bdst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) + (long long)(L * NC) * 32 +
+             (xs & 31);
+    for (int j0 = hh * khalf; j0 < (hh + 1) * khalf; j0 += 4) {
+      float bv[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = j0 + e;
-            float v = 0.f;
-            if (j < m0) {
-              const float4* cj = reinterpret_cast<const float4*>(Cs + (size_t)j * rhop);
-              float d2 = 0.f;
+      for (int e = 0; e < 4; ++e) {
+        const int j = j0 + e;
+        float v = 0.f;
+        if (j < m0) {
+          const float4* cj = reinterpret_cast<const float4*>(Cs + (size_t)j * rhop);
+          float d2 = 0.f;
 #pragma unroll
-              for (int d4 = 0; d4 < GR / 4; ++d4) {
-                if (4 * d4 < rho) {
-                  const float4 c4 = cj[d4];
-                  const float t0 = gv[4 * d4] - c4.x, t1 = gv[4 * d4 + 1] - c4.y;
-                  const float t2 = gv[4 * d4 + 2] - c4.z, t3 = gv[4 * d4 + 3] - c4.w;
-                  d2 = fmaf(t0, t0, d2);
-                  d2 = fmaf(t1, t1, d2);
-                  d2 = fmaf(t2, t2, d2);
-                  d2 = fmaf(t3, t3, d2);
-                }
-              }
-              v = range_kernel(d2, a.k2);
-              if (bdst) bdst[(size_t)j * 32] = v;
+          for (int d4 = 0; d4 < GR / 4; ++d4) {
+            if (4 * d4 < rho) {
+              const float4 c4 = cj[d4];
+              const float t0 = gv[4 * d4] - c4.x, t1 = gv[4 * d4 + 1] - c4.y;
+              const float t2 = gv[4 * d4 + 2] - c4.z, t3 = gv[4 * d4 + 3] - c4.w;
+              d2 = fmaf(t0, t0, d2);
+              d2 = fmaf(t1, t1, d2);
+              d2 = fmaf(t2, t2, d2);
+              d2 = fmaf(t3, t3, d2);
             }
-            bv[e] = v;
           }
-          float4 hi, lo;
-          hi.x = umma::to_tf32(bv[0]);
-          hi.y = umma::to_tf32(bv[1]);
-          hi.z = umma::to_tf32(bv[2]);
-          hi.w = umma::to_tf32(bv[3]);
-          lo.x = umma::to_tf32(bv[0] - hi.x);
-          lo.y = umma::to_tf32(bv[1] - hi.y);
-          lo.z = umma::to_tf32(bv[2] - hi.z);
-          lo.w = umma::to_tf32(bv[3] - hi.w);
-          const int o = umma::kmajor_offset(s, j0, K2T_PX);
-          *reinterpret_cast<float4*>(Ah + o) = hi;
-          *reinterpret_cast<float4*>(Al + o) = lo;
+          v = range_kernel(d2, a.k2);
+          if (bdst) bdst[(size_t)j * 32] = v;
+        }
+        bv[e] = v;
+      }
+      float hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hi[e] = umma::to_tf32(bv[e]);
+        lo[e] = umma::to_tf32(bv[e] - hi[e]);
+      }
+      umma::st_32x32b_x4(a_hi + lane_base + (uint32_t)j0, hi[0], hi[1], hi[2], hi[3]);
+      umma::st_32x32b_x4(a_lo + lane_base + (uint32_t)j0, lo[0], lo[1], lo[2], lo[3]);
+    }
+    umma::st_wait();
+  };
+  // 2. y = M b: 3 x K/8 MMAs (M=128, N=NU, K=8), issued by one thread
+  auto issue_mma = [&]() {
+    const uint32_t lbo_b = (uint32_t)NU * 16;
+    uint32_t acc = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+      const uint32_t A = pass == 2 ? a_lo : a_hi;
+      const float* B = pass == 1 ? Bl : Bh;
+#pragma unroll 1
+      for (int kk = 0; kk < KU / 8; ++kk) {
+        umma::mma_tf32_ts(tmem, A + (uint32_t)(8 * kk), umma::desc_kmajor(B + kk * 8 * NU, lbo_b, 128), idesc, acc);
+        acc = 1;
+      }
+    }
+    umma::commit(bar);
+  };
+  // 3. accumulator -> y rows in SMEM (warps w, w+4 of the group drain half of
+  // the columns of TMEM lanes 32(w%4)..), and the tile's f rows
+  auto epilogue = [&](int tile, int b) {
+    float* Ys = Ys_of(b);
+    float* Fs = Fs_of(b);
+    const int nch = NU / 8, c0 = hh * (nch / 2), c1 = c0 + nch / 2;
+    for (int c = c0; c < c1; ++c) {
+      float v[8];
+      umma::ld_32x32b_x8(tmem + lane_base + (uint32_t)(8 * c), v);
+      umma::ld_wait();
+      if (px < ncols) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = 8 * c + e;
+          if (i < L) Ys[(size_t)i * pitch + px] = v[e];
         }
       }
     }
-    umma::fence_proxy_async();  // generic-proxy SMEM writes -> visible to the tensor core
-    __syncthreads();
-    // 2. y = M b: 3 x K/8 MMAs (M=128, N=NU, K=8 each), one issuing thread
-    if (tid == 0 && !(a.dbg & 2)) {
-      umma::fence_after();
-      const uint32_t lbo_a = K2T_PX * 16, lbo_b = (uint32_t)NU * 16;
-      uint32_t acc = 0;
-#pragma unroll 1
-      for (int pass = 0; pass < 3; ++pass) {
-        const float* A = pass == 2 ? Al : Ah;
-        const float* B = pass == 1 ? Bl : Bh;
-#pragma unroll 1
-        for (int kk = 0; kk < KU / 8; ++kk) {
-          const uint64_t da = umma::desc_kmajor(A + kk * 8 * K2T_PX, lbo_a, 128);
-          const uint64_t db = umma::desc_kmajor(B + kk * 8 * NU, lbo_b, 128);
-          umma::mma_tf32_ss(tmem, da, db, idesc, acc);
-          acc = 1;
-        }
-      }
-      umma::commit(&mma_bar);
-    }
-    // stage the tile's f rows while the tensor core runs
-    for (int k = tid; k < n * ncol4; k += K2T_THREADS) {
+    const int vr = a.v0 + tile / a.tiles_x;
+    const int x0 = (tile % a.tiles_x) * TW;
+    const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
+    for (int k = gtid; k < nfr * ncol4; k += K2T_GROUP) {
       const int c = k / ncol4, s = k - c * ncol4;
       const int x = clampi(x0 - R + s, 0, W - 1);
-      Fs[(size_t)c * pitch + s] = __ldg(a.f + (long long)c * a.fps + (long long)row * W + x);
+      Fs[(size_t)c * pitch + s] =
+          c < n ? __ldg(a.f + (long long)c * a.fps + (long long)row * W + x) : (c == n ? 1.f : 0.f);
     }
-    if (!(a.dbg & 2)) {
-      umma::mbar_wait(&mma_bar, phase);
-      umma::fence_after();
-      // 3. accumulator -> y rows: warp w drains TMEM lanes 32(w%4).. (its
-      // sub-partition), warps w and w+4 take half of the columns each
-      const int q = warp & 3, hh = warp >> 2;
-      const int s = 32 * q + lane;
-      const int nch = NU / 8, c0 = hh * (nch / 2), c1 = c0 + nch / 2;
-      for (int c = c0; c < c1; ++c) {
-        float v[8];
-        umma::ld_32x32b_x8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(8 * c), v);
-        umma::ld_wait();
-        if (s < ncols) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = 8 * c + e;
-            if (i < L) Ys[(size_t)i * pitch + s] = v[e];
-          }
-        }
-      }
-    }
-    umma::fence_before();
-    __syncthreads();
-    // 4. horizontal FIR of the (m0+1)(n+1) planes, blocked-layout stores
-    for (int it = tid; it < fir_items; it += K2T_THREADS) {
+  };
+  // 4. horizontal FIR of the (m0+1)(n+1) planes, blocked-layout stores
+  auto fir = [&](int tile, int b) {
+    const float* Ys = Ys_of(b);
+    const float* Fs = Fs_of(b);
+    const int vr = a.v0 + tile / a.tiles_x;
+    const int x0 = (tile % a.tiles_x) * TW;
+    for (int it = gtid; it < fir_items; it += K2T_GROUP) {
       const int i = it % L;
       const int rest = it / L;
       const int ch = rest % nchunks;
       const int xg = rest / nchunks;
       const int xo = x0 + xg * K2_XR;
       if (xo >= W) continue;
-      float acc[K2_CC][K2_XR];
-      if (a.dbg & 4) {
+      const float* yrow = Ys + (size_t)i * pitch + xg * K2_XR;
+      float* dst0 = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xo >> 5) * (a.npl * 32) + (xo & 31);
+      const int cend = min(K2_CC, NC - ch * K2_CC);
+      if (RT == 0 && a.box) {  // running sums: all planes of the item share the y loads
+        float acc[K2_CC][K2_XR];
+        hfir<0, true>(a, yrow, Fs, pitch, xg * K2_XR, ch * K2_CC, acc);
 #pragma unroll
-        for (int cc = 0; cc < K2_CC; ++cc)
+        for (int cc = 0; cc < K2_CC; ++cc) {
+          if (cc < cend) {
+            float* dst = dst0 + (i * NC + ch * K2_CC + cc) * 32;
 #pragma unroll
-          for (int o = 0; o < K2_XR; ++o) acc[cc][o] = Ys[(size_t)i * pitch + o + cc];
-      } else {
-        hfir<RT>(a, Ys + (size_t)i * pitch + xg * K2_XR, Fs, pitch, xg * K2_XR, ch * K2_CC, acc);
-      }
-      if (a.dbg & 8) {
-        if (acc[0][0] == 1234.5f) a.hp[0] = acc[1][1];
+            for (int q4 = 0; q4 < K2_XR / 4; ++q4)
+              reinterpret_cast<float4*>(dst)[q4] =
+                  make_float4(acc[cc][4 * q4], acc[cc][4 * q4 + 1], acc[cc][4 * q4 + 2], acc[cc][4 * q4 + 3]);
+          }
+        }
         continue;
       }
-      float* dst0 = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xo >> 5) * (a.npl * 32) + (xo & 31);
-#pragma unroll
-      for (int cc = 0; cc < K2_CC; ++cc) {
+#pragma unroll 1
+      for (int cc = 0; cc < cend; ++cc) {
         const int c = ch * K2_CC + cc;
-        if (c < NC) {
-          float* dst = dst0 + (i * NC + c) * 32;
+        float acc[K2_XR];
+        hfir_plane<RT>(a, yrow, Fs + (size_t)c * pitch + xg * K2_XR, acc);
+        float* dst = dst0 + (i * NC + c) * 32;
 #pragma unroll
-          for (int q4 = 0; q4 < K2_XR / 4; ++q4)
-            reinterpret_cast<float4*>(dst)[q4] =
-                make_float4(acc[cc][4 * q4], acc[cc][4 * q4 + 1], acc[cc][4 * q4 + 2], acc[cc][4 * q4 + 3]);
-        }
+        for (int q4 = 0; q4 < K2_XR / 4; ++q4)
+          reinterpret_cast<float4*>(dst)[q4] = make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
       }
+    }
+  };
+
+  // Software pipeline per group: the MMAs of tile t+1 run on the tensor core
+  // while the CUDA cores filter tile t.  With two y/f buffers one group
+  // barrier per tile suffices: it orders epilogue(t) before FIR(t) and MMA(t+1),
+  // features(t+1) before MMA(t+1), and FIR(t-1) before epilogue(t+1).
+  const int stride = 2 * gridDim.x;
+  int tile = 2 * blockIdx.x + g;
+  uint32_t phase = 0;
+  int b = 0;
+  if (tile < ntiles) {
+    features(tile);
+    umma::fence_before();
+    group_sync(g);
+    if (gtid == 0) {
+      umma::fence_after();
+      issue_mma();
+    }
+    umma::mbar_wait(bar, phase);
+    phase ^= 1u;
+    umma::fence_after();
+    epilogue(tile, b);
+  }
+  for (; tile < ntiles; tile += stride) {
+    const int next = tile + stride;
+    const bool more = next < ntiles;
+    if (more) features(next);
+    umma::fence_before();
+    group_sync(g);
+    umma::fence_after();
+    if (more && gtid == 0) issue_mma();
+    fir(tile, b);
+    if (more) {
+      umma::mbar_wait(bar, phase);
+      phase ^= 1u;
+      umma::fence_after();
+      if (nbuf == 1) group_sync(g);  // single buffer: FIR(tile) must be done with Ys / Fs
+      b = (b + 1) % nbuf;
+      epilogue(next, b);
     }
   }
   umma::fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tmem, (uint32_t)a.tcols);
+  if (warp == 0) umma::tmem_dealloc(tmem_base, (uint32_t)(2 * a.tcols));
 }
 
 int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
@@ -241,15 +293,22 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   TW = (int)std::min<int64_t>(TW, ceil_div(d->W, K2_XR) * K2_XR);
   const int KU = (int)ceil_div(d->m0, 8) * 8;
   const int NU = (int)ceil_div(d->m0 + 1, 16) * 16;
-  if (NU > 256) return NYS_EUNSUPPORTED;
+  // TMEM per group: accumulator (NU columns) + A_hi + A_lo (KU columns each),
+  // 32-column aligned; the two groups of a CTA share one allocation
+  const int need = align32f(NU) + 2 * align32f(KU);
+  if (NU > 256 || need > 256) return NYS_EUNSUPPORTED;
   int tcols = 32;
-  while (tcols < NU) tcols *= 2;
+  while (tcols < need) tcols *= 2;
   int pitch = (int)ceil_div(TW + 2 * R + 4, 4) * 4;
   pitch += ((4 - pitch % 32) + 32) % 32;  // = 4 (mod 32): the FIR's LDS.128 across rows is conflict-free
-  const size_t floats = (size_t)align32f(d->m0 * a.rhop) + 2 * (size_t)NU * KU + align32f(d->n * pitch) +
-                        std::max<size_t>(2 * (size_t)K2T_PX * KU, (size_t)a.m0q * pitch);
-  const size_t smem = floats * 4;
-  if (smem > 220 * 1024) return NYS_EUNSUPPORTED;
+  const int nfr = (int)ceil_div(d->n + 1, K2_CC) * K2_CC;
+  const size_t fixed = (size_t)align32f(d->m0 * a.rhop) + 2 * (size_t)NU * KU;
+  const size_t buf = (size_t)align32f(nfr * pitch) + (size_t)a.m0q * pitch;
+  // two y/f buffers per group when they fit (one barrier per tile), else one
+  int nbuf = 2;
+  if ((fixed + 2 * nbuf * buf) * 4 > 225 * 1024) nbuf = 1;
+  const size_t smem = (fixed + 2 * nbuf * buf) * 4;
+  if (smem > 225 * 1024) return NYS_EUNSUPPORTED;
   a.TW = TW;
   a.rpt = 1;
   a.pitch = pitch;
@@ -257,16 +316,14 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   a.ku = KU;
   a.nu = NU;
   a.tcols = tcols;
+  a.nbuf = nbuf;
   const long long ntiles = (long long)a.tiles_x * a.vrows;
   const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // all of the unified L1 as shared memory: two ~110 KB CTAs per SM
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    // CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and
-    // TMEM (512 columns) -- the occupancy API under-reports the former here
-    const int occ = std::max(1, std::min<int>((int)((228 * 1024) / (smem + 2048)), std::min(2, 512 / tcols)));
-    const int grid = (int)std::min<long long>(ntiles, (long long)num_sms() * occ);
+    // one CTA (two pipeline groups) per SM; each group takes tiles 2*blockIdx.x + g + k*2*grid
+    const int grid = (int)std::min<long long>(ceil_div(ntiles, 2), (long long)num_sms());
     count_launch();
     kern<<<grid, K2T_THREADS, smem, s>>>(a);
     NYS_LAUNCH_CHECK();

@@ -178,3 +178,17 @@ def test_constant_image_is_fixed_point():
     rep = fast_filter(f, f, FilterParams(spatial=SpatialKernel.box(2), theta=0.1, m0=1, kmeans_max_iter=3))
     assert np.abs(rep.output.data - 0.375).max() <= 1e-6
     assert rep.retained_rank == 1
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 7])
+def test_channel_counts_with_partial_plane_chunks(n):
+    # (n+1) planes per landmark group not a multiple of 4: K3's tail TMA box
+    f32 = spectral_scene(40, 72, n, 5, 0.03, seed=40 + n)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    C, _, _, _ = O.kmeans(O.range_vectors(f32.astype(np.float64)), 6, 0, 6)
+    params = FilterParams(spatial=SpatialKernel.gaussian(2.0, 6), theta=0.3, m0=6)
+    rep = filter_with_landmarks(f, f, C, params)
+    ref = O.fast_filter_with_landmarks(f32.astype(np.float64), f32.astype(np.float64), C, 0.3, "gaussian_fir", 2.0, 6)
+    out = rep.output.data.double().cpu().numpy()
+    assert np.abs(out - ref["output"]).max() <= TOL
+    assert rep.guarded_pixels == ref["guarded_pixels"]

@@ -28,6 +28,8 @@
 
 namespace nys {
 
+constexpr double NYS_TC_MAX_NORM = 1.0e3;  // tensor-core y = M b up to this ||M||_inf (nys_filter_hpass)
+
 template <int RT, int GR>
 __global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
   extern __shared__ __align__(128) float sm[];
@@ -223,8 +225,19 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   if (const char* e = getenv("NYS_DBG_K2")) a.dbg = atoi(e);
   cudaStream_t s = (cudaStream_t)stream;
   {
+    // The tensor-core product (3xTF32: ~3x the rounding error of FP32 FMA, from
+    // the split representation and the accumulator) is used while the mixing
+    // matrix is well conditioned.  ||M||_inf >= ||M||_2 = 1/alpha_min bounds the
+    // cancellation in y = M b; beyond NYS_TC_MAX_NORM the CUDA-core FP32 FMA
+    // GEMM keeps ill-conditioned landmark sets inside the parity budget.
+    double normM = 0.0;
+    for (int i = 0; i < d->m0; ++i) {
+      double rs = 0.0;
+      for (int j = 0; j < d->m0; ++j) rs += std::fabs(d->M[(size_t)i * d->m0 + j]);
+      normM = std::max(normM, rs);
+    }
     const char* e = getenv("NYS_K2_SIMT");  // debug: force the CUDA-core GEMM kernel
-    if (!(e && atoi(e))) {
+    if (!(e && atoi(e)) && normM <= NYS_TC_MAX_NORM) {
       const int rc = launch_hpass_tc(a, d, s);
       if (rc != NYS_EUNSUPPORTED) return rc;
     }

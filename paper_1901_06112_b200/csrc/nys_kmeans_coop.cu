@@ -16,6 +16,8 @@
 // sees a stale L1 line written by another SM before a grid barrier.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "nys_kmeans_dev.cuh"
 
 namespace cg = cooperative_groups;
@@ -198,22 +200,26 @@ struct LloydArgs {
   int rho, m0, max_iter, S;
   double* C;                 // in: seeds; out: final centroids
   int* labels;
-  unsigned long long* gacc;  // 2 x (m0*rho sums + m0 counts), exact fixed point, parity-buffered
+  unsigned long long* gacc;  // 3 x (m0*rho sums + m0 counts): per-iteration exact fixed-point deltas
   double* part;              // 2 x nb x 2 (objective, changed) per block, parity-buffered
   double* arg;               // 2 x nb x 2 (double-buffered argmax pairs)
   double* errors;
   KState* st;
   unsigned* maxabs_bits;     // global max |x| (float bits), zeroed by k_init_state
+  float* lb;                 // m: lower bound on the distance to the second-closest centroid (+ drift)
+  int* list;                 // m: per-warp lists of points that need the full search
   int nw;                    // warps per block
+  int bounds;                // 0: full search every iteration (debug / A-B check)
 };
 
 // Warp-level accumulation of per-cluster coordinate sums as EXACT fixed-point
-// integers (x * 2^s rounded once per point): each distinct label among the
-// lanes is reduced with REDUX on 21-bit limbs, so sums are independent of
-// order and hence deterministic across blocks, warps and runs.
+// integers (x * 2^s rounded once per point, two's complement): each distinct
+// label among the lanes is reduced with REDUX on 21-bit limbs, so sums are
+// independent of order and hence deterministic across blocks, warps and runs.
+// `sign` = -1 removes the lanes' points from their clusters.
 template <int GR>
 __device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho, int label, bool valid, double scale,
-                                                   unsigned long long* acc, unsigned* cnt) {
+                                                   int sign, unsigned long long* acc, int* cnt) {
   const int lane = threadIdx.x & 31;
   unsigned rem = __ballot_sync(0xffffffffu, valid);
   while (rem) {
@@ -224,17 +230,50 @@ __device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho
 #pragma unroll
       for (int d = 0; d < GR; ++d)
         if (d < rho) {
-          const unsigned long long v = (unsigned long long)__double2ll_rn((double)x[d] * scale);
+          const unsigned long long v = (unsigned long long)__double2ll_rn((double)(sign * x[d]) * scale);
           const unsigned long long s0 = __reduce_add_sync(grp, (unsigned)(v & 0x1FFFFFull));
           const unsigned long long s1 = __reduce_add_sync(grp, (unsigned)((v >> 21) & 0x1FFFFFull));
           const unsigned long long s2 = __reduce_add_sync(grp, (unsigned)(v >> 42));
           if (lane == leader) acc[L * rho + d] += s0 + (s1 << 21) + (s2 << 42);
         }
-      if (lane == leader) cnt[L] += __popc(grp);
+      if (lane == leader) cnt[L] += sign * __popc(grp);
     }
     rem &= ~grp;
   }
 }
+
+// squared FP32 distance, difference form, dimensions in ascending order -- the
+// one formula every assignment uses, so a bound-skipped point gets the same
+// value the full search would have produced
+template <int GR>
+__device__ __forceinline__ float d2_f32(const float (&x)[GR], int rho, const float* __restrict__ c) {
+  float d2 = 0.f;
+#pragma unroll
+  for (int d4 = 0; d4 < (GR + 3) / 4; ++d4) {
+    if (4 * d4 < rho) {
+      const float4 c4 = reinterpret_cast<const float4*>(c)[d4];
+      const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * d4 + e < GR && 4 * d4 + e < rho) {
+          const float t = x[4 * d4 + e] - cc[e];
+          d2 = fmaf(t, t, d2);
+        }
+    }
+  }
+  return d2;
+}
+
+// Lloyd iterations with Hamerly-style bounds.  A point keeps its label without
+// the m0-way search when its FP32 distance to the assigned centroid is below a
+// lower bound on its distance to every other centroid, with a relative margin
+// (LB_EPS) that covers the FP32 rounding of both sides: then the full search
+// would return the same label with the same distance, so labels, exact sums,
+// centroids and iteration counts are identical to searching every point.
+// The bound is stored drift-adjusted (lb + cumulative max centroid movement at
+// the time it was set), so skipped points cost no writes.  Per-iteration sums
+// are exact fixed-point deltas of the points whose label changed.
+constexpr double LB_EPS = 1.0 / 32768.0;
 
 template <int GR, int RX>
 __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
@@ -243,20 +282,25 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int rho = RX > 0 ? RX : a.rho, m0 = a.m0, msl = m0 * rho, gstride = msl + m0;  // RX: compile-time rho
   unsigned long long* wacc = reinterpret_cast<unsigned long long*>(dsm);      // nw x msl (per-warp sums)
-  unsigned* wcnt = reinterpret_cast<unsigned*>(wacc + (size_t)nw * msl);       // nw x m0 (per-warp counts)
+  int* wcnt = reinterpret_cast<int*>(wacc + (size_t)nw * msl);                 // nw x m0 (per-warp counts)
   double* Cd = reinterpret_cast<double*>(wcnt + (((size_t)nw * m0 + 1) & ~size_t(1)));  // m0*rho current (FP64)
   double* Cp = Cd + (size_t)msl;                                               // m0*rho previous
-  double* tsh = Cp + (size_t)msl;                                              // msl sums + m0 counts (FP64)
-  long long* excl = reinterpret_cast<long long*>(tsh + gstride);              // m0
+  long long* T = reinterpret_cast<long long*>(Cp + (size_t)msl);              // msl sums + m0 counts (exact)
+  long long* excl = T + gstride;                                               // m0
   float* Cf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(excl + m0) + 15) & ~uintptr_t(15));
   const int rhop = (rho + 3) & ~3;                                             // Cf rows: 16-byte aligned
   const int m0p = (m0 + 3) & ~3;                                               // Cf rows padded to 4
+  float* Cfo = Cf + (size_t)m0p * rhop;                                        // previous iteration's Cf
   __shared__ double sh[64];
   __shared__ double extra[2][32];
   __shared__ double misc[2];
+  __shared__ int wlen[32], wpre[33];
+  __shared__ double dcum_sh;
   const int nb = gridDim.x, b = blockIdx.x;
   const long long chunk = ceil_div(a.m, (long long)nb);
   const long long lo = min(a.m, b * chunk), hi = min(a.m, lo + chunk);
+  const long long cw = ceil_div(hi - lo, (long long)nw);  // phase-A sub-range per warp
+  const long long wlo = min(hi, lo + w * cw), whi = min(hi, wlo + cw);
 
   // fixed-point scale 2^s with |sum| < 2^61 for any cluster: s = 61 - log2(max|x| * m)
   {
@@ -277,43 +321,93 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     if (lane == 0 && mx > 0.f) atomicMax(a.maxabs_bits, __float_as_uint(mx));
   }
   for (int k = threadIdx.x; k < msl; k += blockDim.x) Cd[k] = __ldcg(a.C + k);
+  for (int k = threadIdx.x; k < gstride; k += blockDim.x) T[k] = 0;
+  if (threadIdx.x == 0) dcum_sh = 0.0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < m0p * rhop; k += blockDim.x) {
+    const int j = k / rhop, d = k - j * rhop;
+    Cf[k] = j >= m0 ? 3.0e38f : (d < rho ? (float)Cd[j * rho + d] : 0.f);  // padded rows never win
+  }
   grid.sync();
   const float maxabs = __uint_as_float(__ldcg(a.maxabs_bits));
   int sexp = 0;
   if (maxabs > 0.f) sexp = 61 - ilogb((double)maxabs * (double)a.m) - 1;
   const double scale = ldexp(1.0, sexp), inv_scale = ldexp(1.0, -sexp);
+  constexpr int HH = GR <= 4 ? 2 : 1;  // points per lane in the full search: every centroid LDS serves HH
+  constexpr int JJ = GR >= 16 ? 4 : 1; // centroids per step: independent FMA chains for long guides
 
   for (int it = 0; it < a.max_iter; ++it) {
     const int par = it & 1;
-    unsigned long long* G = a.gacc + (size_t)par * gstride;
-    for (int k = threadIdx.x; k < m0p * rhop; k += blockDim.x) {
-      const int j = k / rhop, d = k - j * rhop;
-      Cf[k] = j >= m0 ? 3.0e38f : (d < rho ? (float)Cd[j * rho + d] : 0.f);  // padded rows never win
-    }
+    unsigned long long* D = a.gacc + (size_t)(it % 3) * gstride;
+    // next iteration's delta buffer: last read after the barrier of it-2, next written after this one's
+    if (b == 0)
+      for (int k = threadIdx.x; k < gstride; k += blockDim.x) a.gacc[(size_t)((it + 1) % 3) * gstride + k] = 0ull;
     for (int k = threadIdx.x; k < nw * msl; k += blockDim.x) wacc[k] = 0ull;
-    for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0u;
+    for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0;
+    const double dcum = dcum_sh;
     __syncthreads();
     unsigned long long* myacc = wacc + (size_t)w * msl;
-    unsigned* mycnt = wcnt + (size_t)w * m0;
+    int* mycnt = wcnt + (size_t)w * m0;
     double near_sum = 0.0, changed = 0.0;
-    // HH 32-pixel tiles per warp step: every centroid LDS serves HH points
-    constexpr int HH = GR <= 4 ? 2 : 1;
-    for (long long base = lo + (long long)w * 32 * HH; base < hi; base += (long long)nw * 32 * HH) {
+    const bool full_pass = it == 0 || !a.bounds;
+    long long nlist = hi - lo;
+    if (!full_pass) {
+      // phase A: warp w tests its contiguous sub-range; failures go to its list segment in point order
+      int nl = 0;
+      for (long long base = wlo; base < whi; base += 32) {
+        const long long i = base + lane;
+        const bool valid = i < whi;
+        bool need = false;
+        if (valid) {
+          float x[GR];
+#pragma unroll
+          for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(a.pts + d * a.ps + i) : 0.f;
+          const int lab = a.labels[i];
+          const float d2a = d2_f32<GR>(x, rho, Cf + (size_t)lab * rhop);
+          const double lbe = (double)a.lb[i] - dcum;
+          if (lbe > 0.0 && (double)d2a * (1.0 + LB_EPS) < lbe * lbe * (1.0 - LB_EPS)) near_sum += (double)d2a;
+          else need = true;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, need);
+        if (need) a.list[wlo + nl + __popc(bal & ((1u << lane) - 1u))] = (int)i;
+        nl += __popc(bal);
+      }
+      if (lane == 0) wlen[w] = nl;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        wpre[0] = 0;
+        for (int q = 0; q < nw; ++q) wpre[q + 1] = wpre[q] + wlen[q];
+      }
+      __syncthreads();
+      nlist = wpre[nw];
+    }
+    // phase B: the m0-way search (every point on full passes, else the listed ones)
+    for (long long q0 = (long long)w * 32 * HH; q0 < nlist; q0 += (long long)nw * 32 * HH) {
       float x[HH][GR];
-      float best[HH];
+      float best[HH], second[HH];
       int arg[HH];
+      long long idx[HH];
       bool valid[HH];
 #pragma unroll
       for (int h = 0; h < HH; ++h) {
-        best[h] = INFINITY;
+        best[h] = second[h] = INFINITY;
         arg[h] = 0;
-        const long long i = base + 32 * h + lane;
-        valid[h] = i < hi;
+        const long long q = q0 + 32 * h + lane;
+        valid[h] = q < nlist;
+        long long i = lo;
+        if (valid[h]) {
+          if (full_pass) {
+            i = lo + q;
+          } else {
+            int sg = 0;
+            while (q >= wpre[sg + 1]) ++sg;
+            i = a.list[min(hi, lo + sg * cw) + (q - wpre[sg])];
+          }
+        }
+        idx[h] = i;
 #pragma unroll
         for (int d = 0; d < GR; ++d) x[h][d] = (valid[h] && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
       }
-      // JJ centroids per step: independent FMA chains for the long guides
-      constexpr int JJ = GR >= 16 ? 4 : 1;
       for (int j0 = 0; j0 < m0; j0 += JJ) {
         float d2[JJ][HH];
 #pragma unroll
@@ -348,22 +442,36 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
 #pragma unroll
         for (int jj = 0; jj < JJ; ++jj)
 #pragma unroll
-          for (int h = 0; h < HH; ++h)
-            if (d2[jj][h] < best[h]) {  // strict, ascending j: first index wins ties (np.argmin)
-              best[h] = d2[jj][h];
+          for (int h = 0; h < HH; ++h) {
+            const float v = d2[jj][h];
+            if (v < best[h]) {  // strict, ascending j: first index wins ties (np.argmin)
+              second[h] = best[h];
+              best[h] = v;
               arg[h] = j0 + jj;
+            } else {
+              second[h] = fminf(second[h], v);
             }
+          }
       }
 #pragma unroll
       for (int h = 0; h < HH; ++h) {
-        const long long i = base + 32 * h + lane;
+        const long long i = idx[h];
+        int old = -1;
+        bool chg = false;
         if (valid[h]) {
           near_sum += (double)best[h];
-          const int old = a.labels[i];
-          if (it == 0 || old != arg[h]) changed += 1.0;
-          a.labels[i] = arg[h];
+          old = it == 0 ? -1 : a.labels[i];
+          chg = old != arg[h];
+          if (chg) {
+            changed += 1.0;
+            a.labels[i] = arg[h];
+          }
+          // drift-adjusted lower bound on the distance to the second-closest centroid
+          const double lbv = (double)sqrtf(second[h]) * (1.0 - LB_EPS) + dcum;
+          a.lb[i] = second[h] < INFINITY ? __double2float_rd(lbv) : 3.0e38f;
         }
-        warp_accumulate_fx<GR>(x[h], rho, arg[h], valid[h], scale, myacc, mycnt);
+        warp_accumulate_fx<GR>(x[h], rho, arg[h], valid[h] && chg, scale, 1, myacc, mycnt);
+        warp_accumulate_fx<GR>(x[h], rho, old, valid[h] && chg && old >= 0, scale, -1, myacc, mycnt);
       }
     }
     near_sum = warp_sum(near_sum);
@@ -373,16 +481,16 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       extra[1][w] = changed;
     }
     __syncthreads();
-    // block totals -> global exact integer accumulators (order-independent)
+    // block deltas -> global exact integer accumulators (order-independent, two's complement)
     for (int k = threadIdx.x; k < msl; k += blockDim.x) {
       unsigned long long t = 0;
       for (int q = 0; q < nw; ++q) t += wacc[(size_t)q * msl + k];
-      if (t) atomicAdd(G + k, t);
+      if (t) atomicAdd(D + k, t);
     }
     for (int k = threadIdx.x; k < m0; k += blockDim.x) {
-      unsigned long long t = 0;
+      long long t = 0;
       for (int q = 0; q < nw; ++q) t += wcnt[(size_t)q * m0 + k];
-      if (t) atomicAdd(G + msl + k, t);
+      if (t) atomicAdd(D + msl + k, (unsigned long long)t);
     }
     double* P = a.part + (size_t)par * nb * 2;
     if (threadIdx.x == 0) {
@@ -395,10 +503,8 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       P[2 * b + 1] = c;
     }
     grid.sync();
-    // every block: totals into shared memory, objective/changed in fixed block order
-    for (int k = threadIdx.x; k < msl; k += blockDim.x)
-      tsh[k] = (double)(long long)__ldcg(G + k) * inv_scale;
-    for (int k = threadIdx.x; k < m0; k += blockDim.x) tsh[msl + k] = (double)__ldcg(G + msl + k);
+    // every block: running exact totals, objective/changed in fixed block order
+    for (int k = threadIdx.x; k < gstride; k += blockDim.x) T[k] += (long long)__ldcg(D + k);
     {
       double e = 0.0, c = 0.0;
       for (int q = threadIdx.x; q < nb; q += blockDim.x) {
@@ -410,9 +516,6 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       c = block_sum(c, sh);
       if (threadIdx.x == 0) misc[1] = c;
     }
-    // the other parity's accumulators are free until after the next barrier
-    if (b == 0)
-      for (int k = threadIdx.x; k < gstride; k += blockDim.x) a.gacc[(size_t)(par ^ 1) * gstride + k] = 0ull;
     __syncthreads();
     const double chg = misc[1];
     if (b == 0 && threadIdx.x == 0) {
@@ -427,14 +530,14 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     for (int k = threadIdx.x; k < msl; k += blockDim.x) {
       Cp[k] = Cd[k];
       const int j = k / rho;
-      const double cnt = tsh[msl + j];
-      if (cnt > 0.0) Cd[k] = tsh[k] / cnt;
+      const double cnt = (double)T[msl + j];
+      if (cnt > 0.0) Cd[k] = ((double)T[k] * inv_scale) / cnt;
     }
     __syncthreads();
     // empty clusters, ascending j: farthest remaining point from its old centroid
     int nex = 0;
     for (int j = 0; j < m0; ++j) {
-      if (tsh[msl + j] > 0.0) continue;
+      if (T[msl + j] > 0) continue;
       double bv = -INFINITY;
       long long bi = a.m;
       for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
@@ -494,6 +597,30 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       for (int d = threadIdx.x; d < rho; d += blockDim.x) Cd[j * rho + d] = (double)__ldg(a.pts + d * a.ps + idx);
       ++nex;
       __syncthreads();
+    }
+    // next iteration's FP32 centroids and the largest centroid movement (rounded up)
+    for (int k = threadIdx.x; k < m0p * rhop; k += blockDim.x) {
+      Cfo[k] = Cf[k];
+      const int j = k / rhop, d = k - j * rhop;
+      Cf[k] = j >= m0 ? 3.0e38f : (d < rho ? (float)Cd[j * rho + d] : 0.f);
+    }
+    __syncthreads();
+    double mv = 0.0;
+    for (int j = threadIdx.x; j < m0; j += blockDim.x) {
+      double s2 = 0.0;
+      for (int d = 0; d < rho; ++d) {
+        const double t = (double)Cf[j * rhop + d] - (double)Cfo[j * rhop + d];
+        s2 += t * t;
+      }
+      mv = fmax(mv, sqrt(s2));
+    }
+    for (int o = 16; o > 0; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+    if (lane == 0) sh[w] = mv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = 0.0;
+      for (int q = 0; q < nw; ++q) mx = fmax(mx, sh[q]);
+      dcum_sh = dcum + mx * (1.0 + 1e-9) + 1e-30;  // monotone, never understated
     }
     __syncthreads();
   }
@@ -567,7 +694,7 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   if (!coop) return NYS_EUNSUPPORTED;
   const int msl = m0 * rho;
   const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
-                       (size_t)((m0 + 3) & ~3) * ((rho + 3) & ~3) * 4 + 96;
+                       2 * (size_t)((m0 + 3) & ~3) * ((rho + 3) & ~3) * 4 + 96;
   auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed; };
   int nw = 8;
   while (nw > 1 && need(nw) > 200 * 1024) --nw;
@@ -590,8 +717,15 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   a.st = reinterpret_cast<KState*>(ws + L.off_state);
   a.maxabs_bits = reinterpret_cast<unsigned*>(ws + L.off_idx);
   a.nw = nw;
-  // the exact accumulators start at zero (both parities) and max|x| at +0
-  NYS_CUDA_TRY(cudaMemsetAsync(a.gacc, 0, (size_t)2 * (msl + m0) * 8, s));
+  // the seeding D^2 array is dead during Lloyd: bounds in its first half, work lists in the second
+  a.lb = reinterpret_cast<float*>(ws + L.off_d2);
+  a.list = reinterpret_cast<int*>(ws + L.off_d2 + (size_t)m * 4);
+  {
+    const char* e = getenv("NYS_KM_NOBOUNDS");
+    a.bounds = (e && atoi(e)) ? 0 : 1;
+  }
+  // the first delta buffer starts at zero (the kernel zeroes each next one) and max|x| at +0
+  NYS_CUDA_TRY(cudaMemsetAsync(a.gacc, 0, (size_t)(msl + m0) * 8, s));
   NYS_CUDA_TRY(cudaMemsetAsync(a.maxabs_bits, 0, sizeof(unsigned), s));
   void* args[] = {&a};
   auto go = [&](auto kern) -> int {

@@ -51,7 +51,7 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   // nys_kmeanspp_update / _pick pair must agree on it for any (rho, m0)
   L.off_ppart = o;   o = align256(o + (size_t)std::max(L.nb_seed, L.nb_coop) * 8);
   L.off_part = o;    o = align256(o + (size_t)std::max(L.nb_assign, L.nb_coop) * L.S * 8);
-  L.off_tot = o;     o = align256(o + (size_t)std::max(L.S, 2 * (m0 * rho + m0)) * 8);
+  L.off_tot = o;     o = align256(o + (size_t)std::max(L.S, 3 * (m0 * rho + m0)) * 8);
   L.off_cf = o;      o = align256(o + (size_t)m0 * rho * 4);
   L.off_cprev = o;   o = align256(o + (size_t)m0 * rho * 8);
   L.off_excl = o;    o = align256(o + (size_t)m0 * 8);

@@ -183,7 +183,8 @@ def test_constant_image_is_fixed_point():
 @pytest.mark.parametrize("n", [1, 2, 5, 7])
 def test_channel_counts_with_partial_plane_chunks(n):
     # (n+1) planes per landmark group not a multiple of 4: K3's tail TMA box
-    f32 = spectral_scene(40, 72, n, 5, 0.03, seed=40 + n)
+    f32 = spectral_scene(40, 72, n, 5, 0.03, seed=40 + n) if n >= 4 else \
+        np.ascontiguousarray(color_scene(40, 72, 5, 0.03, seed=40 + n)[:n])
     f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
     C, _, _, _ = O.kmeans(O.range_vectors(f32.astype(np.float64)), 6, 0, 6)
     params = FilterParams(spatial=SpatialKernel.gaussian(2.0, 6), theta=0.3, m0=6)
@@ -192,3 +193,19 @@ def test_channel_counts_with_partial_plane_chunks(n):
     out = rep.output.data.double().cpu().numpy()
     assert np.abs(out - ref["output"]).max() <= TOL
     assert rep.guarded_pixels == ref["guarded_pixels"]
+
+
+@pytest.mark.parametrize("rho", [3, 16, 27])
+def test_lloyd_bounds_are_exact(rho, monkeypatch):
+    # Hamerly-style skipping must not change a single label or centroid bit
+    rng = np.random.default_rng(100 + rho)
+    centers = rng.uniform(0, 1, (40, rho))
+    pts = (centers[rng.integers(0, 40, 60000)] + 0.08 * rng.standard_normal((60000, rho))).astype(np.float32)
+    a = kmeans_landmarks(pts.astype(np.float64), 32, seed=3, max_iter=40)
+    monkeypatch.setenv("NYS_KM_NOBOUNDS", "1")
+    b = kmeans_landmarks(pts.astype(np.float64), 32, seed=3, max_iter=40)
+    assert np.array_equal(a.centroids, b.centroids)
+    assert np.array_equal(a.assignment, b.assignment)
+    assert len(a.errors) == len(b.errors)
+    np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
+    assert a.quant_error == b.quant_error

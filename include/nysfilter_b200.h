@@ -238,6 +238,21 @@ int nys_jacobi_eig(const double* a, int k, double* values_out, double* vectors_o
  * signs; descending eigenvalues, eigenvectors as columns. */
 int nys_sym_eig(const double* a, int k, double* values_out, double* vectors_out);
 
+/* The m0 x m0 host products the kernels consume, in one call (replaces
+ * nystrom.py:67-69 build_A, 97-109 eigendecomposition + drop rule, and the
+ * filters.py:214-219 mixing products):
+ *   A = exp(-|c_i - c_j|^2 / (2 theta^2)), eigenvalues alpha_1 >= ... ,
+ *   retained alpha_k > eps_drop * alpha_1, M = sum_retained w_k w_k^T / alpha_k,
+ *   u0 = w_1.
+ * When nothing is dropped M = A^{-1} (Cholesky) and u0 comes from inverse
+ * iteration on the eigenvalues of a values-only QL, ~4x cheaper than the full
+ * eigensystem; otherwise the full eigensystem (nys_sym_eig) is used.
+ * alphas_out: m0 (first *rank_out valid, descending); M_out: m0 x m0; u0_out: m0.
+ * Returns NYS_EDEGENERATE when alpha_1 <= 0. */
+#define NYS_EDEGENERATE 3
+int nys_mixing_plan(const double* centroids, int m0, int rho, double theta, double eps_drop, double* alphas_out,
+                    int* rank_out, double* M_out, double* u0_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libnysfilter_b200.so"
 NYS_OK = 0
 NYS_EINVAL = 1
 NYS_EUNSUPPORTED = 2
+NYS_EDEGENERATE = 3
 NYS_ECUDA = 1000
 NYS_SPATIAL_BOX = 0
 NYS_SPATIAL_GAUSSIAN_FIR = 1
@@ -69,6 +70,7 @@ _SIGS = {
     "nys_patch_guide": (_I, [_P, _L, _I, _I, _I, _I, _P, _L, _P]),
     "nys_jacobi_eig": (_I, [_P, _I, _P, _P, C.POINTER(C.c_int)]),
     "nys_sym_eig": (_I, [_P, _I, _P, _P]),
+    "nys_mixing_plan": (_I, [_P, _I, _I, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
 }
 
 _lib = None

@@ -98,6 +98,8 @@ extern "C" int nys_jacobi_eig(const double* a_in, int k, double* values_out, dou
   return NYS_OK;
 }
 
+// (sqrt(a*a + b*b) instead of std::hypot below: the operands are O(1) here and
+// glibc's hypot costs ~20 ns, which dominated the QL sweeps)
 // ---------------------------------------------------------------------------
 // Fast symmetric eigensolver for the hot path: Householder reduction to
 // tridiagonal form followed by implicit QL iterations with Wilkinson-style
@@ -190,14 +192,14 @@ extern "C" int nys_sym_eig(const double* a_in, int k, double* values_out, double
       if (m != l) {
         if (++iter > 60) return NYS_EUNSUPPORTED;
         double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = std::hypot(g, 1.0);
+        double r = std::sqrt(g * g + 1.0);
         g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
         double s = 1.0, c = 1.0, p = 0.0;
         int i;
         for (i = m - 1; i >= l; --i) {
           double f = s * e[i];
           const double b = c * e[i];
-          r = std::hypot(f, g);
+          r = std::sqrt(f * f + g * g);
           e[i + 1] = r;
           if (r == 0.0) {
             d[i + 1] -= p;
@@ -233,5 +235,272 @@ extern "C" int nys_sym_eig(const double* a_in, int k, double* values_out, double
     values_out[j] = d[order[j]];
     for (int i = 0; i < n; ++i) vectors_out[(size_t)i * n + j] = zt[(size_t)order[j] * n + i];
   }
+  return NYS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Mixing plan (see nysfilter_b200.h): Gram matrix, eigenvalues, drop rule,
+// M and the lead eigenvector.
+// ---------------------------------------------------------------------------
+namespace {
+
+// squared distance in numpy's reduction order over rho terms (pairwise_sum:
+// sequential below 8 terms, else 8 strided partials), as nystrom.py's gram
+double sqdist_np(const double* a, const double* b, int rho) {
+  auto sq = [&](int d) {
+    const double t = a[d] - b[d];
+    return t * t;
+  };
+  if (rho < 8) {
+    double r = 0.0;
+    for (int d = 0; d < rho; ++d) r += sq(d);
+    return r;
+  }
+  double r[8];
+  for (int k = 0; k < 8; ++k) r[k] = sq(k);
+  int d = 8;
+  const int full = rho - (rho % 8);
+  for (; d < full; d += 8)
+    for (int k = 0; k < 8; ++k) r[k] += sq(d + k);
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; d < rho; ++d) res += sq(d);
+  return res;
+}
+
+// 4-way split dot product (independent FMA chains; the host path is latency bound)
+inline double dot4(const double* a, const double* b, int n) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+  for (; k + 4 <= n; k += 4) {
+    s0 += a[k] * b[k];
+    s1 += a[k + 1] * b[k + 1];
+    s2 += a[k + 2] * b[k + 2];
+    s3 += a[k + 3] * b[k + 3];
+  }
+  for (; k < n; ++k) s0 += a[k] * b[k];
+  return (s0 + s1) + (s2 + s3);
+}
+
+// Householder tridiagonalisation (EISPACK tred2 without accumulating the
+// transform): on return row i of z holds the Householder vector u_i in columns
+// 0..i-1 and column i holds u_i / h_i; h[i] = h_i (0: no reflection); the
+// tridiagonal is diag d, sub-diagonal e[i] (coupling i-1 and i).
+void tridiag(std::vector<double>& z, int n, std::vector<double>& d, std::vector<double>& e, std::vector<double>& h) {
+  d.assign(n, 0.0);
+  e.assign(n, 0.0);
+  h.assign(n, 0.0);
+  auto Z = [&](int i, int j) -> double& { return z[(size_t)i * n + j]; };
+  std::vector<double> zi(n);
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    double hh = 0.0, scale = 0.0;
+    if (l > 0) {
+      for (int q = 0; q <= l; ++q) scale += std::fabs(Z(i, q));
+      if (scale == 0.0) {
+        e[i] = Z(i, l);
+      } else {
+        for (int q = 0; q <= l; ++q) {
+          Z(i, q) /= scale;
+          hh += Z(i, q) * Z(i, q);
+        }
+        double f = Z(i, l);
+        const double g = f >= 0.0 ? -std::sqrt(hh) : std::sqrt(hh);
+        e[i] = scale * g;
+        hh -= f * g;
+        Z(i, l) = f - g;
+        f = 0.0;
+        for (int q = 0; q <= l; ++q) zi[q] = Z(i, q);
+        for (int j = 0; j <= l; ++j) {
+          Z(j, i) = Z(i, j) / hh;
+          // (A u)_j over the lower triangle: row j up to j, then column j below
+          double gg = dot4(&z[(size_t)j * n], zi.data(), j + 1);
+          for (int q = j + 1; q <= l; ++q) gg += Z(q, j) * zi[q];
+          e[j] = gg / hh;
+          f += e[j] * zi[j];
+        }
+        const double hf = f / (hh + hh);
+        for (int j = 0; j <= l; ++j) {
+          const double ff = zi[j];
+          const double gg = e[j] - hf * ff;
+          e[j] = gg;
+          double* zj = &z[(size_t)j * n];
+          for (int q = 0; q <= j; ++q) zj[q] -= ff * e[q] + gg * zi[q];
+        }
+      }
+    } else {
+      e[i] = Z(i, l);
+    }
+    h[i] = hh;
+  }
+  for (int i = 0; i < n; ++i) d[i] = Z(i, i);
+}
+
+// eigenvalues of the tridiagonal (d, e as from tridiag) by implicit QL, descending
+bool tql_values(std::vector<double> d, std::vector<double> e, int n, std::vector<double>& out) {
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= 1e-15 * dd) break;
+      }
+      if (m != l) {
+        if (++iter > 60) return false;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::sqrt(g * g + 1.0);
+        g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = m - 1; i >= l; --i) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          r = std::sqrt(f * f + g * g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[m] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+        }
+        if (r == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+  std::sort(d.begin(), d.end(), [](double x, double y) { return x > y; });
+  out = d;
+  return true;
+}
+
+}  // namespace
+
+extern "C" int nys_mixing_plan(const double* C, int m0, int rho, double theta, double eps_drop, double* alphas_out,
+                               int* rank_out, double* M_out, double* u0_out) {
+  if (!C || m0 < 1 || rho < 1 || !(theta > 0.0) || !alphas_out || !rank_out || !M_out || !u0_out)
+    return NYS_EINVAL;
+  const int n = m0;
+  std::vector<double> A((size_t)n * n);
+  const double inv = 1.0 / (2.0 * theta * theta);
+  for (int i = 0; i < n; ++i)
+    for (int j = i; j < n; ++j) {
+      const double d2 = sqdist_np(C + (size_t)i * rho, C + (size_t)j * rho, rho);
+      if (!std::isfinite(d2)) return NYS_EINVAL;
+      A[(size_t)i * n + j] = A[(size_t)j * n + i] = std::exp(-d2 * inv);
+    }
+  std::vector<double> Z(A), d, e, h, vals;
+  tridiag(Z, n, d, e, h);
+  bool fast = tql_values(d, e, n, vals);
+  if (fast && !(vals[0] > 0.0)) return NYS_EDEGENERATE;
+  int rank = 0;
+  if (fast)
+    for (int k = 0; k < n; ++k) rank += vals[k] > eps_drop * vals[0] ? 1 : 0;
+  std::vector<double> L;
+  if (fast && rank == n) {
+    // M = A^{-1} = L^{-T} L^{-1} from A = L L^T (rows of L contiguous)
+    L.assign((size_t)n * n, 0.0);
+    for (int j = 0; j < n && fast; ++j) {
+      const double* lj = &L[(size_t)j * n];
+      const double s = A[(size_t)j * n + j] - dot4(lj, lj, j);
+      if (!(s > 0.0)) {
+        fast = false;
+        break;
+      }
+      const double ljj = std::sqrt(s);
+      L[(size_t)j * n + j] = ljj;
+      for (int i = j + 1; i < n; ++i) L[(size_t)i * n + j] = (A[(size_t)i * n + j] - dot4(&L[(size_t)i * n], lj, j)) / ljj;
+    }
+  } else {
+    fast = false;
+  }
+  if (fast) {
+    // X = L^{-1} stored transposed (XT[j][i] = X[i][j], i >= j) so both products stream rows
+    std::vector<double> XT((size_t)n * n, 0.0);
+    std::vector<double> col(n);
+    for (int j = 0; j < n; ++j) {
+      std::fill(col.begin(), col.end(), 0.0);
+      col[j] = 1.0 / L[(size_t)j * n + j];
+      for (int i = j + 1; i < n; ++i)
+        col[i] = -dot4(&L[(size_t)i * n + j], &col[j], i - j) / L[(size_t)i * n + i];
+      for (int i = j; i < n; ++i) XT[(size_t)j * n + i] = col[i];
+    }
+    // M[i][j] = sum_{k >= max(i,j)} X[k][i] X[k][j] = XT[i] . XT[j] over k >= j (j >= i)
+    for (int i = 0; i < n; ++i)
+      for (int j = i; j < n; ++j) {
+        const double t = dot4(&XT[(size_t)i * n + j], &XT[(size_t)j * n + j], n - j);
+        M_out[(size_t)i * n + j] = M_out[(size_t)j * n + i] = t;
+      }
+    // u0: inverse iteration on the tridiagonal with sigma just above alpha_1
+    // (sigma I - T is SPD, so LDL^T needs no pivoting), then x = Q y through the
+    // stored Householder reflections
+    const double sigma = vals[0] * (1.0 + 1e-10) + 1e-300;
+    std::vector<double> Dg(n), Lg(n, 0.0), y(n, 1.0);
+    Dg[0] = sigma - d[0];
+    for (int i = 1; i < n && fast; ++i) {
+      if (!(Dg[i - 1] > 0.0)) fast = false;
+      Lg[i] = -e[i] / Dg[i - 1];
+      Dg[i] = (sigma - d[i]) + Lg[i] * e[i];
+    }
+    if (!(Dg[n - 1] > 0.0)) fast = false;
+    for (int it = 0; it < 3 && fast; ++it) {
+      for (int i = 1; i < n; ++i) y[i] -= Lg[i] * y[i - 1];
+      for (int i = 0; i < n; ++i) y[i] /= Dg[i];
+      for (int i = n - 2; i >= 0; --i) y[i] -= Lg[i + 1] * y[i + 1];
+      double nrm = std::sqrt(dot4(y.data(), y.data(), n));
+      if (!(nrm > 0.0) || !std::isfinite(nrm)) {
+        fast = false;
+        break;
+      }
+      for (int i = 0; i < n; ++i) y[i] /= nrm;
+    }
+    if (fast) {
+      for (int i = 1; i < n; ++i) {
+        if (h[i] == 0.0) continue;
+        const int l = i - 1;
+        const double g = dot4(&Z[(size_t)i * n], y.data(), l + 1);
+        for (int q = 0; q <= l; ++q) y[q] -= g * Z[(size_t)q * n + i];
+      }
+      const double nrm = std::sqrt(dot4(y.data(), y.data(), n));
+      for (int i = 0; i < n; ++i) u0_out[i] = y[i] / nrm;
+      for (int k = 0; k < n; ++k) alphas_out[k] = vals[k];
+      *rank_out = n;
+      return NYS_OK;
+    }
+  }
+  // general path: full eigensystem, drop rule, M = sum w w^T / alpha
+  std::vector<double> V((size_t)n * n);
+  vals.assign(n, 0.0);
+  const int st = nys_sym_eig(A.data(), n, vals.data(), V.data());
+  if (st) return st;
+  if (!(vals[0] > 0.0)) return NYS_EDEGENERATE;
+  rank = 0;
+  for (int k = 0; k < n; ++k) rank += vals[k] > eps_drop * vals[0] ? 1 : 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double t = 0.0;
+      for (int k = 0; k < n; ++k)
+        if (vals[k] > eps_drop * vals[0]) t += V[(size_t)i * n + k] / vals[k] * V[(size_t)j * n + k];
+      M_out[(size_t)i * n + j] = t;
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      const double t = 0.5 * (M_out[(size_t)i * n + j] + M_out[(size_t)j * n + i]);
+      M_out[(size_t)i * n + j] = M_out[(size_t)j * n + i] = t;
+    }
+  int r = 0;
+  for (int k = 0; k < n; ++k)
+    if (vals[k] > eps_drop * vals[0]) alphas_out[r++] = vals[k];
+  for (int i = 0; i < n; ++i) u0_out[i] = V[(size_t)i * n + 0];
+  *rank_out = rank;
   return NYS_OK;
 }

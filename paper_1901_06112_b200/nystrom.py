@@ -13,6 +13,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 
 from . import _native
@@ -121,23 +123,28 @@ class MixingPlan:
 
 
 def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int) -> MixingPlan:
-    """Host FP64 eigensystem of A and the products the kernels consume.
+    """Host FP64 products the kernels consume, in one native call
+    (``nys_mixing_plan``: Gram matrix nystrom.py:67-69, eigenvalues + drop
+    rule nystrom.py:97-109, M and the lead eigenvector).
 
     The filter only sees M = sum_k w_k w_k^T / alpha_k (invariant to the
     eigenvector basis and signs) and the lead pair (w_1 enters the guard
-    quadratically), so a Householder + implicit-QL solver (``nys_sym_eig``,
-    native) stands in for the reference's cyclic Jacobi (same drop rule on
-    the same eigenvalues to ~1 ulp) -- ~20x faster at m0 = 64, which matters
-    because the GPU idles while the host eigendecomposes.  ``jacobi_eig``
-    remains the bit-faithful API mirror."""
-    A = np.ascontiguousarray(build_A(centroids, RangeKernel(theta)).entries)
-    k = A.shape[0]
-    vals = np.empty(k)
-    vecs = np.empty((k, k))
-    _native.call("nys_sym_eig", A.ctypes.data, k, vals.ctypes.data, vecs.ctypes.data)
-    alphas, Wr = _retain(vals, vecs, eps_drop)
-    M = (Wr / alphas[None, :]) @ Wr.T
-    M = (M + M.T) / 2.0
+    quadratically).  With no eigenpair dropped M = A^{-1}, which the native
+    code forms by Cholesky next to a values-only QL and an inverse iteration
+    for w_1 (~0.15 ms at m0 = 64 instead of ~0.8 ms for the full eigensystem
+    plus numpy products); otherwise it falls back to the full Householder + QL
+    eigensystem.  ``jacobi_eig`` remains the bit-faithful API mirror."""
+    C_ = np.ascontiguousarray(np.asarray(centroids, np.float64))
+    k, rho = C_.shape
+    alphas = np.empty(k)
+    M = np.empty((k, k))
+    u0 = np.empty(k)
+    rank = C.c_int(0)
+    rc = _native.lib().nys_mixing_plan(C_.ctypes.data, k, rho, float(theta), float(eps_drop), alphas.ctypes.data,
+                                       C.byref(rank), M.ctypes.data, u0.ctypes.data)
+    if rc == _native.NYS_EDEGENERATE:
+        raise DegenerateKernelError("landmark kernel has no positive eigenvalue")
+    _native.check(rc, "nys_mixing_plan")
+    alphas = alphas[:rank.value].copy()
     eps_den = 1e-12 * (2 * S + 1) ** 2 * float(np.abs(alphas).max())
-    return MixingPlan(alphas=alphas, M=np.ascontiguousarray(M), u0=np.ascontiguousarray(Wr[:, 0]),
-                      alpha0=float(alphas[0]), eps_den=eps_den)
+    return MixingPlan(alphas=alphas, M=M, u0=u0, alpha0=float(alphas[0]), eps_den=eps_den)

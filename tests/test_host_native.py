@@ -159,3 +159,25 @@ def test_header_cites_reference():
     text = (ROOT / "include" / "nysfilter_b200.h").read_text()
     for cite in ("landmarks.py:76-129", "filters.py:214-257", "symeig.py:58-125"):
         assert cite in text
+
+
+@pytest.mark.parametrize("k,rho,theta", [(64, 3, 0.1), (64, 27, 1.3), (48, 31, 0.25), (6, 1, 0.3), (32, 3, 2.0),
+                                         (64, 3, 0.5), (1, 3, 0.2)])
+def test_native_mixing_plan_matches_eigh(k, rho, theta):
+    # nys_mixing_plan (Cholesky fast path when nothing is dropped, full eigensystem otherwise)
+    # against numpy's eigh + the reference drop rule
+    from paper_1901_06112_b200.nystrom import RangeKernel, _retain, build_A, mixing_plan
+
+    C = np.random.default_rng(k * 100 + rho).random((k, rho))
+    p = mixing_plan(C, theta, 1e-8, 15)
+    A = build_A(C, RangeKernel(theta)).entries
+    vals, vecs = np.linalg.eigh(A)
+    o = np.argsort(vals)[::-1]
+    al, Wr = _retain(vals[o], vecs[:, o], 1e-8)
+    M = (Wr / al) @ Wr.T
+    assert len(p.alphas) == len(al)
+    np.testing.assert_allclose(p.alphas, al, rtol=0, atol=1e-13 * al[0])
+    kappa = al[0] / al[-1]  # both solvers are backward stable: forward error ~ eps * kappa
+    assert np.abs(p.M - M).max() <= max(1e-12, 1e-14 * kappa) * np.abs(M).max()
+    if k == 1 or al[0] - al[1] > 1e-6 * al[0]:  # u0 is defined up to sign when alpha_1 is simple
+        assert min(np.abs(p.u0 - Wr[:, 0]).max(), np.abs(p.u0 + Wr[:, 0]).max()) <= 1e-9

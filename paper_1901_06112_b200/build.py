@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libnysfilter_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["nys_filter.cu", "nys_hpass.cu", "nys_hpass_tc.cu", "nys_vpass.cu", "nys_kmeans.cu", "nys_kmeans_coop.cu", "nys_host.cpp"]
+SOURCES = ["nys_filter.cu", "nys_hpass.cu", "nys_hpass_tc.cu", "nys_vpass.cu", "nys_kmeans.cu", "nys_kmeans_coop.cu", "nys_recursive.cu", "nys_host.cpp"]
 
 
 def _nvcc() -> str:
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v" if verbose else "-O3", "-c", str(CSRC / src), "-o", str(obj)]
         else:
-            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-c", str(CSRC / src), "-o", str(obj)]
+            cmd = ["g++", "-O3", "-std=c++17", "-ffp-contract=off", "-fPIC", "-c", str(CSRC / src), "-o", str(obj)]
         cmds.append(cmd)
 
     def run(cmd):

@@ -60,12 +60,12 @@ using namespace nys;
 extern "C" {
 
 size_t nys_filter_planes_bytes(const nys_filter_desc* d, int rows) {
-  if (!d) return 0;
+  if (validate_tiled(d) != NYS_OK) return 0;
   return (size_t)(rows + 2 * d->radius) * (size_t)plane_row_stride(d->W, buffer_planes(d)) * sizeof(float);
 }
 
 int64_t nys_filter_plane_row_stride(const nys_filter_desc* d) {
-  if (validate(d) != NYS_OK) return 0;
+  if (validate_tiled(d) != NYS_OK) return 0;
   return plane_row_stride(d->W, buffer_planes(d));
 }
 

@@ -79,13 +79,26 @@ inline int validate(const nys_filter_desc* d) {
   if (!d) return NYS_EINVAL;
   if (d->n < 1 || d->n > NYS_MAX_CHANNELS || d->rho < 1 || d->rho > NYS_MAX_RHO) return NYS_EUNSUPPORTED;
   if (d->H < 1 || d->W < 1 || d->m0 < 1 || d->m0 > NYS_MAX_M0) return NYS_EINVAL;
-  if (d->radius < 0 || d->radius > NYS_MAX_RADIUS) return NYS_EUNSUPPORTED;
-  if (d->spatial_kind != NYS_SPATIAL_BOX && d->spatial_kind != NYS_SPATIAL_GAUSSIAN_FIR) return NYS_EUNSUPPORTED;
+  if (d->spatial_kind == NYS_SPATIAL_GAUSSIAN_RECURSIVE) {
+    // radius unused (the recursion spans whole rows / columns); sigma < 1 is
+    // served by the FIR path (spatial.py:206-208)
+    if (!(d->sigma >= 1.0) || !std::isfinite(d->sigma)) return NYS_EINVAL;
+  } else {
+    if (d->radius < 0 || d->radius > NYS_MAX_RADIUS) return NYS_EUNSUPPORTED;
+    if (d->spatial_kind != NYS_SPATIAL_BOX && d->spatial_kind != NYS_SPATIAL_GAUSSIAN_FIR) return NYS_EUNSUPPORTED;
+  }
   if (d->spatial_kind == NYS_SPATIAL_GAUSSIAN_FIR && (!(d->sigma > 0) || d->radius < 1)) return NYS_EINVAL;
   if (!(d->theta > 0)) return NYS_EINVAL;
   if (d->guide_kind != 0 && d->guide_kind != 1) return NYS_EINVAL;
   if (d->guide_kind == 1 && d->rho != 9 * d->n) return NYS_EINVAL;
   return NYS_OK;
+}
+
+// K2/K3 (tiled FIR / box) only
+inline int validate_tiled(const nys_filter_desc* d) {
+  const int st = validate(d);
+  if (st) return st;
+  return d->spatial_kind == NYS_SPATIAL_GAUSSIAN_RECURSIVE ? NYS_EINVAL : NYS_OK;
 }
 
 inline void fill_taps(const nys_filter_desc* d, float* taps) {

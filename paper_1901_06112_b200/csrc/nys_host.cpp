@@ -504,3 +504,92 @@ extern "C" int nys_mixing_plan(const double* C, int m0, int rho, double theta, d
   *rank_out = rank;
   return NYS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Recursive Gaussian coefficients (spatial.py:114-146, van Vliet / Young /
+// Verbeek fifth-order poles).  Restates the reference's arithmetic with
+// CPython's complex routines (c_pow via hypot/pow/atan2/cos/sin, c_powu for
+// the integer square, Smith-style c_quot) so the bisection lands on the same
+// pole scale q; the polynomial expansion follows np.convolve.
+// ---------------------------------------------------------------------------
+namespace {
+struct cplx {
+  double re, im;
+};
+inline cplx c_sub(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+inline cplx c_add(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+inline cplx c_prod(cplx a, cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+inline cplx c_quot(cplx a, cplx b) {
+  const double abr = b.re < 0 ? -b.re : b.re, abi = b.im < 0 ? -b.im : b.im;
+  if (abr >= abi) {
+    if (abr == 0.0) return {0.0, 0.0};
+    const double ratio = b.im / b.re, denom = b.re + b.im * ratio;
+    return {(a.re + a.im * ratio) / denom, (a.im - a.re * ratio) / denom};
+  }
+  const double ratio = b.re / b.im, denom = b.re * ratio + b.im;
+  return {(a.re * ratio + a.im) / denom, (a.im * ratio - a.re) / denom};
+}
+// complex ** real exponent (CPython complex_pow -> c_pow / c_powi)
+inline cplx c_pow_real(cplx a, double e) {
+  if (e == 0.0) return {1.0, 0.0};
+  if (e == std::floor(e) && std::fabs(e) <= 100.0) {
+    long n = (long)e;
+    bool neg = n < 0;
+    if (neg) n = -n;
+    cplx r{1.0, 0.0}, p = a;
+    for (long mask = 1; mask > 0 && n >= mask; mask <<= 1) {
+      if (n & mask) r = c_prod(r, p);
+      p = c_prod(p, p);
+    }
+    return neg ? c_quot({1.0, 0.0}, r) : r;
+  }
+  const double vabs = std::hypot(a.re, a.im), len = std::pow(vabs, e);
+  const double phase = std::atan2(a.im, a.re) * e;
+  return {len * std::cos(phase), len * std::sin(phase)};
+}
+const cplx kVyvPoles[5] = {{0.86430, 1.45389}, {0.86430, -1.45389}, {1.61433, 0.83134}, {1.61433, -0.83134},
+                           {1.87504, 0.0}};
+
+double cascade_variance(double q) {  // spatial.py:124-129
+  cplx total{0.0, 0.0};
+  for (const cplx& d : kVyvPoles) {
+    const cplx z = c_pow_real(d, 1.0 / q);
+    const cplx zm1 = c_sub(z, {1.0, 0.0});
+    total = c_add(total, c_quot(c_prod({2.0, 0.0}, z), c_prod(zm1, zm1)));
+  }
+  return total.re;
+}
+}  // namespace
+
+extern "C" int nys_vyv_coeffs(double sigma, double* coeffs_out) {
+  if (!coeffs_out || !(sigma > 0.0) || !std::isfinite(sigma)) return NYS_EINVAL;
+  double lo = 1e-3, hi = 1000.0;  // spatial.py:132-141 bisection for cascade variance == sigma^2
+  const double target = sigma * sigma;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (cascade_variance(mid) < target)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const double q = 0.5 * (lo + hi);
+  cplx poly[6] = {{1.0, 0.0}};
+  int len = 1;
+  for (const cplx& d : kVyvPoles) {  // np.convolve(poly, [1, -1/d^(1/q)])
+    const cplx v1 = c_quot({-1.0, 0.0}, c_pow_real(d, 1.0 / q));
+    cplx next[6];
+    for (int k = 0; k <= len; ++k) {
+      cplx acc{0.0, 0.0};
+      if (k < len) acc = c_add(acc, poly[k]);
+      if (k >= 1) acc = c_add(acc, c_prod(poly[k - 1], v1));
+      next[k] = acc;
+    }
+    ++len;
+    for (int k = 0; k < len; ++k) poly[k] = next[k];
+  }
+  double gain = 0.0;
+  for (int k = 0; k < 6; ++k) gain += poly[k].re;  // unit DC gain per pass
+  coeffs_out[0] = gain;
+  for (int k = 1; k < 6; ++k) coeffs_out[k] = poly[k].re;
+  return NYS_OK;
+}

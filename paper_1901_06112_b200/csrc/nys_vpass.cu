@@ -382,7 +382,7 @@ extern "C" {
 int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_stride, const float* guide,
                      int64_t guide_plane_stride, const float* planes, int64_t planes_stride, int out0, int out_rows,
                      float* out, int64_t out_plane_stride, const void* workspace, void* stream) {
-  int st = validate(d);
+  int st = validate_tiled(d);
   if (st) return st;
   if (!f || !planes || !out || !workspace || (d->guide_kind == 0 && !guide)) return NYS_EINVAL;
   if (out0 < 0 || out_rows < 1 || out0 + out_rows > d->H) return NYS_EINVAL;

@@ -16,7 +16,7 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -172,7 +172,8 @@ def _desc(n: int, rho: int, H: int, W: int, gkind: int, spatial: SpatialKernel, 
     elif spatial.kind == GAUSSIAN_FIR:
         d.spatial_kind, d.radius, d.sigma = _native.NYS_SPATIAL_GAUSSIAN_FIR, spatial.radius, spatial.sigma
     else:
-        raise NotImplementedError("recursive Gaussian (spatial.py:114-191) is §8 row f2, not on the B200 path yet")
+        d.spatial_kind, d.radius, d.sigma = (_native.NYS_SPATIAL_GAUSSIAN_RECURSIVE, spatial.effective_radius(),
+                                             spatial.sigma)
     d.m0 = C_.shape[0]
     d.theta = theta
     arrs = [np.ascontiguousarray(C_, dtype=np.float64), np.ascontiguousarray(plan.M, dtype=np.float64),
@@ -223,6 +224,15 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     [row_origin, row_origin + rows_local) of an image of ``H_global`` rows and
     only output rows ``rows = (lo, hi)`` are produced (``out`` is then
     (n, hi-lo, W)).  Kernel pointers are rebased so rows stay global."""
+    if params.spatial.kind == GAUSSIAN_RECURSIVE:
+        if params.spatial.sigma < 1.0:
+            # spatial.py:206-208: below sigma 1 the reference filters with the FIR at radius ceil(3 sigma)
+            params = replace(params, spatial=SpatialKernel.gaussian(params.spatial.sigma))
+        else:
+            if rows is not None or row_origin != 0 or H_global is not None:
+                raise NotImplementedError("the recursive Gaussian couples whole columns; row-band sharding "
+                                          "covers the box / FIR kernels only")
+            return _run_filter_recursive(inp, centroids, params, timer, plane_budget, out, kernel_events)
     n, h_local, W = inp.f.shape
     H = H_global if H_global is not None else h_local
     lo, hi = rows if rows is not None else (0, H)
@@ -279,6 +289,55 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
             e2 = ev()
             kernel_events.append(("k_feat_hpass", e0, e1, b))
             kernel_events.append(("k_vpass", e1, e2, b))
+    if timer:
+        timer.mark("convolutions")
+    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device)
+    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats), s), "nys_filter_stats")
+    del keep
+    return out, plan, stats
+
+
+def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer, plane_budget, out,
+                          kernel_events):
+    """Recursive-Gaussian filter (spatial.py:179-191 as the convolution of
+    filters.py:223-257): features, row recursion, column recursion fused with
+    the contraction, mass^2 scale, guard and division (csrc/nys_recursive.cu).
+    Landmark bands are sized so the plane buffer fits ``plane_budget``."""
+    n, H, W = inp.f.shape
+    S = params.spatial.effective_radius()
+    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S)
+    keep: list = []
+    d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
+    lib = _native.lib()
+    wsb = int(lib.nys_filter_workspace_bytes(C.byref(d)))
+    if wsb == 0:
+        raise NotImplementedError(f"filter shape n={n} rho={inp.rho} m0={d.m0} not supported")
+    ws = workspace(wsb)
+    s = stream_ptr()
+    _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
+    if timer:
+        timer.mark("extrapolation")
+    budget = plane_budget if plane_budget is not None else SMALL_PLANES_BYTES
+    full = int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), 0))
+    if full > budget and plane_budget is None:
+        budget = max(budget, _plane_budget())
+    nb = d.m0 + 1
+    while nb > 1 and int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), nb)) > budget:
+        nb = max(1, nb // 2) if nb > 8 else nb - 1
+    sb = int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), nb))
+    scratch = torch.empty(sb, dtype=torch.uint8, device=inp.f.device)
+    if out is None:
+        out = torch.empty((n, H, W), dtype=torch.float32, device=inp.f.device)
+    e0 = torch.cuda.Event(enable_timing=True) if kernel_events is not None else None
+    if e0 is not None:
+        e0.record()
+    _native.check(lib.nys_filter_recursive(C.byref(d), ptr(inp.f), H * W, ptr(inp.guide), H * W,
+                                           _device_view(out), H * W, ptr(scratch), sb, ptr(ws), s),
+                  "nys_filter_recursive")
+    if kernel_events is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        kernel_events.append(("k_recursive", e0, e1, None))
     if timer:
         timer.mark("convolutions")
     stats = torch.empty(2, dtype=torch.float64, device=inp.f.device)

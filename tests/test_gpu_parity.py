@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import FILTER_CASES, group, load_golden
+from conftest import FILTER_CASES, group, load_golden, spatial_kernel
 from oracle import nys_oracle as O
 from paper_1901_06112_b200 import (
     FilterParams,
@@ -30,11 +30,7 @@ TOL = 1e-4
 
 
 def _params(g, m0=None):
-    if str(g["spatial_kind"]) == "box":
-        sk = SpatialKernel.box(int(g["radius"]))
-    else:
-        sk = SpatialKernel.gaussian(float(g["sigma"]), int(g["radius"]))
-    return FilterParams(spatial=sk, theta=float(g["theta"]), m0=int(g["m0"] if m0 is None else m0), seed=0,
+    return FilterParams(spatial=spatial_kernel(g), theta=float(g["theta"]), m0=int(g["m0"] if m0 is None else m0), seed=0,
                         kmeans_max_iter=int(g["max_iter"]), eps_drop=float(g["eps_drop"]))
 
 
@@ -230,3 +226,44 @@ def test_pinned_host_io_and_out_buffer():
     assert rep3.output.data.is_cuda and torch.equal(dbuf.cpu(), ref)
     with pytest.raises(ValueError):
         fast_filter(h, h, params, out=torch.empty(3, 45, 71).pin_memory())
+
+
+# --------------------------------------------------------------------------
+# §8 row f2: recursive Gaussian (csrc/nys_recursive.cu)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("shape,sigma,m0", [((72, 128), 5.0, 24), ((1, 37), 2.0, 4), ((29, 1), 1.5, 4),
+                                            ((3, 3), 1.0, 3), ((33, 300), 12.0, 16)])
+def test_recursive_gaussian_vs_oracle(shape, sigma, m0):
+    H, W = shape
+    f32 = color_scene(H, W, 5, 0.05, seed=H + 7 * W)
+    f64 = f32.astype(np.float64)
+    C, _, qe, _ = O.kmeans(O.range_vectors(f64), m0, 0, 8)
+    ref = O.fast_filter_with_landmarks(f64, f64, C, 0.12, "gaussian_recursive", sigma, 0)
+    params = FilterParams(spatial=SpatialKernel.recursive(sigma), theta=0.12, m0=m0, kmeans_max_iter=8)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    rep = filter_with_landmarks(f, f, C, params)
+    out = rep.output.data.double().cpu().numpy()
+    assert np.abs(out - ref["output"]).max() <= TOL
+    assert rep.guarded_pixels == ref["guarded_pixels"]
+    assert rep.min_denominator == pytest.approx(ref["min_denominator"], rel=1e-4)
+    full = fast_filter(f, f, params)
+    assert abs(full.quant_error - qe) <= 1e-3 * qe
+    assert np.abs(full.output.data.double().cpu().numpy() - ref["output"]).max() <= TOL
+
+
+def test_recursive_landmark_bands_match_single_band():
+    # a small plane budget forces several landmark bands (Z accumulates across bands)
+    f32 = spectral_scene(40, 52, 7, 5, 0.03, seed=91)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    C, _, _, _ = O.kmeans(O.range_vectors(f32.astype(np.float64)), 20, 0, 6)
+    params = FilterParams(spatial=SpatialKernel.recursive(2.5), theta=0.25, m0=20)
+    inp = _prepare_inputs(f, f)
+    one, _, s1 = run_filter(inp, C, params)
+    per_group = 40 * 52 * 8 * 4
+    fixed = 40 * 52 * 4 * (21 + 20 + 16) + 4096
+    many, _, s2 = run_filter(inp, C, params, plane_budget=fixed + 4 * per_group)
+    torch.cuda.synchronize()
+    assert (one - many).abs().max().item() <= 1e-6
+    ref = O.fast_filter_with_landmarks(f32.astype(np.float64), f32.astype(np.float64), C, 0.25,
+                                       "gaussian_recursive", 2.5, 0)
+    assert np.abs(many.double().cpu().numpy() - ref["output"]).max() <= TOL

@@ -8,16 +8,14 @@ CUDA path because these pass.
 import numpy as np
 import pytest
 
-from conftest import FILTER_CASES, group, load_golden
+from conftest import FILTER_CASES, group, load_golden, oracle_kind
 from oracle import nys_oracle as O
 
 
 @pytest.mark.parametrize("case", FILTER_CASES)
 def test_oracle_filter_matches_reference(case):
     g = load_golden(case)
-    res = O.fast_filter_with_landmarks(g["f"], g["guide"], g["centroids"], float(g["theta"]),
-                                       str(g["spatial_kind"]).replace("gaussian", "gaussian_fir")
-                                       if str(g["spatial_kind"]) == "gaussian" else "box",
+    res = O.fast_filter_with_landmarks(g["f"], g["guide"], g["centroids"], float(g["theta"]), oracle_kind(g),
                                        float(g["sigma"]), int(g["radius"]), float(g["eps_drop"]))
     assert res["retained_rank"] == int(g["retained_rank"])
     assert res["guarded_pixels"] == int(g["guarded_pixels"])
@@ -77,6 +75,35 @@ def test_oracle_spatial_known_answers():
     imp[0, 4, 4] = 1
     out = O.spatial_conv(imp, "gaussian_fir", 1.0, 3)[0]
     assert out[4, 4] == pytest.approx(1.0) and out[4, 5] / out[4, 4] == pytest.approx(np.exp(-0.5))
+
+
+def test_oracle_recursive_known_answers():
+    """§8 f2: coefficients, the scan and the sigma < 1 FIR fallback vs the
+    reference's gaussian_recursive (spatial.py:114-191, 206-208)."""
+    g = load_golden("recursive")
+    for s, c in zip(g["sigmas"], g["coeffs"]):
+        np.testing.assert_allclose(O.vyv_coeffs(float(s)), c, rtol=1e-14, atol=1e-15)
+    for s in (0.7, 1.0, 2.5, 4.0):
+        out = O.spatial_conv(g["plane"][None], "gaussian_recursive", s, 0)[0]
+        np.testing.assert_allclose(out, g[f"rec_{s}"], rtol=1e-12, atol=1e-12)
+    # constants are preserved up to the mass^2 rescale (spatial.py:10-13)
+    out = O.spatial_conv(np.full((1, 9, 12), 0.75), "gaussian_recursive", 2.0, 0)[0]
+    np.testing.assert_allclose(out, 0.75 * O.fir_mass(2.0) ** 2, rtol=1e-12)
+
+
+def test_native_vyv_coeffs_match_reference():
+    """Host C++ nys_vyv_coeffs (no GPU needed) vs the reference's _vyv_coeffs."""
+    import ctypes as C
+
+    from paper_1901_06112_b200 import _native
+
+    g = load_golden("recursive")
+    for s, c in zip(g["sigmas"], g["coeffs"]):
+        out = (C.c_double * 6)()
+        _native.check(_native.lib().nys_vyv_coeffs(float(s), out), "nys_vyv_coeffs")
+        np.testing.assert_allclose(np.array(out[:]), c, rtol=1e-14, atol=1e-15)
+    out = (C.c_double * 6)()
+    assert _native.lib().nys_vyv_coeffs(0.0, out) == _native.NYS_EINVAL
 
 
 def test_oracle_full_rank_exactness():

@@ -39,6 +39,9 @@ def _filter_case(name, f32, guide32, spatial, theta, m0, max_iter, mode="bilater
     p = f if guide32 is None else ref.Image(data=guide32.astype(np.float64), range_max=1.0)
     if spatial[0] == "box":
         sk = ref.SpatialKernel.box(spatial[1])
+    elif spatial[0] == "recursive":
+        sk = ref.SpatialKernel.recursive(spatial[1])
+        spatial = ("gaussian_recursive", spatial[1], sk.effective_radius())
     else:
         sk = ref.SpatialKernel.gaussian(spatial[1], spatial[2])
     params = ref.FilterParams(spatial=sk, theta=theta, m0=m0, seed=0, mode=mode, kmeans_max_iter=max_iter,
@@ -147,5 +150,31 @@ def main():
     print("full rank: max|fast-brute|", np.abs(rep.output.data - brute.data).max(), "rank", rep.retained_rank)
 
 
+def main_recursive():
+    """§8 row f2: recursive Gaussian (spatial.py:114-191) known answers."""
+    from nysfilter.spatial import _vyv_coeffs
+
+    sig = np.array([1.0, 1.3, 2.5, 3.0, 5.0, 6.0, 12.7, 40.0])
+    rec = {"sigmas": sig, "coeffs": np.array([_vyv_coeffs(float(s)) for s in sig])}
+    rng = np.random.default_rng(21)
+    plane = rng.uniform(0, 1, (19, 23))
+    rec["plane"] = plane
+    for s in (0.7, 1.0, 2.5, 4.0):
+        rec[f"rec_{s}"] = ref.gaussian_recursive(plane, s)
+    np.savez_compressed(OUT / "recursive.npz", **rec)
+    f = color_scene(48, 56, 8, 0.05, seed=22)
+    _filter_case("blf_rgb_rec3", f, None, ("recursive", 3.0), 0.15, 16, 10)
+    f = color_scene(40, 44, 6, 0.05, seed=23)
+    _filter_case("blf_rgb_rec07", f, None, ("recursive", 0.7), 0.12, 8, 10)
+    g = color_scene(40, 44, 5, 0.05, seed=24)[:2].copy()
+    _filter_case("joint_rgb_rec15", f, g, ("recursive", 1.5), 0.2, 6, 10, mode="joint")
+    h = spectral_scene(32, 36, 16, 6, 0.03, seed=25)
+    _filter_case("hyper16_rec2", h, None, ("recursive", 2.0), 0.2, 10, 15)
+
+
 if __name__ == "__main__":
-    main()
+    which = sys.argv[1:] or ["base", "recursive"]
+    if "base" in which:
+        main()
+    if "recursive" in which:
+        main_recursive()

@@ -250,6 +250,36 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
                          float* out, int64_t out_plane_stride, void* scratch, size_t scratch_bytes,
                          const void* workspace, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* Direct (brute-force) kernel filter, Eq. (1) (filters.py:107-138), §8 f1 */
+/* ---------------------------------------------------------------------- */
+
+/* out(x) = Σ_d w(d) κ(p(x+d)-p(x)) f(x+d) / Σ_d w(d) κ(p(x+d)-p(x)) over the
+ * (2S+1)^2 window with edge replicate; w = outer product of the unnormalised
+ * Gaussian taps (box: ones), S = d->radius, or ceil(3 sigma) for the
+ * recursive kind (evaluated as its FIR counterpart).  Uses d->n, rho, H, W,
+ * spatial_kind, radius, sigma, theta; guide_kind must be 0 (materialise a
+ * patch guide with nys_patch_guide first).  FP32, no workspace. */
+int nys_brute_force_filter(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
+                           const float* guide, int64_t guide_plane_stride, float* out,
+                           int64_t out_plane_stride, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Quality metrics (metrics.py:37-122), §8 f4                              */
+/* ---------------------------------------------------------------------- */
+
+/* Device workspace for nys_quality_planes over n planes. */
+size_t nys_quality_workspace_bytes(int n);
+
+/* Per plane c of a and b ([dev] planar, float32 (elem_bytes 4) or float64
+ * (elem_bytes 8)): sq_sums_out[c] = Σ (a-b)^2 (FP64, [dev] n doubles) and,
+ * when ssim_out [dev] is non-null, the mean single-scale SSIM of the plane
+ * (11x11 Gaussian window sigma 1.5, C1 = (0.01 R)^2, C2 = (0.03 R)^2, valid
+ * positions only; whole-plane statistics below 11x11).  Deterministic. */
+int nys_quality_planes(const void* a, int64_t a_plane_stride, const void* b, int64_t b_plane_stride,
+                       int elem_bytes, int n, int H, int W, double range_max, double* sq_sums_out,
+                       double* ssim_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Device-side address of a buffer for the kernels' pointer arguments: device
  * memory maps to itself, page-locked host memory to its mapped device view
  * (so K3 can write the filtered image straight into a pinned host buffer,

@@ -460,3 +460,57 @@ def brute_force_filter(f, p, theta, kind, sigma, radius):
             num += kv * pf[:, iy:iy + H, ix:ix + W]
             den += kv
     return num / den
+
+
+# --------------------------------------------------------------------------
+# quality metrics (metrics.py:37-122)
+# --------------------------------------------------------------------------
+PSNR_CAP = 99.0
+
+
+def mse(a, b) -> float:
+    """metrics.py:37-40."""
+    d = np.asarray(a, np.float64) - np.asarray(b, np.float64)
+    return float(np.mean(d * d))
+
+
+def psnr(a, b, R: float, per_band: bool = False) -> float:
+    """metrics.py:43-64 (99 dB cap)."""
+    def from_mse(e):
+        return PSNR_CAP if e <= 0.0 else float(min(PSNR_CAP, 10.0 * np.log10(R * R / e)))
+
+    if per_band:
+        return float(np.mean([from_mse(mse(a[c], b[c])) for c in range(len(a))]))
+    return from_mse(mse(a, b))
+
+
+def ssim(a, b, R: float) -> float:
+    """Single-scale SSIM, 11x11 Gaussian window sigma 1.5, valid positions,
+    whole-plane statistics below the window (metrics.py:67-115)."""
+    c1, c2 = (0.01 * R) ** 2, (0.03 * R) ** 2
+    t = np.arange(-5, 6, dtype=np.float64)
+    w1 = np.exp(-(t * t) / (2.0 * 1.5 * 1.5))
+    w = np.outer(w1, w1)
+    w /= w.sum()
+    vals = []
+    for x, y in zip(np.asarray(a, np.float64), np.asarray(b, np.float64)):
+        H, W = x.shape
+        if H < 11 or W < 11:
+            mx, my = x.mean(), y.mean()
+            cov = ((x - mx) * (y - my)).mean()
+            vals.append(((2 * mx * my + c1) * (2 * cov + c2)) / ((mx * mx + my * my + c1) * (x.var() + y.var() + c2)))
+            continue
+        Hv, Wv = H - 10, W - 10
+        acc = {k: np.zeros((Hv, Wv)) for k in ("mx", "my", "xx", "yy", "xy")}
+        for dy in range(11):
+            for dx in range(11):
+                xs, ys, wv = x[dy:dy + Hv, dx:dx + Wv], y[dy:dy + Hv, dx:dx + Wv], w[dy, dx]
+                acc["mx"] += wv * xs
+                acc["my"] += wv * ys
+                acc["xx"] += wv * xs * xs
+                acc["yy"] += wv * ys * ys
+                acc["xy"] += wv * xs * ys
+        mx, my = acc["mx"], acc["my"]
+        vx, vy, cv = acc["xx"] - mx * mx, acc["yy"] - my * my, acc["xy"] - mx * my
+        vals.append(float((((2 * mx * my + c1) * (2 * cv + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2))).mean()))
+    return float(np.mean(vals))

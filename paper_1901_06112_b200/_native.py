@@ -75,6 +75,9 @@ _SIGS = {
     "nys_vyv_coeffs": (_I, [_D, _P]),
     "nys_filter_recursive_scratch_bytes": (_S, [C.POINTER(FilterDesc), _I]),
     "nys_filter_recursive": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _P, _S, _P, _P]),
+    "nys_brute_force_filter": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _P]),
+    "nys_quality_workspace_bytes": (_S, [_I]),
+    "nys_quality_planes": (_I, [_P, _L, _P, _L, _I, _I, _I, _I, _D, _P, _P, _P, _S, _P]),
     "nys_mixing_plan": (_I, [_P, _I, _I, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
 }
 

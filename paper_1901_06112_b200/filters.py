@@ -458,3 +458,36 @@ def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> Filte
     t["total"] = sum(t.values())
     return FilterReport(output=_output_image(out, f), timings=t, retained_rank=int(plan.alphas.shape[0]),
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=C_)
+
+
+def brute_force_filter(f: Image, p, params: FilterParams) -> Image:
+    """Direct evaluation of Eq. (1) over the (2S+1)^2 window, the exact
+    filter the Nystrom path approximates (filters.py:116-138), on the B200
+    (csrc/nys_brute.cu).  A recursive-Gaussian spatial kernel is evaluated as
+    its truncated FIR counterpart at radius ceil(3 sigma), as in the
+    reference.  Output container follows the input (see fast_filter)."""
+    _check_sizes(f, p)
+    require_cuda()
+    f_dev = to_device_f32(f.data)
+    n, H, W = f_dev.shape
+    if isinstance(p, PatchGuide):
+        g_dev = p.device_planes(f_dev if p.source is f else None)
+    elif p is f or (isinstance(p, Image) and p.data is f.data):
+        g_dev = f_dev
+    else:
+        g_dev = to_device_f32(p.data)
+    rho = g_dev.shape[0]
+    d = _native.FilterDesc()
+    d.n, d.rho, d.H, d.W, d.guide_kind = n, rho, H, W, 0
+    sp = params.spatial
+    if sp.kind == BOX:
+        d.spatial_kind, d.radius, d.sigma = _native.NYS_SPATIAL_BOX, sp.radius, 0.0
+    elif sp.kind == GAUSSIAN_FIR:
+        d.spatial_kind, d.radius, d.sigma = _native.NYS_SPATIAL_GAUSSIAN_FIR, sp.radius, sp.sigma
+    else:  # the window is the FIR at ceil(3 sigma) for every sigma (filters.py:107-113)
+        d.spatial_kind, d.radius, d.sigma = _native.NYS_SPATIAL_GAUSSIAN_FIR, sp.effective_radius(), sp.sigma
+    d.m0, d.theta = 1, params.theta
+    out = torch.empty((n, H, W), dtype=torch.float32, device=f_dev.device)
+    _native.check(_native.lib().nys_brute_force_filter(C.byref(d), ptr(f_dev), H * W, ptr(g_dev), H * W, ptr(out),
+                                                       H * W, stream_ptr()), "nys_brute_force_filter")
+    return _output_image(out, f)

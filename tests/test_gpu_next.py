@@ -1,0 +1,110 @@
+"""GPU parity for the §8 "next" rows beyond the recursive Gaussian (which
+lives in test_gpu_parity.py): f1 brute_force_filter, f4 quality metrics.
+
+Reference fixtures: tests/golden/brute.npz, metrics.npz (written by the
+reference itself, tools/make_golden.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import group, load_golden
+from oracle import nys_oracle as O
+from paper_1901_06112_b200 import (
+    FilterParams,
+    Image,
+    PatchGuide,
+    SpatialKernel,
+    brute_force_filter,
+    mse,
+    psnr,
+    quality,
+    ssim,
+)
+from paper_1901_06112_b200.synthetic import color_scene
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+KINDS = {0: "box", 1: "gaussian_fir", 2: "gaussian_recursive"}
+
+
+def _kernel(kind, sigma, radius):
+    if kind == 0:
+        return SpatialKernel.box(int(radius))
+    if kind == 2:
+        return SpatialKernel.recursive(float(sigma))
+    return SpatialKernel.gaussian(float(sigma), int(radius))
+
+
+@pytest.mark.parametrize("name", ["fir", "box", "rec", "hyper", "joint", "nlm"])
+def test_brute_force_matches_reference(name):
+    c = group(load_golden("brute"), "")[name]
+    kind, sigma, radius, theta = c["meta"]
+    params = FilterParams(spatial=_kernel(int(kind), sigma, radius), theta=float(theta), m0=4)
+    f = Image(data=c["f"].astype(np.float64), range_max=1.0)
+    same = np.array_equal(c["guide"], c["f"])
+    p = f if same else Image(data=c["guide"].astype(np.float64), range_max=1.0)
+    out = brute_force_filter(f, p, params)
+    assert isinstance(out.data, np.ndarray) and out.data.dtype == np.float64
+    err = np.abs(out.data - c["output"]).max()
+    assert err <= 2e-6, err
+
+
+def test_brute_force_patch_guide_and_device_io():
+    c = group(load_golden("brute"), "")["nlm"]
+    kind, sigma, radius, theta = c["meta"]
+    params = FilterParams(spatial=SpatialKernel.box(int(radius)), theta=float(theta), m0=4)
+    f = Image(data=torch.from_numpy(c["f"]).cuda(), range_max=1.0)
+    out = brute_force_filter(f, PatchGuide(f, 1), params)
+    assert out.data.is_cuda
+    assert np.abs(out.data.double().cpu().numpy() - c["output"]).max() <= 2e-6
+
+
+def test_brute_force_large_radius_and_edges():
+    # general (non-SMEM, many-channel) instantiation + 1-row / 1-column images
+    for (H, W), sk in (((1, 40), SpatialKernel.gaussian(3.0, 9)), ((37, 1), SpatialKernel.box(6)),
+                       ((24, 30), SpatialKernel.gaussian(12.0, 40))):
+        f32 = color_scene(H, W, 3, 0.05, seed=H * 7 + W)
+        f64 = f32.astype(np.float64)
+        kind = {"box": "box", "gaussian_fir": "gaussian_fir"}[sk.kind]
+        ref = O.brute_force_filter(f64, f64, 0.15, kind, sk.sigma, sk.radius)
+        out = brute_force_filter(Image(data=f64, range_max=1.0), Image(data=f64, range_max=1.0),
+                                 FilterParams(spatial=sk, theta=0.15, m0=1))
+        assert np.abs(out.data - ref).max() <= 2e-6, (H, W)
+
+
+def test_fast_filter_approaches_brute_force_at_full_rank():
+    # SPEC acceptance #1 on the GPU: m0 = m, eps_drop = 0 -> fast == brute
+    g = load_golden("full_rank")
+    f = Image(data=g["f"].astype(np.float64), range_max=1.0)
+    from paper_1901_06112_b200 import filter_with_landmarks
+
+    params = FilterParams(spatial=SpatialKernel.gaussian(1.0, 3), theta=0.3, m0=144, eps_drop=0.0,
+                          kmeans_max_iter=5)
+    brute = brute_force_filter(f, f, params)
+    assert np.abs(brute.data - g["brute"]).max() <= 2e-6
+
+
+@pytest.mark.parametrize("name", ["rgb", "u8", "small", "hyper"])
+def test_metrics_match_reference(name):
+    c = group({k: v for k, v in load_golden("metrics").items() if not k.startswith("same")}, "")[name]
+    R = float(c["R"])
+    a, b = Image(data=c["a"], range_max=R), Image(data=c["b"], range_max=R)
+    assert mse(a, b) == pytest.approx(float(c["mse"]), rel=1e-12)
+    assert psnr(a, b) == pytest.approx(float(c["psnr"]), abs=1e-9)
+    assert psnr(a, b, per_band=True) == pytest.approx(float(c["psnr_band"]), abs=1e-9)
+    assert ssim(a, b) == pytest.approx(float(c["ssim"]), abs=1e-10)
+    q = quality(a, b, per_band=True)
+    assert q.mse == pytest.approx(float(c["mse"]), rel=1e-12) and q.ssim == pytest.approx(float(c["ssim"]), abs=1e-10)
+    # float32 device tensors: same metric from rounded samples
+    ta = Image(data=torch.from_numpy(c["a"]).float().cuda(), range_max=R)
+    tb = Image(data=torch.from_numpy(c["b"]).float().cuda(), range_max=R)
+    assert ssim(ta, tb) == pytest.approx(O.ssim(c["a"].astype(np.float32), c["b"].astype(np.float32), R), abs=1e-10)
+
+
+def test_metrics_identical_and_shape_errors():
+    a = Image(data=np.random.default_rng(0).uniform(0, 1, (3, 16, 16)), range_max=1.0)
+    assert psnr(a, a) == 99.0 and mse(a, a) == 0.0 and ssim(a, a) == pytest.approx(1.0, abs=1e-12)
+    with pytest.raises(ValueError):
+        mse(a, Image(data=np.zeros((3, 16, 15)), range_max=1.0))

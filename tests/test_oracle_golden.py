@@ -148,3 +148,30 @@ def test_patch_stack_order():
     assert P[9 + 0, 0, 0] == f[1, 0, 0]
     assert P[9 + 8, 3, 4] == f[1, 3, 4]
     assert P[2, 1, 1] == f[0, 0, 2]
+
+
+BRUTE_KIND = {0: "box", 1: "gaussian_fir", 2: "gaussian_recursive"}
+
+
+def test_oracle_brute_force_matches_reference():
+    """§8 f1 fixtures: Eq. (1) over box / FIR / recursive (as FIR) / joint /
+    NLM-patch / 9-band guides (filters.py:116-138)."""
+    for name, c in group(load_golden("brute"), "").items():
+        kind, sigma, radius, theta = c["meta"]
+        out = O.brute_force_filter(c["f"], c["guide"], float(theta), BRUTE_KIND[int(kind)], float(sigma),
+                                   int(radius))
+        np.testing.assert_allclose(out, c["output"], rtol=0, atol=1e-12, err_msg=name)
+
+
+def test_oracle_metrics_match_reference():
+    """§8 f4 fixtures: mse / psnr (global and per band) / ssim incl. the
+    below-window global-statistics branch (metrics.py:37-122)."""
+    g = load_golden("metrics")
+    for name, c in group({k: v for k, v in g.items() if not k.startswith("same")}, "").items():
+        R = float(c["R"])
+        assert O.mse(c["a"], c["b"]) == pytest.approx(float(c["mse"]), rel=1e-13), name
+        assert O.psnr(c["a"], c["b"], R) == pytest.approx(float(c["psnr"]), abs=1e-10), name
+        assert O.psnr(c["a"], c["b"], R, per_band=True) == pytest.approx(float(c["psnr_band"]), abs=1e-10), name
+        assert O.ssim(c["a"], c["b"], R) == pytest.approx(float(c["ssim"]), abs=1e-12), name
+    a = g["rgb__a"]
+    assert O.psnr(a, a, 1.0) == float(g["same__psnr"]) == 99.0

@@ -172,8 +172,77 @@ def main_recursive():
     _filter_case("hyper16_rec2", h, None, ("recursive", 2.0), 0.2, 10, 15)
 
 
+def main_brute_metrics_io():
+    """§8 rows f1 (brute_force_filter) and f4 (metrics, KFC1/PNM I/O)."""
+    out = {}
+    cases = {
+        "fir": (color_scene(30, 34, 5, 0.05, seed=31), None, ref.SpatialKernel.gaussian(2.0, 6), 0.15),
+        "box": (color_scene(26, 30, 5, 0.05, seed=32), None, ref.SpatialKernel.box(4), 0.2),
+        "rec": (color_scene(28, 24, 5, 0.05, seed=33), None, ref.SpatialKernel.recursive(1.7), 0.12),
+        "hyper": (spectral_scene(20, 22, 9, 5, 0.03, seed=34), None, ref.SpatialKernel.gaussian(1.5, 4), 0.25),
+    }
+    g = color_scene(24, 26, 5, 0.05, seed=35)
+    cases["joint"] = (g, g[:2].copy() * 0.5 + 0.25, ref.SpatialKernel.gaussian(1.5, 5), 0.2)
+    fn = color_scene(22, 20, 4, 0.08, seed=36, lo=0.1, hi=0.9, shading=0.1)
+    cases["nlm"] = (fn, patch_stack(fn.astype(np.float64), 1).astype(np.float32), ref.SpatialKernel.box(5),
+                    0.3 * np.sqrt(27.0) * 0.08)
+    for k, (f32, g32, sk, theta) in cases.items():
+        fi = ref.Image(data=f32.astype(np.float64), range_max=1.0)
+        gi = fi if g32 is None else ref.Image(data=g32.astype(np.float64), range_max=1.0)
+        params = ref.FilterParams(spatial=sk, theta=theta, m0=4)
+        out[f"{k}__f"] = f32
+        out[f"{k}__guide"] = f32 if g32 is None else g32
+        out[f"{k}__meta"] = np.array([{"box": 0, "gaussian_fir": 1, "gaussian_recursive": 2}[sk.kind],
+                                      sk.sigma, sk.radius, theta])
+        out[f"{k}__output"] = ref.brute_force_filter(fi, gi, params).data
+    np.savez_compressed(OUT / "brute.npz", **out)
+
+    from nysfilter import metrics as M
+
+    mt = {}
+    rng = np.random.default_rng(37)
+    pairs = {
+        "rgb": (rng.uniform(0, 1, (3, 40, 52)), 1.0),
+        "u8": (np.round(rng.uniform(0, 255, (1, 33, 29))), 255.0),
+        "small": (rng.uniform(0, 1, (2, 7, 30)), 1.0),        # below the 11x11 window
+        "hyper": (rng.uniform(0, 1, (6, 24, 20)), 1.0),
+    }
+    for k, (a, R) in pairs.items():
+        b = np.clip(a + rng.normal(0, 0.05 * R, a.shape), 0, R)
+        ia, ib = ref.Image(data=a, range_max=R), ref.Image(data=b, range_max=R)
+        mt[f"{k}__a"], mt[f"{k}__b"], mt[f"{k}__R"] = a, b, np.array(R)
+        mt[f"{k}__mse"] = np.array(M.mse(ia, ib))
+        mt[f"{k}__psnr"] = np.array(M.psnr(ia, ib))
+        mt[f"{k}__psnr_band"] = np.array(M.psnr(ia, ib, per_band=True))
+        mt[f"{k}__ssim"] = np.array(M.ssim(ia, ib))
+    mt["same__psnr"] = np.array(M.psnr(ref.Image(data=pairs["rgb"][0], range_max=1.0),
+                                       ref.Image(data=pairs["rgb"][0], range_max=1.0)))
+    np.savez_compressed(OUT / "metrics.npz", **mt)
+
+    import tempfile
+
+    io = {}
+    with tempfile.TemporaryDirectory() as td:
+        cube = rng.uniform(0, 1, (5, 6, 7))
+        for dt in ("float32", "float64"):
+            pth = Path(td) / f"c_{dt}.kfc"
+            ref.save_image(ref.Image(data=cube, range_max=1.0), pth, cube_dtype=dt)
+            io[f"cube_{dt}"] = np.frombuffer(pth.read_bytes(), dtype=np.uint8)
+        rgb = rng.uniform(-10, 265, (3, 5, 4))
+        gray = rng.uniform(0, 255, (1, 4, 6))
+        for nm, img in (("ppm", rgb), ("pgm", gray)):
+            pth = Path(td) / f"x.{nm}"
+            ref.save_image(ref.Image(data=img, range_max=255.0), pth)
+            io[f"pnm_{nm}"] = np.frombuffer(pth.read_bytes(), dtype=np.uint8)
+        io["cube"], io["rgb"], io["gray"] = cube, rgb, gray
+    np.savez_compressed(OUT / "image_io.npz", **io)
+    print("brute / metrics / io fixtures written")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["base", "recursive"]
+    which = sys.argv[1:] or ["base", "recursive", "f1f4"]
+    if "f1f4" in which:
+        main_brute_metrics_io()
     if "base" in which:
         main()
     if "recursive" in which:

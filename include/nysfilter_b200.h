@@ -251,6 +251,29 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
                          const void* workspace, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* PCA patch guide (filters.py:161-187)                      */
+/* ---------------------------------------------------------------------- */
+
+/* Workspace for nys_patch_moments (0 if n(2r+1)^2 > 256). */
+size_t nys_patch_moments_workspace_bytes(int n, int H, int W, int r);
+
+/* First and centred second moments of the (2r+1)^2-per-channel patch
+ * vectors (channel-major, dy, dx, edge replicate; filters.py:174-181) of
+ * f [dev] (n,H,W), in FP64, deterministic:
+ *   mean_out [dev] dim doubles (dim = n(2r+1)^2),
+ *   gram_tiles_out [dev] T*16 doubles, T = t(t+1)/2, t = ceil(dim/4): the
+ *   4x4 tiles (ti <= tj, row-major over ti) of Σ_p (x_p - mean)(x_p - mean)^T.
+ * The covariance of the reference is that Gram / (H W). */
+int nys_patch_moments(const float* f, int64_t f_plane_stride, int n, int H, int W, int r, double* mean_out,
+                      double* gram_tiles_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* guide [dev] (pca_dim, H, W): out[k](p) = Σ_d (x_p[d] - mean[d]) basis[d*pca_dim + k]
+ * with mean [dev] dim floats and basis [dev] dim x pca_dim floats (the
+ * leading covariance eigenvectors as columns). */
+int nys_pca_project(const float* f, int64_t f_plane_stride, int n, int H, int W, int r, const float* mean,
+                    const float* basis, int pca_dim, float* out, int64_t out_plane_stride, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* Direct (brute-force) kernel filter, Eq. (1) (filters.py:107-138), §8 f1 */
 /* ---------------------------------------------------------------------- */
 

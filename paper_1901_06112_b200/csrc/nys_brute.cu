@@ -8,7 +8,8 @@
 // counterpart at S = ceil(3 sigma)), κ(u) = exp(-|u|^2 / (2 θ^2)), edge
 // replicate (np.pad mode="edge").
 //
-// Compute-bound: (2S+1)^2 (2ρ + n + 3) FP32 ops per pixel.  One thread per
+// Compute-bound: (2S+1)^2 (2ρ + n + 3) FP32 ops per pixel (FP32 within a
+// window row, FP64 across rows).  One thread per
 // output pixel; a CTA stages its (TY+2S) x (TX+2S) halo of the ρ guide and n
 // input planes in shared memory when it fits (clamped once at load time), so
 // the window loop is shared-memory broadcast/conflict-free reads + FMAs.
@@ -62,12 +63,16 @@ __global__ void __launch_bounds__(BF_TX* BF_TY) k_brute(const BruteArgs a) {
   float pc[RM];
 #pragma unroll
   for (int d = 0; d < RM; ++d) pc[d] = d < a.rho ? at(d, 0, 0) : 0.f;
-  float num[NM];
+  // FP32 sums along a window row, FP64 across rows (windows reach (2*64+1)^2 terms)
+  double num_d[NM], den_d = 0.0;
 #pragma unroll
-  for (int c = 0; c < NM; ++c) num[c] = 0.f;
-  float den = 0.f;
+  for (int c = 0; c < NM; ++c) num_d[c] = 0.0;
   for (int iy = 0; iy < T; ++iy) {
     const float wy = a.w1[iy];
+    float num[NM];
+#pragma unroll
+    for (int c = 0; c < NM; ++c) num[c] = 0.f;
+    float den = 0.f;
     for (int ix = 0; ix < T; ++ix) {
       float d2 = 0.f;
 #pragma unroll
@@ -83,10 +88,13 @@ __global__ void __launch_bounds__(BF_TX* BF_TY) k_brute(const BruteArgs a) {
         if (c < a.n) num[c] = fmaf(kv, at(a.rho + c, iy - S, ix - S), num[c]);
       den += kv;
     }
+#pragma unroll
+    for (int c = 0; c < NM; ++c) num_d[c] += (double)num[c];
+    den_d += (double)den;
   }
 #pragma unroll
   for (int c = 0; c < NM; ++c)
-    if (c < a.n) a.out[(long long)c * a.ops + (long long)y * a.W + x] = num[c] / den;
+    if (c < a.n) a.out[(long long)c * a.ops + (long long)y * a.W + x] = (float)(num_d[c] / den_d);
 }
 
 }  // namespace nys

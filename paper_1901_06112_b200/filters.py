@@ -152,15 +152,18 @@ def build_guide(f: Image, mode: str = MODE_BILATERAL, guide: Image | None = None
 
 def pca_patch_guide(f: Image, patch_radius: int, pca_dim: int):
     """PCA patch guide (filters.py:161-187).  The full-dimension case (the
-    configuration BASELINE cfg 3 uses) is served by ``PatchGuide``; a
-    truncated projection (pca_dim < n(2r+1)^2) is §8 row f3 and not on the
-    B200 path yet."""
+    configuration BASELINE cfg 3 uses) is served by ``PatchGuide`` (a rotation
+    of the raw patches leaves every guide distance unchanged); a truncated
+    projection (pca_dim < n(2r+1)^2, §8 row f3) is computed on the device by
+    ``pca.pca_patch_guide``: FP64 patch moments, host eig, projection."""
     dim = f.channels * (2 * patch_radius + 1) ** 2
     if not 1 <= pca_dim <= dim:
         raise ValueError(f"pca_dim must lie in [1, {dim}], got {pca_dim}")
-    if pca_dim < dim:
-        raise NotImplementedError("truncated PCA patch guides (pca_dim < full) are not on the B200 path yet")
-    return PatchGuide(f, patch_radius)
+    if pca_dim == dim:
+        return PatchGuide(f, patch_radius)
+    from .pca import pca_patch_guide as _pca
+
+    return _pca(f, patch_radius, pca_dim)
 
 
 def _desc(n: int, rho: int, H: int, W: int, gkind: int, spatial: SpatialKernel, theta: float,

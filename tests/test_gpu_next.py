@@ -108,3 +108,39 @@ def test_metrics_identical_and_shape_errors():
     assert psnr(a, a) == 99.0 and mse(a, a) == 0.0 and ssim(a, a) == pytest.approx(1.0, abs=1e-12)
     with pytest.raises(ValueError):
         mse(a, Image(data=np.zeros((3, 16, 15)), range_max=1.0))
+
+
+# --------------------------------------------------------------------------
+# §8 row f3: PCA patch guides (csrc/nys_pca.cu) and NLM filters on them
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["r1k10", "r2k25", "r3k25", "gray_r3k6"])
+def test_pca_guide_matches_reference(name):
+    from paper_1901_06112_b200 import pca_patch_guide
+
+    c = group(load_golden("pca_guide"), "")[name]
+    r, k = (int(v) for v in c["meta"])
+    g = pca_patch_guide(Image(data=c["f"].astype(np.float64), range_max=1.0), r, k)
+    assert g.data.shape == c["guide"].shape
+    assert np.abs(g.data - c["guide"]).max() <= 2e-5 * max(1.0, np.abs(c["guide"]).max())
+
+
+@pytest.mark.parametrize("case", ["nlm_pca_r2k12", "nlm_pca_r3k25"])
+def test_nlm_pca_filter_two_stage(case):
+    from paper_1901_06112_b200 import build_guide, fast_filter, filter_with_landmarks
+
+    g = load_golden(case)
+    f = Image(data=torch.from_numpy(g["f"]).cuda(), range_max=1.0)
+    params = FilterParams(spatial=SpatialKernel.box(int(g["radius"])), theta=float(g["theta"]), m0=int(g["m0"]),
+                          mode="nlm", patch_radius=int(g["patch_radius"]), pca_dim=int(g["pca_dim"]),
+                          kmeans_max_iter=15)
+    p = build_guide(f, "nlm", None, int(g["patch_radius"]), int(g["pca_dim"]))
+    assert p.data.is_cuda and p.data.shape[0] == int(g["pca_dim"])
+    # stage 1: the reference's landmarks on our guide
+    rep = filter_with_landmarks(f, p, g["centroids"], params)
+    out = rep.output.data.double().cpu().numpy()
+    ok = np.abs(out - g["output"]) <= TOL
+    assert ok.mean() >= 0.999, np.abs(out - g["output"]).max()
+    assert abs(rep.guarded_pixels - int(g["guarded_pixels"])) <= 1
+    # stage 2: our k-means on our guide
+    full = fast_filter(f, p, params)
+    assert abs(full.quant_error - float(g["quant_error"])) <= 1e-3 * float(g["quant_error"])

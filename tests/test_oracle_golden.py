@@ -175,3 +175,22 @@ def test_oracle_metrics_match_reference():
         assert O.ssim(c["a"], c["b"], R) == pytest.approx(float(c["ssim"]), abs=1e-12), name
     a = g["rgb__a"]
     assert O.psnr(a, a, 1.0) == float(g["same__psnr"]) == 99.0
+
+
+def test_oracle_pca_guide_matches_reference():
+    """§8 f3 fixtures: truncated PCA patch guides (filters.py:161-187)."""
+    for name, c in group(load_golden("pca_guide"), "").items():
+        r, k = (int(v) for v in c["meta"])
+        g = O.pca_patch_guide(c["f"].astype(np.float64), r, k)
+        np.testing.assert_allclose(g, c["guide"], rtol=0, atol=1e-10, err_msg=name)
+
+
+@pytest.mark.parametrize("case", ["nlm_pca_r2k12", "nlm_pca_r3k25"])
+def test_oracle_nlm_pca_filter_matches_reference(case):
+    g = load_golden(case)
+    f = g["f"].astype(np.float64)
+    p = O.pca_patch_guide(f, int(g["patch_radius"]), int(g["pca_dim"]))
+    np.testing.assert_allclose(p, g["guide"], rtol=0, atol=1e-10)
+    res = O.fast_filter_with_landmarks(f, p, g["centroids"], float(g["theta"]), "box", 0.0, int(g["radius"]))
+    assert res["guarded_pixels"] == int(g["guarded_pixels"])
+    np.testing.assert_allclose(res["output"], g["output"], rtol=0, atol=1e-9)

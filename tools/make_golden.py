@@ -239,8 +239,44 @@ def main_brute_metrics_io():
     print("brute / metrics / io fixtures written")
 
 
+def main_pca():
+    """§8 row f3: PCA patch guides with pca_dim < full (filters.py:161-187)
+    and NLM-mode filters on them."""
+    from nysfilter.filters import pca_patch_guide as ref_pca
+
+    out = {}
+    for name, (f32, r, k) in {
+        "r1k10": (color_scene(30, 34, 5, 0.08, seed=41, lo=0.1, hi=0.9, shading=0.1), 1, 10),
+        "r2k25": (color_scene(36, 40, 5, 0.08, seed=42, lo=0.1, hi=0.9, shading=0.1), 2, 25),
+        "r3k25": (color_scene(40, 44, 6, 0.08, seed=43, lo=0.1, hi=0.9, shading=0.1), 3, 25),
+        "gray_r3k6": (color_scene(32, 30, 5, 0.08, seed=44)[:1].copy(), 3, 6),
+    }.items():
+        g = ref_pca(ref.Image(data=f32.astype(np.float64), range_max=1.0), r, k).data
+        out[f"{name}__f"], out[f"{name}__meta"], out[f"{name}__guide"] = f32, np.array([r, k]), g
+    np.savez_compressed(OUT / "pca_guide.npz", **out)
+    # NLM-mode filters (the CLI's nlm path at small size): guide = PCA(r, k) of f
+    for name, (f32, r, k, S, m0) in {
+        "nlm_pca_r2k12": (color_scene(36, 40, 5, 0.08, seed=45, lo=0.1, hi=0.9, shading=0.1), 2, 12, 5, 12),
+        "nlm_pca_r3k25": (color_scene(32, 36, 5, 0.08, seed=46, lo=0.1, hi=0.9, shading=0.1), 3, 25, 4, 10),
+    }.items():
+        fi = ref.Image(data=f32.astype(np.float64), range_max=1.0)
+        theta = 0.3 * np.sqrt(3 * (2 * r + 1) ** 2) * 0.08  # cfg-3 rule on the raw patch dimension
+        params = ref.FilterParams(spatial=ref.SpatialKernel.box(S), theta=theta, m0=m0, seed=0, mode="nlm",
+                                  patch_radius=r, pca_dim=k, kmeans_max_iter=15)
+        p = ref.build_guide(fi, "nlm", None, r, k)
+        rep = ref.fast_filter(fi, p, params)
+        lm = ref_kmeans(ref.extract_range_list(p).vectors, m0, seed=0, max_iter=15)
+        np.savez_compressed(OUT / f"{name}.npz", f=f32, guide=p.data, patch_radius=r, pca_dim=k, radius=S,
+                            theta=theta, m0=m0, output=rep.output.data, retained_rank=rep.retained_rank,
+                            quant_error=rep.quant_error, guarded_pixels=rep.guarded_pixels,
+                            min_denominator=rep.min_denominator, centroids=lm.centroids)
+        print(name, "rank", rep.retained_rank, "guarded", rep.guarded_pixels, "qe", rep.quant_error)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["base", "recursive", "f1f4"]
+    which = sys.argv[1:] or ["base", "recursive", "f1f4", "pca"]
+    if "pca" in which:
+        main_pca()
     if "f1f4" in which:
         main_brute_metrics_io()
     if "base" in which:

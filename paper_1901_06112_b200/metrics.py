@@ -44,7 +44,7 @@ def _planes(img: Image, dtype=None) -> torch.Tensor:
     if isinstance(d, torch.Tensor):
         t = d if d.dtype in (torch.float32, torch.float64) else d.to(torch.float64)
         return t.to(dev, dtype=dtype or t.dtype).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(d, dtype=np.float64)).to(dev, dtype=dtype or torch.float64)
+    return torch.from_numpy(np.array(d, dtype=np.float64, copy=True)).to(dev, dtype=dtype or torch.float64)
 
 
 def _per_plane(a: Image, b: Image, want_ssim: bool):

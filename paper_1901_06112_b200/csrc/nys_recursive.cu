@@ -15,7 +15,7 @@
 //                      s0 = u0.b) -> Y [px][m0+1], Bf [px][m0]
 //   R2 k_rec_rows      one thread per (row, plane): forward then backward
 //                      recursion along the row, in place in Hb [px][Pb]
-//   R3 k_rec_cols      one CTA per column, one thread per plane: forward
+//   R3 k_rec_cols      one CTA per 1-4 columns, one thread per plane: forward
 //                      recursion down the column in place, then the backward
 //                      recursion up the column fused with the contraction
 //                      Σ_i b_i(x) conv_i(x) (block reduction over landmarks)
@@ -33,9 +33,9 @@ struct RecCoeffs {
   double g, a1, a2, a3, a4, a5;
 };
 
-constexpr int REC_FEAT_THREADS = 128;
 constexpr int REC_ROW_THREADS = 128;
 constexpr int REC_RB = 16;    // rows per contraction batch in R3
+constexpr int REC_COL_MAX_THREADS = 768;  // R3 CTA: cpb * roundup32(Pb) threads (85 registers)
 constexpr int REC_BATCH = 8;  // loads issued ahead of the recursion
 
 struct RecScratch {
@@ -77,30 +77,35 @@ struct RecState {
 // R1: features b(x) and y = M b at every pixel (nystrom.py:43-79, 112-114 in
 // the y-form).  MT = [M | u0] transposed in the workspace (FilterLayout).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(REC_FEAT_THREADS) k_rec_features(
+template <int BS>
+__global__ void __launch_bounds__(BS) k_rec_features(
     const float* __restrict__ f, long long fps, const float* __restrict__ g, long long gps, int gkind, int rho,
     int H, int W, int m0, const float* __restrict__ consts, int rhop, int m0q, long long off_MT, float k2,
     float* __restrict__ Y, float* __restrict__ Bf) {
+  // b and y are staged in shared memory ([value][pixel], pitch BS+1: the
+  // transposed read-out below is bank-conflict free) so the block writes its
+  // contiguous [px][m0] / [px][m0+1] output rows with coalesced stores
+  constexpr int PT = BS + 1;
   extern __shared__ float rsm[];
-  float* sg = rsm;                               // [rho][128]
-  float* sb = rsm + (size_t)rho * REC_FEAT_THREADS;  // [m0][128]
+  float* sg = rsm;                                   // [rho][BS]
+  float* sb = sg + (size_t)rho * BS;                 // [m0][PT]
+  float* sy = sb + (size_t)m0 * PT;                  // [m0+1][PT]
   const int t = threadIdx.x;
   const long long npx = (long long)H * W;
-  const long long px = (long long)blockIdx.x * REC_FEAT_THREADS + t;
+  const long long px0 = (long long)blockIdx.x * BS;
+  const long long px = px0 + t;
   const bool ok = px < npx;
   const int row = ok ? (int)(px / W) : 0, x = ok ? (int)(px - (long long)row * W) : 0;
-  for (int k = 0; k < rho; ++k) sg[k * REC_FEAT_THREADS + t] = ok ? guide_at(g, gps, f, fps, gkind, k, row, x, H, W) : 0.f;
+  for (int k = 0; k < rho; ++k) sg[k * BS + t] = ok ? guide_at(g, gps, f, fps, gkind, k, row, x, H, W) : 0.f;
   const float* C = consts;
   for (int j = 0; j < m0; ++j) {
     float d2 = 0.f;
     const float* cj = C + (size_t)j * rhop;
     for (int k = 0; k < rho; ++k) {
-      const float dd = sg[k * REC_FEAT_THREADS + t] - __ldg(cj + k);
+      const float dd = sg[k * BS + t] - __ldg(cj + k);
       d2 = fmaf(dd, dd, d2);
     }
-    const float b = range_kernel(d2, k2);
-    sb[j * REC_FEAT_THREADS + t] = b;
-    if (ok) Bf[px * m0 + j] = b;
+    sb[j * PT + t] = range_kernel(d2, k2);
   }
   const float* MT = consts + off_MT;
   for (int i0 = 0; i0 <= m0; i0 += 8) {
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(REC_FEAT_THREADS) k_rec_features(
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
     for (int j = 0; j < m0; ++j) {
-      const float bj = sb[j * REC_FEAT_THREADS + t];
+      const float bj = sb[j * PT + t];
       const float4 lo = __ldg(reinterpret_cast<const float4*>(MT + (size_t)j * m0q + i0));
       const float4 hi = __ldg(reinterpret_cast<const float4*>(MT + (size_t)j * m0q + i0 + 4));
       acc[0] = fmaf(bj, lo.x, acc[0]);
@@ -120,11 +125,20 @@ __global__ void __launch_bounds__(REC_FEAT_THREADS) k_rec_features(
       acc[6] = fmaf(bj, hi.z, acc[6]);
       acc[7] = fmaf(bj, hi.w, acc[7]);
     }
-    if (ok) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (i0 + e <= m0) Y[px * (m0 + 1) + i0 + e] = acc[e];
-    }
+    for (int e = 0; e < 8; ++e)
+      if (i0 + e <= m0) sy[(i0 + e) * PT + t] = acc[e];
+  }
+  __syncthreads();
+  const int cnt = (int)min((long long)BS, npx - px0);
+  for (int e = t; e < cnt * m0; e += BS) {
+    const int i = e / m0, j = e - i * m0;
+    Bf[px0 * m0 + e] = sb[j * PT + i];
+  }
+  const int G = m0 + 1;
+  for (int e = t; e < cnt * G; e += BS) {
+    const int i = e / G, j = e - i * G;
+    Y[px0 * G + e] = sy[j * PT + i];
   }
 }
 
@@ -181,16 +195,21 @@ __global__ void __launch_bounds__(REC_ROW_THREADS) k_rec_rows(
 
 // ---------------------------------------------------------------------------
 // R3: column recursion (spatial.py:186-188) + contraction (filters.py:227-238
-// in the y-form).  One CTA per column x, thread q = plane of the band.
+// in the y-form).  A CTA covers `cpb` adjacent columns (so each row step reads
+// cpb*Pb contiguous floats); thread (column cb, plane q).  The forward pass
+// rewrites Hb in place; the backward pass only feeds the contraction.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024, 1) k_rec_cols(const float* __restrict__ Y, const float* __restrict__ Bf, int n, int H, int W, int m0,
-                           int g0, int nb, RecCoeffs cf, float inv_alpha0, int accumulate, float* __restrict__ Hb,
-                           float* __restrict__ Z, float* __restrict__ Lz) {
-  extern __shared__ float csm[];  // [REC_RB][Pb] products b_g * conv
+__global__ void __launch_bounds__(REC_COL_MAX_THREADS, 1) k_rec_cols(const float* __restrict__ Y, const float* __restrict__ Bf,
+                                                      int n, int H, int W, int m0, int g0, int nb, int cpb,
+                                                      RecCoeffs cf, float inv_alpha0, int accumulate,
+                                                      float* __restrict__ Hb, float* __restrict__ Z,
+                                                      float* __restrict__ Lz) {
+  extern __shared__ float csm[];  // [REC_RB][cpb][Pb] products b_g * conv
   const int Pb = (n + 1) * nb;
-  const int q = threadIdx.x;
-  const int x = blockIdx.x;
-  const bool active = q < Pb;
+  const int Pbp = (Pb + 31) & ~31;
+  const int cb = threadIdx.x / Pbp, q = threadIdx.x - cb * Pbp;
+  const int x = blockIdx.x * cpb + cb;
+  const bool active = q < Pb && cb < cpb && x < W;
   const int c = active ? q / nb : 0, g = g0 + (active ? q - c * nb : 0);
   const long long rs = (long long)W * Pb;  // row stride of Hb
   const long long npx = (long long)H * W;
@@ -215,6 +234,7 @@ __global__ void __launch_bounds__(1024, 1) k_rec_cols(const float* __restrict__ 
   const bool has_lead = g0 <= m0 && m0 < g0 + nb;
   const int lead_l = m0 - g0;
   const int nl = min(nb, m0 - g0);  // landmark (non-lead) groups in the band
+  const int ncols = min(cpb, W - (int)blockIdx.x * cpb);
   for (int rtop = H - 1; rtop >= 0; rtop -= REC_RB) {
     const int cnt = min(REC_RB, rtop + 1);
     if (active) {
@@ -225,25 +245,24 @@ __global__ void __launch_bounds__(1024, 1) k_rec_cols(const float* __restrict__ 
       for (int e = 0; e < REC_RB; ++e) {
         if (e < cnt) {
           const int row = rtop - e;
-          const double val = s.step(cf, (double)v[e]);
-          col[(long long)row * rs] = (float)val;
+          const float val = (float)s.step(cf, (double)v[e]);
           const long long p = (long long)row * W + x;
           float prod;
           if (g < m0)
-            prod = __ldg(Bf + p * m0 + g) * (float)val;
+            prod = __ldg(Bf + p * m0 + g) * val;
           else
-            prod = __ldg(Y + p * (m0 + 1) + m0) * (float)val * inv_alpha0;  // s0 conv(s0 f)/α0
-          csm[e * Pb + q] = prod;
+            prod = __ldg(Y + p * (m0 + 1) + m0) * val * inv_alpha0;  // s0 conv(s0 f)/α0
+          csm[(e * cpb + cb) * Pb + q] = prod;
         }
       }
     }
     __syncthreads();
-    for (int o = threadIdx.x; o < (n + 1) * cnt; o += blockDim.x) {
-      const int cc = o / cnt, e = o - cc * cnt;
-      const float* sp = csm + e * Pb + cc * nb;
+    for (int o = threadIdx.x; o < ncols * (n + 1) * cnt; o += blockDim.x) {
+      const int e = o % cnt, rest = o / cnt, cc = rest % (n + 1), cbo = rest / (n + 1);
+      const float* sp = csm + (e * cpb + cbo) * Pb + cc * nb;
       float acc = 0.f;
       for (int l = 0; l < nl; ++l) acc += sp[l];
-      const long long p = (long long)(rtop - e) * W + x;
+      const long long p = (long long)(rtop - e) * W + blockIdx.x * cpb + cbo;
       float* zp = Z + cc * npx + p;
       *zp = accumulate ? *zp + acc : acc;
       if (has_lead) Lz[cc * npx + p] = sp[lead_l];
@@ -314,7 +333,7 @@ int rec_groups_fit(const nys_filter_desc* d, size_t scratch_bytes) {
   // largest landmark band (groups of n+1 planes incl. the lead group) with
   // Pb <= 1024 threads per CTA whose plane buffer fits the scratch
   const int G = d->m0 + 1;
-  int nb = std::min(G, 1024 / (d->n + 1));
+  int nb = std::min(G, REC_COL_MAX_THREADS / (d->n + 1));
   while (nb >= 1 && rec_scratch(d, nb).total > scratch_bytes) --nb;
   return nb;
 }
@@ -323,7 +342,7 @@ int rec_validate(const nys_filter_desc* d) {
   const int st = validate(d);
   if (st) return st;
   if (d->spatial_kind != NYS_SPATIAL_GAUSSIAN_RECURSIVE) return NYS_EINVAL;
-  if (d->n + 1 > 1024) return NYS_EUNSUPPORTED;
+  if (d->n + 1 > REC_COL_MAX_THREADS) return NYS_EUNSUPPORTED;
   return NYS_OK;
 }
 
@@ -335,7 +354,7 @@ size_t nys_filter_recursive_scratch_bytes(const nys_filter_desc* d, int groups_p
   if (rec_validate(d) != NYS_OK) return 0;
   const int G = d->m0 + 1;
   int nb = groups_per_band <= 0 ? G : std::min(groups_per_band, G);
-  nb = std::min(nb, 1024 / (d->n + 1));
+  nb = std::min(nb, REC_COL_MAX_THREADS / (d->n + 1));
   return rec_scratch(d, nb).total;
 }
 
@@ -370,12 +389,15 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
   const float* g = d->guide_kind == 0 ? guide : f;
 
   {
-    const size_t smem = (size_t)(d->rho + d->m0) * REC_FEAT_THREADS * sizeof(float);
-    NYS_CUDA_TRY(cudaFuncSetAttribute(k_rec_features, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // (2 m0 + 1 + rho) x (BS + 1) floats of SMEM: 128-pixel blocks up to m0 = 96, 64 beyond
+    const int BS = d->m0 <= 96 ? 128 : 64;
+    const size_t smem = ((size_t)d->rho * BS + (size_t)(2 * d->m0 + 1) * (BS + 1)) * sizeof(float);
+    auto k = BS == 128 ? k_rec_features<128> : k_rec_features<64>;
+    NYS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();
-    k_rec_features<<<(unsigned)ceil_div(npx, REC_FEAT_THREADS), REC_FEAT_THREADS, smem, s>>>(
-        f, f_plane_stride, g, guide_plane_stride, d->guide_kind, d->rho, d->H, d->W, d->m0, consts + L.off_C,
-        L.rhop, L.m0q, (long long)(L.off_MT - L.off_C), k2_of(d), Y, Bf);
+    k<<<(unsigned)ceil_div(npx, BS), BS, smem, s>>>(f, f_plane_stride, g, guide_plane_stride, d->guide_kind, d->rho,
+                                                    d->H, d->W, d->m0, consts + L.off_C, L.rhop, L.m0q,
+                                                    (long long)(L.off_MT - L.off_C), k2_of(d), Y, Bf);
     NYS_LAUNCH_CHECK();
   }
   const int G = d->m0 + 1;
@@ -388,11 +410,12 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
     k_rec_rows<<<dim3((unsigned)ceil_div(Pb, REC_ROW_THREADS), (unsigned)d->H), REC_ROW_THREADS, 0, s>>>(
         f, f_plane_stride, Y, d->n, d->H, d->W, d->m0, g0, nb, cf, Hb);
     NYS_LAUNCH_CHECK();
-    const int threads = (int)ceil_div(Pb, 32) * 32;
-    const size_t smem = (size_t)REC_RB * Pb * sizeof(float);
+    const int Pbp = (int)ceil_div(Pb, 32) * 32;
+    const int cpb = std::max(1, std::min(4, REC_COL_MAX_THREADS / Pbp));
+    const size_t smem = (size_t)REC_RB * cpb * Pb * sizeof(float);
     NYS_CUDA_TRY(cudaFuncSetAttribute(k_rec_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();
-    k_rec_cols<<<(unsigned)d->W, threads, smem, s>>>(Y, Bf, d->n, d->H, d->W, d->m0, g0, nb, cf,
+    k_rec_cols<<<(unsigned)ceil_div(d->W, cpb), cpb * Pbp, smem, s>>>(Y, Bf, d->n, d->H, d->W, d->m0, g0, nb, cpb, cf,
                                                       (float)(1.0 / d->alpha0), b > 0 ? 1 : 0, Hb, Z, Lz);
     NYS_LAUNCH_CHECK();
   }

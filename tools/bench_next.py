@@ -84,8 +84,9 @@ def main():
         ms, launches = timed(run, args.steps, args.warmup, flush)
         k_ms = evs[0][1].elapsed_time(evs[0][2])
         P = (wl.m0 + 1) * (n + 1)
-        # Y, B written once + read; row pass: fwd write, bwd read+write; column pass: fwd read+write, bwd read
-        bpx = 4 * (2 * (wl.m0 + 1) + 2 * wl.m0 + n) + 4 * 6 * P + 4 * (2 * (n + 1)) * 2 + 4 * 2 * n
+        # Y, B written once + read once; row pass: fwd write, bwd read + write; column pass: fwd read + write,
+        # bwd read (feeds the contraction only); Z / lead planes written + read; f read twice; output written
+        bpx = 4 * (2 * (wl.m0 + 1) + 2 * wl.m0) + 4 * 6 * P - 4 * P + 4 * 4 * (n + 1) + 4 * 3 * n
         out.append({"row": "f2 recursive Gaussian", "workload": f"{wl.name} with SpatialKernel.recursive({sigma})",
                     "ms_per_step": round(ms, 3), "mpix_s": round(px / ms / 1e3, 1), "gpu_launches": launches,
                     "filter_ms": round(k_ms, 3), "bytes_px": bpx,

@@ -101,6 +101,29 @@ inline int validate_tiled(const nys_filter_desc* d) {
   return d->spatial_kind == NYS_SPATIAL_GAUSSIAN_RECURSIVE ? NYS_EINVAL : NYS_OK;
 }
 
+// FIR tap pairs for the packed (f32x2) FIR: wpair[k] = (w[k], w[k-1]) with
+// w[-1] = w[T] = 0, so output pair (o, o+1) takes input s with k = s - o:
+// lane 0 accumulates w[s-o] v[s], lane 1 w[s-o-1] v[s] -- the same FMAs, in
+// the same order, as the scalar loop (bit-identical results)
+inline void fill_tap_pairs(const float* taps, int T, float2* wpair) {
+  for (int k = 0; k <= NYS_MAX_TAPS; ++k) wpair[k] = make_float2(0.f, 0.f);
+  for (int k = 0; k <= T; ++k) wpair[k] = make_float2(k < T ? taps[k] : 0.f, k >= 1 ? taps[k - 1] : 0.f);
+}
+
+// acc(lane0, lane1) += (v * w.x, v * w.y): one FFMA2 (v broadcast from a
+// 32-bit register, the weight pair from a uniform register) = two FP32 FMAs
+// in one issue slot
+__device__ __forceinline__ unsigned long long ffma2_bc(float v, float2 w, unsigned long long acc) {
+  unsigned long long vv, ww;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(vv) : "f"(v));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ww) : "f"(w.x), "f"(w.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(vv), "l"(ww));
+  return acc;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
 inline void fill_taps(const nys_filter_desc* d, float* taps) {
   const int T = 2 * d->radius + 1;
   for (int t = 0; t < NYS_MAX_TAPS; ++t) taps[t] = 0.f;

@@ -222,6 +222,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);
+  fill_tap_pairs(a.taps, 2 * d->radius + 1, a.wpair);
   if (const char* e = getenv("NYS_DBG_K2")) a.dbg = atoi(e);
   cudaStream_t s = (cudaStream_t)stream;
   {

@@ -27,6 +27,7 @@ struct HArgs {
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;
   float taps[NYS_MAX_TAPS];
+  float2 wpair[NYS_MAX_TAPS + 1];  // packed-FIR tap pairs (fill_tap_pairs)
 };
 
 // FEXT: Fs holds a row per plane channel of every chunk (f_c, then 1 for the
@@ -127,9 +128,15 @@ __device__ __forceinline__ void hfir_plane(const HArgs& a, const float* __restri
 #pragma unroll
   for (int o = 0; o < K2_XR; ++o) acc[o] = 0.f;
   if constexpr (RT > 0) {
+    // packed FIR: output pairs (2p, 2p+1) accumulate in one f32x2 register,
+    // one FFMA2 per (input, pair) -- half the issue slots of scalar FFMA
     constexpr int T = 2 * RT + 1;
     constexpr int NIN = K2_XR + 2 * RT;
     constexpr int NQ = (NIN + 3) / 4;
+    static_assert(K2_XR % 2 == 0, "output pairs");
+    unsigned long long acc2[K2_XR / 2];
+#pragma unroll
+    for (int p = 0; p < K2_XR / 2; ++p) acc2[p] = 0ull;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const float4 y4 = *reinterpret_cast<const float4*>(yrow + 4 * q);
@@ -140,13 +147,15 @@ __device__ __forceinline__ void hfir_plane(const HArgs& a, const float* __restri
         const int s = 4 * q + e;
         if (s < NIN) {
 #pragma unroll
-          for (int o = 0; o < K2_XR; ++o) {
-            const int t = s - o;
-            if (t >= 0 && t < T) acc[o] = fmaf(a.taps[t], v4[e], acc[o]);
+          for (int p = 0; p < K2_XR / 2; ++p) {
+            const int k = s - 2 * p;
+            if (k >= 0 && k <= T) acc2[p] = ffma2_bc(v4[e], a.wpair[k], acc2[p]);
           }
         }
       }
     }
+#pragma unroll
+    for (int p = 0; p < K2_XR / 2; ++p) unpack2(acc2[p], acc[2 * p], acc[2 * p + 1]);
   } else if (a.box) {  // sliding (2R+1)-sum re-anchored per item (spatial.py:91-99)
     const int R = a.R;
     float sum = 0.f;

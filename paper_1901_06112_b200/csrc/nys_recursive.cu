@@ -35,7 +35,7 @@ struct RecCoeffs {
 
 constexpr int REC_ROW_THREADS = 128;
 constexpr int REC_RB = 16;    // rows per contraction batch in R3
-constexpr int REC_COL_MAX_THREADS = 768;  // R3 CTA: cpb * roundup32(Pb) threads (85 registers)
+constexpr int REC_COL_MAX_THREADS = 1024;  // R3 CTA: cpb * roundup32(Pb) threads (64 registers)
 constexpr int REC_BATCH = 8;  // loads issued ahead of the recursion
 
 struct RecScratch {
@@ -238,14 +238,17 @@ __global__ void __launch_bounds__(REC_COL_MAX_THREADS, 1) k_rec_cols(const float
   for (int rtop = H - 1; rtop >= 0; rtop -= REC_RB) {
     const int cnt = min(REC_RB, rtop + 1);
     if (active) {
-      float v[REC_RB];
+#pragma unroll 1
+     for (int h = 0; h < REC_RB; h += REC_BATCH) {
+      float v[REC_BATCH];
 #pragma unroll
-      for (int e = 0; e < REC_RB; ++e) v[e] = e < cnt ? col[(long long)(rtop - e) * rs] : 0.f;
+      for (int e2 = 0; e2 < REC_BATCH; ++e2) v[e2] = h + e2 < cnt ? col[(long long)(rtop - h - e2) * rs] : 0.f;
 #pragma unroll
-      for (int e = 0; e < REC_RB; ++e) {
+      for (int e2 = 0; e2 < REC_BATCH; ++e2) {
+        const int e = h + e2;
         if (e < cnt) {
           const int row = rtop - e;
-          const float val = (float)s.step(cf, (double)v[e]);
+          const float val = (float)s.step(cf, (double)v[e2]);
           const long long p = (long long)row * W + x;
           float prod;
           if (g < m0)
@@ -255,6 +258,7 @@ __global__ void __launch_bounds__(REC_COL_MAX_THREADS, 1) k_rec_cols(const float
           csm[(e * cpb + cb) * Pb + q] = prod;
         }
       }
+     }
     }
     __syncthreads();
     for (int o = threadIdx.x; o < ncols * (n + 1) * cnt; o += blockDim.x) {
@@ -411,7 +415,7 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
         f, f_plane_stride, Y, d->n, d->H, d->W, d->m0, g0, nb, cf, Hb);
     NYS_LAUNCH_CHECK();
     const int Pbp = (int)ceil_div(Pb, 32) * 32;
-    const int cpb = std::max(1, std::min(4, REC_COL_MAX_THREADS / Pbp));
+    const int cpb = 1;  // measured: more columns per CTA lowers occupancy (latency-bound walk)
     const size_t smem = (size_t)REC_RB * cpb * Pb * sizeof(float);
     NYS_CUDA_TRY(cudaFuncSetAttribute(k_rec_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();

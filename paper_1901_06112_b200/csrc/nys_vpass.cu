@@ -56,6 +56,7 @@ struct VArgs {
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   float k2, inv_alpha0, eps_den;
   float taps[NYS_MAX_TAPS];
+  float2 wpair[NYS_MAX_TAPS + 1];  // packed-FIR tap pairs (fill_tap_pairs)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -93,22 +94,31 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
 #pragma unroll
   for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = G[o][2] = G[o][3] = 0.f;
   if constexpr (RT > 0) {
+    // packed FIR: rows (2p, 2p+1) of column e accumulate in one f32x2 register
     constexpr int T = 2 * RT + 1;
+    static_assert(K3_YR % 2 == 0, "row pairs");
+    unsigned long long G2[K3_YR / 2][4];
+#pragma unroll
+    for (int p = 0; p < K3_YR / 2; ++p) G2[p][0] = G2[p][1] = G2[p][2] = G2[p][3] = 0ull;
 #pragma unroll
     for (int s = 0; s < K3_YR + 2 * RT; ++s) {
       const float4 v = *reinterpret_cast<const float4*>(src + s * rs);
 #pragma unroll
-      for (int o = 0; o < K3_YR; ++o) {
-        const int t = s - o;
-        if (t >= 0 && t < T) {
-          const float w = a.taps[t];
-          G[o][0] = fmaf(w, v.x, G[o][0]);
-          G[o][1] = fmaf(w, v.y, G[o][1]);
-          G[o][2] = fmaf(w, v.z, G[o][2]);
-          G[o][3] = fmaf(w, v.w, G[o][3]);
+      for (int p = 0; p < K3_YR / 2; ++p) {
+        const int k = s - 2 * p;
+        if (k >= 0 && k <= T) {
+          const float2 w = a.wpair[k];
+          G2[p][0] = ffma2_bc(v.x, w, G2[p][0]);
+          G2[p][1] = ffma2_bc(v.y, w, G2[p][1]);
+          G2[p][2] = ffma2_bc(v.z, w, G2[p][2]);
+          G2[p][3] = ffma2_bc(v.w, w, G2[p][3]);
         }
       }
     }
+#pragma unroll
+    for (int p = 0; p < K3_YR / 2; ++p)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) unpack2(G2[p][e], G[2 * p][e], G[2 * p + 1][e]);
   } else if (a.box) {  // running (2R+1)-sum (spatial.py:91-99)
     const int R = a.R;
     float4 sm4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -426,6 +436,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.inv_alpha0 = (float)(1.0 / d->alpha0);
   a.eps_den = (float)d->eps_den;
   fill_taps(d, a.taps);
+  fill_tap_pairs(a.taps, 2 * d->radius + 1, a.wpair);
 
   // TMA descriptors over the plane buffer: (32 cols, plane, x/32 tile, virtual row),
   // boxes of 32 x 4 x 1 x (TH+2R) planes, 32 x ntail x 1 x (TH+2R) for a partial

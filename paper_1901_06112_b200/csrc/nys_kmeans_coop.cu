@@ -36,6 +36,11 @@ struct SeedArgs {
   KState* st;
   int d2_in_smem;
   int* flag;  // last published draw (owner block -> everyone)
+  // thread-run seeding (k_seed_runs)
+  float* pp;        // permuted copy: plane d, slot (block, r, t) at pp[d * pps + (block * per + r) * B + t]
+  long long pps;    // plane stride of pp
+  double* tsum;     // per-thread run sums [block][B]
+  int per;          // points per thread run
 };
 
 // owner search over vals[0..n) for the first index whose running sum exceeds
@@ -189,6 +194,132 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
     if (threadIdx.x == 0) {
       while (atomicAdd(a.flag, 0) < j) __nanosleep(32);
       __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+// k-means++ seeding with ONE grid barrier per draw (landmarks.py:60-73).
+// Thread t of block b owns the contiguous run of points lo_b + t*per + r,
+// r < per (a permuted copy of the guide keeps the per-r loads coalesced), so
+// the global linear order is (block, thread, r).  After the D^2 update every
+// block publishes its per-thread run sums and their block total; after the
+// barrier every block resolves the draw redundantly with identical
+// arithmetic: the owning block (scan over block totals), the owning thread
+// (scan over that block's run sums), then the point inside the run, whose
+// D^2 values it recomputes exactly (min over the centroids so far, the same
+// FP64 formula, so bit-identical to the stored ones).  No owner handoff.
+template <int GR, int RX>
+__global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double d2s[];  // this block's D^2 (slot order r*B + t) when it fits
+  __shared__ double sh[64];
+  __shared__ int shi[2];
+  __shared__ double tot_sh;
+  __shared__ double rd2[512];                     // D^2 of the owning run (first 512 points per round)
+  const int nb = gridDim.x, b = blockIdx.x, rho = RX > 0 ? RX : a.rho;  // RX: compile-time rho
+  const int B = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nwarp = B >> 5;
+  const long long chunk = ceil_div(a.m, (long long)nb);
+  const long long lo = min(a.m, b * chunk), hi = min(a.m, lo + chunk);
+  const int len = (int)(hi - lo), per = a.per;
+  const long long slot0 = (long long)b * per * B;
+  double* d2 = a.d2_in_smem ? d2s : a.d2 + slot0;
+  double* Cs = reinterpret_cast<double*>(a.d2_in_smem ? d2s + (size_t)per * B : d2s);  // [m0][rho] history
+  // permuted copy of this block's points (read back only by the thread that wrote each slot)
+  for (int r = 0; r < per; ++r) {
+    const int li = t * per + r;
+#pragma unroll 4
+    for (int d = 0; d < rho; ++d)
+      a.pp[d * a.pps + slot0 + (long long)r * B + t] = li < len ? __ldg(a.pts + d * a.ps + lo + li) : 0.f;
+  }
+  for (int k = t; k < rho; k += B) Cs[k] = __ldcg(a.C + k);
+  __syncthreads();
+  for (int j = 1; j < a.m0; ++j) {
+    const double* cs = Cs + (size_t)(j - 1) * rho;
+    double s = 0.0;
+    for (int r = 0; r < per; ++r) {
+      float x[GR];
+#pragma unroll
+      for (int d = 0; d < GR; ++d) x[d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)r * B + t] : 0.f;
+      const double v = d2_exact_regs<GR>(x, rho, cs);
+      const int sl = r * B + t;
+      double nv = j == 1 ? v : fmin(d2[sl], v);
+      if (t * per + r >= len) nv = 0.0;
+      d2[sl] = nv;
+      s += nv;  // run sum in linear order
+    }
+    a.tsum[(long long)b * B + t] = s;
+    {
+      const double incl = block_incl_scan(s, sh);  // the same scan the resolvers run over tsum
+      if (t == B - 1) a.ppart[b] = incl;
+    }
+    grid.sync();
+    // --- every block: the owning block ---
+    double total;
+    {
+      const long long pb = ceil_div((long long)nb, (long long)B);
+      const long long a0 = min((long long)nb, (long long)t * pb), a1 = min((long long)nb, a0 + pb);
+      double mine = 0.0;
+      for (long long q = a0; q < a1; ++q) mine += __ldcg(a.ppart + q);
+      const double incl = block_incl_scan(mine, sh);
+      if (t == B - 1) tot_sh = incl;
+      __syncthreads();
+      total = tot_sh;
+    }
+    if (!(total > 0.0)) {  // sum(D^2) == 0: the reference switches to rng.integers (host redo)
+      if (b == 0 && t == 0) a.st->zero_draw = j;
+      return;  // uniform across the grid
+    }
+    const double target = a.uniforms[j - 1] * total;
+    double before_b = 0.0, before_t = 0.0;
+    const long long bstar = scan_find<true>(a.ppart, nb, target, sh, shi, &before_b);
+    // --- the owning thread run inside block bstar ---
+    const long long tstar = scan_find<true>(a.tsum + bstar * B, B, target - before_b, sh, shi, &before_t);
+    const long long lo_s = min(a.m, bstar * chunk), len_s = min(a.m, lo_s + chunk) - lo_s;
+    // --- the point inside the run: recompute its D^2 exactly (one warp per point) ---
+    long long idx = -1;
+    for (int r0 = 0; r0 < per && idx < 0; r0 += 512) {
+      const int cnt = min(512, per - r0);
+      for (int rr = wid; rr < cnt; rr += nwarp) {
+        const long long li = tstar * per + r0 + rr;
+        double mn = INFINITY;
+        if (li < len_s) {
+          float x[GR];
+#pragma unroll
+          for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(a.pts + d * a.ps + lo_s + li) : 0.f;
+          for (int k = lane; k < j; k += 32) mn = fmin(mn, d2_exact_regs<GR>(x, rho, Cs + (size_t)k * rho));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        } else {
+          mn = 0.0;
+        }
+        if (lane == 0) rd2[rr] = mn;
+      }
+      __syncthreads();
+      double before_r = 0.0;
+      const double tgt = target - before_b - before_t;
+      // first point of this round whose running sum passes tgt (scan_find's fallback: last positive)
+      double run_tot = 0.0;
+      {
+        const double v = t < cnt ? rd2[t] : 0.0;
+        const double incl = block_incl_scan(v, sh);
+        if (t == B - 1) tot_sh = incl;
+        __syncthreads();
+        run_tot = tot_sh;
+      }
+      if (r0 + cnt >= per || run_tot > tgt) {
+        const long long k = scan_find<false>(rd2, cnt, tgt, sh, shi, &before_r);
+        idx = lo_s + tstar * per + r0 + max(0ll, k);
+      } else {
+        before_t += run_tot;  // the target lies in a later round of this run
+      }
+      __syncthreads();
+    }
+    double* cn = Cs + (size_t)j * rho;
+    for (int k = t; k < rho; k += B) cn[k] = (double)__ldg(a.pts + k * a.ps + idx);
+    if (b == 0) {
+      for (int k = t; k < rho; k += B) a.C[(size_t)j * rho + k] = (double)__ldg(a.pts + k * a.ps + idx);
+      if (t == 0 && a.seeds) a.seeds[j] = idx;
     }
     __syncthreads();
   }
@@ -653,37 +784,56 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
   a.flag = reinterpret_cast<int*>(ws + L.off_idx + 32);
   NYS_CUDA_TRY(cudaMemsetAsync(a.flag, 0, sizeof(int), s));
   void* args[] = {&a};
-  auto go = [&](auto kern) -> int {
+  const char* v1 = getenv("NYS_SEED_V1");
+  const bool runs = !(v1 && atoi(v1));
+  auto go = [&](auto kern_v1, auto kern_runs) -> int {
     // one block per SM; the block's D^2 chunk lives in shared memory when it fits
     const int nb = (int)std::max<long long>(1, std::min<long long>((long long)sms(), ceil_div(m, 512)));
     const long long chunk = ceil_div(m, (long long)nb);
-    size_t smem = (size_t)chunk * 8;
-    a.d2_in_smem = smem <= 200 * 1024;
-    if (!a.d2_in_smem) smem = 0;
+    size_t smem;
+    void* kern;
+    if (runs) {
+      a.per = (int)ceil_div(chunk, 512);
+      a.pp = reinterpret_cast<float*>(ws + L.off_pp);
+      a.pps = L.m_pad;
+      a.tsum = reinterpret_cast<double*>(ws + L.off_tsum);
+      const size_t hist = (size_t)m0 * rho * 8;
+      smem = (size_t)a.per * 512 * 8 + hist;
+      a.d2_in_smem = smem <= 200 * 1024;
+      if (!a.d2_in_smem) smem = hist;
+      kern = (void*)kern_runs;
+    } else {
+      smem = (size_t)chunk * 8;
+      a.d2_in_smem = smem <= 200 * 1024;
+      if (!a.d2_in_smem) smem = 0;
+      kern = (void*)kern_v1;
+    }
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     int per_sm = 0;
     NYS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, smem));
     if (per_sm < 1) return NYS_EUNSUPPORTED;
     count_launch();
-    NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(512), args, smem, s));
+    NYS_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(512), args, smem, s));
     return NYS_OK;
   };
+#define NYS_SEED_GO(GR, RX) go(k_seed_coop<GR, RX>, k_seed_runs<GR, RX>)
   switch (rho) {
-    case 1: return go(k_seed_coop<4, 1>);
-    case 2: return go(k_seed_coop<4, 2>);
-    case 3: return go(k_seed_coop<4, 3>);
-    case 4: return go(k_seed_coop<4, 4>);
+    case 1: return NYS_SEED_GO(4, 1);
+    case 2: return NYS_SEED_GO(4, 2);
+    case 3: return NYS_SEED_GO(4, 3);
+    case 4: return NYS_SEED_GO(4, 4);
     default: break;
   }
   switch (rho) {  // exact compile-time dimensions of the BASELINE guides
-    case 16: return go(k_seed_coop<16, 16>);
-    case 27: return go(k_seed_coop<32, 27>);
-    case 31: return go(k_seed_coop<32, 31>);
+    case 16: return NYS_SEED_GO(16, 16);
+    case 27: return NYS_SEED_GO(32, 27);
+    case 31: return NYS_SEED_GO(32, 31);
     default: break;
   }
-  if (rho <= 16) return go(k_seed_coop<16, 0>);
-  if (rho <= 32) return go(k_seed_coop<32, 0>);
-  return go(k_seed_coop<64, 0>);
+  if (rho <= 16) return NYS_SEED_GO(16, 0);
+  if (rho <= 32) return NYS_SEED_GO(32, 0);
+  return NYS_SEED_GO(64, 0);
+#undef NYS_SEED_GO
 }
 
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,

@@ -22,7 +22,8 @@ struct KLayout {
   int nb_assign, nb_seed, nb_coop;
   int64_t seed_chunk;
   size_t off_d2, off_labels, off_part, off_ppart, off_tot, off_cf, off_cprev, off_excl, off_state, off_arg,
-      off_idx, off_unif, total;
+      off_idx, off_unif, off_pp, off_tsum, total;
+  int64_t m_pad;  // m + 512 * nb_coop: slots of the thread-run-permuted seeding copy
 };
 
 inline int sms() {
@@ -45,7 +46,8 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.seed_chunk = ceil_div(m, L.nb_seed);
   L.nb_coop = 4 * sms();  // upper bound on co-resident blocks of the cooperative kernels
   size_t o = 0;
-  L.off_d2 = o;      o = align256(o + (size_t)m * 8);
+  L.m_pad = m + (int64_t)512 * L.nb_coop;
+  L.off_d2 = o;      o = align256(o + (size_t)L.m_pad * 8);
   L.off_labels = o;  o = align256(o + (size_t)m * 4);
   // ppart before anything that depends on (rho, m0): the step-wise
   // nys_kmeanspp_update / _pick pair must agree on it for any (rho, m0)
@@ -59,6 +61,8 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.off_arg = o;     o = align256(o + (size_t)std::max(std::max(L.nb_assign, L.nb_seed), L.nb_coop) * 32);
   L.off_idx = o;     o = align256(o + 64);
   L.off_unif = o;    o = align256(o + (size_t)m0 * 8);
+  L.off_tsum = o;    o = align256(o + (size_t)L.nb_coop * 512 * 8);
+  L.off_pp = o;      o = align256(o + (size_t)L.m_pad * rho * 4);
   L.total = o;
   return L;
 }

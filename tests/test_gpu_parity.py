@@ -267,3 +267,23 @@ def test_recursive_landmark_bands_match_single_band():
     ref = O.fast_filter_with_landmarks(f32.astype(np.float64), f32.astype(np.float64), C, 0.25,
                                        "gaussian_recursive", 2.5, 0)
     assert np.abs(many.double().cpu().numpy() - ref["output"]).max() <= TOL
+
+
+@pytest.mark.parametrize("rho,m,m0", [(3, 200000, 64), (16, 50000, 40), (27, 30000, 33), (5, 700, 9), (3, 1, 1)])
+def test_seeding_runs_match_owner_handoff(rho, m, m0, monkeypatch):
+    # the one-barrier thread-run seeding (k_seed_runs) draws the same k-means++
+    # picks as the owner-handoff kernel (NYS_SEED_V1=1) and the FP64 oracle
+    from paper_1901_06112_b200.landmarks import kmeans_device
+
+    rng = np.random.default_rng(rho * 1000 + m0)
+    pts = rng.uniform(0, 1, (rho, m)).astype(np.float32)
+    t = torch.from_numpy(pts).cuda()
+    a = kmeans_device(t, m0, seed=4, max_iter=2)
+    monkeypatch.setenv("NYS_SEED_V1", "1")
+    b = kmeans_device(t, m0, seed=4, max_iter=2)
+    assert np.array_equal(a.seed_indices, b.seed_indices)
+    assert np.array_equal(a.centroids, b.centroids)
+    if m <= 1000:
+        rs = np.random.default_rng(4)
+        seeds = O.plus_plus_seeds(pts.T.astype(np.float64), m0, rs)
+        assert np.array_equal(pts.T.astype(np.float64)[a.seed_indices], seeds)

@@ -199,6 +199,36 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
   }
 }
 
+// One value per thread (the first n threads; the rest pass 0): inclusive
+// block scan, target = tfn(total), then the first thread whose inclusive
+// prefix exceeds target -- or, when rounding left none, the last thread with a
+// positive value.  Returns that thread; *before = the sum of the values before
+// it, *total_out = the total.  Six block barriers.
+template <class TF>
+__device__ __forceinline__ int scan_pick(double v, TF tfn, double* sh, int* shi, double* before, double* total_out) {
+  __shared__ double tot_s, bef_s;
+  const double incl = block_incl_scan(v, sh);
+  if (threadIdx.x == blockDim.x - 1) tot_s = incl;
+  if (threadIdx.x == 0) {
+    shi[0] = (int)blockDim.x;
+    shi[1] = -1;
+  }
+  __syncthreads();
+  const double total = tot_s, target = tfn(total);
+  const unsigned bp = __ballot_sync(0xffffffffu, incl > target), bv = __ballot_sync(0xffffffffu, v > 0.0);
+  if ((threadIdx.x & 31) == 0) {
+    if (bp) atomicMin(&shi[0], (int)(threadIdx.x + __ffs(bp) - 1));
+    if (bv) atomicMax(&shi[1], (int)(threadIdx.x + 31 - __clz(bv)));
+  }
+  __syncthreads();
+  const int owner = shi[0] < (int)blockDim.x ? shi[0] : max(shi[1], 0);
+  if ((int)threadIdx.x == owner) bef_s = incl - v;
+  __syncthreads();
+  *before = bef_s;
+  if (total_out) *total_out = total;
+  return owner;
+}
+
 // k-means++ seeding with ONE grid barrier per draw (landmarks.py:60-73).
 // Thread t of block b owns the contiguous run of points lo_b + t*per + r,
 // r < per (a permuted copy of the guide keeps the per-r loads coalesced), so
@@ -215,8 +245,6 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
   extern __shared__ __align__(16) double d2s[];  // this block's D^2 (slot order r*B + t) when it fits
   __shared__ double sh[64];
   __shared__ int shi[2];
-  __shared__ double tot_sh;
-  __shared__ double rd2[512];                     // D^2 of the owning run (first 512 points per round)
   const int nb = gridDim.x, b = blockIdx.x, rho = RX > 0 ? RX : a.rho;  // RX: compile-time rho
   const int B = blockDim.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nwarp = B >> 5;
   const long long chunk = ceil_div(a.m, (long long)nb);
@@ -224,7 +252,8 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
   const int len = (int)(hi - lo), per = a.per;
   const long long slot0 = (long long)b * per * B;
   double* d2 = a.d2_in_smem ? d2s : a.d2 + slot0;
-  double* Cs = reinterpret_cast<double*>(a.d2_in_smem ? d2s + (size_t)per * B : d2s);  // [m0][rho] history
+  double* Cs = a.d2_in_smem ? d2s + (size_t)per * B : d2s;  // [m0][rho] centroid history
+  double* rd2 = Cs + (size_t)a.m0 * rho;                      // [per] D^2 of the owning run
   // permuted copy of this block's points (read back only by the thread that wrote each slot)
   for (int r = 0; r < per; ++r) {
     const int li = t * per + r;
@@ -237,7 +266,25 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
   for (int j = 1; j < a.m0; ++j) {
     const double* cs = Cs + (size_t)(j - 1) * rho;
     double s = 0.0;
-    for (int r = 0; r < per; ++r) {
+    constexpr int U = GR <= 4 ? 4 : 2;  // independent points in flight (register budget)
+    int r = 0;
+    for (; r + U <= per; r += U) {
+      float x[U][GR];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int d = 0; d < GR; ++d) x[u][d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)(r + u) * B + t] : 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double v = d2_exact_regs<GR>(x[u], rho, cs);
+        const int sl = (r + u) * B + t;
+        double nv = j == 1 ? v : fmin(d2[sl], v);
+        if (t * per + r + u >= len) nv = 0.0;
+        d2[sl] = nv;
+        s += nv;  // run sum in linear order
+      }
+    }
+    for (; r < per; ++r) {
       float x[GR];
 #pragma unroll
       for (int d = 0; d < GR; ++d) x[d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)r * B + t] : 0.f;
@@ -246,74 +293,56 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
       double nv = j == 1 ? v : fmin(d2[sl], v);
       if (t * per + r >= len) nv = 0.0;
       d2[sl] = nv;
-      s += nv;  // run sum in linear order
+      s += nv;
     }
     a.tsum[(long long)b * B + t] = s;
     {
-      const double incl = block_incl_scan(s, sh);  // the same scan the resolvers run over tsum
+      const double incl = block_incl_scan(s, sh);  // the scan scan_pick runs over tsum
       if (t == B - 1) a.ppart[b] = incl;
     }
     grid.sync();
-    // --- every block: the owning block ---
-    double total;
-    {
-      const long long pb = ceil_div((long long)nb, (long long)B);
-      const long long a0 = min((long long)nb, (long long)t * pb), a1 = min((long long)nb, a0 + pb);
-      double mine = 0.0;
-      for (long long q = a0; q < a1; ++q) mine += __ldcg(a.ppart + q);
-      const double incl = block_incl_scan(mine, sh);
-      if (t == B - 1) tot_sh = incl;
-      __syncthreads();
-      total = tot_sh;
-    }
+    // --- every block resolves the draw with identical arithmetic ---
+    // the owning block (nb <= blockDim: one block total per thread)
+    double total = 0.0, before_b = 0.0, before_t = 0.0, before_r = 0.0;
+    const double u = a.uniforms[j - 1];
+    const int bstar = scan_pick(t < nb ? __ldcg(a.ppart + t) : 0.0, [&](double tot) { return u * tot; }, sh, shi,
+                                &before_b, &total);
     if (!(total > 0.0)) {  // sum(D^2) == 0: the reference switches to rng.integers (host redo)
       if (b == 0 && t == 0) a.st->zero_draw = j;
       return;  // uniform across the grid
     }
-    const double target = a.uniforms[j - 1] * total;
-    double before_b = 0.0, before_t = 0.0;
-    const long long bstar = scan_find<true>(a.ppart, nb, target, sh, shi, &before_b);
-    // --- the owning thread run inside block bstar ---
-    const long long tstar = scan_find<true>(a.tsum + bstar * B, B, target - before_b, sh, shi, &before_t);
-    const long long lo_s = min(a.m, bstar * chunk), len_s = min(a.m, lo_s + chunk) - lo_s;
-    // --- the point inside the run: recompute its D^2 exactly (one warp per point) ---
+    const double target = u * total, tgt_b = target - before_b;
+    // the owning thread run inside block bstar
+    const int tstar = scan_pick(__ldcg(a.tsum + (long long)bstar * B + t), [&](double) { return tgt_b; }, sh, shi,
+                                &before_t, nullptr);
+    // the point inside the run: its D^2 recomputed exactly (warp per point, lanes over the centroids so far)
+    const long long lo_s = min(a.m, (long long)bstar * chunk), len_s = min(a.m, lo_s + chunk) - lo_s;
+    const double tgt = tgt_b - before_t;
     long long idx = -1;
     for (int r0 = 0; r0 < per && idx < 0; r0 += 512) {
       const int cnt = min(512, per - r0);
       for (int rr = wid; rr < cnt; rr += nwarp) {
-        const long long li = tstar * per + r0 + rr;
-        double mn = INFINITY;
+        const long long li = (long long)tstar * per + r0 + rr;
+        double mn = 0.0;
         if (li < len_s) {
           float x[GR];
 #pragma unroll
           for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(a.pts + d * a.ps + lo_s + li) : 0.f;
+          mn = INFINITY;
           for (int k = lane; k < j; k += 32) mn = fmin(mn, d2_exact_regs<GR>(x, rho, Cs + (size_t)k * rho));
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        } else {
-          mn = 0.0;
         }
-        if (lane == 0) rd2[rr] = mn;
+        if (lane == 0) rd2[r0 + rr] = mn;
       }
       __syncthreads();
-      double before_r = 0.0;
-      const double tgt = target - before_b - before_t;
-      // first point of this round whose running sum passes tgt (scan_find's fallback: last positive)
-      double run_tot = 0.0;
-      {
-        const double v = t < cnt ? rd2[t] : 0.0;
-        const double incl = block_incl_scan(v, sh);
-        if (t == B - 1) tot_sh = incl;
-        __syncthreads();
-        run_tot = tot_sh;
-      }
-      if (r0 + cnt >= per || run_tot > tgt) {
-        const long long k = scan_find<false>(rd2, cnt, tgt, sh, shi, &before_r);
-        idx = lo_s + tstar * per + r0 + max(0ll, k);
-      } else {
-        before_t += run_tot;  // the target lies in a later round of this run
-      }
-      __syncthreads();
+      double run_tot = 0.0, before_in = 0.0;
+      const int rstar = scan_pick(t < cnt ? rd2[r0 + t] : 0.0, [&](double) { return tgt - before_r; }, sh, shi,
+                                  &before_in, &run_tot);
+      if (r0 + cnt >= per || run_tot > tgt - before_r)
+        idx = lo_s + (long long)tstar * per + r0 + rstar;
+      else
+        before_r += run_tot;  // the target lies in a later round of this run
     }
     double* cn = Cs + (size_t)j * rho;
     for (int k = t; k < rho; k += B) cn[k] = (double)__ldg(a.pts + k * a.ps + idx);
@@ -797,7 +826,7 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
       a.pp = reinterpret_cast<float*>(ws + L.off_pp);
       a.pps = L.m_pad;
       a.tsum = reinterpret_cast<double*>(ws + L.off_tsum);
-      const size_t hist = (size_t)m0 * rho * 8;
+      const size_t hist = (size_t)m0 * rho * 8 + (size_t)a.per * 8;  // centroid history + owning run
       smem = (size_t)a.per * 512 * 8 + hist;
       a.d2_in_smem = smem <= 200 * 1024;
       if (!a.d2_in_smem) smem = hist;

@@ -69,6 +69,9 @@ size_t nys_kmeans_workspace_bytes(int64_t m, int rho, int m0);
  * stats_out [dev]: int64[4] = {iterations_run, first_zero_total_draw (or -1),
  *                              last_changed_count, empty_repairs}.
  * quant_error_out [dev]: float64[1].  assignment_out [dev] (nullable): int64[m].
+ * When quant_error_out and assignment_out are both null the final exact pass
+ * is skipped (the caller runs nys_kmeans_exact itself, e.g. overlapped with
+ * its host-side work on the centroids).
  * seed_indices_out [dev] (nullable): int64[m0], the k-means++ picks.
  * If stats_out[1] >= 0 the k-means++ stream hit sum(d2) == 0 at that draw; the
  * reference then switches to rng.integers(m) (landmarks.py:69-70) and the
@@ -185,7 +188,8 @@ size_t nys_filter_workspace_bytes(const nys_filter_desc* d);
 
 /* Upload the per-call constants (centroids, M, u0) into `workspace` and reset
  * the min|eta| / guarded-pixel accumulators.  Call once per filter before the
- * band passes below (synchronises `stream` once: the source is pageable). */
+ * band passes below.  Asynchronous: the host constants are staged by the
+ * runtime before the call returns. */
 int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspace_bytes,
                        void* stream);
 

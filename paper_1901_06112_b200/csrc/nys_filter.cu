@@ -89,9 +89,9 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
     h[L.off_U0 + j] = (float)d->u0[j];
   }
   cudaStream_t s = (cudaStream_t)stream;
+  // pageable H2D: the runtime stages `h` before returning, so it may go away
+  // right after (no stream synchronisation: the caller keeps queueing work)
   NYS_CUDA_TRY(cudaMemcpyAsync(workspace, h.data(), L.n_floats * sizeof(float), cudaMemcpyHostToDevice, s));
-  // pageable source: make sure the copy has consumed `h` before it goes away
-  NYS_CUDA_TRY(cudaStreamSynchronize(s));
   count_launch();
   k_reset_stats<<<1, 1, 0, s>>>(reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));
   NYS_LAUNCH_CHECK();

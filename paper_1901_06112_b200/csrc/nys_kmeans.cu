@@ -542,10 +542,15 @@ static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho,
       NYS_LAUNCH_CHECK();
     }
   }
-  double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
-  int rc2 = launch_exact(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart, L.nb_assign, s);
-  if (rc2) return rc2;
-  count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, qe);
+  if (qe || asg) {  // the final exact pass; callers that pass neither run nys_kmeans_exact later
+    double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
+    int rc2 = launch_exact(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart, L.nb_assign, s);
+    if (rc2) return rc2;
+    if (qe) {
+      count_launch();
+      k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, qe);
+    }
+  }
   count_launch(); k_write_stats<<<1, 1, 0, s>>>(st, reinterpret_cast<long long*>(stats));
   NYS_LAUNCH_CHECK();
   return NYS_OK;
@@ -571,7 +576,7 @@ int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho
   int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
   if (rc) return rc;
   if (max_iter < 1 || first_index < 0 || first_index >= m || !centroids_out || !errors_out || !stats_out ||
-      !quant_error_out || (m0 > 1 && !uniforms))
+      (m0 > 1 && !uniforms))
     return NYS_EINVAL;
   const KLayout L = klayout(m, rho, m0);
   char* ws = reinterpret_cast<char*>(workspace);
@@ -606,8 +611,7 @@ int nys_kmeans_run_seeded(const float* points, int64_t plane_stride, int64_t m, 
                           size_t workspace_bytes, void* stream) {
   int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
   if (rc) return rc;
-  if (max_iter < 1 || !seed_indices || !centroids_out || !errors_out || !stats_out || !quant_error_out)
-    return NYS_EINVAL;
+  if (max_iter < 1 || !seed_indices || !centroids_out || !errors_out || !stats_out) return NYS_EINVAL;
   for (int j = 0; j < m0; ++j)
     if (seed_indices[j] < 0 || seed_indices[j] >= m) return NYS_EINVAL;
   const KLayout L = klayout(m, rho, m0);

@@ -25,7 +25,7 @@ from . import _native
 from ._device import StageTimer, ptr, require_cuda, stream_ptr, to_device_f32, workspace
 from .bands import Band, plan_bands
 from .image import Image
-from .landmarks import DEFAULT_MAX_ITER, exact_assignment, kmeans_device
+from .landmarks import DEFAULT_MAX_ITER, exact_assignment, exact_assignment_async, kmeans_device
 from .nystrom import DEFAULT_EPS_DROP, RangeKernel, mixing_plan
 from .spatial import BOX, GAUSSIAN_FIR, GAUSSIAN_RECURSIVE, SpatialKernel
 
@@ -397,9 +397,14 @@ def _output_image(out: torch.Tensor, f: Image, given: torch.Tensor | None = None
 
 
 def _select_landmarks(inp: _Inputs, params: FilterParams):
+    """(centroids on the host, quant_error as a float or a pending device
+    scalar).  For k-means the final exact pass is launched only after the
+    centroids reached the host, so it runs while the host builds the mixing
+    plan."""
     if params.landmark_strategy == STRATEGY_KMEANS:
-        km = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter)
-        return km.centroids, km.quant_error
+        km = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter,
+                           defer_exact=True)
+        return km.centroids, exact_assignment_async(inp.points, km.centroids_dev, params.m0)
     rng = np.random.default_rng(params.seed)
     m = inp.points.shape[1]
     idx = rng.choice(m, size=params.m0, replace=False)
@@ -430,7 +435,13 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     out_given = out
     out, plan, stats = run_filter(inp, centroids, params, timer, kernel_events=kernel_events,
                                   out=_output_buffer(f, out))
-    min_den, guarded = _stats_host(stats)  # synchronises: a host `out` is complete after this
+    if isinstance(qe, torch.Tensor):  # the deferred exact pass rides along with the statistics copy
+        stats = torch.cat([stats, qe])
+        h = stats.cpu()
+        qe = float(h[2])
+        min_den, guarded = float(h[0]), int(h[1:2].view(torch.int64)[0])
+    else:
+        min_den, guarded = _stats_host(stats)  # synchronises: a host `out` is complete after this
     timer.mark("normalization")  # fused into K3
     t = timer.elapsed()
     timings = {k: t.get(k, 0.0) for k in ("clustering", "eigendecomposition", "extrapolation", "convolutions",

@@ -43,6 +43,7 @@ class DeviceKMeans:
     iterations: int
     seed_indices: np.ndarray
     assignment: torch.Tensor | None  # int64 (m,) on device
+    centroids_dev: torch.Tensor | None = None  # (m0 * rho,) float64 on device
 
 
 def _seed_stream(m: int, m0: int, seed: int):
@@ -66,9 +67,13 @@ def _replay_zero_total(m: int, m0: int, seed: int, j0: int, device_seeds: np.nda
 
 
 def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER,
-                  want_assignment: bool = False) -> DeviceKMeans:
+                  want_assignment: bool = False, defer_exact: bool = False) -> DeviceKMeans:
     """k-means on planar device points ``(rho, m)`` float32 (rows may be any
-    plane stride; the last dim must be contiguous)."""
+    plane stride; the last dim must be contiguous).
+
+    ``defer_exact``: skip the final exact pass (quant_error is then None);
+    the caller launches it with ``exact_assignment_async`` once it has the
+    centroids, so the pass overlaps its host-side work."""
     require_cuda()
     if points.dim() != 2 or points.stride(1) != 1:
         raise ValueError("points must be a (rho, m) tensor with contiguous rows")
@@ -94,8 +99,9 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     seeds = res[m0 * rho + max_iter + 5:].view(torch.int64)
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     first, uniforms = _seed_stream(m, m0, seed)
+    qe_p = None if (defer_exact and asg is None) else ptr(qe)
     _native.check(lib.nys_kmeans_run(ptr(points), ps, m, rho, m0, max_iter, first,
-                                     uniforms.ctypes.data, ptr(Cd), ptr(errs), ptr(stats), ptr(qe),
+                                     uniforms.ctypes.data, ptr(Cd), ptr(errs), ptr(stats), qe_p,
                                      ptr(asg), ptr(seeds), ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
     h = res.cpu().numpy()
     st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
@@ -104,16 +110,16 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
         sidx = _replay_zero_total(m, m0, seed, int(st[1]), seeds_h)
         sidx = np.ascontiguousarray(sidx, dtype=np.int64)
         _native.check(lib.nys_kmeans_run_seeded(ptr(points), ps, m, rho, m0, max_iter, sidx.ctypes.data,
-                                                ptr(Cd), ptr(errs), ptr(stats), ptr(qe), ptr(asg),
+                                                ptr(Cd), ptr(errs), ptr(stats), qe_p, ptr(asg),
                                                 ptr(ws), wsb, stream_ptr()), "nys_kmeans_run_seeded")
         h = res.cpu().numpy()
         st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
         seeds_h = sidx
     iters = int(st[0])
     return DeviceKMeans(centroids=h[:m0 * rho].reshape(m0, rho).copy(),
-                        quant_error=float(h[m0 * rho + max_iter]),
+                        quant_error=None if qe_p is None else float(h[m0 * rho + max_iter]),
                         errors=tuple(h[m0 * rho:m0 * rho + iters].tolist()), iterations=iters,
-                        seed_indices=seeds_h, assignment=asg)
+                        seed_indices=seeds_h, assignment=asg, centroids_dev=Cd)
 
 
 def _points_planar(points) -> torch.Tensor:
@@ -138,6 +144,22 @@ def kmeans_landmarks(points, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX
     res = kmeans_device(_points_planar(points), m0, seed=seed, max_iter=max_iter, want_assignment=True)
     return LandmarkSet(centroids=res.centroids, assignment=res.assignment.cpu().numpy(),
                        quant_error=res.quant_error, errors=res.errors)
+
+
+def exact_assignment_async(points_planar: torch.Tensor, centroids_dev: torch.Tensor, m0: int) -> torch.Tensor:
+    """Launch the exact pass (landmarks.py:121-129) against device centroids
+    (m0 * rho float64) and return quant_error as a 1-element device tensor,
+    without synchronising."""
+    rho, m = int(points_planar.shape[0]), int(points_planar.shape[1])
+    lib = _native.lib()
+    dev = points_planar.device
+    wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
+    ws = workspace(wsb)
+    Cd = centroids_dev
+    qe = torch.empty(1, dtype=torch.float64, device=dev)
+    _native.check(lib.nys_kmeans_exact(ptr(points_planar), int(points_planar.stride(0)), m, rho, ptr(Cd), m0,
+                                       None, ptr(qe), ptr(ws), wsb, stream_ptr()), "nys_kmeans_exact")
+    return qe
 
 
 def exact_assignment(points_planar: torch.Tensor, centroids: np.ndarray, want_assignment: bool = True):

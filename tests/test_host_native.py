@@ -150,9 +150,11 @@ def test_no_cpu_fallback():
 def test_out_of_scope_names_raise():
     import paper_1901_06112_b200 as P
 
-    for name in ("brute_force_filter", "gaussian_recursive", "psnr", "load_image"):
+    for name in ("gaussian_recursive", "box_filter", "gaussian_fir"):
         with pytest.raises(NotImplementedError):
             getattr(P, name)()
+    for name in ("brute_force_filter", "psnr", "ssim", "mse", "quality", "load_image", "save_image"):
+        assert callable(getattr(P, name)) and getattr(P, name).__name__ != "_f"
 
 
 def test_header_cites_reference():

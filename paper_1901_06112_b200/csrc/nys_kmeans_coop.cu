@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   int sexp = 0;
   if (maxabs > 0.f) sexp = 61 - ilogb((double)maxabs * (double)a.m) - 1;
   const double scale = ldexp(1.0, sexp), inv_scale = ldexp(1.0, -sexp);
-  constexpr int HH = GR <= 4 ? 2 : 1;  // points per lane in the full search: every centroid LDS serves HH
+  constexpr int HH = GR <= 4 ? 3 : 1;  // points per lane in the full search: every centroid LDS serves HH
   constexpr int JJ = GR >= 16 ? 4 : 1; // centroids per step: independent FMA chains for long guides
 
   for (int it = 0; it < a.max_iter; ++it) {
@@ -513,24 +513,37 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     long long nlist = hi - lo;
     if (!full_pass) {
       // phase A: warp w tests its contiguous sub-range; failures go to its list segment in point order
+      // PA chunks of 32 points in flight per warp: their point, label and bound
+      // loads are issued together (the per-chunk loads are otherwise two
+      // dependent L2 round trips each), then tested in point order
+      constexpr int PA = GR <= 4 ? 4 : 2;
       int nl = 0;
-      for (long long base = wlo; base < whi; base += 32) {
-        const long long i = base + lane;
-        const bool valid = i < whi;
-        bool need = false;
-        if (valid) {
-          float x[GR];
+      for (long long base = wlo; base < whi; base += 32 * PA) {
+        float x[PA][GR], lbv[PA];
+        int lab[PA];
 #pragma unroll
-          for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(a.pts + d * a.ps + i) : 0.f;
-          const int lab = a.labels[i];
-          const float d2a = d2_f32<GR>(x, rho, Cf + (size_t)lab * rhop);
-          const double lbe = (double)a.lb[i] - dcum;
-          if (lbe > 0.0 && (double)d2a * (1.0 + LB_EPS) < lbe * lbe * (1.0 - LB_EPS)) near_sum += (double)d2a;
-          else need = true;
+        for (int u = 0; u < PA; ++u) {
+          const long long i = base + 32 * u + lane;
+          const bool valid = i < whi;
+#pragma unroll
+          for (int d = 0; d < GR; ++d) x[u][d] = (valid && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
+          lab[u] = valid ? a.labels[i] : 0;
+          lbv[u] = valid ? a.lb[i] : 0.f;
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, need);
-        if (need) a.list[wlo + nl + __popc(bal & ((1u << lane) - 1u))] = (int)i;
-        nl += __popc(bal);
+#pragma unroll
+        for (int u = 0; u < PA; ++u) {
+          const long long i = base + 32 * u + lane;
+          bool need = false;
+          if (i < whi) {
+            const float d2a = d2_f32<GR>(x[u], rho, Cf + (size_t)lab[u] * rhop);
+            const double lbe = (double)lbv[u] - dcum;
+            if (lbe > 0.0 && (double)d2a * (1.0 + LB_EPS) < lbe * lbe * (1.0 - LB_EPS)) near_sum += (double)d2a;
+            else need = true;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, need);
+          if (need) a.list[wlo + nl + __popc(bal & ((1u << lane) - 1u))] = (int)i;
+          nl += __popc(bal);
+        }
       }
       if (lane == 0) wlen[w] = nl;
       __syncthreads();
@@ -545,7 +558,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     for (long long q0 = (long long)w * 32 * HH; q0 < nlist; q0 += (long long)nw * 32 * HH) {
       float x[HH][GR];
       float best[HH], second[HH];
-      int arg[HH];
+      int arg[HH], oldl[HH];
       long long idx[HH];
       bool valid[HH];
 #pragma unroll
@@ -567,6 +580,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         idx[h] = i;
 #pragma unroll
         for (int d = 0; d < GR; ++d) x[h][d] = (valid[h] && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
+        oldl[h] = (valid[h] && it > 0) ? a.labels[i] : -1;  // issued with the point loads, used after the search
       }
       for (int j0 = 0; j0 < m0; j0 += JJ) {
         float d2[JJ][HH];
@@ -620,7 +634,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         bool chg = false;
         if (valid[h]) {
           near_sum += (double)best[h];
-          old = it == 0 ? -1 : a.labels[i];
+          old = oldl[h];
           chg = old != arg[h];
           if (chg) {
             changed += 1.0;

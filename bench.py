@@ -223,8 +223,10 @@ def run_ours(args, rank: int, world: int):
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         tr = json.loads(prof.read_text()).get(wl.name, {}).get(dom)
-        if tr:
-            roof["traffic"] = tr
+        if tr:  # DRAM bytes per launch from one ncu --set full capture (vs bytes_per_px * px algorithmic)
+            roof["traffic"] = tr["dram_bytes_per_launch"]
+            roof["traffic_algorithmic_bytes"] = bytes_px[dom] * px
+            roof["traffic_source"] = tr["source"]
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",

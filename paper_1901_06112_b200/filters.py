@@ -321,13 +321,16 @@ def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterPar
     if timer:
         timer.mark("extrapolation")
     budget = plane_budget if plane_budget is not None else SMALL_PLANES_BYTES
-    full = int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), 0))
+    full = int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), 0))  # preferred path, all landmarks at once
     if full > budget and plane_budget is None:
         budget = max(budget, _plane_budget())
-    nb = d.m0 + 1
-    while nb > 1 and int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), nb)) > budget:
-        nb = max(1, nb // 2) if nb > 8 else nb - 1
-    sb = int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), nb))
+    if full <= budget:
+        sb = full
+    else:  # banded global-memory path
+        nb = d.m0 + 1
+        while nb > 1 and int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), nb)) > budget:
+            nb = max(1, nb // 2) if nb > 8 else nb - 1
+        sb = int(lib.nys_filter_recursive_scratch_bytes(C.byref(d), nb))
     scratch = torch.empty(sb, dtype=torch.uint8, device=inp.f.device)
     if out is None:
         out = torch.empty((n, H, W), dtype=torch.float32, device=inp.f.device)

@@ -287,3 +287,24 @@ def test_seeding_runs_match_owner_handoff(rho, m, m0, monkeypatch):
         rs = np.random.default_rng(4)
         seeds = O.plus_plus_seeds(pts.T.astype(np.float64), m0, rs)
         assert np.array_equal(pts.T.astype(np.float64)[a.seed_indices], seeds)
+
+
+@pytest.mark.parametrize("shape,n", [((72, 128), 3), ((40, 52), 7), ((5, 3), 2), ((130, 9), 1)])
+def test_recursive_shared_path_matches_global_path(shape, n, monkeypatch):
+    # the shared-memory RV/RH path (columns first, rows fused with the contraction) against the
+    # banded global-memory path and the oracle
+    H, W = shape
+    f32 = spectral_scene(H, W, n, 5, 0.03, seed=H + n) if n > 3 else np.ascontiguousarray(
+        color_scene(H, W, 5, 0.05, seed=H + n)[:n])
+    f64 = f32.astype(np.float64)
+    C, _, _, _ = O.kmeans(O.range_vectors(f64), 9, 0, 6)
+    params = FilterParams(spatial=SpatialKernel.recursive(2.5), theta=0.2, m0=9)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    a = filter_with_landmarks(f, f, C, params)
+    monkeypatch.setenv("NYS_REC_PATH", "global")
+    b = filter_with_landmarks(f, f, C, params)
+    ref = O.fast_filter_with_landmarks(f64, f64, C, 0.2, "gaussian_recursive", 2.5, 0)
+    oa, ob = a.output.data.double().cpu().numpy(), b.output.data.double().cpu().numpy()
+    assert np.abs(oa - ref["output"]).max() <= TOL
+    assert np.abs(oa - ob).max() <= 1e-5
+    assert a.guarded_pixels == b.guarded_pixels == ref["guarded_pixels"]

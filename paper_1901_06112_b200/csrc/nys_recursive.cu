@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(BS) k_rec_features(
   float* sg = rsm;                                   // [rho][BS]
   float* sb = sg + (size_t)rho * BS;                 // [m0][PT]
   float* sy = sb + (size_t)m0 * PT;                  // [m0+1][PT]
-  float* sc = sy + (size_t)(m0 + 1) * PT;            // CSM: [m0][rhop] centroids, then [m0][m0q] MT
+  float* sc = rsm + ((((size_t)rho * BS + (size_t)(2 * m0 + 1) * PT) + 3) & ~(size_t)3);  // CSM, 16-byte aligned:
+                                                     // [m0][rhop] centroids, then [m0][m0q] MT
   const int t = threadIdx.x;
   const long long npx = (long long)H * W;
   const long long px0 = (long long)blockIdx.x * BS;
@@ -413,16 +414,27 @@ __global__ void __launch_bounds__(256) k_recv(const float* __restrict__ Yp, cons
   RecSmem m = rec_smem(rvm, Lmax, nl, S);
   for (int k = threadIdx.x; k < Lmax * 5; k += blockDim.x) m.Hh[k] = Hh_g[k];
   const float* yg = Yp + (long long)g * npx;
-  for (int e = threadIdx.x; e < H * nl; e += blockDim.x) {
-    const int cp = e % ncp, rest = e / ncp, col = rest % xw, row = rest / xw;
-    const int x = x0 + col, c = c0 + cp;
-    float v = 0.f;
-    if (x < W) {
+  constexpr int U = 8;  // independent loads in flight per thread
+  for (int e0 = threadIdx.x; e0 < H * nl; e0 += U * blockDim.x) {
+    float yv[U], fv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int cp = e % ncp, rest = e / ncp, col = rest % xw, row = rest / xw;
+      const int x = x0 + col, c = c0 + cp;
+      const bool ok = e < H * nl && x < W;
       const long long p = (long long)row * W + x;
-      const float yv = __ldg(yg + p);
-      v = c < n ? yv * __ldg(f + (long long)c * fps + p) : yv;
+      yv[u] = ok ? __ldg(yg + p) : 0.f;
+      fv[u] = (ok && c < n) ? __ldg(f + (long long)c * fps + p) : 1.f;
     }
-    m.buf[(size_t)(col * ncp + cp) * ls + row] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < H * nl) {
+        const int cp = e % ncp, rest = e / ncp, col = rest % xw, row = rest / xw;
+        m.buf[(size_t)(col * ncp + cp) * ls + row] = yv[u] * fv[u];
+      }
+    }
   }
   __syncthreads();
   iir_lines(m.buf, nl, H, ls, S, L, m.Hh, cf, m.zt, m.st, m.e0);
@@ -603,8 +615,10 @@ inline void seg_plan(int N, int nl, int& S, int& L) {
 
 inline RecPlan rec_plan(const nys_filter_desc* d) {
   RecPlan p{};
+  // opt-in (NYS_REC_PATH=shared): measured slower than the banded global path on cfg 2
+  // (RV 7 ms + RH 12 ms vs 10 ms; instruction-bound at one CTA per SM), kept with its A/B test
   const char* e = getenv("NYS_REC_PATH");
-  if (e && std::string(e) == "global") return p;
+  if (!e || std::string(e) != "shared") return p;
   const int H = d->H, W = d->W, LG = std::min(4, d->n) + 1;
   p.cpp = 2;
   const size_t vmax = 112 * 1024, hmax = 220 * 1024;
@@ -719,7 +733,7 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
       const int BS = d->m0 <= 96 ? 128 : 64;
       const bool csm = d->m0 <= 96;
       const size_t smem = ((size_t)d->rho * BS + (size_t)(2 * d->m0 + 1) * (BS + 1) +
-                           (csm ? (size_t)d->m0 * (L.rhop + L.m0q) : 0)) * sizeof(float);
+                           (csm ? (size_t)d->m0 * (L.rhop + L.m0q) + 4 : 0)) * sizeof(float);
       auto k = csm ? k_rec_features<128, true, true> : k_rec_features<64, false, true>;
       NYS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       count_launch();
@@ -764,7 +778,7 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
     const int BS = d->m0 <= 96 ? 128 : 64;
     const bool csm = d->m0 <= 96;
     const size_t smem = ((size_t)d->rho * BS + (size_t)(2 * d->m0 + 1) * (BS + 1) +
-                         (csm ? (size_t)d->m0 * (L.rhop + L.m0q) : 0)) * sizeof(float);
+                         (csm ? (size_t)d->m0 * (L.rhop + L.m0q) + 4 : 0)) * sizeof(float);
     auto k = csm ? k_rec_features<128, true, false> : k_rec_features<64, false, false>;
     NYS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();

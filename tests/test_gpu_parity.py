@@ -291,19 +291,24 @@ def test_seeding_runs_match_owner_handoff(rho, m, m0, monkeypatch):
 
 @pytest.mark.parametrize("shape,n", [((72, 128), 3), ((40, 52), 7), ((5, 3), 2), ((130, 9), 1)])
 def test_recursive_shared_path_matches_global_path(shape, n, monkeypatch):
-    # the shared-memory RV/RH path (columns first, rows fused with the contraction) against the
-    # banded global-memory path and the oracle
+    # the opt-in shared-memory RV/RH path (columns first, rows fused with the contraction)
+    # against the default banded global-memory path and the oracle
     H, W = shape
     f32 = spectral_scene(H, W, n, 5, 0.03, seed=H + n) if n > 3 else np.ascontiguousarray(
         color_scene(H, W, 5, 0.05, seed=H + n)[:n])
     f64 = f32.astype(np.float64)
-    C, _, _, _ = O.kmeans(O.range_vectors(f64), 9, 0, 6)
-    params = FilterParams(spatial=SpatialKernel.recursive(2.5), theta=0.2, m0=9)
+    # well-conditioned landmark kernels: a 1-D guide with 5 landmarks at theta 0.35 already has
+    # cond(A) = 6e6, where the FP32 y-form misses 1e-4 on the FIR and recursive paths alike
+    # (tools/dbg_rec.py); the BASELINE configs have cond(A) <= 252
+    m0, theta = (9, 0.2) if n > 1 else (3, 0.5)
+    C, _, _, _ = O.kmeans(O.range_vectors(f64), m0, 0, 6)
+    params = FilterParams(spatial=SpatialKernel.recursive(2.5), theta=theta, m0=m0)
     f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    monkeypatch.setenv("NYS_REC_PATH", "shared")
     a = filter_with_landmarks(f, f, C, params)
-    monkeypatch.setenv("NYS_REC_PATH", "global")
+    monkeypatch.delenv("NYS_REC_PATH")
     b = filter_with_landmarks(f, f, C, params)
-    ref = O.fast_filter_with_landmarks(f64, f64, C, 0.2, "gaussian_recursive", 2.5, 0)
+    ref = O.fast_filter_with_landmarks(f64, f64, C, theta, "gaussian_recursive", 2.5, 0)
     oa, ob = a.output.data.double().cpu().numpy(), b.output.data.double().cpu().numpy()
     assert np.abs(oa - ref["output"]).max() <= TOL
     assert np.abs(oa - ob).max() <= 1e-5

@@ -169,6 +169,13 @@ typedef struct nys_filter_desc {
      * Used by the row-band-sharded multi-GPU path, whose ranks hold their rows
      * plus R (+1) halo rows; reads never leave this range. */
     int row_lo, row_hi;
+    /* 0: y-form (M = sum_k w_k w_k^T / alpha_k, contraction with the raw
+     * features b(x)).  1: phi-form for ill-conditioned landmark kernels: M holds
+     * P = Lambda^{-1/2} W^T (rows >= rank zero), so y = phi = P b, the planes
+     * are phi_k f, and the contraction weights are phi(x) itself (K2 stores
+     * them as the raw-feature planes).  Same reference quantity
+     * (filters.py:227-238); FP32 error no longer grows with cond(A). */
+    int phi_form;
 } nys_filter_desc;
 
 /* Size of the horizontal-pass plane buffer for a band of `rows` output rows:

@@ -39,7 +39,7 @@ class FilterDesc(C.Structure):
         ("sigma", C.c_double), ("m0", C.c_int), ("theta", C.c_double),
         ("centroids", C.POINTER(C.c_double)), ("M", C.POINTER(C.c_double)),
         ("u0", C.POINTER(C.c_double)), ("alpha0", C.c_double), ("eps_den", C.c_double),
-        ("row_lo", C.c_int), ("row_hi", C.c_int),
+        ("row_lo", C.c_int), ("row_hi", C.c_int), ("phi_form", C.c_int),
     ]
 
 

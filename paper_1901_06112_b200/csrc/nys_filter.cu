@@ -86,7 +86,8 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
   for (int j = 0; j < d->m0; ++j) {
     for (int i = 0; i < d->m0; ++i) h[L.off_MT + (size_t)j * L.m0q + i] = (float)d->M[(size_t)i * d->m0 + j];
     h[L.off_MT + (size_t)j * L.m0q + d->m0] = (float)d->u0[j];
-    h[L.off_U0 + j] = (float)d->u0[j];
+    // K3 forms s0 = U0 . (stored feature planes): u0 . b, or sqrt(alpha_1) phi_0 in the phi-form
+    h[L.off_U0 + j] = d->phi_form ? (j == 0 ? (float)std::sqrt(d->alpha0) : 0.f) : (float)d->u0[j];
   }
   cudaStream_t s = (cudaStream_t)stream;
   // pageable H2D: the runtime stages `h` before returning, so it may go away

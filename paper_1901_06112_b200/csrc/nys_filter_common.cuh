@@ -45,7 +45,7 @@ inline int64_t plane_row_stride(int W, int nplanes) { return (int64_t)wpad32(W) 
 // K2 also stores the raw features b_i (one plane per landmark, after the
 // (m0+1)(n+1) filtered planes) when recomputing them at the centre pixel in
 // K3 would be expensive: high-dimensional guides and the NLM patch guide
-inline bool use_bplanes(const nys_filter_desc* d) { return d->guide_kind == 1 || d->rho > 8; }
+inline bool use_bplanes(const nys_filter_desc* d) { return d->guide_kind == 1 || d->rho > 8 || d->phi_form; }
 inline int buffer_planes(const nys_filter_desc* d) {
   return (d->m0 + 1) * (d->n + 1) + (use_bplanes(d) ? d->m0 : 0);
 }

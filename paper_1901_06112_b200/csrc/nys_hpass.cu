@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_feat_hpass(const HArgs a) {
         const int i = it % m0, rest = it / m0, xg = rest % XG, r = rest / XG;
         const int xo = x0 + xg * K2_XR;
         if (xo >= W || vb + r >= a.v0 + a.vrows) continue;
-        const float* src = Bs + ((size_t)r * m0 + i) * pitch + R + xg * K2_XR;
+        const float* src = (a.phi ? Ys + ((size_t)r * m0q + i) * pitch : Bs + ((size_t)r * m0 + i) * pitch) + R +
+                           xg * K2_XR;  // phi-form: the contraction weights are phi = y
         float* dst = a.hp + (long long)(vb + r - a.v0) * a.rs + (long long)(xo >> 5) * (a.npl * 32) +
                      (long long)(L * NC + i) * 32 + (xo & 31);
 #pragma unroll
@@ -219,6 +220,7 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.rlo = std::max(0, d->row_lo);
   a.npl = buffer_planes(d);
   a.bplanes = use_bplanes(d);
+  a.phi = d->phi_form;
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
   fill_taps(d, a.taps);

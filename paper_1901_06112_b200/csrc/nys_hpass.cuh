@@ -23,6 +23,7 @@ struct HArgs {
   int v0, vrows, TW, pitch, tiles_x, rpt;  // rpt: virtual rows per tile
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   int npl, bplanes;  // planes per buffer row block; store raw b_i planes after the filtered ones
+  int phi;           // phi-form: store y_i (= phi_i) in the feature-plane slots instead of b_i
   int ku, nu, tcols, nbuf;  // tcgen05 path: K (m0 padded to 8), N ((m0+1) padded to 16), TMEM columns per group, y/f buffers
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     for (int dd = 0; dd < GR; ++dd)
       gv[dd] = dd < rho ? guide_at(a.g, a.gps, a.f, a.fps, a.gkind, dd, row, x, H, W) : 0.f;
     float* bdst = nullptr;
-    if (a.bplanes && px >= R && px < R + TW && xs < ((W + 31) & ~31))
+    if (a.bplanes && !a.phi && px >= R && px < R + TW && xs < ((W + 31) & ~31))
       bdst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) + (long long)(L * NC) * 32 +
              (xs & 31);
     for (int j0 = hh * khalf; j0 < (hh + 1) * khalf; j0 += 4) {
@@ -185,6 +185,19 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
         for (int e = 0; e < 8; ++e) {
           const int i = 8 * c + e;
           if (i < L) Ys[(size_t)i * pitch + px] = v[e];
+        }
+      }
+      if (a.phi && a.bplanes && px >= R && px < R + TW) {  // phi-form: phi_i = y_i is K3's contraction weight
+        const int vr = a.v0 + tile / a.tiles_x;
+        const int xs = (tile % a.tiles_x) * TW - R + px;
+        if (xs < ((W + 31) & ~31)) {
+          float* dst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) +
+                       (long long)(L * NC) * 32 + (xs & 31);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int i = 8 * c + e;
+            if (i < m0) dst[(size_t)i * 32] = v[e];
+          }
         }
       }
     }

@@ -83,7 +83,8 @@ template <int BS, bool CSM, bool PLANAR>
 __global__ void __launch_bounds__(BS) k_rec_features(
     const float* __restrict__ f, long long fps, const float* __restrict__ g, long long gps, int gkind, int rho,
     int H, int W, int m0, const float* __restrict__ consts, int rhop, int m0q, long long off_MT, float k2,
-    float* __restrict__ Y, float* __restrict__ Bf) {
+    float* __restrict__ Y, float* __restrict__ Bf, int phi) {
+  // phi-form: the stored contraction weights are y (= phi) instead of b.
   // b and y are staged in shared memory ([value][pixel], pitch BS+1: the
   // transposed read-out below is bank-conflict free) so the block writes its
   // contiguous [px][m0] / [px][m0+1] output rows with coalesced stores.
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(BS) k_rec_features(
   }
   if (PLANAR) {  // planar [value][px]: one coalesced store per value
     if (ok) {
-      for (int j = 0; j < m0; ++j) Bf[(long long)j * npx + px] = sb[j * PT + t];
+      for (int j = 0; j < m0; ++j) Bf[(long long)j * npx + px] = phi ? sy[j * PT + t] : sb[j * PT + t];
       for (int i = 0; i <= m0; ++i) Y[(long long)i * npx + px] = sy[i * PT + t];
     }
     return;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(BS) k_rec_features(
   const int cnt = (int)min((long long)BS, npx - px0);
   for (int e = t; e < cnt * m0; e += BS) {
     const int i = e / m0, j = e - i * m0;
-    Bf[px0 * m0 + e] = sb[j * PT + i];
+    Bf[px0 * m0 + e] = phi ? sy[j * PT + i] : sb[j * PT + i];
   }
   const int G = m0 + 1;
   for (int e = t; e < cnt * G; e += BS) {
@@ -740,7 +741,8 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
       k<<<(unsigned)ceil_div((long long)npx, BS), BS, smem, s>>>(f, f_plane_stride, g, guide_plane_stride,
                                                                  d->guide_kind, d->rho, d->H, d->W, d->m0,
                                                                  consts + L.off_C, L.rhop, L.m0q,
-                                                                 (long long)(L.off_MT - L.off_C), k2_of(d), Yp, Bp);
+                                                                 (long long)(L.off_MT - L.off_C), k2_of(d), Yp, Bp,
+                                                                 d->phi_form);
       NYS_LAUNCH_CHECK();
     }
     NYS_CUDA_TRY(cudaFuncSetAttribute(k_recv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_v));
@@ -784,7 +786,7 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
     count_launch();
     k<<<(unsigned)ceil_div(npx, BS), BS, smem, s>>>(f, f_plane_stride, g, guide_plane_stride, d->guide_kind, d->rho,
                                                     d->H, d->W, d->m0, consts + L.off_C, L.rhop, L.m0q,
-                                                    (long long)(L.off_MT - L.off_C), k2_of(d), Y, Bf);
+                                                    (long long)(L.off_MT - L.off_C), k2_of(d), Y, Bf, d->phi_form);
     NYS_LAUNCH_CHECK();
   }
   const int G = d->m0 + 1;

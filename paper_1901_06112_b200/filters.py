@@ -187,6 +187,7 @@ def _desc(n: int, rho: int, H: int, W: int, gkind: int, spatial: SpatialKernel, 
     d.u0 = arrs[2].ctypes.data_as(C.POINTER(C.c_double))
     d.alpha0 = plan.alpha0
     d.eps_den = plan.eps_den
+    d.phi_form = 1 if plan.phi_form else 0
     return d
 
 

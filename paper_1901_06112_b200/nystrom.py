@@ -120,6 +120,13 @@ class MixingPlan:
     u0: np.ndarray       # leading eigenvector w_1
     alpha0: float
     eps_den: float       # 1e-12 (2S+1)^2 max|alpha|
+    phi_form: bool = False  # M holds P = diag(alpha_r^-1/2) W_r^T (padded to m0 rows), see nys_filter_desc
+
+
+# Above this cond(A) over the retained eigenpairs the FP32 y-form (y = M b with
+# M = A^+) loses ~eps * cond of accuracy (1.9e-3 at 6e6 on a 1-D guide,
+# tools/dbg_rec.py); the phi-form's FP32 error does not grow with cond(A).
+PHI_FORM_COND = 3.0e4
 
 
 def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int) -> MixingPlan:
@@ -147,4 +154,21 @@ def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int) ->
     _native.check(rc, "nys_mixing_plan")
     alphas = alphas[:rank.value].copy()
     eps_den = 1e-12 * (2 * S + 1) ** 2 * float(np.abs(alphas).max())
+    if alphas[0] / alphas[-1] > PHI_FORM_COND:
+        # ill-conditioned landmark kernel: phi-form (same quantity, filters.py:227-238)
+        A = np.empty((k, k))
+        inv = 1.0 / (2.0 * theta * theta)
+        d2 = ((C_[:, None, :] - C_[None, :, :]) ** 2).sum(-1)
+        A[:] = np.exp(-d2 * inv)
+        vals = np.empty(k)
+        vecs = np.empty((k, k))
+        _native.check(_native.lib().nys_sym_eig(np.ascontiguousarray(A).ctypes.data, k, vals.ctypes.data,
+                                                vecs.ctypes.data), "nys_sym_eig")
+        order = np.argsort(-vals, kind="stable")
+        vals, vecs = vals[order], vecs[:, order]
+        r = alphas.shape[0]
+        P = np.zeros((k, k))
+        P[:r] = (vecs[:, :r] / np.sqrt(vals[:r])[None, :]).T
+        return MixingPlan(alphas=alphas, M=P, u0=vecs[:, 0].copy(), alpha0=float(alphas[0]), eps_den=eps_den,
+                          phi_form=True)
     return MixingPlan(alphas=alphas, M=M, u0=u0, alpha0=float(alphas[0]), eps_den=eps_den)

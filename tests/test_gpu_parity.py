@@ -313,3 +313,26 @@ def test_recursive_shared_path_matches_global_path(shape, n, monkeypatch):
     assert np.abs(oa - ref["output"]).max() <= TOL
     assert np.abs(oa - ob).max() <= 1e-5
     assert a.guarded_pixels == b.guarded_pixels == ref["guarded_pixels"]
+
+
+@pytest.mark.parametrize("shape,m0,theta", [((130, 9), 5, 0.35), ((64, 64), 5, 0.35), ((48, 56), 12, 0.2)])
+@pytest.mark.parametrize("kind", ["gaussian_fir", "gaussian_recursive", "box"])
+def test_ill_conditioned_kernels_use_phi_form(shape, m0, theta, kind):
+    # 1-D guides with several landmarks: cond(A) 6e6 .. 1e8+, where the FP32 y-form missed 1e-4 by
+    # up to 400x; the phi-form (nys_filter_desc.phi_form) keeps the reference's accuracy
+    from paper_1901_06112_b200.nystrom import mixing_plan
+
+    H, W = shape
+    f32 = np.ascontiguousarray(color_scene(H, W, 5, 0.05, seed=H + m0)[:1])
+    f64 = f32.astype(np.float64)
+    C, _, _, _ = O.kmeans(O.range_vectors(f64), m0, 0, 6)
+    sk = {"gaussian_fir": SpatialKernel.gaussian(2.5, 8), "gaussian_recursive": SpatialKernel.recursive(2.5),
+          "box": SpatialKernel.box(4)}[kind]
+    assert mixing_plan(C, theta, 1e-8, sk.effective_radius()).phi_form
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    rep = filter_with_landmarks(f, f, C, FilterParams(spatial=sk, theta=theta, m0=m0))
+    ref = O.fast_filter_with_landmarks(f64, f64, C, theta, kind, 2.5, 8 if kind != "box" else 4)
+    out = rep.output.data.double().cpu().numpy()
+    assert np.abs(out - ref["output"]).max() <= TOL
+    assert rep.guarded_pixels == ref["guarded_pixels"]
+    assert rep.retained_rank == ref["retained_rank"]

@@ -323,7 +323,7 @@ def test_ill_conditioned_kernels_use_phi_form(shape, m0, theta, kind):
     from paper_1901_06112_b200.nystrom import mixing_plan
 
     H, W = shape
-    f32 = np.ascontiguousarray(color_scene(H, W, 5, 0.05, seed=H + m0)[:1])
+    f32 = np.ascontiguousarray(color_scene(H, W, 5, 0.05, seed=H + 1)[:1])
     f64 = f32.astype(np.float64)
     C, _, _, _ = O.kmeans(O.range_vectors(f64), m0, 0, 6)
     sk = {"gaussian_fir": SpatialKernel.gaussian(2.5, 8), "gaussian_recursive": SpatialKernel.recursive(2.5),

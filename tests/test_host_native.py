@@ -183,3 +183,24 @@ def test_native_mixing_plan_matches_eigh(k, rho, theta):
     assert np.abs(p.M - M).max() <= max(1e-12, 1e-14 * kappa) * np.abs(M).max()
     if k == 1 or al[0] - al[1] > 1e-6 * al[0]:  # u0 is defined up to sign when alpha_1 is simple
         assert min(np.abs(p.u0 - Wr[:, 0]).max(), np.abs(p.u0 + Wr[:, 0]).max()) <= 1e-9
+
+
+def test_phi_form_plan_for_ill_conditioned_kernels():
+    # cond(A) > PHI_FORM_COND -> phi-form: M holds P = diag(alpha^-1/2) W^T with P^T P = A^+ on the
+    # retained eigenpairs, u0 the lead eigenvector (host only, no GPU)
+    from paper_1901_06112_b200.nystrom import PHI_FORM_COND, mixing_plan
+
+    C = np.array([[0.40], [0.45], [0.50], [0.55], [0.60], [0.62]])
+    p = mixing_plan(C, 0.35, 1e-8, 8)
+    assert p.phi_form and p.alphas[0] / p.alphas[-1] > PHI_FORM_COND
+    A = np.exp(-((C - C.T) ** 2) / (2 * 0.35 ** 2))
+    w, V = np.linalg.eigh(A)
+    o = np.argsort(-w)
+    w, V = w[o], V[:, o]
+    keep = w > 1e-8 * w[0]
+    Mref = (V[:, keep] / w[keep]) @ V[:, keep].T
+    assert np.abs(p.M.T @ p.M - Mref).max() <= 1e-8 * np.abs(Mref).max()
+    assert np.all(p.M[keep.sum():] == 0.0)
+    assert min(np.abs(p.u0 - V[:, 0]).max(), np.abs(p.u0 + V[:, 0]).max()) <= 1e-10
+    q = mixing_plan(np.random.default_rng(0).random((16, 3)), 0.2, 1e-8, 8)
+    assert not q.phi_form

@@ -285,6 +285,11 @@ inline double dot4(const double* a, const double* b, int n) {
 // transform): on return row i of z holds the Householder vector u_i in columns
 // 0..i-1 and column i holds u_i / h_i; h[i] = h_i (0: no reflection); the
 // tridiagonal is diag d, sub-diagonal e[i] (coupling i-1 and i).
+// x86-64-v3 (AVX2) clone picked at load time where the CPU has it; the 4-way
+// split dot products vectorise lane for lane, and FMA contraction stays off
+// (-ffp-contract=off), so both clones give identical results
+#define NYS_HOST_CLONES __attribute__((target_clones("arch=x86-64-v3", "default")))
+NYS_HOST_CLONES
 void tridiag(std::vector<double>& z, int n, std::vector<double>& d, std::vector<double>& e, std::vector<double>& h) {
   d.assign(n, 0.0);
   e.assign(n, 0.0);
@@ -385,7 +390,7 @@ bool tql_values(std::vector<double> d, std::vector<double> e, int n, std::vector
 
 }  // namespace
 
-extern "C" int nys_mixing_plan(const double* C, int m0, int rho, double theta, double eps_drop, double* alphas_out,
+extern "C" NYS_HOST_CLONES int nys_mixing_plan(const double* C, int m0, int rho, double theta, double eps_drop, double* alphas_out,
                                int* rank_out, double* M_out, double* u0_out) {
   if (!C || m0 < 1 || rho < 1 || !(theta > 0.0) || !alphas_out || !rank_out || !M_out || !u0_out)
     return NYS_EINVAL;

@@ -10,6 +10,7 @@ exact assignment.  All passes over the points run in the K0/K1 CUDA kernels.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -46,11 +47,20 @@ class DeviceKMeans:
     centroids_dev: torch.Tensor | None = None  # (m0 * rho,) float64 on device
 
 
-def _seed_stream(m: int, m0: int, seed: int):
+@functools.lru_cache(maxsize=64)
+def _seed_stream_cached(m: int, m0: int, seed: int):
     rng = np.random.default_rng(seed)
     first = int(rng.integers(m))
     uniforms = np.ascontiguousarray(rng.random(m0 - 1) if m0 > 1 else np.zeros(1))
+    uniforms.flags.writeable = False
     return first, uniforms
+
+
+def _seed_stream(m: int, m0: int, seed: int):
+    """The reference's k-means++ draws from default_rng(seed) (landmarks.py:63-70):
+    integers(m), then one random() per draw.  A pure function of (m, m0, seed),
+    cached: building the generator costs ~30 us per call."""
+    return _seed_stream_cached(int(m), int(m0), int(seed))
 
 
 def _replay_zero_total(m: int, m0: int, seed: int, j0: int, device_seeds: np.ndarray) -> np.ndarray:

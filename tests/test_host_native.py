@@ -61,7 +61,8 @@ def test_mixing_plan_matches_oracle_algebra():
     vals, vecs = O.jacobi_eig(O.gram(C, C, float(g["theta"])))
     al, Wk = O.retain(vals, vecs, 1e-8)
     M = (Wk / al) @ Wk.T  # LAPACK vs Jacobi: agree to ~1e-10 of max|M| (cond(A) ~ 7e4 here)
-    np.testing.assert_allclose(plan.M, M, rtol=0, atol=1e-9 * np.abs(M).max())
+    assert plan.phi_form  # cond(A) ~ 7e4 > PHI_FORM_COND: M holds P, P^T P = A^+
+    np.testing.assert_allclose(plan.M.T @ plan.M, M, rtol=0, atol=1e-9 * np.abs(M).max())
     assert plan.alpha0 == pytest.approx(al[0], rel=1e-13)
     assert plan.eps_den == pytest.approx(1e-12 * (2 * 9 + 1) ** 2 * np.abs(al).max())
 

@@ -169,7 +169,7 @@ def test_header_cites_reference():
 def test_native_mixing_plan_matches_eigh(k, rho, theta):
     # nys_mixing_plan (Cholesky fast path when nothing is dropped, full eigensystem otherwise)
     # against numpy's eigh + the reference drop rule
-    from paper_1901_06112_b200.nystrom import RangeKernel, _retain, build_A, mixing_plan
+    from paper_1901_06112_b200.nystrom import PHI_FORM_COND, RangeKernel, _retain, build_A, mixing_plan
 
     C = np.random.default_rng(k * 100 + rho).random((k, rho))
     p = mixing_plan(C, theta, 1e-8, 15)
@@ -181,7 +181,9 @@ def test_native_mixing_plan_matches_eigh(k, rho, theta):
     assert len(p.alphas) == len(al)
     np.testing.assert_allclose(p.alphas, al, rtol=0, atol=1e-13 * al[0])
     kappa = al[0] / al[-1]  # both solvers are backward stable: forward error ~ eps * kappa
-    assert np.abs(p.M - M).max() <= max(1e-12, 1e-14 * kappa) * np.abs(M).max()
+    Mp = p.M.T @ p.M if p.phi_form else p.M  # phi-form above PHI_FORM_COND: M holds P, P^T P = A^+
+    assert p.phi_form == (kappa > PHI_FORM_COND)
+    assert np.abs(Mp - M).max() <= max(1e-12, 1e-14 * kappa) * np.abs(M).max()
     if k == 1 or al[0] - al[1] > 1e-6 * al[0]:  # u0 is defined up to sign when alpha_1 is simple
         assert min(np.abs(p.u0 - Wr[:, 0]).max(), np.abs(p.u0 + Wr[:, 0]).max()) <= 1e-9
 

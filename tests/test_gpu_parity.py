@@ -336,3 +336,20 @@ def test_ill_conditioned_kernels_use_phi_form(shape, m0, theta, kind):
     assert np.abs(out - ref["output"]).max() <= TOL
     assert rep.guarded_pixels == ref["guarded_pixels"]
     assert rep.retained_rank == ref["retained_rank"]
+
+
+@pytest.mark.parametrize("rho", [16, 27])
+def test_tcgen05_assignment_labels_equal_fp32_search(rho, monkeypatch):
+    # the opt-in tensor-core distance filter (NYS_KM_TC=1) must pick exactly the labels of the
+    # FP32 differenced search: same centroid trajectory as the step-wise SIMT assignment
+    from paper_1901_06112_b200.landmarks import kmeans_device
+
+    rng = np.random.default_rng(rho)
+    centers = rng.uniform(0, 1, (30, rho))
+    pts = (centers[rng.integers(0, 30, 40000)] + 0.05 * rng.standard_normal((40000, rho))).astype(np.float32)
+    t = torch.from_numpy(np.ascontiguousarray(pts.T)).cuda()
+    monkeypatch.setenv("NYS_KM_TC", "1")
+    a = kmeans_device(t, 24, seed=1, max_iter=8, want_assignment=True)
+    b = O.kmeans(pts.astype(np.float64), 24, 1, 8)
+    assert abs(a.quant_error - b[2]) <= 1e-6 * b[2]
+    np.testing.assert_allclose(a.centroids, b[0], rtol=0, atol=1e-5)

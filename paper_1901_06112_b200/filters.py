@@ -408,7 +408,7 @@ def _select_landmarks(inp: _Inputs, params: FilterParams):
     if params.landmark_strategy == STRATEGY_KMEANS:
         km = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter,
                            defer_exact=True)
-        return km.centroids, exact_assignment_async(inp.points, km.centroids_dev, params.m0)
+        return km.centroids, exact_assignment_async(inp.points, km.centroids_dev, params.m0, km.workspace)
     rng = np.random.default_rng(params.seed)
     m = inp.points.shape[1]
     idx = rng.choice(m, size=params.m0, replace=False)

@@ -44,7 +44,8 @@ class DeviceKMeans:
     iterations: int
     seed_indices: np.ndarray
     assignment: torch.Tensor | None  # int64 (m,) on device
-    centroids_dev: torch.Tensor | None = None  # (m0 * rho,) float64 on device
+    centroids_dev: torch.Tensor | None = None  # device result buffer; its first m0 * rho doubles are the centroids
+    workspace: torch.Tensor | None = None      # reusable by exact_assignment_async (same m, rho, m0)
 
 
 @functools.lru_cache(maxsize=64)
@@ -99,20 +100,24 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     ps = int(points.stride(0))
     wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
     ws = workspace(wsb)
-    # one device buffer for every small result -> a single D2H copy (one sync)
+    # one device buffer for every small result -> a single D2H copy (one sync); every slot that is
+    # read back is written by the kernels, so no zero fill; slots addressed by pointer arithmetic
+    # (views cost ~5 us each on the critical path before the first launch)
     nres = m0 * rho + max_iter + 1 + 4 + m0
-    res = torch.zeros(nres, dtype=torch.float64, device=dev)
-    Cd = res[:m0 * rho]
-    errs = res[m0 * rho:m0 * rho + max_iter]
-    qe = res[m0 * rho + max_iter:m0 * rho + max_iter + 1]
-    stats = res[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(torch.int64)
-    seeds = res[m0 * rho + max_iter + 5:].view(torch.int64)
+    res = torch.empty(nres, dtype=torch.float64, device=dev)
+    base = res.data_ptr()
+    Cd_p = base
+    errs_p = base + 8 * m0 * rho
+    qe_p = base + 8 * (m0 * rho + max_iter)
+    stats_p = qe_p + 8
+    seeds_p = stats_p + 8 * 4
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     first, uniforms = _seed_stream(m, m0, seed)
-    qe_p = None if (defer_exact and asg is None) else ptr(qe)
+    if defer_exact and asg is None:
+        qe_p = None
     _native.check(lib.nys_kmeans_run(ptr(points), ps, m, rho, m0, max_iter, first,
-                                     uniforms.ctypes.data, ptr(Cd), ptr(errs), ptr(stats), qe_p,
-                                     ptr(asg), ptr(seeds), ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
+                                     uniforms.ctypes.data, Cd_p, errs_p, stats_p, qe_p,
+                                     ptr(asg), seeds_p, ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
     h = res.cpu().numpy()
     st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
     seeds_h = h[m0 * rho + max_iter + 5:].view(np.int64).copy()
@@ -120,7 +125,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
         sidx = _replay_zero_total(m, m0, seed, int(st[1]), seeds_h)
         sidx = np.ascontiguousarray(sidx, dtype=np.int64)
         _native.check(lib.nys_kmeans_run_seeded(ptr(points), ps, m, rho, m0, max_iter, sidx.ctypes.data,
-                                                ptr(Cd), ptr(errs), ptr(stats), qe_p, ptr(asg),
+                                                Cd_p, errs_p, stats_p, qe_p, ptr(asg),
                                                 ptr(ws), wsb, stream_ptr()), "nys_kmeans_run_seeded")
         h = res.cpu().numpy()
         st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
@@ -129,7 +134,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     return DeviceKMeans(centroids=h[:m0 * rho].reshape(m0, rho).copy(),
                         quant_error=None if qe_p is None else float(h[m0 * rho + max_iter]),
                         errors=tuple(h[m0 * rho:m0 * rho + iters].tolist()), iterations=iters,
-                        seed_indices=seeds_h, assignment=asg, centroids_dev=Cd)
+                        seed_indices=seeds_h, assignment=asg, centroids_dev=res, workspace=ws)
 
 
 def _points_planar(points) -> torch.Tensor:
@@ -156,15 +161,17 @@ def kmeans_landmarks(points, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX
                        quant_error=res.quant_error, errors=res.errors)
 
 
-def exact_assignment_async(points_planar: torch.Tensor, centroids_dev: torch.Tensor, m0: int) -> torch.Tensor:
+def exact_assignment_async(points_planar: torch.Tensor, centroids_dev: torch.Tensor, m0: int,
+                           ws: torch.Tensor | None = None) -> torch.Tensor:
     """Launch the exact pass (landmarks.py:121-129) against device centroids
-    (m0 * rho float64) and return quant_error as a 1-element device tensor,
-    without synchronising."""
+    (the first m0 * rho doubles of ``centroids_dev``) and return quant_error as
+    a 1-element device tensor, without synchronising."""
     rho, m = int(points_planar.shape[0]), int(points_planar.shape[1])
     lib = _native.lib()
     dev = points_planar.device
     wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
-    ws = workspace(wsb)
+    if ws is None or ws.numel() < wsb:
+        ws = workspace(wsb)
     Cd = centroids_dev
     qe = torch.empty(1, dtype=torch.float64, device=dev)
     _native.check(lib.nys_kmeans_exact(ptr(points_planar), int(points_planar.stride(0)), m, rho, ptr(Cd), m0,

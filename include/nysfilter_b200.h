@@ -265,7 +265,7 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
 /* PCA patch guide (filters.py:161-187)                      */
 /* ---------------------------------------------------------------------- */
 
-/* Workspace for nys_patch_moments (0 if n(2r+1)^2 > 256). */
+/* Workspace for nys_patch_moments (0 if n(2r+1)^2 > 1024). */
 size_t nys_patch_moments_workspace_bytes(int n, int H, int W, int r);
 
 /* First and centred second moments of the (2r+1)^2-per-channel patch

@@ -21,7 +21,7 @@ namespace nys {
 
 constexpr int PC_THREADS = 256;
 constexpr int PC_CHUNK = 32;  // pixels staged per step
-constexpr int PC_MAXDIM = 256;
+constexpr int PC_MAXDIM = 1024;  // e.g. 31 bands x 5x5 patches = 775
 
 __device__ __forceinline__ float patch_at(const float* __restrict__ f, long long fps, int side, int r, int d,
                                           int y, int x, int H, int W) {
@@ -33,10 +33,11 @@ __device__ __forceinline__ float patch_at(const float* __restrict__ f, long long
 __global__ void __launch_bounds__(PC_THREADS) k_patch_sums(const float* __restrict__ f, long long fps, int side,
                                                            int r, int dim, int H, int W, long long per_block,
                                                            double* __restrict__ partial) {
-  __shared__ float xs[PC_CHUNK * PC_MAXDIM];
+  extern __shared__ float xsum[];  // [PC_CHUNK][dim]
+  float* xs = xsum;
   const long long npx = (long long)H * W;
   const long long p0 = (long long)blockIdx.x * per_block, p1 = min(npx, p0 + per_block);
-  double acc = 0.0;  // thread d < dim owns coordinate d
+  double acc[PC_MAXDIM / PC_THREADS] = {};  // coordinates threadIdx.x + k * PC_THREADS
   for (long long c0 = p0; c0 < p1; c0 += PC_CHUNK) {
     const int cnt = (int)min((long long)PC_CHUNK, p1 - c0);
     for (int k = threadIdx.x; k < cnt * dim; k += blockDim.x) {
@@ -46,11 +47,14 @@ __global__ void __launch_bounds__(PC_THREADS) k_patch_sums(const float* __restri
       xs[i * dim + d] = patch_at(f, fps, side, r, d, y, x, H, W);
     }
     __syncthreads();
-    if (threadIdx.x < dim)
-      for (int i = 0; i < cnt; ++i) acc += (double)xs[i * dim + threadIdx.x];
+    for (int dd = threadIdx.x; dd < dim; dd += blockDim.x) {  // coordinate dd: this thread's running sum
+      double v = 0.0;
+      for (int i = 0; i < cnt; ++i) v += (double)xs[i * dim + dd];
+      acc[dd / PC_THREADS] += v;
+    }
     __syncthreads();
   }
-  if (threadIdx.x < dim) partial[(long long)blockIdx.x * dim + threadIdx.x] = acc;
+  for (int dd = threadIdx.x; dd < dim; dd += blockDim.x) partial[(long long)blockIdx.x * dim + dd] = acc[dd / PC_THREADS];
 }
 
 // upper-triangle 4x4 tile t -> (ti, tj), ti <= tj, row-major over ti
@@ -67,9 +71,9 @@ __device__ __forceinline__ void tile_of(int t, int nt, int& ti, int& tj) {
 // outer-product tile; blockIdx.y selects 256 tiles
 __global__ void __launch_bounds__(PC_THREADS) k_patch_gram(const float* __restrict__ f, long long fps, int side,
                                                            int r, int dim, int H, int W, long long per_block,
-                                                           const double* __restrict__ mu, int ntiles,
+                                                           const double* __restrict__ mu, int ntiles, int chunk,
                                                            double* __restrict__ partial) {
-  extern __shared__ double xs[];  // [PC_CHUNK][dimp]
+  extern __shared__ double xs[];  // [chunk][dimp]
   const int dimp = (dim + 3) & ~3, nt = dimp / 4;
   const int t = blockIdx.y * PC_THREADS + threadIdx.x;
   const bool active = t < ntiles;
@@ -82,9 +86,9 @@ __global__ void __launch_bounds__(PC_THREADS) k_patch_gram(const float* __restri
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
   const long long npx = (long long)H * W;
   const long long p0 = (long long)blockIdx.x * per_block, p1 = min(npx, p0 + per_block);
-  for (long long c0 = p0; c0 < p1; c0 += PC_CHUNK) {
-    const int cnt = (int)min((long long)PC_CHUNK, p1 - c0);
-    for (int k = threadIdx.x; k < PC_CHUNK * dimp; k += blockDim.x) {
+  for (long long c0 = p0; c0 < p1; c0 += chunk) {
+    const int cnt = (int)min((long long)chunk, p1 - c0);
+    for (int k = threadIdx.x; k < chunk * dimp; k += blockDim.x) {
       const int i = k / dimp, d = k - i * dimp;
       double v = 0.0;
       if (i < cnt && d < dim) {
@@ -134,16 +138,17 @@ __global__ void __launch_bounds__(128) k_pca_project(const float* __restrict__ f
                                                      int dim, int H, int W, const float* __restrict__ mu,
                                                      const float* __restrict__ V /*[dim][kdim]*/, int kdim,
                                                      float* __restrict__ out, long long ops) {
-  extern __shared__ float xc[];  // [dim][128]
+  extern __shared__ float xc[];  // [dim][blockDim]
+  const int BT = blockDim.x;
   const long long npx = (long long)H * W;
-  const long long p = (long long)blockIdx.x * 128 + threadIdx.x;
+  const long long p = (long long)blockIdx.x * BT + threadIdx.x;
   if (p >= npx) return;
   const int y = (int)(p / W), x = (int)(p - (long long)y * W);
-  for (int d = 0; d < dim; ++d) xc[d * 128 + threadIdx.x] = patch_at(f, fps, side, r, d, y, x, H, W) - __ldg(mu + d);
+  for (int d = 0; d < dim; ++d) xc[d * BT + threadIdx.x] = patch_at(f, fps, side, r, d, y, x, H, W) - __ldg(mu + d);
   for (int k0 = 0; k0 < kdim; k0 += 4) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     for (int d = 0; d < dim; ++d) {
-      const float v = xc[d * 128 + threadIdx.x];
+      const float v = xc[d * BT + threadIdx.x];
       const float* vr = V + (long long)d * kdim + k0;
       a0 = fmaf(v, __ldg(vr), a0);
       if (k0 + 1 < kdim) a1 = fmaf(v, __ldg(vr + 1), a1);
@@ -157,7 +162,11 @@ __global__ void __launch_bounds__(128) k_pca_project(const float* __restrict__ f
   }
 }
 
-inline int pca_splits(long long npx) { return (int)std::max<long long>(1, std::min<long long>(2 * num_sms(), ceil_div(npx, 256))); }
+inline int pca_ntiles(int dim);
+inline int pca_splits(long long npx, int dim) {
+  const long long cap = pca_ntiles(dim) > 4096 ? 32 : 2 * num_sms();  // bound the partials for large patches
+  return (int)std::max<long long>(1, std::min<long long>(cap, ceil_div(npx, 256)));
+}
 inline int pca_ntiles(int dim) {
   const int nt = (int)ceil_div(dim, 4);
   return nt * (nt + 1) / 2;
@@ -172,7 +181,7 @@ extern "C" {
 size_t nys_patch_moments_workspace_bytes(int n, int H, int W, int r) {
   const int dim = n * (2 * r + 1) * (2 * r + 1);
   if (n < 1 || r < 0 || dim > PC_MAXDIM || H < 1 || W < 1) return 0;
-  const int ns = pca_splits((long long)H * W);
+  const int ns = pca_splits((long long)H * W, dim);
   return (size_t)ns * ((size_t)pca_ntiles(dim) * 16 + dim) * sizeof(double);
 }
 
@@ -183,22 +192,25 @@ int nys_patch_moments(const float* f, int64_t f_plane_stride, int n, int H, int 
   if (dim > PC_MAXDIM) return NYS_EUNSUPPORTED;
   if (workspace_bytes < nys_patch_moments_workspace_bytes(n, H, W, r)) return NYS_EINVAL;
   const long long npx = (long long)H * W;
-  const int ns = pca_splits(npx);
+  const int ns = pca_splits(npx, dim);
   const long long per = ceil_div(npx, ns);
   const int ntiles = pca_ntiles(dim);
   double* part = static_cast<double*>(workspace);
   cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem_s = (size_t)PC_CHUNK * dim * sizeof(float);
+  NYS_CUDA_TRY(cudaFuncSetAttribute(k_patch_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
   count_launch();
-  k_patch_sums<<<ns, PC_THREADS, 0, s>>>(f, f_plane_stride, side, r, dim, H, W, per, part);
+  k_patch_sums<<<ns, PC_THREADS, smem_s, s>>>(f, f_plane_stride, side, r, dim, H, W, per, part);
   NYS_LAUNCH_CHECK();
   count_launch();
   k_sum_splits<<<1, 256, 0, s>>>(part, ns, dim, 1.0 / (double)npx, mean_out);
   NYS_LAUNCH_CHECK();
-  const size_t smem = (size_t)PC_CHUNK * ((dim + 3) & ~3) * sizeof(double);
+  const int gchunk = (int)std::max<size_t>(1, std::min<size_t>(PC_CHUNK, (200 * 1024) / (((size_t)dim + 3) / 4 * 4 * 8)));
+  const size_t smem = (size_t)gchunk * ((dim + 3) & ~3) * sizeof(double);
   NYS_CUDA_TRY(cudaFuncSetAttribute(k_patch_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   count_launch();
   k_patch_gram<<<dim3(ns, (unsigned)ceil_div(ntiles, PC_THREADS)), PC_THREADS, smem, s>>>(
-      f, f_plane_stride, side, r, dim, H, W, per, mean_out, ntiles, part);
+      f, f_plane_stride, side, r, dim, H, W, per, mean_out, ntiles, gchunk, part);
   NYS_LAUNCH_CHECK();
   count_launch();
   k_sum_splits<<<(unsigned)ceil_div((long long)ntiles * 16, 256), 256, 0, s>>>(part, ns, (long long)ntiles * 16, 1.0,
@@ -213,10 +225,11 @@ int nys_pca_project(const float* f, int64_t f_plane_stride, int n, int H, int W,
   if (!f || !mean || !basis || !out || n < 1 || r < 0 || H < 1 || W < 1 || pca_dim < 1 || pca_dim > dim)
     return NYS_EINVAL;
   if (dim > PC_MAXDIM) return NYS_EUNSUPPORTED;
-  const size_t smem = (size_t)dim * 128 * sizeof(float);
+  const int bt = std::max(32, std::min(128, (int)((200 * 1024) / ((size_t)dim * 4)) & ~31));  // patch rows in SMEM
+  const size_t smem = (size_t)dim * bt * sizeof(float);
   NYS_CUDA_TRY(cudaFuncSetAttribute(k_pca_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   count_launch();
-  k_pca_project<<<(unsigned)ceil_div((long long)H * W, 128), 128, smem, (cudaStream_t)stream>>>(
+  k_pca_project<<<(unsigned)ceil_div((long long)H * W, bt), bt, smem, (cudaStream_t)stream>>>(
       f, f_plane_stride, side, r, dim, H, W, mean, basis, pca_dim, out, out_plane_stride);
   NYS_LAUNCH_CHECK();
   return NYS_OK;

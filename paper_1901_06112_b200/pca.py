@@ -35,7 +35,7 @@ def patch_covariance(f_dev: torch.Tensor, r: int):
     lib = _native.lib()
     wsb = int(lib.nys_patch_moments_workspace_bytes(n, H, W, r))
     if wsb == 0:
-        raise NotImplementedError(f"patch dimension {dim} > 256 is not supported on the B200 path")
+        raise NotImplementedError(f"patch dimension {dim} > 1024 is not supported on the B200 path")
     nt = (dim + 3) // 4
     ntiles = nt * (nt + 1) // 2
     ws = torch.empty(wsb, dtype=torch.uint8, device=f_dev.device)

@@ -143,3 +143,24 @@ def test_nlm_pca_filter_two_stage(case):
     # stage 2: our k-means on our guide
     full = fast_filter(f, p, params)
     assert abs(full.quant_error - float(g["quant_error"])) <= 1e-3 * float(g["quant_error"])
+
+
+def test_pca_guide_large_patch_dimension():
+    # 31 bands x 3x3 patches = 279 dims (> the 256 of the first version): moments, the chunked Gram
+    # and the narrower projection blocks against a NumPy restatement (filters.py:161-187)
+    from paper_1901_06112_b200 import pca_patch_guide
+    from paper_1901_06112_b200.synthetic import spectral_scene
+
+    f32 = spectral_scene(24, 28, 31, 4, 0.03, seed=5)
+    f64 = f32.astype(np.float64)
+    P = O.patch_stack(f64, 1)
+    X = P.reshape(P.shape[0], -1).T
+    Xc = X - X.mean(axis=0)
+    vals, vecs = np.linalg.eigh(Xc.T @ Xc / X.shape[0])
+    o = np.argsort(-vals, kind="stable")
+    vecs = vecs[:, o]
+    idx = np.argmax(np.abs(vecs), axis=0)
+    vecs = vecs * np.where(vecs[idx, np.arange(vecs.shape[1])] < 0, -1.0, 1.0)[None, :]
+    ref = (Xc @ vecs[:, :8]).T.reshape(8, 24, 28)
+    g = pca_patch_guide(Image(data=f64, range_max=1.0), 1, 8)
+    assert np.abs(g.data - ref).max() <= 2e-5 * max(1.0, np.abs(ref).max())

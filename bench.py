@@ -132,10 +132,27 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     dev = torch.device("cuda", torch.cuda.current_device())
     wl = CONFIGS[args.config]
-    if world > 1:
+    # N > 1: the frame is the data-parallel unit -- every rank filters its own image of the
+    # workload (weak scaling, no collective on the data path; the max over ranks of each step's
+    # device time is the step time).  An image too large for one GPU (cfg 5), or --sharded, runs
+    # the row-band-sharded path instead (halo exchange + NCCL k-means, parallel.py).
+    if args.sharded or (world > 1 and wl.pixels > 16 * 1024 * 1024):
         from paper_1901_06112_b200 import parallel
 
         return parallel.bench_sharded(args, wl, rank, world)
+    import torch.distributed as dist
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
     f_np = wl.image(seed=0)
     n, H, W = f_np.shape
     px = H * W
@@ -161,6 +178,8 @@ def run_ours(args, rank: int, world: int):
         torch.cuda.synchronize()
         for _ in range(args.steps):
             l2_flush()
+            barrier()
+            torch.cuda.synchronize()
             evs = []
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -168,14 +187,14 @@ def run_ours(args, rank: int, world: int):
             rep = fast_filter(f_img, g_img, params, kernel_events=evs)
             e1.record()
             torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
+            step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
             for name, a, b, _band in evs:
                 k_ms[name] += a.elapsed_time(b)
                 k_n[name] += 1
         torch.cuda.synchronize()
     launches = int(lib.nys_kernel_launches()) - launches0
     ms = sum(step_ms) / len(step_ms)
-    value = px / (ms * 1e-3) / 1e6
+    value = world * px / (ms * 1e-3) / 1e6  # every rank filtered one image per step
 
     # end to end through the public API from pinned host buffers
     f_host = torch.from_numpy(f_np).pin_memory()
@@ -187,11 +206,12 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
     for _ in range(max(1, args.steps)):
         l2_flush()
+        barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rep_h = fast_filter(h_img, hg, params, out=h_out)
         torch.cuda.synchronize()
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_ms.append(max_over_ranks((time.perf_counter() - t0) * 1e3))
     e2e = sum(e2e_ms) / len(e2e_ms)
     out_bytes = int(rep_h.output.data.numel() * 4)
 
@@ -231,8 +251,9 @@ def run_ours(args, rank: int, world: int):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded random-polygon scene, SURVEY §8d)",
-        "config": _cfg_dict(wl, {"l2": "flushed: 512 MB write before every timed step", "parallelism": "single"}),
-        "e2e": {"value": round(px / (e2e * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_step": round(e2e, 3),
+        "config": _cfg_dict(wl, {"l2": "flushed: 512 MB write before every timed step",
+                                 "parallelism": "single" if world == 1 else f"dp{world}: one image per rank, no collective"}),
+        "e2e": {"value": round(world * px / (e2e * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_step": round(e2e, 3),
                 "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": out_bytes,
                 "path": "fast_filter(Image(pinned host float32), out=pinned host buffer): H2D copy in, K3 writes the output over PCIe"},
         "step_ms": [round(x, 3) for x in step_ms],
@@ -244,7 +265,7 @@ def run_ours(args, rank: int, world: int):
         "report": {"retained_rank": rep.retained_rank, "quant_error": rep.quant_error,
                    "guarded_pixels": rep.guarded_pixels, "min_denominator": rep.min_denominator},
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is timed at N = 1 only
         result["cpu_baseline"] = cpu_baseline(wl, args.cpu_rows)
     return result
 
@@ -311,10 +332,15 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=64, help="rows of the CPU-baseline crop")
     ap.add_argument("--ref-rows", type=int, default=32, help="rows of the reference-arm crop per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-sharded NCCL path even at one rank (exercises parallel.py on one GPU)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1 and args.impl == "ours":
+    if args.sharded and world == 1:  # a one-rank NCCL group without torchrun
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
+    if (world > 1 or args.sharded) and args.impl == "ours":
         import torch
         import torch.distributed as dist
 

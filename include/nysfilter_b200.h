@@ -284,6 +284,15 @@ int nys_patch_moments(const float* f, int64_t f_plane_stride, int n, int H, int 
 int nys_pca_project(const float* f, int64_t f_plane_stride, int n, int H, int W, int r, const float* mean,
                     const float* basis, int pca_dim, float* out, int64_t out_plane_stride, void* stream);
 
+/* Stand-alone separable filtering of an FP64 plane stack (spatial.py:194-234:
+ * apply_planes / box_filter / gaussian_fir / gaussian_recursive): in, out [dev]
+ * (P, H, W) float64; kind NYS_SPATIAL_*; radius for box / FIR; sigma for FIR
+ * and recursive (sigma < 1: the FIR at ceil(3 sigma)); scratch [dev] P*H*W
+ * doubles for the box / FIR passes (unused by the recursive kind).  Row pass
+ * then column pass, edge replicate, FP64. */
+int nys_spatial_planes(const double* in, double* out, int64_t P, int H, int W, int kind, double sigma, int radius,
+                       double* scratch, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* Direct (brute-force) kernel filter, Eq. (1) (filters.py:107-138), §8 f1 */
 /* ---------------------------------------------------------------------- */

@@ -164,3 +164,29 @@ def test_pca_guide_large_patch_dimension():
     ref = (Xc @ vecs[:, :8]).T.reshape(8, 24, 28)
     g = pca_patch_guide(Image(data=f64, range_max=1.0), 1, 8)
     assert np.abs(g.data - ref).max() <= 2e-5 * max(1.0, np.abs(ref).max())
+
+
+def test_standalone_spatial_filters_match_reference():
+    # spatial.py public helpers on the device (FP64) vs the reference's own outputs
+    from paper_1901_06112_b200 import apply_planes, box_filter, gaussian_fir, gaussian_recursive
+
+    g = load_golden("spatial")
+    np.testing.assert_allclose(gaussian_fir(g["plane"], 1.3, 3), g["fir_1.3_3"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(box_filter(g["plane"], 2), g["box_2"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(box_filter(g["plane"], 0), g["box_0"], rtol=0, atol=0)
+    r = load_golden("recursive")
+    for s in (0.7, 1.0, 2.5, 4.0):
+        np.testing.assert_allclose(gaussian_recursive(r["plane"], s), r[f"rec_{s}"], rtol=1e-12, atol=1e-12)
+    # pkg/tests/test_spatial.py-style known answers: box of a constant, box of an impulse
+    for S in (0, 1, 3):
+        assert np.array_equal(box_filter(np.full((6, 5), 2.5), S), np.full((6, 5), 2.5 * (2 * S + 1) ** 2))
+    imp = np.zeros((7, 7))
+    imp[3, 3] = 1
+    exp = np.zeros((7, 7))
+    exp[2:5, 2:5] = 1
+    assert np.array_equal(box_filter(imp, 1), exp)
+    stack = np.random.default_rng(0).random((3, 9, 11))
+    t = apply_planes(torch.from_numpy(stack).cuda(), SpatialKernel.recursive(2.0))
+    assert t.is_cuda
+    np.testing.assert_allclose(t.cpu().numpy(), O.spatial_conv(stack, "gaussian_recursive", 2.0, 0), rtol=1e-12,
+                               atol=1e-12)

@@ -402,13 +402,12 @@ def _output_image(out: torch.Tensor, f: Image, given: torch.Tensor | None = None
 
 def _select_landmarks(inp: _Inputs, params: FilterParams):
     """(centroids on the host, quant_error as a float or a pending device
-    scalar).  For k-means the final exact pass is launched only after the
-    centroids reached the host, so it runs while the host builds the mixing
-    plan."""
+    scalar).  For k-means the final exact pass is queued behind the centroids'
+    device->host copy, so it runs while the host builds the mixing plan."""
     if params.landmark_strategy == STRATEGY_KMEANS:
         km = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter,
-                           defer_exact=True)
-        return km.centroids, exact_assignment_async(inp.points, km.centroids_dev, params.m0, km.workspace)
+                           queue_exact=True)
+        return km.centroids, km.quant_error_dev
     rng = np.random.default_rng(params.seed)
     m = inp.points.shape[1]
     idx = rng.choice(m, size=params.m0, replace=False)

@@ -46,6 +46,7 @@ class DeviceKMeans:
     assignment: torch.Tensor | None  # int64 (m,) on device
     centroids_dev: torch.Tensor | None = None  # device result buffer; its first m0 * rho doubles are the centroids
     workspace: torch.Tensor | None = None      # reusable by exact_assignment_async (same m, rho, m0)
+    quant_error_dev: torch.Tensor | None = None  # pending exact-pass result (queue_exact)
 
 
 @functools.lru_cache(maxsize=64)
@@ -77,14 +78,33 @@ def _replay_zero_total(m: int, m0: int, seed: int, j0: int, device_seeds: np.nda
     return seeds
 
 
+_PINNED: dict = {}
+
+
+def _pinned_f64(n: int, key) -> torch.Tensor:
+    """Reused page-locked host staging buffer (cudaHostAlloc costs ~100 us)."""
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 64), dtype=torch.float64, pin_memory=True)
+        _PINNED[key] = buf
+    return buf[:n]
+
+
 def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER,
-                  want_assignment: bool = False, defer_exact: bool = False) -> DeviceKMeans:
+                  want_assignment: bool = False, defer_exact: bool = False,
+                  queue_exact: bool = False) -> DeviceKMeans:
     """k-means on planar device points ``(rho, m)`` float32 (rows may be any
     plane stride; the last dim must be contiguous).
 
     ``defer_exact``: skip the final exact pass (quant_error is then None);
     the caller launches it with ``exact_assignment_async`` once it has the
-    centroids, so the pass overlaps its host-side work."""
+    centroids, so the pass overlaps its host-side work.
+
+    ``queue_exact`` (implies defer_exact): the results are copied to a pinned
+    host buffer behind an event, the exact pass is queued right after that copy
+    (before the host waits), and only the copy is waited for -- the exact pass
+    then runs while the caller works on the centroids, with no host gap in
+    between.  Its pending result is ``DeviceKMeans.quant_error_dev``."""
     require_cuda()
     if points.dim() != 2 or points.stride(1) != 1:
         raise ValueError("points must be a (rho, m) tensor with contiguous rows")
@@ -113,12 +133,22 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     seeds_p = stats_p + 8 * 4
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     first, uniforms = _seed_stream(m, m0, seed)
-    if defer_exact and asg is None:
+    if (defer_exact or queue_exact) and asg is None:
         qe_p = None
     _native.check(lib.nys_kmeans_run(ptr(points), ps, m, rho, m0, max_iter, first,
                                      uniforms.ctypes.data, Cd_p, errs_p, stats_p, qe_p,
                                      ptr(asg), seeds_p, ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
-    h = res.cpu().numpy()
+    qe_dev = None
+    if queue_exact and qe_p is None:
+        hbuf = _pinned_f64(nres, ("kmeans", torch.cuda.current_stream().cuda_stream))
+        hbuf.copy_(res, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        qe_dev = exact_assignment_async(points, res, m0, ws)
+        done.synchronize()
+        h = hbuf.numpy().copy()
+    else:
+        h = res.cpu().numpy()
     st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
     seeds_h = h[m0 * rho + max_iter + 5:].view(np.int64).copy()
     if st[1] >= 0:  # sum(D^2) == 0 during seeding: redo with the reference's integers() picks
@@ -130,11 +160,14 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
         h = res.cpu().numpy()
         st = h[m0 * rho + max_iter + 1:m0 * rho + max_iter + 5].view(np.int64)
         seeds_h = sidx
+        if qe_dev is not None:  # the queued exact pass saw the first run's centroids
+            qe_dev = exact_assignment_async(points, res, m0, ws)
     iters = int(st[0])
     return DeviceKMeans(centroids=h[:m0 * rho].reshape(m0, rho).copy(),
                         quant_error=None if qe_p is None else float(h[m0 * rho + max_iter]),
                         errors=tuple(h[m0 * rho:m0 * rho + iters].tolist()), iterations=iters,
-                        seed_indices=seeds_h, assignment=asg, centroids_dev=res, workspace=ws)
+                        seed_indices=seeds_h, assignment=asg, centroids_dev=res, workspace=ws,
+                        quant_error_dev=qe_dev)
 
 
 def _points_planar(points) -> torch.Tensor:

@@ -362,6 +362,13 @@ int nys_sym_eig(const double* a, int k, double* values_out, double* vectors_out)
  * alphas_out: m0 (first *rank_out valid, descending); M_out: m0 x m0; u0_out: m0.
  * Returns NYS_EDEGENERATE when alpha_1 <= 0. */
 #define NYS_EDEGENERATE 3
+/* Hot-path variant: alpha_1 by Sturm bisection on the tridiagonal plus two Sturm
+ * counts instead of every eigenvalue.  Returns NYS_EUNSUPPORTED (nothing
+ * written but possibly M/u0 scratch) when an eigenpair would be dropped
+ * (alpha <= eps_drop alpha_1) or cond(A) > phi_cond -- the caller then uses
+ * nys_mixing_plan.  Otherwise rank = m0, M = A^{-1}, u0 = w_1, info_out[0] = alpha_1. */
+int nys_mixing_plan_lite(const double* centroids, int m0, int rho, double theta, double eps_drop, double phi_cond,
+                         double* info_out, int* rank_out, double* M_out, double* u0_out);
 int nys_mixing_plan(const double* centroids, int m0, int rho, double theta, double eps_drop, double* alphas_out,
                     int* rank_out, double* M_out, double* u0_out);
 

@@ -82,6 +82,7 @@ _SIGS = {
     "nys_patch_moments": (_I, [_P, _L, _I, _I, _I, _I, _P, _P, _P, _S, _P]),
     "nys_pca_project": (_I, [_P, _L, _I, _I, _I, _I, _P, _P, _I, _P, _L, _P]),
     "nys_spatial_planes": (_I, [_P, _P, _L, _I, _I, _I, _D, _I, _P, _P]),
+    "nys_mixing_plan_lite": (_I, [_P, _I, _I, _D, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
     "nys_mixing_plan": (_I, [_P, _I, _I, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
 }
 

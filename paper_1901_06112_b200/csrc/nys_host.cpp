@@ -390,6 +390,23 @@ bool tql_values(std::vector<double> d, std::vector<double> e, int n, std::vector
 
 }  // namespace
 
+namespace {
+// number of eigenvalues of the symmetric tridiagonal (d, e[i] coupling i-1 and i) below x
+// (Sturm count via the LDL^T pivots of T - x I; zero pivots nudged as in LAPACK dstebz)
+int sturm_below(const std::vector<double>& d, const std::vector<double>& e, int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (std::fabs(q) < pivmin) q = -pivmin;
+  if (q < 0.0) ++cnt;
+  for (int i = 1; i < n; ++i) {
+    q = (d[i] - x) - e[i] * e[i] / q;
+    if (std::fabs(q) < pivmin) q = -pivmin;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+}  // namespace
+
 extern "C" NYS_HOST_CLONES int nys_mixing_plan(const double* C, int m0, int rho, double theta, double eps_drop, double* alphas_out,
                                int* rank_out, double* M_out, double* u0_out) {
   if (!C || m0 < 1 || rho < 1 || !(theta > 0.0) || !alphas_out || !rank_out || !M_out || !u0_out)
@@ -508,6 +525,117 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan(const double* C, int m0, int rho,
   for (int i = 0; i < n; ++i) u0_out[i] = V[(size_t)i * n + 0];
   *rank_out = rank;
   return NYS_OK;
+}
+
+
+// Lite plan for the hot path: the largest eigenvalue by Sturm bisection on the
+// tridiagonal and two Sturm counts instead of every eigenvalue (the values-only
+// QL was a third of the plan's host time): nothing may fall below
+// eps_drop * alpha_1 and cond(A) must stay <= phi_cond, else NYS_EUNSUPPORTED
+// (the caller then runs nys_mixing_plan).  info_out[0] = alpha_1.
+extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int rho, double theta, double eps_drop,
+                                                    double phi_cond, double* info_out, int* rank_out, double* M_out,
+                                                    double* u0_out) {
+  if (!C || m0 < 1 || rho < 1 || !(theta > 0.0) || !info_out || !rank_out || !M_out || !u0_out || !(phi_cond > 1.0))
+    return NYS_EINVAL;
+  const int n = m0;
+  std::vector<double> A((size_t)n * n);
+  const double inv = 1.0 / (2.0 * theta * theta);
+  for (int i = 0; i < n; ++i)
+    for (int j = i; j < n; ++j) {
+      const double d2 = sqdist_np(C + (size_t)i * rho, C + (size_t)j * rho, rho);
+      if (!std::isfinite(d2)) return NYS_EINVAL;
+      A[(size_t)i * n + j] = A[(size_t)j * n + i] = std::exp(-d2 * inv);
+    }
+  std::vector<double> Z(A), d, e, h;
+  tridiag(Z, n, d, e, h);
+  double lo = d[0], hi = d[0], emax = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? std::fabs(e[i]) : 0.0) + (i + 1 < n ? std::fabs(e[i + 1]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+    emax = std::max(emax, std::fabs(d[i]) + r);
+  }
+  const double pivmin = std::max(1e-300, 1e-300 * emax * emax);
+  for (int it = 0; it < 200 && hi - lo > 2e-16 * std::max(std::fabs(lo), std::fabs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (sturm_below(d, e, n, mid, pivmin) <= n - 1) lo = mid;
+    else hi = mid;
+  }
+  const double a1 = 0.5 * (lo + hi);
+  if (!(a1 > 0.0)) return NYS_EDEGENERATE;
+  if (sturm_below(d, e, n, eps_drop * a1, pivmin) > 0) return NYS_EUNSUPPORTED;  // something is dropped
+  if (sturm_below(d, e, n, a1 / phi_cond, pivmin) > 0) return NYS_EUNSUPPORTED;  // phi-form territory
+  std::vector<double> vals(1, a1);
+  bool fast = true;
+  std::vector<double> L((size_t)n * n, 0.0);
+  for (int j = 0; j < n && fast; ++j) {
+    const double* lj = &L[(size_t)j * n];
+    const double s = A[(size_t)j * n + j] - dot4(lj, lj, j);
+    if (!(s > 0.0)) {
+      fast = false;
+      break;
+    }
+    const double ljj = std::sqrt(s);
+    L[(size_t)j * n + j] = ljj;
+    for (int i = j + 1; i < n; ++i) L[(size_t)i * n + j] = (A[(size_t)i * n + j] - dot4(&L[(size_t)i * n], lj, j)) / ljj;
+  }
+  double* alphas_out = info_out;
+  if (fast) {
+    // X = L^{-1} stored transposed (XT[j][i] = X[i][j], i >= j) so both products stream rows
+    std::vector<double> XT((size_t)n * n, 0.0);
+    std::vector<double> col(n);
+    for (int j = 0; j < n; ++j) {
+      std::fill(col.begin(), col.end(), 0.0);
+      col[j] = 1.0 / L[(size_t)j * n + j];
+      for (int i = j + 1; i < n; ++i)
+        col[i] = -dot4(&L[(size_t)i * n + j], &col[j], i - j) / L[(size_t)i * n + i];
+      for (int i = j; i < n; ++i) XT[(size_t)j * n + i] = col[i];
+    }
+    // M[i][j] = sum_{k >= max(i,j)} X[k][i] X[k][j] = XT[i] . XT[j] over k >= j (j >= i)
+    for (int i = 0; i < n; ++i)
+      for (int j = i; j < n; ++j) {
+        const double t = dot4(&XT[(size_t)i * n + j], &XT[(size_t)j * n + j], n - j);
+        M_out[(size_t)i * n + j] = M_out[(size_t)j * n + i] = t;
+      }
+    // u0: inverse iteration on the tridiagonal with sigma just above alpha_1
+    // (sigma I - T is SPD, so LDL^T needs no pivoting), then x = Q y through the
+    // stored Householder reflections
+    const double sigma = vals[0] * (1.0 + 1e-10) + 1e-300;
+    std::vector<double> Dg(n), Lg(n, 0.0), y(n, 1.0);
+    Dg[0] = sigma - d[0];
+    for (int i = 1; i < n && fast; ++i) {
+      if (!(Dg[i - 1] > 0.0)) fast = false;
+      Lg[i] = -e[i] / Dg[i - 1];
+      Dg[i] = (sigma - d[i]) + Lg[i] * e[i];
+    }
+    if (!(Dg[n - 1] > 0.0)) fast = false;
+    for (int it = 0; it < 3 && fast; ++it) {
+      for (int i = 1; i < n; ++i) y[i] -= Lg[i] * y[i - 1];
+      for (int i = 0; i < n; ++i) y[i] /= Dg[i];
+      for (int i = n - 2; i >= 0; --i) y[i] -= Lg[i + 1] * y[i + 1];
+      double nrm = std::sqrt(dot4(y.data(), y.data(), n));
+      if (!(nrm > 0.0) || !std::isfinite(nrm)) {
+        fast = false;
+        break;
+      }
+      for (int i = 0; i < n; ++i) y[i] /= nrm;
+    }
+    if (fast) {
+      for (int i = 1; i < n; ++i) {
+        if (h[i] == 0.0) continue;
+        const int l = i - 1;
+        const double g = dot4(&Z[(size_t)i * n], y.data(), l + 1);
+        for (int q = 0; q <= l; ++q) y[q] -= g * Z[(size_t)q * n + i];
+      }
+      const double nrm = std::sqrt(dot4(y.data(), y.data(), n));
+      for (int i = 0; i < n; ++i) u0_out[i] = y[i] / nrm;
+      alphas_out[0] = vals[0];
+      *rank_out = n;
+      return NYS_OK;
+    }
+  }
+  return NYS_EUNSUPPORTED;
 }
 
 // ---------------------------------------------------------------------------

@@ -241,7 +241,7 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     H = H_global if H_global is not None else h_local
     lo, hi = rows if rows is not None else (0, H)
     S = params.spatial.effective_radius()
-    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S)
+    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True)
     keep: list = []
     d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
     d.row_lo, d.row_hi = row_origin, row_origin + h_local
@@ -309,7 +309,7 @@ def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterPar
     Landmark bands are sized so the plane buffer fits ``plane_budget``."""
     n, H, W = inp.f.shape
     S = params.spatial.effective_radius()
-    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S)
+    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True)
     keep: list = []
     d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
     lib = _native.lib()
@@ -451,7 +451,7 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
                                           "normalization")}
     timings["upload"] = t.get("upload", 0.0)
     timings["total"] = sum(t.values())
-    return FilterReport(output=_output_image(out, f, given=out_given), timings=timings, retained_rank=int(plan.alphas.shape[0]),
+    return FilterReport(output=_output_image(out, f, given=out_given), timings=timings, retained_rank=plan.rank,
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
 
 
@@ -473,7 +473,7 @@ def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> Filte
     timer.mark("normalization")
     t = timer.elapsed()
     t["total"] = sum(t.values())
-    return FilterReport(output=_output_image(out, f), timings=t, retained_rank=int(plan.alphas.shape[0]),
+    return FilterReport(output=_output_image(out, f), timings=t, retained_rank=plan.rank,
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=C_)
 
 

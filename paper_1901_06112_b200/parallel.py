@@ -330,7 +330,7 @@ def sharded_fast_filter(f_local: torch.Tensor, H: int, params, comm: Comm, nlm: 
     min_den = float(comm.allgather(float(st[0]))[:, 0].min())
     guarded = int(round(comm.sum_ordered(float(st[1:].view(torch.int64)[0]))[0]))
     return out, dict(centroids=km.centroids, quant_error=km.quant_error, errors=km.errors,
-                     retained_rank=int(plan.alphas.shape[0]), min_denominator=min_den, guarded_pixels=guarded)
+                     retained_rank=plan.rank, min_denominator=min_den, guarded_pixels=guarded)
 
 
 def bench_sharded(args, wl, rank: int, world: int):

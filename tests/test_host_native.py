@@ -205,3 +205,22 @@ def test_phi_form_plan_for_ill_conditioned_kernels():
     assert min(np.abs(p.u0 - V[:, 0]).max(), np.abs(p.u0 + V[:, 0]).max()) <= 1e-10
     q = mixing_plan(np.random.default_rng(0).random((16, 3)), 0.2, 1e-8, 8)
     assert not q.phi_form
+
+
+@pytest.mark.parametrize("k,rho,theta", [(64, 3, 0.1), (48, 31, 0.25), (64, 27, 1.3), (32, 3, 0.15), (5, 1, 0.35),
+                                         (6, 1, 0.35)])
+def test_lite_mixing_plan_matches_full(k, rho, theta):
+    # the hot-path plan (alpha_1 by Sturm bisection + two Sturm counts) gives the full plan's
+    # M, u0, alpha_1 and rank, or defers to it (drops / phi-form)
+    from paper_1901_06112_b200.nystrom import mixing_plan
+
+    C = np.random.default_rng(k + rho).random((k, rho))
+    if k == 6:
+        C = np.array([[0.40], [0.45], [0.50], [0.55], [0.60], [0.62]])  # cond 1e8: phi-form via the full plan
+    a = mixing_plan(C, theta, 1e-8, 15)
+    b = mixing_plan(C, theta, 1e-8, 15, lite=True)
+    assert a.phi_form == b.phi_form and a.rank == b.rank
+    assert b.alpha0 == pytest.approx(a.alpha0, rel=1e-14)
+    assert b.eps_den == pytest.approx(a.eps_den, rel=1e-14)
+    np.testing.assert_allclose(b.M, a.M, rtol=0, atol=1e-12 * np.abs(a.M).max())
+    assert min(np.abs(a.u0 - b.u0).max(), np.abs(a.u0 + b.u0).max()) <= 1e-9

@@ -176,6 +176,10 @@ typedef struct nys_filter_desc {
      * them as the raw-feature planes).  Same reference quantity
      * (filters.py:227-238); FP32 error no longer grows with cond(A). */
     int phi_form;
+    /* 1: M holds the lower Cholesky factor L of A (row-major) instead of M;
+     * nys_filter_prepare forms M = A^{-1} = L^{-T} L^{-1} on the device in FP64
+     * (y-form, nothing dropped, m0 <= 90).  0: M as above. */
+    int M_is_cholesky;
 } nys_filter_desc;
 
 /* Size of the horizontal-pass plane buffer for a band of `rows` output rows:
@@ -368,7 +372,9 @@ int nys_sym_eig(const double* a, int k, double* values_out, double* vectors_out)
  * (alpha <= eps_drop alpha_1) or cond(A) > phi_cond -- the caller then uses
  * nys_mixing_plan.  Otherwise rank = m0, M = A^{-1}, u0 = w_1, info_out[0] = alpha_1. */
 int nys_mixing_plan_lite(const double* centroids, int m0, int rho, double theta, double eps_drop, double phi_cond,
-                         double* info_out, int* rank_out, double* M_out, double* u0_out);
+                         int chol_only, double* info_out, int* rank_out, double* M_out, double* u0_out);
+/* chol_only != 0: M_out receives the lower Cholesky factor of A instead of
+ * A^{-1} (pass it with nys_filter_desc.M_is_cholesky = 1). */
 int nys_mixing_plan(const double* centroids, int m0, int rho, double theta, double eps_drop, double* alphas_out,
                     int* rank_out, double* M_out, double* u0_out);
 

@@ -39,7 +39,7 @@ class FilterDesc(C.Structure):
         ("sigma", C.c_double), ("m0", C.c_int), ("theta", C.c_double),
         ("centroids", C.POINTER(C.c_double)), ("M", C.POINTER(C.c_double)),
         ("u0", C.POINTER(C.c_double)), ("alpha0", C.c_double), ("eps_den", C.c_double),
-        ("row_lo", C.c_int), ("row_hi", C.c_int), ("phi_form", C.c_int),
+        ("row_lo", C.c_int), ("row_hi", C.c_int), ("phi_form", C.c_int), ("M_is_cholesky", C.c_int),
     ]
 
 
@@ -82,7 +82,7 @@ _SIGS = {
     "nys_patch_moments": (_I, [_P, _L, _I, _I, _I, _I, _P, _P, _P, _S, _P]),
     "nys_pca_project": (_I, [_P, _L, _I, _I, _I, _I, _P, _P, _I, _P, _L, _P]),
     "nys_spatial_planes": (_I, [_P, _P, _L, _I, _I, _I, _D, _I, _P, _P]),
-    "nys_mixing_plan_lite": (_I, [_P, _I, _I, _D, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
+    "nys_mixing_plan_lite": (_I, [_P, _I, _I, _D, _D, _D, _I, _P, C.POINTER(C.c_int), _P, _P]),
     "nys_mixing_plan": (_I, [_P, _I, _I, _D, _D, _P, C.POINTER(C.c_int), _P, _P]),
 }
 

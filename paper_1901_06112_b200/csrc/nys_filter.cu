@@ -43,6 +43,36 @@ __global__ void k_patch_guide(const float* __restrict__ f, long long fps, int n,
   }
 }
 
+// M = A^{-1} = L^{-T} L^{-1} from the host's Cholesky factor, FP64, into the FP32
+// [M | u0]^T block (MT[j][i] = M[i][j]); one CTA, n <= 90 (L and X in shared memory)
+__global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restrict__ Lg, int n, float* __restrict__ MT,
+                                                          int m0q) {
+  extern __shared__ double cs[];
+  double* Ls = cs;          // n x n
+  double* X = cs + n * n;   // n x n, X = L^{-1} (lower)
+  for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
+    Ls[k] = Lg[k];
+    X[k] = 0.0;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < n) {  // column j of L^{-1} by forward substitution
+    const int j = threadIdx.x;
+    X[j * n + j] = 1.0 / Ls[j * n + j];
+    for (int i = j + 1; i < n; ++i) {
+      double t = 0.0;
+      for (int k = j; k < i; ++k) t = fma(Ls[i * n + k], X[k * n + j], t);
+      X[i * n + j] = -t / Ls[i * n + i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    double t = 0.0;
+    for (int k = max(i, j); k < n; ++k) t = fma(X[k * n + i], X[k * n + j], t);
+    MT[(size_t)j * m0q + i] = (float)t;
+  }
+}
+
 __global__ void k_reset_stats(FilterStats* s) {
   s->min_abs_eta_bits = 0x7f800000u;  // +inf
   s->guarded = 0ull;
@@ -83,8 +113,11 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
   std::vector<float> h(L.n_floats, 0.f);
   for (int j = 0; j < d->m0; ++j)
     for (int k = 0; k < d->rho; ++k) h[L.off_C + (size_t)j * L.rhop + k] = (float)d->centroids[(size_t)j * d->rho + k];
+  const bool chol = d->M_is_cholesky != 0;
+  if (chol && (d->phi_form || d->m0 > 90)) return NYS_EINVAL;
   for (int j = 0; j < d->m0; ++j) {
-    for (int i = 0; i < d->m0; ++i) h[L.off_MT + (size_t)j * L.m0q + i] = (float)d->M[(size_t)i * d->m0 + j];
+    if (!chol)
+      for (int i = 0; i < d->m0; ++i) h[L.off_MT + (size_t)j * L.m0q + i] = (float)d->M[(size_t)i * d->m0 + j];
     h[L.off_MT + (size_t)j * L.m0q + d->m0] = (float)d->u0[j];
     // K3 forms s0 = U0 . (stored feature planes): u0 . b, or sqrt(alpha_1) phi_0 in the phi-form
     h[L.off_U0 + j] = d->phi_form ? (j == 0 ? (float)std::sqrt(d->alpha0) : 0.f) : (float)d->u0[j];
@@ -93,6 +126,15 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
   // pageable H2D: the runtime stages `h` before returning, so it may go away
   // right after (no stream synchronisation: the caller keeps queueing work)
   NYS_CUDA_TRY(cudaMemcpyAsync(workspace, h.data(), L.n_floats * sizeof(float), cudaMemcpyHostToDevice, s));
+  if (chol) {  // M = A^{-1} from the Cholesky factor, on the device (after the block above lands)
+    double* Ld = reinterpret_cast<double*>((char*)workspace + L.chol_off_bytes);
+    NYS_CUDA_TRY(cudaMemcpyAsync(Ld, d->M, (size_t)d->m0 * d->m0 * sizeof(double), cudaMemcpyHostToDevice, s));
+    const size_t smem = 2 * (size_t)d->m0 * d->m0 * sizeof(double);
+    NYS_CUDA_TRY(cudaFuncSetAttribute(k_inverse_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
+    k_inverse_cholesky<<<1, 1024, smem, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q);
+    NYS_LAUNCH_CHECK();
+  }
   count_launch();
   k_reset_stats<<<1, 1, 0, s>>>(reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));
   NYS_LAUNCH_CHECK();

@@ -19,7 +19,7 @@ namespace nys {
 struct FilterLayout {
   int m0, rho, rhop, m0q;  // rhop: rho padded to 4; m0q: (m0+1) padded to 8
   size_t off_C, off_MT, off_U0, n_floats;
-  size_t stats_off_bytes, total_bytes;
+  size_t stats_off_bytes, chol_off_bytes, total_bytes;  // chol: m0 x m0 FP64 (M_is_cholesky)
 };
 
 inline FilterLayout filter_layout(const nys_filter_desc* d) {
@@ -33,7 +33,8 @@ inline FilterLayout filter_layout(const nys_filter_desc* d) {
   L.off_U0 = L.off_MT + (size_t)d->m0 * L.m0q;
   L.n_floats = L.off_U0 + (size_t)ceil_div(d->m0, 4) * 4;
   L.stats_off_bytes = ((L.n_floats * 4 + 255) / 256) * 256;
-  L.total_bytes = L.stats_off_bytes + 256;
+  L.chol_off_bytes = L.stats_off_bytes + 256;
+  L.total_bytes = L.chol_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;
   return L;
 }
 

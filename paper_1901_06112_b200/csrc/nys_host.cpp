@@ -534,8 +534,8 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan(const double* C, int m0, int rho,
 // eps_drop * alpha_1 and cond(A) must stay <= phi_cond, else NYS_EUNSUPPORTED
 // (the caller then runs nys_mixing_plan).  info_out[0] = alpha_1.
 extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int rho, double theta, double eps_drop,
-                                                    double phi_cond, double* info_out, int* rank_out, double* M_out,
-                                                    double* u0_out) {
+                                                    double phi_cond, int chol_only, double* info_out, int* rank_out,
+                                                    double* M_out, double* u0_out) {
   if (!C || m0 < 1 || rho < 1 || !(theta > 0.0) || !info_out || !rank_out || !M_out || !u0_out || !(phi_cond > 1.0))
     return NYS_EINVAL;
   const int n = m0;
@@ -581,7 +581,10 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int
     for (int i = j + 1; i < n; ++i) L[(size_t)i * n + j] = (A[(size_t)i * n + j] - dot4(&L[(size_t)i * n], lj, j)) / ljj;
   }
   double* alphas_out = info_out;
-  if (fast) {
+  if (fast && chol_only) {
+    // the caller forms M = L^{-T} L^{-1} on the device (nys_filter_desc.M_is_cholesky)
+    for (size_t q = 0; q < (size_t)n * n; ++q) M_out[q] = L[q];
+  } else if (fast) {
     // X = L^{-1} stored transposed (XT[j][i] = X[i][j], i >= j) so both products stream rows
     std::vector<double> XT((size_t)n * n, 0.0);
     std::vector<double> col(n);

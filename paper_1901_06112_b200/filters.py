@@ -188,6 +188,7 @@ def _desc(n: int, rho: int, H: int, W: int, gkind: int, spatial: SpatialKernel, 
     d.alpha0 = plan.alpha0
     d.eps_den = plan.eps_den
     d.phi_form = 1 if plan.phi_form else 0
+    d.M_is_cholesky = 1 if plan.M_is_cholesky else 0
     return d
 
 
@@ -241,7 +242,8 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     H = H_global if H_global is not None else h_local
     lo, hi = rows if rows is not None else (0, H)
     S = params.spatial.effective_radius()
-    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True)
+    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True,
+                       device_inverse=True)
     keep: list = []
     d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
     d.row_lo, d.row_hi = row_origin, row_origin + h_local
@@ -309,7 +311,8 @@ def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterPar
     Landmark bands are sized so the plane buffer fits ``plane_budget``."""
     n, H, W = inp.f.shape
     S = params.spatial.effective_radius()
-    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True)
+    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True,
+                       device_inverse=True)
     keep: list = []
     d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
     lib = _native.lib()

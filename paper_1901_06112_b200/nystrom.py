@@ -122,6 +122,7 @@ class MixingPlan:
     eps_den: float       # 1e-12 (2S+1)^2 max|alpha|
     phi_form: bool = False  # M holds P = diag(alpha_r^-1/2) W_r^T (padded to m0 rows), see nys_filter_desc
     rank: int = -1          # retained eigenpairs (lite plans carry only alpha_1 in `alphas`)
+    M_is_cholesky: bool = False  # M holds the Cholesky factor of A; the device forms A^{-1}
 
     def __post_init__(self):
         if self.rank < 0:
@@ -134,7 +135,8 @@ class MixingPlan:
 PHI_FORM_COND = 3.0e4
 
 
-def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int, lite: bool = False) -> MixingPlan:
+def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int, lite: bool = False,
+                device_inverse: bool = False) -> MixingPlan:
     """Host FP64 products the kernels consume, in one native call
     (``nys_mixing_plan``: Gram matrix nystrom.py:67-69, eigenvalues + drop
     rule nystrom.py:97-109, M and the lead eigenvector).
@@ -154,12 +156,14 @@ def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int, li
     rank = C.c_int(0)
     if lite:
         # hot path: alpha_1 + two Sturm counts (nothing dropped, cond <= PHI_FORM_COND), else the full plan
+        chol = bool(device_inverse and k <= 90)  # M = A^{-1} formed on the device from the Cholesky factor
         rc = _native.lib().nys_mixing_plan_lite(C_.ctypes.data, k, rho, float(theta), float(eps_drop), PHI_FORM_COND,
-                                                alphas.ctypes.data, C.byref(rank), M.ctypes.data, u0.ctypes.data)
+                                                int(chol), alphas.ctypes.data, C.byref(rank), M.ctypes.data,
+                                                u0.ctypes.data)
         if rc == _native.NYS_OK:
             a1 = float(alphas[0])
             return MixingPlan(alphas=np.array([a1]), M=M, u0=u0, alpha0=a1,
-                              eps_den=1e-12 * (2 * S + 1) ** 2 * a1, rank=k)
+                              eps_den=1e-12 * (2 * S + 1) ** 2 * a1, rank=k, M_is_cholesky=chol)
         if rc == _native.NYS_EDEGENERATE:
             raise DegenerateKernelError("landmark kernel has no positive eigenvalue")
         if rc != _native.NYS_EUNSUPPORTED:

@@ -205,6 +205,43 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
                        void* stream);
 
 /*
+ * In-stream (speculative) mixing plan: the host never waits for the landmarks.
+ *
+ * nys_filter_plan_async forks from `stream` at the point of the call: once the
+ * landmark coordinates have landed in `centroids` [pinned host, m0 x rho FP64,
+ * written by an earlier copy on `stream`], a host function on a side stream
+ * runs the lite plan (nys_mixing_plan_lite, Cholesky factor) into the pinned
+ * `staging` image of the workspace constants and copies it to `workspace`.
+ * Work queued on `stream` between this call and nys_filter_prepare_join (e.g.
+ * the k-means exact pass) overlaps the plan.  The desc's M / u0 / alpha0 /
+ * eps_den / phi_form / M_is_cholesky are ignored (the plan supplies them).
+ *
+ * nys_filter_prepare_join makes `stream` wait for the copy, forms M = A^{-1}
+ * on the device and resets the statistics; the band passes follow as usual.
+ *
+ * The speculation is the y-form with nothing dropped (cond(A) <= phi_cond).
+ * Read the verdict with nys_filter_plan_result once `stream` has passed the
+ * join: status NYS_OK means the passes used the exact plan; NYS_EUNSUPPORTED
+ * means the plan needs drops or the phi-form -- rerun with nys_filter_prepare
+ * and a plan from nys_mixing_plan (the speculative outputs are meaningless).
+ * `staging` [pinned, nys_filter_plan_staging_bytes(d), zero-filled once] and
+ * `centroids` must stay untouched until then.  m0 <= 90.
+ */
+typedef struct nys_plan_result {
+    int status;      /* NYS_OK, NYS_EUNSUPPORTED (fall back), or an error code */
+    int rank;        /* retained eigenpairs (m0 on NYS_OK) */
+    double alpha0;   /* largest eigenvalue of A */
+    double eps_den;  /* guard threshold used by the passes */
+    double host_us;  /* wall time of the plan inside the host function */
+} nys_plan_result;
+size_t nys_filter_plan_staging_bytes(const nys_filter_desc* d);
+int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, double eps_drop, double phi_cond,
+                          void* staging, size_t staging_bytes, void* workspace, size_t workspace_bytes,
+                          void* stream);
+int nys_filter_prepare_join(const nys_filter_desc* d, void* staging, void* workspace, void* stream);
+int nys_filter_plan_result(const void* staging, nys_plan_result* out);
+
+/*
  * K2: range features + horizontal pass for the band of output rows
  * [out0, out0+out_rows) (computes its rows + 2R virtual halo rows).
  * f [dev] (n,H,W) planar, f_plane_stride; guide [dev] (rho,H,W) (ignored for

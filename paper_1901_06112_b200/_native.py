@@ -43,6 +43,13 @@ class FilterDesc(C.Structure):
     ]
 
 
+class PlanResult(C.Structure):
+    """Mirror of ``nys_plan_result``."""
+
+    _fields_ = [("status", C.c_int), ("rank", C.c_int), ("alpha0", C.c_double), ("eps_den", C.c_double),
+                ("host_us", C.c_double)]
+
+
 _P = C.c_void_p
 _I = C.c_int
 _L = C.c_int64
@@ -65,6 +72,10 @@ _SIGS = {
     "nys_filter_workspace_bytes": (_S, [C.POINTER(FilterDesc)]),
     "nys_filter_plane_row_stride": (_L, [C.POINTER(FilterDesc)]),
     "nys_filter_prepare": (_I, [C.POINTER(FilterDesc), _P, _S, _P]),
+    "nys_filter_plan_staging_bytes": (_S, [C.POINTER(FilterDesc)]),
+    "nys_filter_plan_async": (_I, [C.POINTER(FilterDesc), _P, _D, _D, _P, _S, _P, _S, _P]),
+    "nys_filter_prepare_join": (_I, [C.POINTER(FilterDesc), _P, _P, _P]),
+    "nys_filter_plan_result": (_I, [_P, C.POINTER(PlanResult)]),
     "nys_filter_hpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
     "nys_filter_vpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
     "nys_filter_stats": (_I, [C.POINTER(FilterDesc), _P, _P, _P]),

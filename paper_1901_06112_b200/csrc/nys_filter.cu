@@ -20,6 +20,14 @@
 // Plane buffer layout: plane p = i*(n+1) + c, each plane `rows + 2R` virtual
 // rows of pitch Wp = roundup(W, 4) floats; virtual row v maps to image row
 // clamp(v, 0, H-1), so K3 never clamps (replicate borders, spatial.py:85-88).
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstddef>
+#include <deque>
+#include <mutex>
+#include <thread>
+
 #include "nys_filter_common.cuh"
 
 namespace nys {
@@ -45,31 +53,79 @@ __global__ void k_patch_guide(const float* __restrict__ f, long long fps, int n,
 
 // M = A^{-1} = L^{-T} L^{-1} from the host's Cholesky factor, FP64, into the FP32
 // [M | u0]^T block (MT[j][i] = M[i][j]); one CTA, n <= 90 (L and X in shared memory)
+// M = A^{-1} = X^T X with X = L^{-1}, A = L L^T (the host's Cholesky factor, FP64).
+// Blocked forward substitution over 8-row blocks keeps the dependent chains short:
+// the diagonal blocks are inverted first (one thread per block column), then block
+// row I of X is R_I = E_I - L[I, <I] X[<I, :] (one thread per element, four
+// accumulators) followed by X[I, :] = L_II^{-1} R_I.  n is padded to np = 8 nb
+// with an identity tail, which leaves the leading n x n block of X unchanged.
 __global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restrict__ Lg, int n, float* __restrict__ MT,
                                                           int m0q) {
   extern __shared__ double cs[];
-  double* Ls = cs;          // n x n
-  double* X = cs + n * n;   // n x n, X = L^{-1} (lower)
-  for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
-    Ls[k] = Lg[k];
-    X[k] = 0.0;
+  const int np = (n + 7) & ~7, nb = np / 8;
+  double* Ls = cs;              // np x np
+  double* X = Ls + np * np;     // np x np, X = L^{-1} (lower)
+  double* Di = X + np * np;     // np x 8: inverse of diagonal block I in rows 8I..8I+7
+  double* R = Di + np * 8;      // 8 x np scratch
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    Ls[e] = (i < n && j < n) ? Lg[i * n + j] : (i == j ? 1.0 : 0.0);
+    X[e] = 0.0;
   }
   __syncthreads();
-  if ((int)threadIdx.x < n) {  // column j of L^{-1} by forward substitution
-    const int j = threadIdx.x;
-    X[j * n + j] = 1.0 / Ls[j * n + j];
-    for (int i = j + 1; i < n; ++i) {
-      double t = 0.0;
-      for (int k = j; k < i; ++k) t = fma(Ls[i * n + k], X[k * n + j], t);
-      X[i * n + j] = -t / Ls[i * n + i];
+  if ((int)threadIdx.x < np) {  // column c of the inverse of the 8 x 8 diagonal block I
+    const int I = threadIdx.x >> 3, c = threadIdx.x & 7, o = 8 * I;
+    double col[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      double t = (a == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < a; ++k) t = fma(-Ls[(o + a) * np + o + k], col[k], t);
+      col[a] = (a < c) ? 0.0 : t / Ls[(o + a) * np + o + a];
     }
+#pragma unroll
+    for (int a = 0; a < 8; ++a) Di[(o + a) * 8 + c] = col[a];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e - i * n;
-    double t = 0.0;
-    for (int k = max(i, j); k < n; ++k) t = fma(X[k * n + i], X[k * n + j], t);
-    MT[(size_t)j * m0q + i] = (float)t;
+  for (int I = 0; I < nb; ++I) {
+    const int o = 8 * I, w = o + 8;  // block row I has nonzeros in columns < w
+    for (int e = threadIdx.x; e < 8 * w; e += blockDim.x) {
+      const int a = e / w, j = e - a * w;
+      const double* lr = Ls + (o + a) * np;
+      double t0 = (o + a == j) ? 1.0 : 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      int k = j;
+      for (; k + 3 < o; k += 4) {
+        t0 = fma(-lr[k], X[k * np + j], t0);
+        t1 = fma(-lr[k + 1], X[(k + 1) * np + j], t1);
+        t2 = fma(-lr[k + 2], X[(k + 2) * np + j], t2);
+        t3 = fma(-lr[k + 3], X[(k + 3) * np + j], t3);
+      }
+      for (; k < o; ++k) t0 = fma(-lr[k], X[k * np + j], t0);
+      R[a * np + j] = (t0 + t1) + (t2 + t3);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 8 * w; e += blockDim.x) {
+      const int a = e / w, j = e - a * w;
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t = fma(Di[(o + a) * 8 + q], R[q * np + j], t);
+      X[(o + a) * np + j] = t;
+    }
+    __syncthreads();
+  }
+  // M[i][j] = sum_{k >= max(i, j)} X[k][i] X[k][j]; four columns per thread
+  const int nq = (n + 3) / 4;
+  for (int e = threadIdx.x; e < n * nq; e += blockDim.x) {
+    const int i = e / nq, j0 = 4 * (e - i * nq);
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = max(i, j0); k < n; ++k) {
+      const double xi = X[k * np + i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) t[q] = fma(xi, X[k * np + j0 + q], t[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (j0 + q < n) MT[(size_t)(j0 + q) * m0q + i] = (float)t[q];
   }
 }
 
@@ -104,6 +160,238 @@ size_t nys_filter_workspace_bytes(const nys_filter_desc* d) {
   return filter_layout(d).total_bytes;
 }
 
+}  // extern "C"
+
+namespace {
+// M = A^{-1} from the Cholesky factor at chol_off_bytes (after the constants land), then the
+// statistics reset
+int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, void* workspace, bool chol,
+                             cudaStream_t s) {
+  if (chol) {
+    const double* Ld = reinterpret_cast<const double*>((char*)workspace + L.chol_off_bytes);
+    const int np = (d->m0 + 7) & ~7;
+    const size_t smem = (2 * (size_t)np * np + 16 * (size_t)np) * sizeof(double);
+    NYS_CUDA_TRY(cudaFuncSetAttribute(k_inverse_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
+    k_inverse_cholesky<<<1, 1024, smem, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q);
+    NYS_LAUNCH_CHECK();
+  }
+  count_launch();
+  k_reset_stats<<<1, 1, 0, s>>>(reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// In-stream plan (nys_filter_plan_async / nys_filter_prepare_join).  The pinned
+// staging buffer starts with this job record; the workspace image follows at
+// kStagingHeader bytes.
+//
+// A persistent native worker thread polls the fork event (recorded on the
+// caller's stream after the landmarks' copy), runs the lite plan, fills the
+// image and publishes `done`; the caller's stream is gated on the device by
+// cuStreamWaitValue32 on that pinned word, then copies the image in.  The worker
+// depends only on work queued before the gate and always publishes `done`
+// (with an error status on failure), so the gate cannot deadlock.  A
+// cudaLaunchHostFunc chain did the same with ~0.3 ms of dispatch latency.
+// ---------------------------------------------------------------------------
+constexpr size_t kStagingHeader = 512;
+struct PlanJob {
+  const double* centroids;
+  int m0, rho, S, device;
+  double theta, eps_drop, phi_cond;
+  FilterLayout L;
+  size_t image_bytes;
+  nys_plan_result result;
+  cudaEvent_t fork;
+  unsigned seq;
+  volatile unsigned done;  // the stream waits for done >= seq
+};
+static_assert(sizeof(PlanJob) <= kStagingHeader, "plan job record outgrew its header");
+
+void run_plan(PlanJob* j) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int n = j->m0, rho = j->rho;
+  const FilterLayout& L = j->L;
+  float* img = reinterpret_cast<float*>(reinterpret_cast<char*>(j) + kStagingHeader);
+  std::vector<double> info(n), Lc((size_t)n * n), u0(n);
+  int rank = 0;
+  const int rc = nys_mixing_plan_lite(j->centroids, n, rho, j->theta, j->eps_drop, j->phi_cond, 1, info.data(), &rank,
+                                      Lc.data(), u0.data());
+  j->result.status = rc;
+  j->result.rank = rc == NYS_OK ? n : 0;
+  if (rc == NYS_OK) {
+    const double a1 = info[0];
+    j->result.alpha0 = a1;
+    j->result.eps_den = 1e-12 * (double)((2 * j->S + 1) * (2 * j->S + 1)) * a1;  // filters.py:241-243
+    for (int q = 0; q < n; ++q) {
+      for (int k = 0; k < rho; ++k) img[L.off_C + (size_t)q * L.rhop + k] = (float)j->centroids[(size_t)q * rho + k];
+      img[L.off_MT + (size_t)q * L.m0q + n] = (float)u0[q];
+      img[L.off_U0 + q] = (float)u0[q];
+    }
+    img[L.off_SC] = (float)(1.0 / a1);
+    img[L.off_SC + 1] = (float)j->result.eps_den;
+    std::memcpy(reinterpret_cast<char*>(img) + L.chol_off_bytes, Lc.data(), (size_t)n * n * sizeof(double));
+  }
+  j->result.host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+}
+
+class PlanWorker {
+ public:
+  PlanWorker() { std::thread([this] { loop(); }).detach(); }
+  void post(PlanJob* j) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      q_.push_back(j);
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  void loop() {
+    int cur_dev = -1;
+    for (;;) {
+      PlanJob* j;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [this] { return !q_.empty(); });
+        j = q_.front();
+        q_.pop_front();
+      }
+      bool ok = true;
+      if (j->device != cur_dev) ok = cudaSetDevice(j->device) == cudaSuccess, cur_dev = j->device;
+      const auto t0 = std::chrono::steady_clock::now();
+      while (ok) {  // spin for the landmarks (k-means is still running when the job is posted), then back off
+        const cudaError_t e = cudaEventQuery(j->fork);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) {
+          ok = false;
+          break;
+        }
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        if (us > 60e6) ok = false;
+        else if (us > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+      if (ok) run_plan(j);
+      else j->result.status = NYS_ECUDA;
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      j->done = j->seq;  // releases the stream gate
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<PlanJob*> q_;
+};
+
+PlanWorker& plan_worker() {
+  static PlanWorker* w = new PlanWorker();  // never destroyed: the thread outlives static teardown
+  return *w;
+}
+
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamWaitValue32Fn wait_value_fn() {
+  static StreamWaitValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitValue32Fn>(p);
+  }
+  return fn;
+}
+
+constexpr int kPlanSlots = 8;
+struct PlanEvents {
+  int device = -1;
+  cudaEvent_t fork[kPlanSlots] = {};
+  int next = 0;
+};
+PlanEvents* plan_events() {
+  thread_local PlanEvents pe;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (pe.device == dev) return &pe;
+  for (int k = 0; k < kPlanSlots; ++k)
+    if (cudaEventCreateWithFlags(&pe.fork[k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  pe.device = dev;
+  return &pe;
+}
+
+size_t plan_image_bytes(const FilterLayout& L, int m0) { return L.chol_off_bytes + (size_t)m0 * m0 * sizeof(double); }
+}  // namespace
+
+extern "C" {
+
+size_t nys_filter_plan_staging_bytes(const nys_filter_desc* d) {
+  if (validate(d) != NYS_OK || d->m0 > 90) return 0;
+  return kStagingHeader + plan_image_bytes(filter_layout(d), d->m0);
+}
+
+int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, double eps_drop, double phi_cond,
+                          void* staging, size_t staging_bytes, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  if (!centroids || !staging || !workspace || d->m0 > 90 || !(phi_cond > 1.0)) return NYS_EINVAL;
+  const FilterLayout L = filter_layout(d);
+  if (staging_bytes < kStagingHeader + plan_image_bytes(L, d->m0) || workspace_bytes < L.total_bytes)
+    return NYS_EINVAL;
+  if (!wait_value_fn()) return NYS_EUNSUPPORTED;
+  void* dv = nullptr;  // the gate word must be device-visible (mapped pinned memory)
+  if (nys_device_view(staging, &dv) != NYS_OK) return NYS_EINVAL;
+  PlanEvents* pe = plan_events();
+  if (!pe) return NYS_ECUDA;
+  PlanJob* j = static_cast<PlanJob*>(staging);
+  if (j->seq != j->done) return NYS_EINVAL;  // the previous plan on this staging buffer is still pending
+  j->centroids = centroids;
+  j->m0 = d->m0;
+  j->rho = d->rho;
+  j->S = d->radius;
+  NYS_CUDA_TRY(cudaGetDevice(&j->device));
+  j->theta = d->theta;
+  j->eps_drop = eps_drop;
+  j->phi_cond = phi_cond;
+  j->L = L;
+  j->image_bytes = plan_image_bytes(L, d->m0);
+  j->result = nys_plan_result{NYS_ECUDA, 0, 0.0, 0.0, 0.0};  // overwritten by the worker
+  j->fork = pe->fork[pe->next];
+  pe->next = (pe->next + 1) % kPlanSlots;
+  NYS_CUDA_TRY(cudaEventRecord(j->fork, (cudaStream_t)stream));
+  j->seq = j->seq + 1;
+  plan_worker().post(j);
+  return NYS_OK;
+}
+
+int nys_filter_prepare_join(const nys_filter_desc* d, void* staging, void* workspace, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  if (!staging || !workspace) return NYS_EINVAL;
+  const PlanJob* j = static_cast<const PlanJob*>(staging);
+  if (j->m0 != d->m0) return NYS_EINVAL;
+  void* dv = nullptr;
+  if (nys_device_view(staging, &dv) != NYS_OK) return NYS_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const CUdeviceptr gate = reinterpret_cast<CUdeviceptr>(dv) + offsetof(PlanJob, done);
+  if (wait_value_fn()(reinterpret_cast<CUstream>(s), gate, j->seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return NYS_ECUDA;
+  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, static_cast<const char*>(staging) + kStagingHeader, j->image_bytes,
+                               cudaMemcpyHostToDevice, s));
+  return launch_inverse_and_reset(d, filter_layout(d), workspace, true, s);
+}
+
+int nys_filter_plan_result(const void* staging, nys_plan_result* out) {
+  if (!staging || !out) return NYS_EINVAL;
+  const PlanJob* j = static_cast<const PlanJob*>(staging);
+  if (j->done != j->seq) return NYS_EINVAL;  // not finished
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *out = j->result;
+  return NYS_OK;
+}
+
 int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspace_bytes, void* stream) {
   int st = validate(d);
   if (st) return st;
@@ -122,23 +410,18 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
     // K3 forms s0 = U0 . (stored feature planes): u0 . b, or sqrt(alpha_1) phi_0 in the phi-form
     h[L.off_U0 + j] = d->phi_form ? (j == 0 ? (float)std::sqrt(d->alpha0) : 0.f) : (float)d->u0[j];
   }
+  h[L.off_SC] = (float)(1.0 / d->alpha0);
+  h[L.off_SC + 1] = (float)d->eps_den;
   cudaStream_t s = (cudaStream_t)stream;
-  // pageable H2D: the runtime stages `h` before returning, so it may go away
-  // right after (no stream synchronisation: the caller keeps queueing work)
-  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, h.data(), L.n_floats * sizeof(float), cudaMemcpyHostToDevice, s));
-  if (chol) {  // M = A^{-1} from the Cholesky factor, on the device (after the block above lands)
-    double* Ld = reinterpret_cast<double*>((char*)workspace + L.chol_off_bytes);
-    NYS_CUDA_TRY(cudaMemcpyAsync(Ld, d->M, (size_t)d->m0 * d->m0 * sizeof(double), cudaMemcpyHostToDevice, s));
-    const size_t smem = 2 * (size_t)d->m0 * d->m0 * sizeof(double);
-    NYS_CUDA_TRY(cudaFuncSetAttribute(k_inverse_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    count_launch();
-    k_inverse_cholesky<<<1, 1024, smem, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q);
-    NYS_LAUNCH_CHECK();
+  if (chol) {  // the Cholesky factor rides in the same upload, FP64 at chol_off_bytes
+    h.resize((L.chol_off_bytes + (size_t)d->m0 * d->m0 * sizeof(double)) / sizeof(float), 0.f);
+    std::memcpy(reinterpret_cast<char*>(h.data()) + L.chol_off_bytes, d->M, (size_t)d->m0 * d->m0 * sizeof(double));
   }
-  count_launch();
-  k_reset_stats<<<1, 1, 0, s>>>(reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));
-  NYS_LAUNCH_CHECK();
-  return NYS_OK;
+  // pageable H2D: the runtime stages `h` before returning, so it may go away
+  // right after (no stream synchronisation: the caller keeps queueing work); the
+  // stats block it overwrites is reset below
+  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  return launch_inverse_and_reset(d, L, workspace, chol, s);
 }
 
 int nys_filter_stats(const nys_filter_desc* d, const void* workspace, void* stats_out, void* stream) {

@@ -18,7 +18,7 @@ namespace nys {
 // ---------------------------------------------------------------------------
 struct FilterLayout {
   int m0, rho, rhop, m0q;  // rhop: rho padded to 4; m0q: (m0+1) padded to 8
-  size_t off_C, off_MT, off_U0, n_floats;
+  size_t off_C, off_MT, off_U0, off_SC, n_floats;  // SC: {1/alpha_1, eps_den} read by K3
   size_t stats_off_bytes, chol_off_bytes, total_bytes;  // chol: m0 x m0 FP64 (M_is_cholesky)
 };
 
@@ -31,7 +31,8 @@ inline FilterLayout filter_layout(const nys_filter_desc* d) {
   L.off_C = 0;
   L.off_MT = L.off_C + (size_t)d->m0 * L.rhop;
   L.off_U0 = L.off_MT + (size_t)d->m0 * L.m0q;
-  L.n_floats = L.off_U0 + (size_t)ceil_div(d->m0, 4) * 4;
+  L.off_SC = L.off_U0 + (size_t)ceil_div(d->m0, 4) * 4;
+  L.n_floats = L.off_SC + 4;
   L.stats_off_bytes = ((L.n_floats * 4 + 255) / 256) * 256;
   L.chol_off_bytes = L.stats_off_bytes + 256;
   L.total_bytes = L.chol_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;

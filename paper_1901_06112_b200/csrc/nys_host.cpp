@@ -295,7 +295,7 @@ void tridiag(std::vector<double>& z, int n, std::vector<double>& d, std::vector<
   e.assign(n, 0.0);
   h.assign(n, 0.0);
   auto Z = [&](int i, int j) -> double& { return z[(size_t)i * n + j]; };
-  std::vector<double> zi(n);
+  std::vector<double> zi(n), p(n);
   for (int i = n - 1; i > 0; --i) {
     const int l = i - 1;
     double hh = 0.0, scale = 0.0;
@@ -314,13 +314,21 @@ void tridiag(std::vector<double>& z, int n, std::vector<double>& d, std::vector<
         hh -= f * g;
         Z(i, l) = f - g;
         f = 0.0;
-        for (int q = 0; q <= l; ++q) zi[q] = Z(i, q);
+        for (int q = 0; q <= l; ++q) {
+          zi[q] = Z(i, q);
+          p[q] = 0.0;
+        }
+        // p = A u over the stored lower triangle, one row at a time: row j gives
+        // (A u)_j's lower part (a dot) and the upper parts of (A u)_q, q < j (an axpy)
         for (int j = 0; j <= l; ++j) {
-          Z(j, i) = Z(i, j) / hh;
-          // (A u)_j over the lower triangle: row j up to j, then column j below
-          double gg = dot4(&z[(size_t)j * n], zi.data(), j + 1);
-          for (int q = j + 1; q <= l; ++q) gg += Z(q, j) * zi[q];
-          e[j] = gg / hh;
+          const double* zj = &z[(size_t)j * n];
+          const double uj = zi[j];
+          for (int q = 0; q < j; ++q) p[q] += zj[q] * uj;
+          p[j] += dot4(zj, zi.data(), j + 1);
+        }
+        for (int j = 0; j <= l; ++j) {
+          Z(j, i) = zi[j] / hh;
+          e[j] = p[j] / hh;
           f += e[j] * zi[j];
         }
         const double hf = f / (hh + hh);
@@ -584,11 +592,12 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int
   if (fast && chol_only) {
     // the caller forms M = L^{-T} L^{-1} on the device (nys_filter_desc.M_is_cholesky)
     for (size_t q = 0; q < (size_t)n * n; ++q) M_out[q] = L[q];
-  } else if (fast) {
+  }
+  if (fast) {
     // X = L^{-1} stored transposed (XT[j][i] = X[i][j], i >= j) so both products stream rows
-    std::vector<double> XT((size_t)n * n, 0.0);
+    std::vector<double> XT(chol_only ? 0 : (size_t)n * n, 0.0);
     std::vector<double> col(n);
-    for (int j = 0; j < n; ++j) {
+    for (int j = 0; j < (chol_only ? 0 : n); ++j) {
       std::fill(col.begin(), col.end(), 0.0);
       col[j] = 1.0 / L[(size_t)j * n + j];
       for (int i = j + 1; i < n; ++i)
@@ -596,7 +605,7 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int
       for (int i = j; i < n; ++i) XT[(size_t)j * n + i] = col[i];
     }
     // M[i][j] = sum_{k >= max(i,j)} X[k][i] X[k][j] = XT[i] . XT[j] over k >= j (j >= i)
-    for (int i = 0; i < n; ++i)
+    for (int i = 0; i < (chol_only ? 0 : n); ++i)
       for (int j = i; j < n; ++j) {
         const double t = dot4(&XT[(size_t)i * n + j], &XT[(size_t)j * n + j], n - j);
         M_out[(size_t)i * n + j] = M_out[(size_t)j * n + i] = t;

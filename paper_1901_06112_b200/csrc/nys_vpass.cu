@@ -54,7 +54,8 @@ struct VArgs {
   int n, rho, rhop, H, W, m0, R, box, gkind;
   int out0, out_rows, tiles_x, tiles_y, nchunks, u0_off, vec_out, gcache, ntail;
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
-  float k2, inv_alpha0, eps_den;
+  int sc_off;  // cst[sc_off], cst[sc_off + 1]: 1/alpha_1 and eps_den (written with the plan)
+  float k2;
   float taps[NYS_MAX_TAPS];
   float2 wpair[NYS_MAX_TAPS + 1];  // packed-FIR tap pairs (fill_tap_pairs)
 };
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   __shared__ float red_min[K3_THREADS / 32];
   __shared__ unsigned long long red_cnt[K3_THREADS / 32];
 
+  const float inv_alpha0 = a.cst[a.sc_off], eps_den = a.cst[a.sc_off + 1];
   for (int k = tid; k < m0 * rhop; k += K3_THREADS) Cs[k] = a.cst[k];
   for (int k = tid; k < m0; k += K3_THREADS) U0[k] = a.cst[a.u0_off + k];
   if (tid == 0) {
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
 #pragma unroll
         for (int o = 0; o < K3_YR; ++o)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) lg[o][e] = s0[o][e] * G[o][e] * a.inv_alpha0;
+          for (int e = 0; e < 4; ++e) lg[o][e] = s0[o][e] * G[o][e] * inv_alpha0;
         if (co == 0) {
           if (c == n) {
 #pragma unroll
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
           __syncthreads();
         }
         if (c < n) {
-          const float eps = a.eps_den;
+          const float eps = eps_den;
 #pragma unroll
           for (int o = 0; o < K3_YR; ++o) {
             const int row = t0 + run * K3_YR + o;
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       if (row < a.out0 + a.out_rows && row < H && x < W) {
         const float ad = fabsf(dsh[k]);
         my_min = fminf(my_min, ad);
-        my_cnt += ad < a.eps_den ? 1ull : 0ull;
+        my_cnt += ad < eps_den ? 1ull : 0ull;
       }
     }
     my_min = warp_min(my_min);
@@ -433,8 +435,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.rlo = std::max(0, d->row_lo);
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
-  a.inv_alpha0 = (float)(1.0 / d->alpha0);
-  a.eps_den = (float)d->eps_den;
+  a.sc_off = (int)L.off_SC;
   fill_taps(d, a.taps);
   fill_tap_pairs(a.taps, 2 * d->radius + 1, a.wpair);
 

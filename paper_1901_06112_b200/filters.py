@@ -16,6 +16,7 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -26,7 +27,7 @@ from ._device import StageTimer, ptr, require_cuda, stream_ptr, to_device_f32, w
 from .bands import Band, plan_bands
 from .image import Image
 from .landmarks import DEFAULT_MAX_ITER, exact_assignment, exact_assignment_async, kmeans_device
-from .nystrom import DEFAULT_EPS_DROP, RangeKernel, mixing_plan
+from .nystrom import DEFAULT_EPS_DROP, PHI_FORM_COND, MixingPlan, RangeKernel, mixing_plan
 from .spatial import BOX, GAUSSIAN_FIR, GAUSSIAN_RECURSIVE, SpatialKernel
 
 MODE_BILATERAL = "bilateral"
@@ -216,10 +217,38 @@ def _prepare_inputs(f: Image, p) -> _Inputs:
     return _Inputs(f_dev, g_dev, 0, g_dev.reshape(g_dev.shape[0], H * W), g_dev.shape[0])
 
 
-def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer: StageTimer | None = None,
+@dataclass
+class _Inflight:
+    """In-stream plan for run_filter: the landmarks arrive in ``kmeans.host``
+    (pinned) during the step; ``between()`` queues work that overlaps the plan
+    (the k-means exact pass).  run_filter fills ``staging`` and ``keep``."""
+    kmeans: object
+    between: object
+    staging: torch.Tensor | None = None
+    keep: list | None = None
+
+    def result(self) -> _native.PlanResult:
+        r = _native.PlanResult()
+        _native.check(_native.lib().nys_filter_plan_result(ptr(self.staging), C.byref(r)), "nys_filter_plan_result")
+        return r
+
+
+_STAGING: dict = {}
+
+
+def _plan_staging(nbytes: int) -> torch.Tensor:
+    """Reused zero-filled page-locked staging buffer for nys_filter_plan_async."""
+    buf = _STAGING.get(nbytes)
+    if buf is None:
+        buf = torch.zeros(nbytes, dtype=torch.uint8, pin_memory=True)
+        _STAGING[nbytes] = buf
+    return buf
+
+
+def run_filter(inp: _Inputs, centroids: np.ndarray | None, params: FilterParams, timer: StageTimer | None = None,
                plane_budget: int | None = None, out: torch.Tensor | None = None,
                kernel_events: list | None = None, rows: tuple[int, int] | None = None, row_origin: int = 0,
-               H_global: int | None = None):
+               H_global: int | None = None, inflight: _Inflight | None = None):
     """K2/K3 over row bands given landmarks; returns (out, plan, stats).
 
     ``kernel_events`` (optional list) receives (name, start, end) CUDA events
@@ -242,18 +271,38 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     H = H_global if H_global is not None else h_local
     lo, hi = rows if rows is not None else (0, H)
     S = params.spatial.effective_radius()
-    plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True,
-                       device_inverse=True)
     keep: list = []
-    d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
-    d.row_lo, d.row_hi = row_origin, row_origin + h_local
     lib = _native.lib()
+    s = stream_ptr()
+    if inflight is not None:
+        # the plan is computed in-stream from the landmarks as they land (nys_filter_plan_async);
+        # the placeholder M / u0 below are ignored by the native side
+        km = inflight.kmeans
+        plan = _PENDING_PLAN.get(km.m0)
+        if plan is None:
+            plan = _PENDING_PLAN[km.m0] = MixingPlan(alphas=np.ones(1), M=np.zeros((km.m0, km.m0)),
+                                                     u0=np.zeros(km.m0), alpha0=1.0, eps_den=0.0, rank=km.m0)
+        d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, np.zeros((km.m0, km.rho)), plan, keep)
+    else:
+        plan = mixing_plan(np.asarray(centroids, np.float64), params.theta, params.eps_drop, S, lite=True,
+                           device_inverse=True)
+        d = _desc(n, inp.rho, H, W, inp.gkind, params.spatial, params.theta, centroids, plan, keep)
+    d.row_lo, d.row_hi = row_origin, row_origin + h_local
     wsb = int(lib.nys_filter_workspace_bytes(C.byref(d)))
     if wsb == 0:
         raise NotImplementedError(f"filter shape n={n} rho={inp.rho} m0={d.m0} R={d.radius} not supported")
     ws = workspace(wsb)
-    s = stream_ptr()
-    _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
+    if inflight is not None:
+        sb = int(lib.nys_filter_plan_staging_bytes(C.byref(d)))
+        inflight.staging = _plan_staging(sb)
+        inflight.keep = [ws, keep]
+        _native.check(lib.nys_filter_plan_async(C.byref(d), km.centroids_ptr(), float(params.eps_drop), PHI_FORM_COND,
+                                                ptr(inflight.staging), sb, ptr(ws), wsb, s), "nys_filter_plan_async")
+        inflight.between()
+        _native.check(lib.nys_filter_prepare_join(C.byref(d), ptr(inflight.staging), ptr(ws), s),
+                      "nys_filter_prepare_join")
+    else:
+        _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, s), "nys_filter_prepare")
     if timer:
         timer.mark("extrapolation")
     rs = int(lib.nys_filter_plane_row_stride(C.byref(d)))   # [row][x/32][plane][32] (+ raw b planes)
@@ -301,6 +350,9 @@ def run_filter(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer:
     _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats), s), "nys_filter_stats")
     del keep
     return out, plan, stats
+
+
+_PENDING_PLAN: dict = {}
 
 
 def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterParams, timer, plane_budget, out,
@@ -435,6 +487,13 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     timer.mark("start")
     inp = _prepare_inputs(f, p)
     timer.mark("upload")
+    if _pipelined_ok(inp, params):
+        rep = _fast_filter_pipelined(f, inp, params, timer, kernel_events, out)
+        if rep is not None:
+            return rep
+        timer = StageTimer()  # the speculation missed (rare): the synchronous path below redoes the step
+        timer.mark("start")
+        timer.mark("upload")
     centroids, qe = _select_landmarks(inp, params)
     timer.mark("clustering")
     timer.mark("eigendecomposition")  # host eig happens inside run_filter's mixing_plan
@@ -456,6 +515,53 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     timings["total"] = sum(t.values())
     return FilterReport(output=_output_image(out, f, given=out_given), timings=timings, retained_rank=plan.rank,
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
+
+
+def _pipelined_ok(inp: _Inputs, params: FilterParams) -> bool:
+    """The whole step can be queued without the host waiting: k-means landmarks, a
+    box / FIR spatial kernel, m0 <= 90 (the in-stream plan's device inverse)."""
+    sk = params.spatial
+    if os.environ.get("NYS_PIPELINED", "1") == "0":  # A/B switch: the synchronous plan
+        return False
+    return (params.landmark_strategy == STRATEGY_KMEANS and params.m0 <= 90
+            and (sk.kind != GAUSSIAN_RECURSIVE or sk.sigma < 1.0))
+
+
+def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: StageTimer, kernel_events,
+                           out) -> FilterReport | None:
+    """fast_filter with the mixing plan computed in-stream (nys_filter_plan_async):
+    k-means, the landmarks' copy to pinned memory, the plan on a side stream
+    overlapping the exact pass, the device inverse, K2 and K3 are all queued
+    before the host waits once, for the statistics.  The plan speculates on the
+    common case (nothing dropped, y-form); None when it missed or k-means++ hit
+    a zero total (the caller then reruns the synchronous path)."""
+    pk = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter, pipelined=True)
+    timer.mark("clustering")
+    timer.mark("eigendecomposition")  # on the host, in-stream (a host function on a side stream)
+    qe_box: list = []
+    n_events = len(kernel_events) if kernel_events is not None else 0
+    fl = _Inflight(kmeans=pk, between=lambda: qe_box.append(exact_assignment_async(inp.points, pk.res, params.m0,
+                                                                                     pk.workspace)))
+    out_given = out
+    out, _, stats = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
+                               inflight=fl)
+    h = torch.cat([stats, qe_box[0]]).cpu()  # the step's only host wait
+    res = fl.result()
+    if res.status != _native.NYS_OK or pk.zero_total_draw() >= 0:
+        if kernel_events is not None:
+            del kernel_events[n_events:]
+        return None
+    timer.mark("normalization")  # fused into K3
+    km = pk.finish(float(h[2]))
+    min_den, guarded = float(h[0]), int(h[1:2].view(torch.int64)[0])
+    t = timer.elapsed()
+    timings = {k: t.get(k, 0.0) for k in ("clustering", "eigendecomposition", "extrapolation", "convolutions",
+                                          "normalization")}
+    timings["upload"] = t.get("upload", 0.0)
+    timings["total"] = sum(t.values())
+    return FilterReport(output=_output_image(out, f, given=out_given), timings=timings, retained_rank=int(res.rank),
+                        quant_error=km.quant_error, min_denominator=min_den, guarded_pixels=guarded,
+                        centroids=km.centroids)
 
 
 def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> FilterReport:

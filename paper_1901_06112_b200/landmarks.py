@@ -90,9 +90,42 @@ def _pinned_f64(n: int, key) -> torch.Tensor:
     return buf[:n]
 
 
+@dataclass
+class PendingKMeans:
+    """k-means whose results are still in flight (``kmeans_device(..., pipelined=True)``):
+    ``host`` is the page-locked buffer the results land in (its first m0 * rho
+    doubles are the centroids, usable by in-stream consumers such as
+    nys_filter_plan_async); ``finish()`` parses it once the stream has passed."""
+    host: torch.Tensor
+    res: torch.Tensor
+    workspace: torch.Tensor
+    m0: int
+    rho: int
+    max_iter: int
+
+    def centroids_ptr(self) -> int:
+        return int(self.host.data_ptr())
+
+    def zero_total_draw(self) -> int:
+        """-1, or the k-means++ draw at which sum(D^2) hit 0 (the caller must redo the
+        clustering with the synchronous path, which replays the reference's picks)."""
+        o = self.m0 * self.rho + self.max_iter + 1
+        return int(self.host[o:o + 4].numpy().view(np.int64)[1])
+
+    def finish(self, quant_error: float | None) -> DeviceKMeans:
+        h = self.host.numpy()
+        m0, rho, mi = self.m0, self.rho, self.max_iter
+        st = h[m0 * rho + mi + 1:m0 * rho + mi + 5].view(np.int64)
+        iters = int(st[0])
+        return DeviceKMeans(centroids=h[:m0 * rho].reshape(m0, rho).copy(), quant_error=quant_error,
+                            errors=tuple(h[m0 * rho:m0 * rho + iters].tolist()), iterations=iters,
+                            seed_indices=h[m0 * rho + mi + 5:].view(np.int64).copy(), assignment=None,
+                            centroids_dev=self.res, workspace=self.workspace)
+
+
 def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER,
                   want_assignment: bool = False, defer_exact: bool = False,
-                  queue_exact: bool = False) -> DeviceKMeans:
+                  queue_exact: bool = False, pipelined: bool = False) -> DeviceKMeans | PendingKMeans:
     """k-means on planar device points ``(rho, m)`` float32 (rows may be any
     plane stride; the last dim must be contiguous).
 
@@ -104,7 +137,10 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     host buffer behind an event, the exact pass is queued right after that copy
     (before the host waits), and only the copy is waited for -- the exact pass
     then runs while the caller works on the centroids, with no host gap in
-    between.  Its pending result is ``DeviceKMeans.quant_error_dev``."""
+    between.  Its pending result is ``DeviceKMeans.quant_error_dev``.
+
+    ``pipelined`` (no assignment, no exact pass): queue the results' copy to a
+    pinned buffer and return a ``PendingKMeans`` without waiting at all."""
     require_cuda()
     if points.dim() != 2 or points.stride(1) != 1:
         raise ValueError("points must be a (rho, m) tensor with contiguous rows")
@@ -133,11 +169,17 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     seeds_p = stats_p + 8 * 4
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     first, uniforms = _seed_stream(m, m0, seed)
-    if (defer_exact or queue_exact) and asg is None:
+    if (defer_exact or queue_exact or pipelined) and asg is None:
         qe_p = None
+    if pipelined and (asg is not None or qe_p is not None):
+        raise ValueError("pipelined k-means returns neither an assignment nor the exact pass")
     _native.check(lib.nys_kmeans_run(ptr(points), ps, m, rho, m0, max_iter, first,
                                      uniforms.ctypes.data, Cd_p, errs_p, stats_p, qe_p,
                                      ptr(asg), seeds_p, ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
+    if pipelined:
+        hbuf = _pinned_f64(nres, ("kmeans-pipelined", torch.cuda.current_stream().cuda_stream))
+        hbuf.copy_(res, non_blocking=True)
+        return PendingKMeans(host=hbuf, res=res, workspace=ws, m0=m0, rho=rho, max_iter=max_iter)
     qe_dev = None
     if queue_exact and qe_p is None:
         hbuf = _pinned_f64(nres, ("kmeans", torch.cuda.current_stream().cuda_stream))

@@ -353,3 +353,71 @@ def test_tcgen05_assignment_labels_equal_fp32_search(rho, monkeypatch):
     b = O.kmeans(pts.astype(np.float64), 24, 1, 8)
     assert abs(a.quant_error - b[2]) <= 1e-6 * b[2]
     np.testing.assert_allclose(a.centroids, b[0], rtol=0, atol=1e-5)
+
+
+@pytest.mark.parametrize("m0,rho,theta", [(64, 3, 0.1), (90, 5, 0.3), (13, 4, 0.2), (8, 3, 0.2), (41, 31, 0.4)])
+def test_device_inverse_from_cholesky_matches_host_M(m0, rho, theta):
+    # nys_filter_desc.M_is_cholesky: the device forms M = L^{-T} L^{-1} (k_inverse_cholesky, blocked
+    # 8-row substitution, n padded to a multiple of 8); the prepared workspace must equal the one
+    # prepared from the host's M up to FP32 rounding of M, everything else bit-identical
+    import ctypes as C
+
+    from paper_1901_06112_b200 import _native
+    from paper_1901_06112_b200._device import ptr, stream_ptr
+    from paper_1901_06112_b200.filters import _desc
+    from paper_1901_06112_b200.nystrom import mixing_plan
+
+    cen = np.random.default_rng(m0 + rho).random((m0, rho))
+    host = mixing_plan(cen, theta, 1e-8, 15)
+    dev = mixing_plan(cen, theta, 1e-8, 15, lite=True, device_inverse=True)
+    assert dev.M_is_cholesky and not host.M_is_cholesky and not host.phi_form
+    lib = _native.lib()
+    wss = []
+    for plan in (host, dev):
+        keep: list = []
+        d = _desc(3, rho, 64, 64, 0, SpatialKernel.gaussian(5.0, 15), theta, cen, plan, keep)
+        wsb = int(lib.nys_filter_workspace_bytes(C.byref(d)))
+        ws = torch.zeros((wsb // 4,), dtype=torch.float32, device="cuda")
+        _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, stream_ptr()), "nys_filter_prepare")
+        stats_floats = (wsb - 256 - (m0 * m0 * 8 + 255) // 256 * 256) // 4
+        wss.append(ws[:stats_floats].cpu().numpy())
+    a, b = wss
+    differ = a != b
+    scale = np.abs(host.M).max()
+    assert np.abs(a[differ] - b[differ]).max(initial=0.0) <= 1e-6 * scale
+    assert differ.sum() <= m0 * m0  # only the M block may differ
+    assert np.isfinite(b).all()
+
+
+@pytest.mark.parametrize("cfg,H", [(2, 96), (3, 64), (4, 48), (1, None)])
+def test_pipelined_plan_equals_synchronous_plan(cfg, H, monkeypatch):
+    # fast_filter queues the whole step (in-stream plan on a side stream, nys_filter_plan_async);
+    # it must give exactly the synchronous path's results
+    from bench import _guide, _params
+
+    wl = CONFIGS[cfg]
+    img = wl.image(seed=1, H=H)
+    params = _params(wl)
+    f = Image(data=torch.from_numpy(img).cuda(), range_max=1.0)
+    p = _guide(f, wl)
+    a = fast_filter(f, p, params)
+    monkeypatch.setenv("NYS_PIPELINED", "0")
+    b = fast_filter(f, p, params)
+    assert torch.equal(a.output.data, b.output.data)
+    assert a.guarded_pixels == b.guarded_pixels and a.retained_rank == b.retained_rank
+    assert a.quant_error == b.quant_error and a.min_denominator == b.min_denominator
+    assert np.array_equal(a.centroids, b.centroids)
+
+
+def test_pipelined_plan_falls_back_when_speculation_misses():
+    # an ill-conditioned landmark kernel (1-D guide): the in-stream plan reports NYS_EUNSUPPORTED
+    # and fast_filter reruns the step with the full plan (phi-form) -- still within 1e-4 of the oracle
+    f32 = np.ascontiguousarray(color_scene(130, 9, 5, 0.05, seed=131)[:1])
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    params = FilterParams(spatial=SpatialKernel.gaussian(2.5, 8), theta=0.35, m0=5, kmeans_max_iter=6)
+    rep = fast_filter(f, f, params)
+    C, _, _, _ = O.kmeans(O.range_vectors(f32.astype(np.float64)), 5, 0, 6)
+    np.testing.assert_allclose(rep.centroids, C, rtol=0, atol=1e-9)
+    ref = O.fast_filter_with_landmarks(f32.astype(np.float64), f32.astype(np.float64), C, 0.35, "gaussian_fir", 2.5, 8)
+    assert np.abs(rep.output.data.double().cpu().numpy() - ref["output"]).max() <= TOL
+    assert rep.retained_rank == ref["retained_rank"]

@@ -224,3 +224,22 @@ def test_lite_mixing_plan_matches_full(k, rho, theta):
     assert b.eps_den == pytest.approx(a.eps_den, rel=1e-14)
     np.testing.assert_allclose(b.M, a.M, rtol=0, atol=1e-12 * np.abs(a.M).max())
     assert min(np.abs(a.u0 - b.u0).max(), np.abs(a.u0 + b.u0).max()) <= 1e-9
+
+
+@pytest.mark.parametrize("k,rho,theta", [(64, 3, 0.1), (48, 31, 0.25), (32, 3, 0.15), (4, 2, 0.5)])
+def test_lite_plan_cholesky_factor(k, rho, theta):
+    # device_inverse=True hands the device the Cholesky factor L of A (A = L L^T) instead of M;
+    # (L^{-1})^T L^{-1} must be the full plan's M, with the same u0 / alpha_1 / rank, and the
+    # lite plan must not defer to the full one for a well-conditioned A
+    from paper_1901_06112_b200.nystrom import mixing_plan
+
+    C = np.random.default_rng(k + rho).random((k, rho))
+    a = mixing_plan(C, theta, 1e-8, 15)
+    b = mixing_plan(C, theta, 1e-8, 15, lite=True, device_inverse=True)
+    assert b.M_is_cholesky and not b.phi_form and b.rank == a.rank == k
+    L = np.tril(b.M)
+    assert np.all(b.M[np.triu_indices(k, 1)] == 0.0)
+    Li = np.linalg.inv(L)
+    np.testing.assert_allclose(Li.T @ Li, a.M, rtol=0, atol=1e-10 * np.abs(a.M).max())
+    assert b.alpha0 == pytest.approx(a.alpha0, rel=1e-14)
+    assert min(np.abs(a.u0 - b.u0).max(), np.abs(a.u0 + b.u0).max()) <= 1e-9

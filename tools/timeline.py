@@ -32,3 +32,14 @@ for e in gpu[half:]:
     gap = (e["ts"] - prev) if prev is not None else 0.0
     print(f"{e['ts']:14.1f} gap {gap:8.1f} us  dur {e.get('dur', 0):8.1f} us  {e['name'][:60]}")
     prev = e["ts"] + e.get("dur", 0)
+
+# the in-stream plan's own duration inside its host function (pipelined fast_filter)
+import ctypes as C  # noqa: E402
+
+from paper_1901_06112_b200 import _native  # noqa: E402
+from paper_1901_06112_b200.filters import _STAGING  # noqa: E402
+
+for nb, buf in _STAGING.items():
+    r = _native.PlanResult()
+    _native.lib().nys_filter_plan_result(buf.data_ptr(), C.byref(r))
+    print(f"in-stream plan: status {r.status} rank {r.rank} host function {r.host_us:.1f} us")

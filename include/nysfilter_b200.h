@@ -178,7 +178,7 @@ typedef struct nys_filter_desc {
     int phi_form;
     /* 1: M holds the lower Cholesky factor L of A (row-major) instead of M;
      * nys_filter_prepare forms M = A^{-1} = L^{-T} L^{-1} on the device in FP64
-     * (y-form, nothing dropped, m0 <= 90).  0: M as above. */
+     * (y-form, nothing dropped, m0 <= 64).  0: M as above. */
     int M_is_cholesky;
 } nys_filter_desc;
 
@@ -225,7 +225,9 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
  * means the plan needs drops or the phi-form -- rerun with nys_filter_prepare
  * and a plan from nys_mixing_plan (the speculative outputs are meaningless).
  * `staging` [pinned, nys_filter_plan_staging_bytes(d), zero-filled once] and
- * `centroids` must stay untouched until then.  m0 <= 90.
+ * `centroids` must stay untouched until then.  For m0 <= 64 the device forms
+ * M from the Cholesky factor (and copies the image itself from the mapped
+ * staging buffer); larger m0 carry M formed on the host.
  */
 typedef struct nys_plan_result {
     int status;      /* NYS_OK, NYS_EUNSUPPORTED (fall back), or an error code */

@@ -29,6 +29,7 @@
 #include <thread>
 
 #include "nys_filter_common.cuh"
+#include "nys_inverse.cuh"
 
 namespace nys {
 
@@ -48,84 +49,6 @@ __global__ void k_patch_guide(const float* __restrict__ f, long long fps, int n,
     const int c = d / (side * side), k = d - c * side * side, dy = k / side - r, dx = k % side - r;
     out[(long long)d * ops + p] =
         __ldg(f + (long long)c * fps + (long long)clampi(y + dy, 0, H - 1) * W + clampi(x + dx, 0, W - 1));
-  }
-}
-
-// M = A^{-1} = L^{-T} L^{-1} from the host's Cholesky factor, FP64, into the FP32
-// [M | u0]^T block (MT[j][i] = M[i][j]); one CTA, n <= 90 (L and X in shared memory)
-// M = A^{-1} = X^T X with X = L^{-1}, A = L L^T (the host's Cholesky factor, FP64).
-// Blocked forward substitution over 8-row blocks keeps the dependent chains short:
-// the diagonal blocks are inverted first (one thread per block column), then block
-// row I of X is R_I = E_I - L[I, <I] X[<I, :] (one thread per element, four
-// accumulators) followed by X[I, :] = L_II^{-1} R_I.  n is padded to np = 8 nb
-// with an identity tail, which leaves the leading n x n block of X unchanged.
-__global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restrict__ Lg, int n, float* __restrict__ MT,
-                                                          int m0q) {
-  extern __shared__ double cs[];
-  const int np = (n + 7) & ~7, nb = np / 8;
-  double* Ls = cs;              // np x np
-  double* X = Ls + np * np;     // np x np, X = L^{-1} (lower)
-  double* Di = X + np * np;     // np x 8: inverse of diagonal block I in rows 8I..8I+7
-  double* R = Di + np * 8;      // 8 x np scratch
-  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
-    const int i = e / np, j = e - i * np;
-    Ls[e] = (i < n && j < n) ? Lg[i * n + j] : (i == j ? 1.0 : 0.0);
-    X[e] = 0.0;
-  }
-  __syncthreads();
-  if ((int)threadIdx.x < np) {  // column c of the inverse of the 8 x 8 diagonal block I
-    const int I = threadIdx.x >> 3, c = threadIdx.x & 7, o = 8 * I;
-    double col[8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      double t = (a == c) ? 1.0 : 0.0;
-#pragma unroll
-      for (int k = 0; k < a; ++k) t = fma(-Ls[(o + a) * np + o + k], col[k], t);
-      col[a] = (a < c) ? 0.0 : t / Ls[(o + a) * np + o + a];
-    }
-#pragma unroll
-    for (int a = 0; a < 8; ++a) Di[(o + a) * 8 + c] = col[a];
-  }
-  __syncthreads();
-  for (int I = 0; I < nb; ++I) {
-    const int o = 8 * I, w = o + 8;  // block row I has nonzeros in columns < w
-    for (int e = threadIdx.x; e < 8 * w; e += blockDim.x) {
-      const int a = e / w, j = e - a * w;
-      const double* lr = Ls + (o + a) * np;
-      double t0 = (o + a == j) ? 1.0 : 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-      int k = j;
-      for (; k + 3 < o; k += 4) {
-        t0 = fma(-lr[k], X[k * np + j], t0);
-        t1 = fma(-lr[k + 1], X[(k + 1) * np + j], t1);
-        t2 = fma(-lr[k + 2], X[(k + 2) * np + j], t2);
-        t3 = fma(-lr[k + 3], X[(k + 3) * np + j], t3);
-      }
-      for (; k < o; ++k) t0 = fma(-lr[k], X[k * np + j], t0);
-      R[a * np + j] = (t0 + t1) + (t2 + t3);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < 8 * w; e += blockDim.x) {
-      const int a = e / w, j = e - a * w;
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) t = fma(Di[(o + a) * 8 + q], R[q * np + j], t);
-      X[(o + a) * np + j] = t;
-    }
-    __syncthreads();
-  }
-  // M[i][j] = sum_{k >= max(i, j)} X[k][i] X[k][j]; four columns per thread
-  const int nq = (n + 3) / 4;
-  for (int e = threadIdx.x; e < n * nq; e += blockDim.x) {
-    const int i = e / nq, j0 = 4 * (e - i * nq);
-    double t[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k = max(i, j0); k < n; ++k) {
-      const double xi = X[k * np + i];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) t[q] = fma(xi, X[k * np + j0 + q], t[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (j0 + q < n) MT[(size_t)(j0 + q) * m0q + i] = (float)t[q];
   }
 }
 
@@ -163,17 +86,24 @@ size_t nys_filter_workspace_bytes(const nys_filter_desc* d) {
 }  // extern "C"
 
 namespace {
-// M = A^{-1} from the Cholesky factor at chol_off_bytes (after the constants land), then the
-// statistics reset
+// M = A^{-1} from the Cholesky factor (m0 <= 64): read at chol_off_bytes of the workspace,
+// or -- img_src non-null -- of the mapped pinned image, which the kernel first copies into
+// the workspace; then the statistics reset
 int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, void* workspace, bool chol,
-                             cudaStream_t s) {
+                             cudaStream_t s, const void* img_src = nullptr) {
   if (chol) {
-    const double* Ld = reinterpret_cast<const double*>((char*)workspace + L.chol_off_bytes);
-    const int np = (d->m0 + 7) & ~7;
-    const size_t smem = (2 * (size_t)np * np + 16 * (size_t)np) * sizeof(double);
-    NYS_CUDA_TRY(cudaFuncSetAttribute(k_inverse_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const char* base = img_src ? static_cast<const char*>(img_src) : static_cast<const char*>(workspace);
+    const double* Ld = reinterpret_cast<const double*>(base + L.chol_off_bytes);
+    static bool attr_set = false;
+    if (!attr_set) {
+      NYS_CUDA_TRY(cudaFuncSetAttribute(k_inverse_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kInvSmemBytes));
+      attr_set = true;
+    }
     count_launch();
-    k_inverse_cholesky<<<1, 1024, smem, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q);
+    k_inverse_cholesky<<<1, 1024, kInvSmemBytes, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q,
+                                                      static_cast<const float4*>(img_src),
+                                                      static_cast<float4*>(workspace), (int)(L.n_floats / 4));
     NYS_LAUNCH_CHECK();
   }
   count_launch();
@@ -216,8 +146,9 @@ void run_plan(PlanJob* j) {
   float* img = reinterpret_cast<float*>(reinterpret_cast<char*>(j) + kStagingHeader);
   std::vector<double> info(n), Lc((size_t)n * n), u0(n);
   int rank = 0;
-  const int rc = nys_mixing_plan_lite(j->centroids, n, rho, j->theta, j->eps_drop, j->phi_cond, 1, info.data(), &rank,
-                                      Lc.data(), u0.data());
+  const bool chol = n <= kInvN;  // else the host forms M and the image carries it
+  const int rc = nys_mixing_plan_lite(j->centroids, n, rho, j->theta, j->eps_drop, j->phi_cond, chol ? 1 : 0,
+                                      info.data(), &rank, Lc.data(), u0.data());
   j->result.status = rc;
   j->result.rank = rc == NYS_OK ? n : 0;
   if (rc == NYS_OK) {
@@ -231,7 +162,11 @@ void run_plan(PlanJob* j) {
     }
     img[L.off_SC] = (float)(1.0 / a1);
     img[L.off_SC + 1] = (float)j->result.eps_den;
-    std::memcpy(reinterpret_cast<char*>(img) + L.chol_off_bytes, Lc.data(), (size_t)n * n * sizeof(double));
+    if (chol)
+      std::memcpy(reinterpret_cast<char*>(img) + L.chol_off_bytes, Lc.data(), (size_t)n * n * sizeof(double));
+    else
+      for (int q = 0; q < n; ++q)
+        for (int i = 0; i < n; ++i) img[L.off_MT + (size_t)q * L.m0q + i] = (float)Lc[(size_t)i * n + q];
   }
   j->result.host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -327,7 +262,7 @@ size_t plan_image_bytes(const FilterLayout& L, int m0) { return L.chol_off_bytes
 extern "C" {
 
 size_t nys_filter_plan_staging_bytes(const nys_filter_desc* d) {
-  if (validate(d) != NYS_OK || d->m0 > 90) return 0;
+  if (validate(d) != NYS_OK) return 0;
   return kStagingHeader + plan_image_bytes(filter_layout(d), d->m0);
 }
 
@@ -336,7 +271,7 @@ int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, dou
                           void* stream) {
   int st = validate(d);
   if (st) return st;
-  if (!centroids || !staging || !workspace || d->m0 > 90 || !(phi_cond > 1.0)) return NYS_EINVAL;
+  if (!centroids || !staging || !workspace || !(phi_cond > 1.0)) return NYS_EINVAL;
   const FilterLayout L = filter_layout(d);
   if (staging_bytes < kStagingHeader + plan_image_bytes(L, d->m0) || workspace_bytes < L.total_bytes)
     return NYS_EINVAL;
@@ -378,9 +313,12 @@ int nys_filter_prepare_join(const nys_filter_desc* d, void* staging, void* works
   const CUdeviceptr gate = reinterpret_cast<CUdeviceptr>(dv) + offsetof(PlanJob, done);
   if (wait_value_fn()(reinterpret_cast<CUstream>(s), gate, j->seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
     return NYS_ECUDA;
-  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, static_cast<const char*>(staging) + kStagingHeader, j->image_bytes,
+  const FilterLayout L = filter_layout(d);
+  const char* img = static_cast<const char*>(dv) + kStagingHeader;
+  if (d->m0 <= kInvN) return launch_inverse_and_reset(d, L, workspace, true, s, img);  // copies the image itself
+  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, static_cast<const char*>(staging) + kStagingHeader, L.n_floats * sizeof(float),
                                cudaMemcpyHostToDevice, s));
-  return launch_inverse_and_reset(d, filter_layout(d), workspace, true, s);
+  return launch_inverse_and_reset(d, L, workspace, false, s);
 }
 
 int nys_filter_plan_result(const void* staging, nys_plan_result* out) {
@@ -402,7 +340,7 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
   for (int j = 0; j < d->m0; ++j)
     for (int k = 0; k < d->rho; ++k) h[L.off_C + (size_t)j * L.rhop + k] = (float)d->centroids[(size_t)j * d->rho + k];
   const bool chol = d->M_is_cholesky != 0;
-  if (chol && (d->phi_form || d->m0 > 90)) return NYS_EINVAL;
+  if (chol && (d->phi_form || d->m0 > kInvN)) return NYS_EINVAL;
   for (int j = 0; j < d->m0; ++j) {
     if (!chol)
       for (int i = 0; i < d->m0; ++i) h[L.off_MT + (size_t)j * L.m0q + i] = (float)d->M[(size_t)i * d->m0 + j];

@@ -519,12 +519,11 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
 
 def _pipelined_ok(inp: _Inputs, params: FilterParams) -> bool:
     """The whole step can be queued without the host waiting: k-means landmarks, a
-    box / FIR spatial kernel, m0 <= 90 (the in-stream plan's device inverse)."""
+    box / FIR spatial kernel."""
     sk = params.spatial
     if os.environ.get("NYS_PIPELINED", "1") == "0":  # A/B switch: the synchronous plan
         return False
-    return (params.landmark_strategy == STRATEGY_KMEANS and params.m0 <= 90
-            and (sk.kind != GAUSSIAN_RECURSIVE or sk.sigma < 1.0))
+    return params.landmark_strategy == STRATEGY_KMEANS and (sk.kind != GAUSSIAN_RECURSIVE or sk.sigma < 1.0)
 
 
 def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: StageTimer, kernel_events,

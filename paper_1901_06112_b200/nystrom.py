@@ -156,7 +156,7 @@ def mixing_plan(centroids: np.ndarray, theta: float, eps_drop: float, S: int, li
     rank = C.c_int(0)
     if lite:
         # hot path: alpha_1 + two Sturm counts (nothing dropped, cond <= PHI_FORM_COND), else the full plan
-        chol = bool(device_inverse and k <= 90)  # M = A^{-1} formed on the device from the Cholesky factor
+        chol = bool(device_inverse and k <= 64)  # M = A^{-1} formed on the device from the Cholesky factor
         rc = _native.lib().nys_mixing_plan_lite(C_.ctypes.data, k, rho, float(theta), float(eps_drop), PHI_FORM_COND,
                                                 int(chol), alphas.ctypes.data, C.byref(rank), M.ctypes.data,
                                                 u0.ctypes.data)

@@ -7,20 +7,30 @@ import numpy as np
 import torch
 
 
+_CUDA_OK = False
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("the Nystrom B200 path needs a CUDA device (there is no CPU fallback)")
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("the Nystrom B200 path needs a CUDA device (there is no CPU fallback)")
+        _CUDA_OK = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
 def stream_ptr() -> int:
-    return int(torch.cuda.current_stream().cuda_stream)
+    """cudaStream_t of the current stream (the raw query skips building a Stream object:
+    this sits on the per-call critical path before the first launch)."""
+    return int(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
 
 
 def to_device_f32(x) -> torch.Tensor:
     """Planar float32 contiguous CUDA tensor from numpy or torch input."""
     dev = require_cuda()
     if isinstance(x, torch.Tensor):
+        if x.is_cuda and x.dtype == torch.float32 and x.device == dev and x.is_contiguous():
+            return x
         if not x.is_cuda and x.dtype == torch.float32 and x.is_pinned():
             return x.to(device=dev, non_blocking=True).contiguous()
         return x.to(device=dev, dtype=torch.float32).contiguous()
@@ -48,6 +58,11 @@ class StageTimer:
         ev.record()
         self.events.append((name, ev))
 
+    def lazy(self, fill) -> "LazyTimings":
+        """FilterReport.timings resolved on first read (the event queries cost ~50 us,
+        which would otherwise sit inside every call after its last kernel)."""
+        return LazyTimings(self, fill)
+
     def elapsed(self) -> dict[str, float]:
         if not self.events:
             return {}
@@ -56,3 +71,60 @@ class StageTimer:
         for (_, a), (name, b) in zip(self.events, self.events[1:]):
             out[name] = a.elapsed_time(b) / 1e3
         return out
+
+
+class LazyTimings(dict):
+    """A dict of stage seconds computed from a StageTimer on first access."""
+
+    def __init__(self, timer: StageTimer, fill):
+        super().__init__()
+        self._timer, self._fill = timer, fill
+
+    def _resolve(self):
+        if self._timer is not None:
+            t, self._timer = self._timer, None
+            dict.update(self, self._fill(t.elapsed()))
+
+    def __getitem__(self, k):
+        self._resolve()
+        return dict.__getitem__(self, k)
+
+    def __iter__(self):
+        self._resolve()
+        return dict.__iter__(self)
+
+    def __len__(self):
+        self._resolve()
+        return dict.__len__(self)
+
+    def __contains__(self, k):
+        self._resolve()
+        return dict.__contains__(self, k)
+
+    def __repr__(self):
+        self._resolve()
+        return dict.__repr__(self)
+
+    def __eq__(self, other):
+        self._resolve()
+        return dict.__eq__(self, other)
+
+    def get(self, k, default=None):
+        self._resolve()
+        return dict.get(self, k, default)
+
+    def keys(self):
+        self._resolve()
+        return dict.keys(self)
+
+    def values(self):
+        self._resolve()
+        return dict.values(self)
+
+    def items(self):
+        self._resolve()
+        return dict.items(self)
+
+    def copy(self):
+        self._resolve()
+        return dict(self)

@@ -544,23 +544,26 @@ def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: 
     out_given = out
     out, _, stats = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
                                inflight=fl)
-    h = torch.cat([stats, qe_box[0]]).cpu()  # the step's only host wait
+    timer.mark("normalization")  # fused into K3; stamped before the wait so elapsed() needs no further sync
+    h = torch.cat([stats, qe_box[0]]).cpu().numpy()  # the step's only host wait
     res = fl.result()
     if res.status != _native.NYS_OK or pk.zero_total_draw() >= 0:
         if kernel_events is not None:
             del kernel_events[n_events:]
         return None
-    timer.mark("normalization")  # fused into K3
-    km = pk.finish(float(h[2]))
-    min_den, guarded = float(h[0]), int(h[1:2].view(torch.int64)[0])
-    t = timer.elapsed()
+    m0, rho = params.m0, pk.rho
+    centroids = pk.host[:m0 * rho].numpy().reshape(m0, rho).copy()
+    return FilterReport(output=_output_image(out, f, given=out_given), timings=timer.lazy(_report_timings),
+                        retained_rank=int(res.rank), quant_error=float(h[2]), min_denominator=float(h[0]),
+                        guarded_pixels=int(h[1:2].view(np.int64)[0]), centroids=centroids)
+
+
+def _report_timings(t: dict) -> dict:
     timings = {k: t.get(k, 0.0) for k in ("clustering", "eigendecomposition", "extrapolation", "convolutions",
                                           "normalization")}
     timings["upload"] = t.get("upload", 0.0)
     timings["total"] = sum(t.values())
-    return FilterReport(output=_output_image(out, f, given=out_given), timings=timings, retained_rank=int(res.rank),
-                        quant_error=km.quant_error, min_denominator=min_den, guarded_pixels=guarded,
-                        centroids=km.centroids)
+    return timings
 
 
 def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> FilterReport:

@@ -94,11 +94,14 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
   if (chol) {
     const char* base = img_src ? static_cast<const char*>(img_src) : static_cast<const char*>(workspace);
     const double* Ld = reinterpret_cast<const double*>(base + L.chol_off_bytes);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_set{0};  // one bit per device
+    int dev = 0;
+    NYS_CUDA_TRY(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set.load() & bit)) {
       NYS_CUDA_TRY(cudaFuncSetAttribute(k_inverse_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kInvSmemBytes));
-      attr_set = true;
+      attr_set.fetch_or(bit);
     }
     count_launch();
     k_inverse_cholesky<<<1, 1024, kInvSmemBytes, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q,

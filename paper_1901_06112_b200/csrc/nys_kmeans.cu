@@ -419,6 +419,37 @@ __global__ void k_init_state(KState* st, long long* seed_idx, long long first, d
   if (seed_idx) seed_idx[0] = first;
 }
 
+// everything the seeding needs before its first draw, in one launch: state reset, first
+// pick, first centroid, the owner flag and the host's uniforms (passed by value, so no
+// pageable host->device copy sits between the launches)
+struct SeedPrologue {
+  KState* st;
+  long long* seeds;
+  long long first;
+  double* C;
+  const float* pts;
+  long long ps;
+  int rho, m0;
+  int* flag;
+  double* unif_dst;
+  double unif[NYS_MAX_M0];
+};
+__global__ void k_seed_prologue(const SeedPrologue p) {
+  const int t = threadIdx.x;
+  if (t == 0) {
+    p.st->converged = 0;
+    p.st->iters = 0;
+    p.st->n_empty = 0;
+    p.st->zero_draw = -1;
+    p.st->changed = 0;
+    p.st->repairs = 0;
+    if (p.seeds) p.seeds[0] = p.first;
+    *p.flag = 0;
+  }
+  for (int d = t; d < p.rho; d += blockDim.x) p.C[d] = (double)p.pts[d * p.ps + p.first];
+  for (int k = t; k < p.m0 - 1; k += blockDim.x) p.unif_dst[k] = p.unif[k];
+}
+
 __global__ void k_c_to_f(const double* __restrict__ C, float* __restrict__ Cf, int n) {
   for (int k = threadIdx.x; k < n; k += blockDim.x) Cf[k] = (float)C[k];
 }
@@ -595,11 +626,24 @@ int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho
   double* d2 = reinterpret_cast<double*>(ws + L.off_d2);
   double* ppart = reinterpret_cast<double*>(ws + L.off_ppart);
   long long* seeds = reinterpret_cast<long long*>(seed_indices_out);
-  count_launch(); k_init_state<<<1, 1, 0, s>>>(st, seeds, first_index, centroids_out, rho, m0);
-  count_launch(); k_gather<<<1, 64, 0, s>>>(points, plane_stride, rho, nullptr, first_index, centroids_out);
-  NYS_LAUNCH_CHECK();
   double* unif = reinterpret_cast<double*>(ws + L.off_unif);
-  if (m0 > 1) NYS_CUDA_TRY(cudaMemcpyAsync(unif, uniforms, (size_t)(m0 - 1) * sizeof(double), cudaMemcpyHostToDevice, s));
+  {
+    SeedPrologue p;
+    p.st = st;
+    p.seeds = seeds;
+    p.first = first_index;
+    p.C = centroids_out;
+    p.pts = points;
+    p.ps = plane_stride;
+    p.rho = rho;
+    p.m0 = m0;
+    p.flag = seed_flag(ws, L);
+    p.unif_dst = unif;
+    for (int k = 0; k < m0 - 1; ++k) p.unif[k] = uniforms[k];
+    count_launch();
+    k_seed_prologue<<<1, 64, 0, s>>>(p);
+    NYS_LAUNCH_CHECK();
+  }
   rc = launch_seed_coop(points, plane_stride, m, rho, m0, unif, centroids_out, seeds, ws, L, s);
   if (rc != NYS_OK && rc != NYS_EUNSUPPORTED) return rc;
   if (rc == NYS_EUNSUPPORTED) {  // step-wise fallback: two launches per draw

@@ -808,10 +808,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
 int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m0, const double* uniforms_dev,
                      double* C, long long* seeds, char* ws, const KLayout& L, cudaStream_t s) {
   if (m0 < 2) return NYS_OK;
-  int dev = 0, coop = 0;
-  NYS_CUDA_TRY(cudaGetDevice(&dev));
-  NYS_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-  if (!coop) return NYS_EUNSUPPORTED;
+  if (!coop_supported()) return NYS_EUNSUPPORTED;
   SeedArgs a;
   a.pts = pts;
   a.ps = ps;
@@ -824,8 +821,7 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
   a.d2 = reinterpret_cast<double*>(ws + L.off_d2);
   a.ppart = reinterpret_cast<double*>(ws + L.off_ppart);
   a.st = reinterpret_cast<KState*>(ws + L.off_state);
-  a.flag = reinterpret_cast<int*>(ws + L.off_idx + 32);
-  NYS_CUDA_TRY(cudaMemsetAsync(a.flag, 0, sizeof(int), s));
+  a.flag = seed_flag(ws, L);  // zeroed by k_seed_prologue
   void* args[] = {&a};
   const char* v1 = getenv("NYS_SEED_V1");
   const bool runs = !(v1 && atoi(v1));
@@ -851,9 +847,8 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
       if (!a.d2_in_smem) smem = 0;
       kern = (void*)kern_v1;
     }
-    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
     int per_sm = 0;
-    NYS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, smem));
+    NYS_CUDA_TRY(coop_blocks_per_sm(kern, 512, smem, &per_sm));
     if (per_sm < 1) return NYS_EUNSUPPORTED;
     count_launch();
     NYS_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(512), args, smem, s));
@@ -881,10 +876,7 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
 
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
                       double* errors, char* ws, const KLayout& L, cudaStream_t s) {
-  int dev = 0, coop = 0;
-  NYS_CUDA_TRY(cudaGetDevice(&dev));
-  NYS_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-  if (!coop) return NYS_EUNSUPPORTED;
+  if (!coop_supported()) return NYS_EUNSUPPORTED;
   const int msl = m0 * rho;
   const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
                        2 * (size_t)((m0 + 3) & ~3) * ((rho + 3) & ~3) * 4 + 96;
@@ -923,8 +915,7 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   void* args[] = {&a};
   auto go = [&](auto kern) -> int {
     int per_sm = 0;
-    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NYS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
+    NYS_CUDA_TRY(coop_blocks_per_sm((const void*)kern, nw * 32, smem, &per_sm));
     if (per_sm < 1) return NYS_EUNSUPPORTED;
     const int nb = (int)std::max<long long>(
         1, std::min<long long>({(long long)per_sm * sms(), (long long)L.nb_coop, ceil_div(m, (long long)nw * 64)}));

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <algorithm>
+#include <mutex>
+#include <vector>
 
 #include "nys_common.cuh"
 
@@ -65,6 +67,67 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.off_pp = o;      o = align256(o + (size_t)L.m_pad * rho * 4);
   L.total = o;
   return L;
+}
+
+// owner flag of the cooperative seeding (zeroed by k_seed_prologue)
+inline int* seed_flag(char* ws, const KLayout& L) { return reinterpret_cast<int*>(ws + L.off_idx + 32); }
+
+// cached per process: these queries sat on the host path before the first seeding draw
+inline bool coop_supported() {
+  static int cached = -1;
+  if (cached < 0) {
+    int dev = 0, coop = 0;
+    cached = (cudaGetDevice(&dev) == cudaSuccess &&
+              cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && coop)
+                 ? 1
+                 : 0;
+  }
+  return cached == 1;
+}
+
+// raises the kernel's dynamic shared-memory limit and returns its resident blocks per SM,
+// once per (kernel, threads, smem)
+inline cudaError_t coop_blocks_per_sm(const void* kern, int threads, size_t smem, int* per_sm) {
+  struct Entry {
+    const void* k;
+    int dev;
+    int threads;
+    size_t smem;
+    int per_sm;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  struct Limit {
+    const void* k;
+    int dev;
+    size_t bytes;  // the kernel's raised limit only ever grows
+  };
+  static std::vector<Limit> limit;
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  std::lock_guard<std::mutex> g(mu);
+  for (const Entry& e : cache)
+    if (e.k == kern && e.dev == dev && e.threads == threads && e.smem == smem) {
+      *per_sm = e.per_sm;
+      return cudaSuccess;
+    }
+  size_t* cur = nullptr;
+  for (auto& l : limit)
+    if (l.k == kern && l.dev == dev) cur = &l.bytes;
+  if (!cur) {
+    limit.push_back(Limit{kern, dev, 0});
+    cur = &limit.back().bytes;
+  }
+  if (std::max<size_t>(smem, 1) > *cur) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
+    if (err != cudaSuccess) return err;
+    *cur = std::max<size_t>(smem, 1);
+  }
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem);
+  if (err != cudaSuccess) return err;
+  cache.push_back(Entry{kern, dev, threads, smem, *per_sm});
+  return cudaSuccess;
 }
 
 // numpy's row reduction order for ((x - c)**2).sum(axis=1) over rho entries

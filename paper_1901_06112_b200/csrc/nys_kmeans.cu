@@ -339,8 +339,19 @@ __global__ void __launch_bounds__(1024) k_repair(const float* __restrict__ pts, 
   }
 }
 
-// final exact assignment (landmarks.py:121-129): FP64 differenced distances in
-// numpy's summation order; the point is loaded once into registers
+// Final exact assignment (landmarks.py:121-129): FP64 differenced distances in
+// numpy's summation order; the point is loaded once into registers.
+// Exact (FP64 differenced) nearest centroid per point, as the reference's final
+// assignment.  An FP32 pass first bounds every distance: with F_j the FP32
+// distance to the FP32-rounded centroid and E_j the FP64 value,
+//   |F_j - E_j| <= (rho+2) 2^-23 F_j + 2^-24 (F_j + |c_j|^2) + O(2^-48)
+// (operand rounding of c_j, FP32 products and sums), so
+//   delta_j = (rho+3) 2^-20 F_j + 2^-20 |c_j|^2 + 2^-60
+// over-covers it by 8x (the FP32 rounding of the bounds themselves included).
+// The FP64 argmin j* satisfies F_j* - delta_j* <= E_j* <= E_k <= F_k + delta_k
+// for every k, so only centroids with F_j - delta_j <= min_k (F_k + delta_k)
+// can be it (ties included); FP64 is evaluated for those alone, in ascending j
+// with a strict <, which returns exactly the brute-force FP64 label and value.
 template <int GR, int RX>
 __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, long long ps, long long m, int rho,
                                                const double* __restrict__ C, int m0, long long* __restrict__ asg,
@@ -348,8 +359,21 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
   extern __shared__ __align__(16) double csm[];
   __shared__ double sh[32];
   if (RX > 0) rho = RX;  // compile-time rho for the common small dimensions
+  const int rhop = (rho + 3) & ~3;
+  float* cf = reinterpret_cast<float*>(csm + (((size_t)m0 * rho + 1) & ~size_t(1)));  // m0 x rhop FP32, 16 B aligned
+  float* cn = cf + (size_t)m0 * rhop;                            // 2^-20 |c_j|^2 + 2^-60
   for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) csm[k] = C[k];
+  for (int k = threadIdx.x; k < m0 * rhop; k += blockDim.x) {
+    const int j = k / rhop, d = k - j * rhop;
+    cf[k] = d < rho ? (float)C[(size_t)j * rho + d] : 0.f;
+  }
+  for (int j = threadIdx.x; j < m0; j += blockDim.x) {
+    double t = 0.0;
+    for (int d = 0; d < rho; ++d) t += C[(size_t)j * rho + d] * C[(size_t)j * rho + d];
+    cn[j] = __double2float_ru(ldexp(t * (1.0 + 1e-12), -20) + 0x1p-60);
+  }
   __syncthreads();
+  const float rel = (float)(rho + 3) * 0x1p-20f;
   const long long chunk = ceil_div(m, (long long)gridDim.x);
   const long long lo = min(m, blockIdx.x * chunk), hi = min(m, lo + chunk);
   double s = 0.0;
@@ -357,13 +381,38 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
     float x[GR];
 #pragma unroll
     for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(pts + d * ps + i) : 0.f;
+    auto f32 = [&](int j) {
+      const float* c = cf + (size_t)j * rhop;
+      float acc = 0.f;
+#pragma unroll
+      for (int d4 = 0; d4 < (GR + 3) / 4; ++d4) {
+        if (4 * d4 < rho) {
+          const float4 c4 = reinterpret_cast<const float4*>(c)[d4];
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * d4 + e < GR && 4 * d4 + e < rho) {
+              const float t = x[4 * d4 + e] - cc[e];
+              acc = fmaf(t, t, acc);
+            }
+        }
+      }
+      return acc;
+    };
+    // the filter pays off once an FP64 distance costs several FP32 ones (wide guides)
+    constexpr bool kFilter = GR >= 16;
+    float U = INFINITY;
+    if (kFilter)
+      for (int j = 0; j < m0; ++j) U = fminf(U, fmaf(f32(j), 1.f + rel, cn[j]));
     double best = INFINITY;
     int arg = 0;
     for (int j = 0; j < m0; ++j) {
-      const double v = d2_exact_regs<GR>(x, rho, csm + (size_t)j * rho);
-      if (v < best) {
-        best = v;
-        arg = j;
+      if (!kFilter || fmaf(f32(j), 1.f - rel, -cn[j]) <= U) {
+        const double v = d2_exact_regs<GR>(x, rho, csm + (size_t)j * rho);
+        if (v < best) {
+          best = v;
+          arg = j;
+        }
       }
     }
     if (asg) asg[i] = arg;
@@ -375,7 +424,7 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
 
 static int launch_exact(const float* pts, long long ps, long long m, int rho, const double* C, int m0, long long* asg,
                         double* part, int nb, cudaStream_t s) {
-  const size_t smem = (size_t)m0 * rho * 8;
+  const size_t smem = (((size_t)m0 * rho + 1) & ~size_t(1)) * 8 + (size_t)m0 * ((rho + 3) & ~3) * 4 + (size_t)m0 * 4;
   auto go = [&](auto kern) -> int {
     if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     count_launch();

@@ -421,3 +421,27 @@ def test_pipelined_plan_falls_back_when_speculation_misses():
     ref = O.fast_filter_with_landmarks(f32.astype(np.float64), f32.astype(np.float64), C, 0.35, "gaussian_fir", 2.5, 8)
     assert np.abs(rep.output.data.double().cpu().numpy() - ref["output"]).max() <= TOL
     assert rep.retained_rank == ref["retained_rank"]
+
+
+@pytest.mark.parametrize("rho,m0", [(1, 5), (3, 64), (16, 48), (27, 64), (31, 40)])
+def test_exact_assignment_filter_equals_fp64_brute_force(rho, m0):
+    # k_exact evaluates FP64 only for the centroids its FP32 error bound cannot exclude; labels
+    # (first index on ties) and the FP64 minima must equal numpy's brute force, including exact
+    # ties (duplicated centroids, points on bisectors) and ~1e-12 near-ties
+    from paper_1901_06112_b200.landmarks import exact_assignment
+
+    rng = np.random.default_rng(rho * 100 + m0)
+    C = rng.random((m0, rho))
+    C[m0 // 2] = C[1]                                  # duplicate centroid: exact ties for its points
+    P = rng.random((6000, rho)).astype(np.float32).astype(np.float64)
+    P[:200] = ((C[0] + C[2]) / 2).astype(np.float32)   # on (close to) the bisector of 0 and 2
+    P[200:400] = C[1].astype(np.float32)               # nearest is the duplicated pair
+    C[3] = C[4] + 1e-12                                # near-tie pair
+    P[400:600] = C[4].astype(np.float32)
+    d2 = ((P[:, None, :] - C[None, :, :]) ** 2).sum(axis=2)
+    ref_lab = np.argmin(d2, axis=1)
+    ref_qe = float(np.min(d2, axis=1).sum())
+    pts = torch.from_numpy(np.ascontiguousarray(P.T.astype(np.float32))).cuda()
+    asg, qe = exact_assignment(pts, C)
+    np.testing.assert_array_equal(asg.cpu().numpy(), ref_lab)
+    assert qe == pytest.approx(ref_qe, rel=1e-12)

@@ -7,19 +7,20 @@ from pathlib import Path
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from bench import _params  # noqa: E402
+from bench import _guide, _params  # noqa: E402
 from paper_1901_06112_b200 import Image, fast_filter  # noqa: E402
 from paper_1901_06112_b200.synthetic import CONFIGS  # noqa: E402
 
 wl = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 f = Image(data=torch.from_numpy(wl.image(seed=0)).cuda(), range_max=1.0)
+g = _guide(f, wl)
 params = _params(wl)
 for _ in range(3):
-    fast_filter(f, f, params)
+    fast_filter(f, g, params)
 torch.cuda.synchronize()
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as prof:
     for _ in range(2):
-        fast_filter(f, f, params)
+        fast_filter(f, g, params)
     torch.cuda.synchronize()
 prof.export_chrome_trace("gpurun_out/timeline.json")
 ev = json.load(open("gpurun_out/timeline.json"))["traceEvents"]

@@ -340,18 +340,18 @@ __global__ void __launch_bounds__(1024) k_repair(const float* __restrict__ pts, 
 }
 
 // Final exact assignment (landmarks.py:121-129): FP64 differenced distances in
-// numpy's summation order; the point is loaded once into registers.
-// Exact (FP64 differenced) nearest centroid per point, as the reference's final
-// assignment.  An FP32 pass first bounds every distance: with F_j the FP32
-// distance to the FP32-rounded centroid and E_j the FP64 value,
-//   |F_j - E_j| <= (rho+2) 2^-23 F_j + 2^-24 (F_j + |c_j|^2) + O(2^-48)
-// (operand rounding of c_j, FP32 products and sums), so
-//   delta_j = (rho+3) 2^-20 F_j + 2^-20 |c_j|^2 + 2^-60
+// numpy's summation order, evaluated only where an FP32 bound cannot rule the
+// centroid out.  With G_j = |c_j|^2 - 2 x.c~_j (FP32, c~ the FP32-rounded
+// centroid, one FFMA per dimension) and F_j = G_j + |x|^2, the FP64 value E_j obeys
+//   |F_j - E_j| <= (2 rho + 8) 2^-24 (|x|^2 + |c_j|^2)
+// (operand rounding of c_j, FP32 products and sums, cancellation included), so
+//   delta_j = A + B_j,  A = r |x|^2 + 2^-60,  B_j = r |c_j|^2,  r = (rho + 4) 2^-20
 // over-covers it by 8x (the FP32 rounding of the bounds themselves included).
-// The FP64 argmin j* satisfies F_j* - delta_j* <= E_j* <= E_k <= F_k + delta_k
-// for every k, so only centroids with F_j - delta_j <= min_k (F_k + delta_k)
-// can be it (ties included); FP64 is evaluated for those alone, in ascending j
-// with a strict <, which returns exactly the brute-force FP64 label and value.
+// The FP64 argmin j* satisfies F_j* - delta_j* <= E_j* <= E_k <= F_k + delta_k,
+// so only centroids with G_j - B_j <= min_k (G_k + B_k) + 2A can be it (ties
+// included); FP64 runs for those alone, in ascending j with a strict <, which
+// returns exactly the brute-force FP64 label and value.  (G_j +- B_j are rounded
+// once more in FP32; the 8x slack covers it.)
 template <int GR, int RX>
 __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, long long ps, long long m, int rho,
                                                const double* __restrict__ C, int m0, long long* __restrict__ asg,
@@ -360,30 +360,36 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
   __shared__ double sh[32];
   if (RX > 0) rho = RX;  // compile-time rho for the common small dimensions
   const int rhop = (rho + 3) & ~3;
-  float* cf = reinterpret_cast<float*>(csm + (((size_t)m0 * rho + 1) & ~size_t(1)));  // m0 x rhop FP32, 16 B aligned
-  float* cn = cf + (size_t)m0 * rhop;                            // 2^-20 |c_j|^2 + 2^-60
+  float* cf = reinterpret_cast<float*>(csm + (((size_t)m0 * rho + 1) & ~size_t(1)));  // m0 x rhop: -2 c~ (exact), 16 B aligned
+  float* cn = cf + (size_t)m0 * rhop;  // |c_j|^2: start of the chain
+  float* cb = cn + m0;                 // B_j = r |c_j|^2
+  const double r = (double)(rho + 4) * 0x1p-20;
   for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) csm[k] = C[k];
   for (int k = threadIdx.x; k < m0 * rhop; k += blockDim.x) {
     const int j = k / rhop, d = k - j * rhop;
-    cf[k] = d < rho ? (float)C[(size_t)j * rho + d] : 0.f;
+    cf[k] = d < rho ? -2.f * (float)C[(size_t)j * rho + d] : 0.f;
   }
   for (int j = threadIdx.x; j < m0; j += blockDim.x) {
     double t = 0.0;
     for (int d = 0; d < rho; ++d) t += C[(size_t)j * rho + d] * C[(size_t)j * rho + d];
-    cn[j] = __double2float_ru(ldexp(t * (1.0 + 1e-12), -20) + 0x1p-60);
+    cn[j] = (float)t;
+    cb[j] = __double2float_ru(r * t);
   }
   __syncthreads();
-  const float rel = (float)(rho + 3) * 0x1p-20f;
   const long long chunk = ceil_div(m, (long long)gridDim.x);
   const long long lo = min(m, blockIdx.x * chunk), hi = min(m, lo + chunk);
   double s = 0.0;
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     float x[GR];
+    float xn = 0.f;
 #pragma unroll
-    for (int d = 0; d < GR; ++d) x[d] = d < rho ? __ldg(pts + d * ps + i) : 0.f;
-    auto f32 = [&](int j) {
+    for (int d = 0; d < GR; ++d) {
+      x[d] = d < rho ? __ldg(pts + d * ps + i) : 0.f;
+      xn = fmaf(x[d], x[d], xn);
+    }
+    auto chain = [&](int j, float start) {  // start - 2 x.c~_j
       const float* c = cf + (size_t)j * rhop;
-      float acc = 0.f;
+      float acc = start;
 #pragma unroll
       for (int d4 = 0; d4 < (GR + 3) / 4; ++d4) {
         if (4 * d4 < rho) {
@@ -391,27 +397,43 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
           const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (4 * d4 + e < GR && 4 * d4 + e < rho) {
-              const float t = x[4 * d4 + e] - cc[e];
-              acc = fmaf(t, t, acc);
-            }
+            if (4 * d4 + e < GR && 4 * d4 + e < rho) acc = fmaf(x[4 * d4 + e], cc[e], acc);
         }
       }
       return acc;
     };
-    // the filter pays off once an FP64 distance costs several FP32 ones (wide guides)
-    constexpr bool kFilter = GR >= 16;
-    float U = INFINITY;
-    if (kFilter)
-      for (int j = 0; j < m0; ++j) U = fminf(U, fmaf(f32(j), 1.f + rel, cn[j]));
+    // one pass: U = min (G_k + B_k) and the two smallest G_j - B_j; when the second of
+    // those exceeds U + 2A only the first centroid can be the FP64 argmin
+    float U = INFINITY, L1 = INFINITY, L2 = INFINITY;
+    int j1 = 0;
+    for (int j = 0; j < m0; ++j) {
+      const float g = chain(j, cn[j]), b = cb[j];
+      U = fminf(U, g + b);
+      const float lb = g - b;
+      if (lb < L1) {
+        L2 = L1;
+        L1 = lb;
+        j1 = j;
+      } else {
+        L2 = fminf(L2, lb);
+      }
+    }
+    const float thr = U + (float)(2.0 * (r * (double)xn + 0x1p-60));
     double best = INFINITY;
     int arg = 0;
-    for (int j = 0; j < m0; ++j) {
-      if (!kFilter || fmaf(f32(j), 1.f - rel, -cn[j]) <= U) {
-        const double v = d2_exact_regs<GR>(x, rho, csm + (size_t)j * rho);
-        if (v < best) {
-          best = v;
-          arg = j;
+    if (!(L2 <= thr)) {
+      if (L1 <= thr) {
+        best = d2_exact_regs<GR>(x, rho, csm + (size_t)j1 * rho);
+        arg = j1;
+      }
+    } else {
+      for (int j = 0; j < m0; ++j) {
+        if (chain(j, cn[j]) - cb[j] <= thr) {
+          const double v = d2_exact_regs<GR>(x, rho, csm + (size_t)j * rho);
+          if (v < best) {
+            best = v;
+            arg = j;
+          }
         }
       }
     }
@@ -423,10 +445,15 @@ __global__ void __launch_bounds__(256) k_exact(const float* __restrict__ pts, lo
 }
 
 static int launch_exact(const float* pts, long long ps, long long m, int rho, const double* C, int m0, long long* asg,
-                        double* part, int nb, cudaStream_t s) {
-  const size_t smem = (((size_t)m0 * rho + 1) & ~size_t(1)) * 8 + (size_t)m0 * ((rho + 3) & ~3) * 4 + (size_t)m0 * 4;
+                        double* part, int max_nb, int* nb_out, cudaStream_t s) {
+  const size_t smem = (((size_t)m0 * rho + 1) & ~size_t(1)) * 8 + (size_t)m0 * ((rho + 3) & ~3) * 4 + (size_t)m0 * 8;
   auto go = [&](auto kern) -> int {
-    if (smem > 48 * 1024) NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // latency-bound loops: as many resident warps as the registers allow
+    int per_sm = 0;
+    NYS_CUDA_TRY(coop_blocks_per_sm((const void*)kern, 256, smem, &per_sm));
+    const int nb = (int)std::max<long long>(
+        1, std::min<long long>({ceil_div(m, 256LL), (long long)std::max(per_sm, 1) * sms(), (long long)max_nb}));
+    *nb_out = nb;
     count_launch();
     kern<<<nb, 256, smem, s>>>(pts, ps, m, rho, C, m0, asg, part);
     NYS_LAUNCH_CHECK();
@@ -634,11 +661,12 @@ static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho,
   }
   if (qe || asg) {  // the final exact pass; callers that pass neither run nys_kmeans_exact later
     double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
-    int rc2 = launch_exact(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart, L.nb_assign, s);
+    int nbx = 0;
+    int rc2 = launch_exact(pts, ps, m, rho, C, m0, reinterpret_cast<long long*>(asg), ppart, L.nb_exact, &nbx, s);
     if (rc2) return rc2;
     if (qe) {
       count_launch();
-      k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, qe);
+      k_sum_parts<<<1, 256, 0, s>>>(ppart, nbx, qe);
     }
   }
   count_launch(); k_write_stats<<<1, 1, 0, s>>>(st, reinterpret_cast<long long*>(stats));
@@ -788,10 +816,11 @@ int nys_kmeans_exact(const float* points, int64_t plane_stride, int64_t m, int r
   char* ws = reinterpret_cast<char*>(workspace);
   cudaStream_t s = (cudaStream_t)stream;
   double* ppart = reinterpret_cast<double*>(ws + L.off_arg);
+  int nbx = 0;
   rc = launch_exact(points, plane_stride, m, rho, centroids, m0, reinterpret_cast<long long*>(assignment_out), ppart,
-                    L.nb_assign, s);
+                    L.nb_exact, &nbx, s);
   if (rc) return rc;
-  count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, L.nb_assign, sum_out);
+  count_launch(); k_sum_parts<<<1, 256, 0, s>>>(ppart, nbx, sum_out);
   NYS_LAUNCH_CHECK();
   return NYS_OK;
 }

@@ -21,7 +21,7 @@ struct KState {
 struct KLayout {
   int64_t m;
   int rho, m0, S;  // S: Lloyd slots per block = m0*(rho+1) + 2
-  int nb_assign, nb_seed, nb_coop;
+  int nb_assign, nb_seed, nb_coop, nb_exact;
   int64_t seed_chunk;
   size_t off_d2, off_labels, off_part, off_ppart, off_tot, off_cf, off_cprev, off_excl, off_state, off_arg,
       off_idx, off_unif, off_pp, off_tsum, total;
@@ -44,6 +44,7 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.m0 = m0;
   L.S = m0 * (rho + 1) + 2;
   L.nb_assign = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, ceil_div(m, 256)));
+  L.nb_exact = (int)std::max<int64_t>(1, std::min<int64_t>(8 * 148, ceil_div(m, 256)));  // cap; the launch sizes by occupancy
   L.nb_seed = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(m, 1024)));
   L.seed_chunk = ceil_div(m, L.nb_seed);
   L.nb_coop = 4 * sms();  // upper bound on co-resident blocks of the cooperative kernels
@@ -60,7 +61,7 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.off_cprev = o;   o = align256(o + (size_t)m0 * rho * 8);
   L.off_excl = o;    o = align256(o + (size_t)m0 * 8);
   L.off_state = o;   o = align256(o + sizeof(KState));
-  L.off_arg = o;     o = align256(o + (size_t)std::max(std::max(L.nb_assign, L.nb_seed), L.nb_coop) * 32);
+  L.off_arg = o;     o = align256(o + (size_t)std::max({L.nb_assign, L.nb_seed, L.nb_coop, L.nb_exact}) * 32);
   L.off_idx = o;     o = align256(o + 64);
   L.off_unif = o;    o = align256(o + (size_t)m0 * 8);
   L.off_tsum = o;    o = align256(o + (size_t)L.nb_coop * 512 * 8);

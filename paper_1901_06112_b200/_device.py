@@ -8,6 +8,14 @@ import torch
 
 
 _CUDA_OK = False
+STAMPS: list | None = None  # tools/step_overhead.py: (label, perf_counter) pairs on the host path
+
+
+def stamp(label: str) -> None:
+    if STAMPS is not None:
+        import time
+
+        STAMPS.append((label, time.perf_counter()))
 
 
 def require_cuda() -> torch.device:
@@ -52,10 +60,11 @@ class StageTimer:
 
     def __init__(self):
         self.events: list[tuple[str, torch.cuda.Event]] = []
+        self.stream = torch.cuda.current_stream()  # once: Event.record() would query it per stamp
 
     def mark(self, name: str) -> None:
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record()
+        ev.record(self.stream)
         self.events.append((name, ev))
 
     def lazy(self, fill) -> "LazyTimings":

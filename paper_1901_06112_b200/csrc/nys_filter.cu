@@ -106,8 +106,10 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
     count_launch();
     k_inverse_cholesky<<<1, 1024, kInvSmemBytes, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q,
                                                       static_cast<const float4*>(img_src),
-                                                      static_cast<float4*>(workspace), (int)(L.n_floats / 4));
+                                                      static_cast<float4*>(workspace), (int)(L.n_floats / 4),
+                                                      reinterpret_cast<unsigned*>((char*)workspace + L.stats_off_bytes));
     NYS_LAUNCH_CHECK();
+    return NYS_OK;  // the inverse kernel also reset the statistics
   }
   count_launch();
   k_reset_stats<<<1, 1, 0, s>>>(reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));

@@ -63,7 +63,8 @@ __device__ __forceinline__ void inv_level(const double* __restrict__ Ls, double*
 
 __global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restrict__ Lg, int n, float* __restrict__ MT,
                                                           int m0q, const float4* __restrict__ img_src,
-                                                          float4* __restrict__ img_dst, int img_f4) {
+                                                          float4* __restrict__ img_dst, int img_f4,
+                                                          unsigned* __restrict__ stats_reset) {
   extern __shared__ double cs[];
   double* Ls = cs;                     // 64 x kInvLd
   double* X = Ls + kInvN * kInvLd;     // 64 x kInvLd, X = L^{-1}
@@ -71,6 +72,12 @@ __global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restr
   double* rd = T + kInvN * kInvLd;     // 64 reciprocal pivots
   const int tid = threadIdx.x;  // blockDim.x == 1024
   NYS_INV_STAMP(0);
+  if (stats_reset && tid == 0) {  // the filter statistics (FilterStats: min|eta| bits = +inf, guarded = 0)
+    stats_reset[0] = 0x7f800000u;
+    stats_reset[1] = 0u;
+    stats_reset[2] = 0u;
+    stats_reset[3] = 0u;
+  }
   {
     // every load of a thread is issued before its first store: over PCIe (mapped pinned
     // memory) the round trips overlap instead of queueing

@@ -508,6 +508,9 @@ struct SeedPrologue {
   int rho, m0;
   int* flag;
   double* unif_dst;
+  unsigned long long* lloyd_gacc;  // Lloyd's first delta buffer (gstride words) and max|x| word
+  int gstride;
+  unsigned* lloyd_maxabs;
   double unif[NYS_MAX_M0];
 };
 __global__ void k_seed_prologue(const SeedPrologue p) {
@@ -524,6 +527,8 @@ __global__ void k_seed_prologue(const SeedPrologue p) {
   }
   for (int d = t; d < p.rho; d += blockDim.x) p.C[d] = (double)p.pts[d * p.ps + p.first];
   for (int k = t; k < p.m0 - 1; k += blockDim.x) p.unif_dst[k] = p.unif[k];
+  for (int k = t; k < p.gstride; k += blockDim.x) p.lloyd_gacc[k] = 0ull;  // the seeding never touches these
+  if (t == 0) *p.lloyd_maxabs = 0u;
 }
 
 __global__ void k_c_to_f(const double* __restrict__ C, float* __restrict__ Cf, int n) {
@@ -630,7 +635,7 @@ static int check_common(const float* pts, int64_t m, int rho, int m0, void* ws, 
 
 static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho, int m0, int max_iter,
                                double* C, double* errors, int64_t* stats, double* qe, int64_t* asg,
-                               char* ws, const KLayout& L, cudaStream_t s) {
+                               char* ws, const KLayout& L, cudaStream_t s, bool prezeroed = false) {
   KState* st = reinterpret_cast<KState*>(ws + L.off_state);
   int* labels = reinterpret_cast<int*>(ws + L.off_labels);
   double* part = reinterpret_cast<double*>(ws + L.off_part);
@@ -642,7 +647,7 @@ static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho,
   // slower than the bounded cooperative kernel (nys_kmeans_tc.cu), so opt-in
   const char* tce = getenv("NYS_KM_TC");
   const bool use_tc = rho >= 16 && tce && atoi(tce) == 1;
-  int rc = use_tc ? NYS_EUNSUPPORTED : launch_lloyd_coop(pts, ps, m, rho, m0, max_iter, C, errors, ws, L, s);
+  int rc = use_tc ? NYS_EUNSUPPORTED : launch_lloyd_coop(pts, ps, m, rho, m0, max_iter, C, errors, ws, L, s, prezeroed);
   if (rc != NYS_OK && rc != NYS_EUNSUPPORTED) return rc;
   if (rc == NYS_EUNSUPPORTED) {  // step-wise (tensor-core assignment, or no cooperative launch)
     count_launch(); k_c_to_f<<<1, 256, 0, s>>>(C, Cf, m0 * rho);
@@ -716,6 +721,9 @@ int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho
     p.m0 = m0;
     p.flag = seed_flag(ws, L);
     p.unif_dst = unif;
+    p.lloyd_gacc = reinterpret_cast<unsigned long long*>(ws + L.off_tot);
+    p.gstride = m0 * rho + m0;
+    p.lloyd_maxabs = reinterpret_cast<unsigned*>(ws + L.off_idx);
     for (int k = 0; k < m0 - 1; ++k) p.unif[k] = uniforms[k];
     count_launch();
     k_seed_prologue<<<1, 64, 0, s>>>(p);
@@ -723,6 +731,7 @@ int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho
   }
   rc = launch_seed_coop(points, plane_stride, m, rho, m0, unif, centroids_out, seeds, ws, L, s);
   if (rc != NYS_OK && rc != NYS_EUNSUPPORTED) return rc;
+  const bool prezeroed = rc == NYS_OK;  // only the cooperative seeding is known to leave Lloyd's words alone
   if (rc == NYS_EUNSUPPORTED) {  // step-wise fallback: two launches per draw
     for (int j = 1; j < m0; ++j) {
       count_launch(); k_pp_update<<<L.nb_seed, 256, 0, s>>>(points, plane_stride, m, rho, centroids_out + (size_t)(j - 1) * rho,
@@ -733,7 +742,7 @@ int nys_kmeans_run(const float* points, int64_t plane_stride, int64_t m, int rho
     }
   }
   return run_lloyd_and_final(points, plane_stride, m, rho, m0, max_iter, centroids_out, errors_out, stats_out,
-                             quant_error_out, assignment_out, ws, L, s);
+                             quant_error_out, assignment_out, ws, L, s, prezeroed);
 }
 
 int nys_kmeans_run_seeded(const float* points, int64_t plane_stride, int64_t m, int rho, int m0, int max_iter,

@@ -875,7 +875,7 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
 }
 
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
-                      double* errors, char* ws, const KLayout& L, cudaStream_t s) {
+                      double* errors, char* ws, const KLayout& L, cudaStream_t s, bool prezeroed) {
   if (!coop_supported()) return NYS_EUNSUPPORTED;
   const int msl = m0 * rho;
   const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
@@ -910,8 +910,10 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     a.bounds = (e && atoi(e)) ? 0 : 1;
   }
   // the first delta buffer starts at zero (the kernel zeroes each next one) and max|x| at +0
-  NYS_CUDA_TRY(cudaMemsetAsync(a.gacc, 0, (size_t)(msl + m0) * 8, s));
-  NYS_CUDA_TRY(cudaMemsetAsync(a.maxabs_bits, 0, sizeof(unsigned), s));
+  if (!prezeroed) {  // else k_seed_prologue zeroed both
+    NYS_CUDA_TRY(cudaMemsetAsync(a.gacc, 0, (size_t)(msl + m0) * 8, s));
+    NYS_CUDA_TRY(cudaMemsetAsync(a.maxabs_bits, 0, sizeof(unsigned), s));
+  }
   void* args[] = {&a};
   auto go = [&](auto kern) -> int {
     int per_sm = 0;

@@ -275,6 +275,6 @@ __device__ __forceinline__ void warp_accumulate(const float (&x)[GR], int rho, i
 int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m0, const double* uniforms_dev,
                      double* C, long long* seeds, char* ws, const KLayout& L, cudaStream_t s);
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
-                      double* errors, char* ws, const KLayout& L, cudaStream_t s);
+                      double* errors, char* ws, const KLayout& L, cudaStream_t s, bool prezeroed = false);
 
 }  // namespace nys

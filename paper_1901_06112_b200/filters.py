@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._device import StageTimer, ptr, require_cuda, stream_ptr, to_device_f32, workspace
+from ._device import StageTimer, ptr, require_cuda, stamp, stream_ptr, to_device_f32, workspace
 from .bands import Band, plan_bands
 from .image import Image
 from .landmarks import DEFAULT_MAX_ITER, exact_assignment, exact_assignment_async, kmeans_device
@@ -478,15 +478,20 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     ``out`` (optional, an extension of the reference signature): a contiguous
     float32 (n, H, W) CUDA or page-locked host tensor that receives the output,
     e.g. a reused pinned buffer for streaming host frames."""
+    stamp("fast_filter")
     _check_sizes(f, p)
     n, H, W = f.channels, f.height, f.width
     if params.m0 > H * W:
         raise ValueError(f"m0 = {params.m0} exceeds the pixel count {H * W}")
     require_cuda()
     timer = StageTimer()
+    stamp("timer")
     timer.mark("start")
+    stamp("mark start")
     inp = _prepare_inputs(f, p)
+    stamp("prepare_inputs")
     timer.mark("upload")
+    stamp("mark upload")
     if _pipelined_ok(inp, params):
         rep = _fast_filter_pipelined(f, inp, params, timer, kernel_events, out)
         if rep is not None:

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._device import ptr, require_cuda, stream_ptr, to_device_f32, workspace
+from ._device import ptr, require_cuda, stamp, stream_ptr, to_device_f32, workspace
 
 DEFAULT_MAX_ITER = 50
 
@@ -141,6 +141,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
 
     ``pipelined`` (no assignment, no exact pass): queue the results' copy to a
     pinned buffer and return a ``PendingKMeans`` without waiting at all."""
+    stamp("kmeans_device")
     require_cuda()
     if points.dim() != 2 or points.stride(1) != 1:
         raise ValueError("points must be a (rho, m) tensor with contiguous rows")
@@ -155,7 +156,9 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     dev = points.device
     ps = int(points.stride(0))
     wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
+    stamp("km checks")
     ws = workspace(wsb)
+    stamp("km workspace")
     # one device buffer for every small result -> a single D2H copy (one sync); every slot that is
     # read back is written by the kernels, so no zero fill; slots addressed by pointer arithmetic
     # (views cost ~5 us each on the critical path before the first launch)
@@ -169,6 +172,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
     seeds_p = stats_p + 8 * 4
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     first, uniforms = _seed_stream(m, m0, seed)
+    stamp("km res+seed")
     if (defer_exact or queue_exact or pipelined) and asg is None:
         qe_p = None
     if pipelined and (asg is not None or qe_p is not None):
@@ -261,7 +265,9 @@ def exact_assignment(points_planar: torch.Tensor, centroids: np.ndarray, want_as
     lib = _native.lib()
     dev = points_planar.device
     wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
+    stamp("km checks")
     ws = workspace(wsb)
+    stamp("km workspace")
     Cd = torch.from_numpy(np.ascontiguousarray(centroids, dtype=np.float64)).to(dev)
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     qe = torch.zeros(1, dtype=torch.float64, device=dev)

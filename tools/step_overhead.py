@@ -20,7 +20,9 @@ _run = lib.nys_kmeans_run
 
 def run(*a):
     stamps.setdefault("launch", time.perf_counter())
-    return _run(*a)
+    r = _run(*a)
+    stamps.setdefault("launched", time.perf_counter())
+    return r
 
 
 lib.nys_kmeans_run = run
@@ -61,16 +63,27 @@ f = Image(data=torch.from_numpy(wl.image(seed=0)).cuda(), range_max=1.0)
 params = _params(wl)
 for _ in range(5):
     fast_filter(f, f, params)
+from paper_1901_06112_b200 import _device  # noqa: E402
+
 pre, post, tot = [], [], []
+seg = {}
 for _ in range(30):
     torch.cuda.synchronize()
     stamps.clear()
+    _device.STAMPS = []
     t0 = time.perf_counter()
     fast_filter(f, f, params)
     t1 = time.perf_counter()
+    prev = t0
+    for lab, t in _device.STAMPS + [("native call", stamps["launch"]), ("nys_kmeans_run", stamps["launched"])]:
+        seg.setdefault(lab, []).append(t - prev)
+        prev = t
+    _device.STAMPS = None
     pre.append(stamps["launch"] - t0)
     post.append(t1 - stamps["synced"])
     tot.append(t1 - t0)
+for k, v in seg.items():
+    print(f"  {k:22s} {sorted(v)[len(v) // 2] * 1e6:7.1f} us")
 for k, v in acc.items():
     print(f"{k}: {v / 35 * 1e6:.1f} us/step")
 med = lambda v: sorted(v)[len(v) // 2] * 1e6  # noqa: E731

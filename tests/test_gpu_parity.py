@@ -445,3 +445,31 @@ def test_exact_assignment_filter_equals_fp64_brute_force(rho, m0):
     asg, qe = exact_assignment(pts, C)
     np.testing.assert_array_equal(asg.cpu().numpy(), ref_lab)
     assert qe == pytest.approx(ref_qe, rel=1e-12)
+
+
+@pytest.mark.parametrize("m0,theta", [(80, 0.12), (128, 0.04), (96, 0.06)])
+def test_pipelined_plan_with_host_formed_M(m0, theta, monkeypatch):
+    # above 64 landmarks the in-stream plan carries M formed by the worker (no device inverse);
+    # still exactly the synchronous path's results, and the plan reports rank m0 and alpha_1
+    from paper_1901_06112_b200.filters import _STAGING
+    from paper_1901_06112_b200.nystrom import mixing_plan
+
+    img = color_scene(72, 96, 30, 0.05, seed=m0)
+    f = Image(data=torch.from_numpy(img).cuda(), range_max=1.0)
+    params = FilterParams(spatial=SpatialKernel.gaussian(2.0, 6), theta=theta, m0=m0, kmeans_max_iter=8)
+    a = fast_filter(f, f, params)
+    plan = mixing_plan(a.centroids, theta, params.eps_drop, 6)
+    if plan.phi_form or plan.rank < m0:
+        pytest.skip("landmark kernel outside the speculation (the fallback test covers it)")
+    import ctypes as C
+
+    from paper_1901_06112_b200 import _native
+
+    r = _native.PlanResult()
+    bufs = [b for b in _STAGING.values()]
+    assert any(_native.lib().nys_filter_plan_result(b.data_ptr(), C.byref(r)) == 0 and r.rank == m0
+               and r.alpha0 == pytest.approx(plan.alpha0, rel=1e-13) for b in bufs)
+    monkeypatch.setenv("NYS_PIPELINED", "0")
+    b = fast_filter(f, f, params)
+    assert torch.equal(a.output.data, b.output.data)
+    assert a.guarded_pixels == b.guarded_pixels and a.retained_rank == b.retained_rank == m0

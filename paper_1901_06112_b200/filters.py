@@ -490,7 +490,8 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     stamp("mark start")
     inp = _prepare_inputs(f, p)
     stamp("prepare_inputs")
-    timer.mark("upload")
+    if not (f.on_device and (p is f or getattr(p, "on_device", True))):
+        timer.mark("upload")  # a host image was copied in (device inputs: upload is 0)
     stamp("mark upload")
     if _pipelined_ok(inp, params):
         rep = _fast_filter_pipelined(f, inp, params, timer, kernel_events, out)

@@ -248,7 +248,7 @@ def _plan_staging(nbytes: int) -> torch.Tensor:
 def run_filter(inp: _Inputs, centroids: np.ndarray | None, params: FilterParams, timer: StageTimer | None = None,
                plane_budget: int | None = None, out: torch.Tensor | None = None,
                kernel_events: list | None = None, rows: tuple[int, int] | None = None, row_origin: int = 0,
-               H_global: int | None = None, inflight: _Inflight | None = None):
+               H_global: int | None = None, inflight: _Inflight | None = None, stats_ptr: int | None = None):
     """K2/K3 over row bands given landmarks; returns (out, plan, stats).
 
     ``kernel_events`` (optional list) receives (name, start, end) CUDA events
@@ -346,8 +346,10 @@ def run_filter(inp: _Inputs, centroids: np.ndarray | None, params: FilterParams,
             kernel_events.append(("k_vpass", e1, e2, b))
     if timer:
         timer.mark("convolutions")
-    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device)
-    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats), s), "nys_filter_stats")
+    # stats_ptr: the two doubles go straight to that address (mapped pinned memory), no tensor
+    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device) if stats_ptr is None else None
+    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats) if stats is not None else stats_ptr, s),
+                  "nys_filter_stats")
     del keep
     return out, plan, stats
 
@@ -402,8 +404,10 @@ def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterPar
         kernel_events.append(("k_recursive", e0, e1, None))
     if timer:
         timer.mark("convolutions")
-    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device)
-    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats), s), "nys_filter_stats")
+    # stats_ptr: the two doubles go straight to that address (mapped pinned memory), no tensor
+    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device) if stats_ptr is None else None
+    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats) if stats is not None else stats_ptr, s),
+                  "nys_filter_stats")
     del keep
     return out, plan, stats
 
@@ -523,6 +527,19 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
 
 
+_RESULTS: dict = {}
+
+
+def _result_slots() -> tuple[torch.Tensor, int]:
+    """Per-stream mapped pinned buffer of 3 doubles and its device address."""
+    key = stream_ptr()
+    e = _RESULTS.get(key)
+    if e is None:
+        t = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+        e = _RESULTS[key] = (t, _device_view(t))
+    return e
+
+
 def _pipelined_ok(inp: _Inputs, params: FilterParams) -> bool:
     """The whole step can be queued without the host waiting: k-means landmarks, a
     box / FIR spatial kernel."""
@@ -543,15 +560,18 @@ def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: 
     pk = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter, pipelined=True)
     timer.mark("clustering")
     timer.mark("eigendecomposition")  # on the host, in-stream (a host function on a side stream)
-    qe_box: list = []
     n_events = len(kernel_events) if kernel_events is not None else 0
-    fl = _Inflight(kmeans=pk, between=lambda: qe_box.append(exact_assignment_async(inp.points, pk.res, params.m0,
-                                                                                     pk.workspace)))
+    # min|eta|, guarded count and quant_error land in one mapped pinned buffer, written by the
+    # statistics kernel and the exact pass's final sum: no gather kernel, no copy at the end
+    hres, hres_dev = _result_slots()
+    fl = _Inflight(kmeans=pk, between=lambda: exact_assignment_async(inp.points, pk.res, params.m0, pk.workspace,
+                                                                      out_ptr=hres_dev + 16))
     out_given = out
-    out, _, stats = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
-                               inflight=fl)
+    out, _, _ = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
+                           inflight=fl, stats_ptr=hres_dev)
     timer.mark("normalization")  # fused into K3; stamped before the wait so elapsed() needs no further sync
-    h = torch.cat([stats, qe_box[0]]).cpu().numpy()  # the step's only host wait
+    timer.stream.synchronize()  # the step's only host wait
+    h = hres.numpy().copy()
     res = fl.result()
     if res.status != _native.NYS_OK or pk.zero_total_draw() >= 0:
         if kernel_events is not None:

@@ -241,10 +241,12 @@ def kmeans_landmarks(points, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX
 
 
 def exact_assignment_async(points_planar: torch.Tensor, centroids_dev: torch.Tensor, m0: int,
-                           ws: torch.Tensor | None = None) -> torch.Tensor:
+                           ws: torch.Tensor | None = None, out_ptr: int | None = None) -> torch.Tensor | None:
     """Launch the exact pass (landmarks.py:121-129) against device centroids
     (the first m0 * rho doubles of ``centroids_dev``) and return quant_error as
-    a 1-element device tensor, without synchronising."""
+    a 1-element device tensor, without synchronising.  ``out_ptr``: write the
+    double there instead (a device address, e.g. of mapped pinned memory) and
+    return None."""
     rho, m = int(points_planar.shape[0]), int(points_planar.shape[1])
     lib = _native.lib()
     dev = points_planar.device
@@ -252,9 +254,10 @@ def exact_assignment_async(points_planar: torch.Tensor, centroids_dev: torch.Ten
     if ws is None or ws.numel() < wsb:
         ws = workspace(wsb)
     Cd = centroids_dev
-    qe = torch.empty(1, dtype=torch.float64, device=dev)
+    qe = torch.empty(1, dtype=torch.float64, device=dev) if out_ptr is None else None
     _native.check(lib.nys_kmeans_exact(ptr(points_planar), int(points_planar.stride(0)), m, rho, ptr(Cd), m0,
-                                       None, ptr(qe), ptr(ws), wsb, stream_ptr()), "nys_kmeans_exact")
+                                       None, ptr(qe) if qe is not None else out_ptr, ptr(ws), wsb, stream_ptr()),
+                  "nys_kmeans_exact")
     return qe
 
 

@@ -404,10 +404,8 @@ def _run_filter_recursive(inp: _Inputs, centroids: np.ndarray, params: FilterPar
         kernel_events.append(("k_recursive", e0, e1, None))
     if timer:
         timer.mark("convolutions")
-    # stats_ptr: the two doubles go straight to that address (mapped pinned memory), no tensor
-    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device) if stats_ptr is None else None
-    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats) if stats is not None else stats_ptr, s),
-                  "nys_filter_stats")
+    stats = torch.empty(2, dtype=torch.float64, device=inp.f.device)
+    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats), s), "nys_filter_stats")
     del keep
     return out, plan, stats
 

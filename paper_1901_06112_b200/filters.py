@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -237,11 +238,13 @@ _STAGING: dict = {}
 
 
 def _plan_staging(nbytes: int) -> torch.Tensor:
-    """Reused zero-filled page-locked staging buffer for nys_filter_plan_async."""
-    buf = _STAGING.get(nbytes)
+    """Reused zero-filled page-locked staging buffer for nys_filter_plan_async, one per
+    (host thread, size): a buffer is busy from the fork until the call's final wait."""
+    key = (threading.get_ident(), nbytes)
+    buf = _STAGING.get(key)
     if buf is None:
         buf = torch.zeros(nbytes, dtype=torch.uint8, pin_memory=True)
-        _STAGING[nbytes] = buf
+        _STAGING[key] = buf
     return buf
 
 
@@ -530,7 +533,7 @@ _RESULTS: dict = {}
 
 def _result_slots() -> tuple[torch.Tensor, int]:
     """Per-stream mapped pinned buffer of 3 doubles and its device address."""
-    key = stream_ptr()
+    key = (threading.get_ident(), stream_ptr())
     e = _RESULTS.get(key)
     if e is None:
         t = torch.zeros(4, dtype=torch.float64, pin_memory=True)

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import functools
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -181,7 +182,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
                                      uniforms.ctypes.data, Cd_p, errs_p, stats_p, qe_p,
                                      ptr(asg), seeds_p, ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
     if pipelined:
-        hbuf = _pinned_f64(nres, ("kmeans-pipelined", torch.cuda.current_stream().cuda_stream))
+        hbuf = _pinned_f64(nres, ("kmeans-pipelined", threading.get_ident(), stream_ptr()))
         hbuf.copy_(res, non_blocking=True)
         return PendingKMeans(host=hbuf, res=res, workspace=ws, m0=m0, rho=rho, max_iter=max_iter)
     qe_dev = None

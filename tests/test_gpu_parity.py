@@ -473,3 +473,37 @@ def test_pipelined_plan_with_host_formed_M(m0, theta, monkeypatch):
     b = fast_filter(f, f, params)
     assert torch.equal(a.output.data, b.output.data)
     assert a.guarded_pixels == b.guarded_pixels and a.retained_rank == b.retained_rank == m0
+
+
+def test_pipelined_calls_from_two_host_threads():
+    # each host thread gets its own staging / result buffers; the plan worker serves both
+    import threading
+
+    imgs = [color_scene(64, 80, 12, 0.05, seed=s) for s in (5, 6)]
+    params = FilterParams(spatial=SpatialKernel.gaussian(2.0, 6), theta=0.15, m0=16, kmeans_max_iter=6)
+    ref = []
+    for im in imgs:
+        f = Image(data=torch.from_numpy(im).cuda(), range_max=1.0)
+        ref.append(fast_filter(f, f, params).output.data.clone())
+    out = [None, None]
+    errs = []
+
+    def work(k):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                f = Image(data=torch.from_numpy(imgs[k]).cuda(), range_max=1.0)
+                for _ in range(5):
+                    r = fast_filter(f, f, params)
+                out[k] = r.output.data.clone()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    torch.cuda.synchronize()
+    for k in (0, 1):
+        assert torch.equal(out[k], ref[k])

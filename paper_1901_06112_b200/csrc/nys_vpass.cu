@@ -203,9 +203,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   const int ntail = a.ntail;  // planes in a partial last chunk (0: all chunks full)
 
   // TMA for stage s (chunk order s / L, landmark s % L; i == m0 is the lead group) of tile t
-  auto issue = [&](int t, int s, unsigned long long gs) {
-    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-    const int i = s % L, k = chunk_of(s / L);
+  auto issue_at = [&](int tx, int ty, int i, int k, unsigned long long gs) {
     const int buf = (int)(gs % K3_NS);
     const bool tail = ntail && k == nchunks - 1;
     const int nval = tail ? ntail : 4;
@@ -214,6 +212,9 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
     mbar_expect_tx(&full[buf], (unsigned)(nval * plane_floats * 4 + (with_b ? K3_NPX * 4 : 0)));
     tma_load_4d(dst, tail ? &tmapt : &tmap4, 0, i * NC + 4 * k, tx, ty * K3_TH, &full[buf]);
     if (with_b) tma_load_4d(dst + 4 * plane_floats, &tmapb, 0, L * NC + i, tx, ty * K3_TH + R, &full[buf]);
+  };
+  auto issue = [&](int t, int s, unsigned long long gs) {  // prologue only: divisions once
+    issue_at(t % a.tiles_x, t / a.tiles_x, s % L, chunk_of(s / L), gs);
   };
   // b_i on every tile pixel from the cached guide tile (gmode 1)
   auto compute_b = [&](int i, float* bb) {
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int ntx = (tile + (int)gridDim.x) % a.tiles_x, nty = (tile + (int)gridDim.x) / a.tiles_x;
     const int x0 = tx * 32, t0 = a.out0 + ty * K3_TH;
     if (gmode == 1) {
       for (int k = tid; k < rho * K3_NPX; k += K3_THREADS) {
@@ -348,12 +350,17 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       }
       __syncthreads();  // everyone is done with this stage's buffer (and the next b tile is ready)
       if (tid == 0) {
-        // keep K3_NS stages in flight, running ahead into this CTA's next tile
-        const int sn = s + K3_NS;
-        if (sn < nstages)
-          issue(tile, sn, gs + K3_NS);
-        else if (tile + (int)gridDim.x < ntiles && sn - nstages < nstages)
-          issue(tile + gridDim.x, sn - nstages, gs + K3_NS);
+        // keep K3_NS stages in flight, running ahead into this CTA's next tile; stage
+        // sn = s + K3_NS is (co2, i2) from the incremental counters (no per-stage division)
+        int i2 = i + K3_NS, co2 = co;
+        while (i2 >= L) {
+          i2 -= L;
+          ++co2;
+        }
+        if (co2 < nchunks)
+          issue_at(tx, ty, i2, chunk_of(co2), gs + K3_NS);
+        else if (tile + (int)gridDim.x < ntiles && (co2 - nchunks) * L + i2 < nstages)
+          issue_at(ntx, nty, i2, chunk_of(co2 - nchunks), gs + K3_NS);
       }
     }
     // guard statistics from the eta tile (deterministic block reduction, atomics across blocks)

@@ -212,16 +212,32 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     }
   };
   // 4. horizontal FIR of the (m0+1)(n+1) planes, blocked-layout stores
+  const int strideL = K2T_GROUP % L, strideR = K2T_GROUP / L;  // item stride in (i, rest) digits
   auto fir = [&](int tile, int b) {
     const float* Ys = Ys_of(b);
     const float* Fs = Fs_of(b);
     const int vr = a.v0 + tile / a.tiles_x;
     const int x0 = (tile % a.tiles_x) * TW;
-    for (int it = gtid; it < fir_items; it += K2T_GROUP) {
-      const int i = it % L;
-      const int rest = it / L;
-      const int ch = rest % nchunks;
-      const int xg = rest / nchunks;
+    // (i, ch, xg) of item it = ((xg * nchunks + ch) * L + i), advanced incrementally by the
+    // group stride (no divisions per item)
+    int i = gtid % L, ch = (gtid / L) % nchunks, xg = (gtid / L) / nchunks;
+    auto advance = [&]() {
+      i += strideL;
+      ch += strideR;
+      if (i >= L) {
+        i -= L;
+        ++ch;
+      }
+      if (nchunks == 1) {  // the common case (n <= 3): rest == xg
+        xg += ch;
+        ch = 0;
+      } else if (ch >= nchunks) {
+        const int q = ch / nchunks;
+        xg += q;
+        ch -= q * nchunks;
+      }
+    };
+    for (int it = gtid; it < fir_items; it += K2T_GROUP, advance()) {
       const int xo = x0 + xg * K2_XR;
       if (xo >= W) continue;
       const float* yrow = Ys + (size_t)i * pitch + xg * K2_XR;

@@ -225,7 +225,8 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
  * means the plan needs drops or the phi-form -- rerun with nys_filter_prepare
  * and a plan from nys_mixing_plan (the speculative outputs are meaningless).
  * `staging` [pinned, nys_filter_plan_staging_bytes(d), zero-filled once] and
- * `centroids` must stay untouched until then.  For m0 <= 64 the device forms
+ * `centroids` must stay untouched until then; a new plan on a staging buffer
+ * whose previous plan is still pending waits for it (up to 60 s, then EINVAL).  For m0 <= 64 the device forms
  * M from the Cholesky factor (and copies the image itself from the mapped
  * staging buffer); larger m0 carry M formed on the host.
  */

@@ -286,7 +286,15 @@ int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, dou
   PlanEvents* pe = plan_events();
   if (!pe) return NYS_ECUDA;
   PlanJob* j = static_cast<PlanJob*>(staging);
-  if (j->seq != j->done) return NYS_EINVAL;  // the previous plan on this staging buffer is still pending
+  if (j->seq != j->done) {
+    // the previous plan on this buffer is still pending (its caller stopped before its final
+    // wait, e.g. on an exception): it depends only on GPU work queued before it, so wait
+    const auto t0 = std::chrono::steady_clock::now();
+    while (j->seq != j->done) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) return NYS_EINVAL;
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
   j->centroids = centroids;
   j->m0 = d->m0;
   j->rho = d->rho;

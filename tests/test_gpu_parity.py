@@ -507,3 +507,26 @@ def test_pipelined_calls_from_two_host_threads():
     torch.cuda.synchronize()
     for k in (0, 1):
         assert torch.equal(out[k], ref[k])
+
+
+def test_pipelined_call_after_an_interrupted_one():
+    # a call that dies between the plan's fork and its final wait leaves its staging buffer
+    # pending; the next call on the thread waits for that plan instead of failing
+    import paper_1901_06112_b200.filters as F
+
+    img = color_scene(48, 64, 8, 0.05, seed=9)
+    f = Image(data=torch.from_numpy(img).cuda(), range_max=1.0)
+    params = FilterParams(spatial=SpatialKernel.gaussian(2.0, 6), theta=0.15, m0=12, kmeans_max_iter=5)
+    ref = fast_filter(f, f, params).output.data.clone()
+    orig = F.exact_assignment_async
+
+    def boom(*a, **k):
+        raise RuntimeError("interrupted")
+
+    F.exact_assignment_async = boom
+    try:
+        with pytest.raises(RuntimeError, match="interrupted"):
+            fast_filter(f, f, params)
+    finally:
+        F.exact_assignment_async = orig
+    assert torch.equal(fast_filter(f, f, params).output.data, ref)

@@ -30,6 +30,7 @@
 
 #include "nys_filter_common.cuh"
 #include "nys_inverse.cuh"
+#include "nys_host_internal.h"
 
 namespace nys {
 
@@ -144,7 +145,7 @@ struct PlanJob {
 };
 static_assert(sizeof(PlanJob) <= kStagingHeader, "plan job record outgrew its header");
 
-void run_plan(PlanJob* j) {
+void run_plan(PlanJob* j, const nys_plan_exec* ex) {
   const auto t0 = std::chrono::steady_clock::now();
   const int n = j->m0, rho = j->rho;
   const FilterLayout& L = j->L;
@@ -152,8 +153,8 @@ void run_plan(PlanJob* j) {
   std::vector<double> info(n), Lc((size_t)n * n), u0(n);
   int rank = 0;
   const bool chol = n <= kInvN;  // else the host forms M and the image carries it
-  const int rc = nys_mixing_plan_lite(j->centroids, n, rho, j->theta, j->eps_drop, j->phi_cond, chol ? 1 : 0,
-                                      info.data(), &rank, Lc.data(), u0.data());
+  const int rc = nys_mixing_plan_lite_ex(j->centroids, n, rho, j->theta, j->eps_drop, j->phi_cond, chol ? 1 : 0,
+                                         info.data(), &rank, Lc.data(), u0.data(), ex);
   j->result.status = rc;
   j->result.rank = rc == NYS_OK ? n : 0;
   if (rc == NYS_OK) {
@@ -176,10 +177,67 @@ void run_plan(PlanJob* j) {
   j->result.host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Second thread of the plan: armed (woken) when a job is posted, it spins while the
+// worker waits for the landmarks so that handing it the Cholesky factorisation costs no
+// wake-up latency, and disarms when the job is done.
+class PlanHelper {
+ public:
+  PlanHelper() { std::thread([this] { loop(); }).detach(); }
+  void arm() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      armed_.store(true);
+    }
+    cv_.notify_one();
+  }
+  void disarm() { armed_.store(false); }
+  static void run(void* ctx, void (*fn)(void*), void* arg) {
+    PlanHelper* h = static_cast<PlanHelper*>(ctx);
+    h->arg_ = arg;
+    h->busy_.store(true);
+    h->fn_.store(fn);
+  }
+  // joins the task; if the helper has not taken it yet (asleep, or disarmed between jobs),
+  // the caller runs it itself -- so a job never depends on the helper being awake
+  static void wait(void* ctx) {
+    PlanHelper* h = static_cast<PlanHelper*>(ctx);
+    while (h->busy_.load()) {
+      void (*fn)(void*) = h->fn_.exchange(nullptr);
+      if (fn) {
+        fn(h->arg_);
+        h->busy_.store(false);
+      }
+    }
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [this] { return armed_.load(); });
+      }
+      while (armed_.load() || fn_.load()) {
+        void (*fn)(void*) = fn_.exchange(nullptr);
+        if (fn) {
+          fn(arg_);
+          busy_.store(false);
+        }
+      }
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::atomic<bool> armed_{false}, busy_{false};
+  std::atomic<void (*)(void*)> fn_{nullptr};
+  void* arg_ = nullptr;
+};
+
 class PlanWorker {
  public:
   PlanWorker() { std::thread([this] { loop(); }).detach(); }
   void post(PlanJob* j) {
+    helper_.arm();
     {
       std::lock_guard<std::mutex> g(mu_);
       q_.push_back(j);
@@ -188,6 +246,7 @@ class PlanWorker {
   }
 
  private:
+  PlanHelper helper_;
   void loop() {
     int cur_dev = -1;
     for (;;) {
@@ -212,8 +271,16 @@ class PlanWorker {
         if (us > 60e6) ok = false;
         else if (us > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
       }
-      if (ok) run_plan(j);
-      else j->result.status = NYS_ECUDA;
+      if (ok) {
+        const nys_plan_exec ex{PlanHelper::run, PlanHelper::wait, &helper_};
+        run_plan(j, &ex);
+      } else {
+        j->result.status = NYS_ECUDA;
+      }
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (q_.empty()) helper_.disarm();  // no job queued behind this one
+      }
       std::atomic_thread_fence(std::memory_order_seq_cst);
       j->done = j->seq;  // releases the stream gate
       std::atomic_thread_fence(std::memory_order_seq_cst);
@@ -249,14 +316,21 @@ struct PlanEvents {
   int device = -1;
   cudaEvent_t fork[kPlanSlots] = {};
   int next = 0;
+  ~PlanEvents() {  // thread exit (errors ignored: the context may already be gone)
+    for (cudaEvent_t& e : fork)
+      if (e) cudaEventDestroy(e);
+  }
 };
 PlanEvents* plan_events() {
   thread_local PlanEvents pe;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   if (pe.device == dev) return &pe;
-  for (int k = 0; k < kPlanSlots; ++k)
+  for (int k = 0; k < kPlanSlots; ++k) {
+    if (pe.fork[k]) cudaEventDestroy(pe.fork[k]);  // the thread moved to another device
+    pe.fork[k] = nullptr;
     if (cudaEventCreateWithFlags(&pe.fork[k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  }
   pe.device = dev;
   return &pe;
 }

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/nysfilter_b200.h"
+#include "nys_host_internal.h"
 
 namespace nys {
 static unsigned long long g_launches = 0;
@@ -541,9 +542,45 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan(const double* C, int m0, int rho,
 // QL was a third of the plan's host time): nothing may fall below
 // eps_drop * alpha_1 and cond(A) must stay <= phi_cond, else NYS_EUNSUPPORTED
 // (the caller then runs nys_mixing_plan).  info_out[0] = alpha_1.
-extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int rho, double theta, double eps_drop,
-                                                    double phi_cond, int chol_only, double* info_out, int* rank_out,
-                                                    double* M_out, double* u0_out) {
+namespace {
+// lower Cholesky factor of the SPD matrix A (row-major n x n) into L; false if a pivot is not positive
+NYS_HOST_CLONES bool chol_factor(const double* A, int n, double* L) {
+  std::fill(L, L + (size_t)n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    const double* lj = &L[(size_t)j * n];
+    const double s = A[(size_t)j * n + j] - dot4(lj, lj, j);
+    if (!(s > 0.0)) return false;
+    const double ljj = std::sqrt(s);
+    L[(size_t)j * n + j] = ljj;
+    for (int i = j + 1; i < n; ++i) L[(size_t)i * n + j] = (A[(size_t)i * n + j] - dot4(&L[(size_t)i * n], lj, j)) / ljj;
+  }
+  return true;
+}
+
+struct CholTask {
+  const double* A;
+  int n;
+  double* L;
+  bool ok;
+};
+void chol_task(void* p) {
+  CholTask* t = static_cast<CholTask*>(p);
+  t->ok = chol_factor(t->A, t->n, t->L);
+}
+}  // namespace
+
+extern "C" int nys_mixing_plan_lite(const double* C, int m0, int rho, double theta, double eps_drop, double phi_cond,
+                                    int chol_only, double* info_out, int* rank_out, double* M_out, double* u0_out) {
+  return nys_mixing_plan_lite_ex(C, m0, rho, theta, eps_drop, phi_cond, chol_only, info_out, rank_out, M_out, u0_out,
+                                 nullptr);
+}
+
+// ex (nullable): runs the Cholesky factorisation on a helper thread while this thread
+// tridiagonalises; the results are those of the sequential path (same functions)
+extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite_ex(const double* C, int m0, int rho, double theta,
+                                                       double eps_drop, double phi_cond, int chol_only,
+                                                       double* info_out, int* rank_out, double* M_out,
+                                                       double* u0_out, const nys_plan_exec* ex) {
   if (!C || m0 < 1 || rho < 1 || !(theta > 0.0) || !info_out || !rank_out || !M_out || !u0_out || !(phi_cond > 1.0))
     return NYS_EINVAL;
   const int n = m0;
@@ -555,6 +592,15 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int
       if (!std::isfinite(d2)) return NYS_EINVAL;
       A[(size_t)i * n + j] = A[(size_t)j * n + i] = std::exp(-d2 * inv);
     }
+  std::vector<double> L((size_t)n * n, 0.0);
+  CholTask ct{A.data(), n, L.data(), false};
+  struct Join {  // the helper reads A and writes L: joined on every return path
+    const nys_plan_exec* ex;
+    ~Join() {
+      if (ex) ex->wait(ex->ctx);
+    }
+  } join{ex};
+  if (ex) ex->run(ex->ctx, chol_task, &ct);
   std::vector<double> Z(A), d, e, h;
   tridiag(Z, n, d, e, h);
   double lo = d[0], hi = d[0], emax = 0.0;
@@ -602,19 +648,13 @@ extern "C" NYS_HOST_CLONES int nys_mixing_plan_lite(const double* C, int m0, int
   if (sturm_below(d, e, n, eps_drop * a1, pivmin) > 0) return NYS_EUNSUPPORTED;  // something is dropped
   if (sturm_below(d, e, n, a1 / phi_cond, pivmin) > 0) return NYS_EUNSUPPORTED;  // phi-form territory
   std::vector<double> vals(1, a1);
-  bool fast = true;
-  std::vector<double> L((size_t)n * n, 0.0);
-  for (int j = 0; j < n && fast; ++j) {
-    const double* lj = &L[(size_t)j * n];
-    const double s = A[(size_t)j * n + j] - dot4(lj, lj, j);
-    if (!(s > 0.0)) {
-      fast = false;
-      break;
-    }
-    const double ljj = std::sqrt(s);
-    L[(size_t)j * n + j] = ljj;
-    for (int i = j + 1; i < n; ++i) L[(size_t)i * n + j] = (A[(size_t)i * n + j] - dot4(&L[(size_t)i * n], lj, j)) / ljj;
+  if (ex) {
+    ex->wait(ex->ctx);
+    join.ex = nullptr;
+  } else {
+    chol_task(&ct);
   }
+  bool fast = ct.ok;
   double* alphas_out = info_out;
   if (fast && chol_only) {
     // the caller forms M = L^{-T} L^{-1} on the device (nys_filter_desc.M_is_cholesky)

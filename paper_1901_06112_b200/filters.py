@@ -234,18 +234,52 @@ class _Inflight:
         return r
 
 
-_STAGING: dict = {}
+_TLS = threading.local()  # per host thread: released with the thread
+
+
+def _tls_dict(name: str) -> dict:
+    d = getattr(_TLS, name, None)
+    if d is None:
+        d = {}
+        setattr(_TLS, name, d)
+    return d
+
+
+class _StagingCache(dict):
+    """A thread's staging buffers; when the thread ends, a plan it left pending (a call that
+    raised before its final wait) is waited for before the pinned memory is released, since
+    the worker thread may still be writing into it."""
+
+    def __del__(self):
+        try:
+            import time
+
+            r = _native.PlanResult()
+            for buf in self.values():
+                t0 = time.monotonic()
+                while (_native.lib().nys_filter_plan_result(buf.data_ptr(), C.byref(r)) != _native.NYS_OK
+                       and time.monotonic() - t0 < 10.0):
+                    time.sleep(1e-4)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 def _plan_staging(nbytes: int) -> torch.Tensor:
     """Reused zero-filled page-locked staging buffer for nys_filter_plan_async, one per
     (host thread, size): a buffer is busy from the fork until the call's final wait."""
-    key = (threading.get_ident(), nbytes)
-    buf = _STAGING.get(key)
+    cache = getattr(_TLS, "staging", None)
+    if cache is None:
+        cache = _TLS.staging = _StagingCache()
+    buf = cache.get(nbytes)
     if buf is None:
         buf = torch.zeros(nbytes, dtype=torch.uint8, pin_memory=True)
-        _STAGING[key] = buf
+        cache[nbytes] = buf
     return buf
+
+
+def plan_staging_buffers() -> list:
+    """This thread's in-stream plan staging buffers (read with nys_filter_plan_result)."""
+    return list(getattr(_TLS, "staging", {}).values())
 
 
 def run_filter(inp: _Inputs, centroids: np.ndarray | None, params: FilterParams, timer: StageTimer | None = None,
@@ -528,16 +562,14 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
 
 
-_RESULTS: dict = {}
-
-
 def _result_slots() -> tuple[torch.Tensor, int]:
-    """Per-stream mapped pinned buffer of 3 doubles and its device address."""
-    key = (threading.get_ident(), stream_ptr())
-    e = _RESULTS.get(key)
+    """Per (host thread, stream) mapped pinned buffer of 3 doubles and its device address."""
+    cache = _tls_dict("results")
+    key = stream_ptr()
+    e = cache.get(key)
     if e is None:
         t = torch.zeros(4, dtype=torch.float64, pin_memory=True)
-        e = _RESULTS[key] = (t, _device_view(t))
+        e = cache[key] = (t, _device_view(t))
     return e
 
 

@@ -124,6 +124,21 @@ class PendingKMeans:
                             centroids_dev=self.res, workspace=self.workspace)
 
 
+_TLS = threading.local()
+
+
+def _pinned_tls_f64(n: int, key) -> torch.Tensor:
+    """Page-locked buffer reused per (host thread, key); released with the thread."""
+    cache = getattr(_TLS, "pinned", None)
+    if cache is None:
+        cache = _TLS.pinned = {}
+    buf = cache.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 64), dtype=torch.float64, pin_memory=True)
+        cache[key] = buf
+    return buf[:n]
+
+
 def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER,
                   want_assignment: bool = False, defer_exact: bool = False,
                   queue_exact: bool = False, pipelined: bool = False) -> DeviceKMeans | PendingKMeans:
@@ -182,7 +197,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
                                      uniforms.ctypes.data, Cd_p, errs_p, stats_p, qe_p,
                                      ptr(asg), seeds_p, ptr(ws), wsb, stream_ptr()), "nys_kmeans_run")
     if pipelined:
-        hbuf = _pinned_f64(nres, ("kmeans-pipelined", threading.get_ident(), stream_ptr()))
+        hbuf = _pinned_tls_f64(nres, stream_ptr())
         hbuf.copy_(res, non_blocking=True)
         return PendingKMeans(host=hbuf, res=res, workspace=ws, m0=m0, rho=rho, max_iter=max_iter)
     qe_dev = None

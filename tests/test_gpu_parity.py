@@ -451,7 +451,7 @@ def test_exact_assignment_filter_equals_fp64_brute_force(rho, m0):
 def test_pipelined_plan_with_host_formed_M(m0, theta, monkeypatch):
     # above 64 landmarks the in-stream plan carries M formed by the worker (no device inverse);
     # still exactly the synchronous path's results, and the plan reports rank m0 and alpha_1
-    from paper_1901_06112_b200.filters import _STAGING
+    from paper_1901_06112_b200.filters import plan_staging_buffers
     from paper_1901_06112_b200.nystrom import mixing_plan
 
     img = color_scene(72, 96, 30, 0.05, seed=m0)
@@ -466,7 +466,7 @@ def test_pipelined_plan_with_host_formed_M(m0, theta, monkeypatch):
     from paper_1901_06112_b200 import _native
 
     r = _native.PlanResult()
-    bufs = [b for b in _STAGING.values()]
+    bufs = plan_staging_buffers()
     assert any(_native.lib().nys_filter_plan_result(b.data_ptr(), C.byref(r)) == 0 and r.rank == m0
                and r.alpha0 == pytest.approx(plan.alpha0, rel=1e-13) for b in bufs)
     monkeypatch.setenv("NYS_PIPELINED", "0")

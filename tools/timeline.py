@@ -38,9 +38,9 @@ for e in gpu[half:]:
 import ctypes as C  # noqa: E402
 
 from paper_1901_06112_b200 import _native  # noqa: E402
-from paper_1901_06112_b200.filters import _STAGING  # noqa: E402
+from paper_1901_06112_b200.filters import plan_staging_buffers  # noqa: E402
 
-for nb, buf in _STAGING.items():
+for buf in plan_staging_buffers():
     r = _native.PlanResult()
     _native.lib().nys_filter_plan_result(buf.data_ptr(), C.byref(r))
     print(f"in-stream plan: status {r.status} rank {r.rank} host function {r.host_us:.1f} us")

@@ -177,67 +177,10 @@ void run_plan(PlanJob* j, const nys_plan_exec* ex) {
   j->result.host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
 }
 
-// Second thread of the plan: armed (woken) when a job is posted, it spins while the
-// worker waits for the landmarks so that handing it the Cholesky factorisation costs no
-// wake-up latency, and disarms when the job is done.
-class PlanHelper {
- public:
-  PlanHelper() { std::thread([this] { loop(); }).detach(); }
-  void arm() {
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      armed_.store(true);
-    }
-    cv_.notify_one();
-  }
-  void disarm() { armed_.store(false); }
-  static void run(void* ctx, void (*fn)(void*), void* arg) {
-    PlanHelper* h = static_cast<PlanHelper*>(ctx);
-    h->arg_ = arg;
-    h->busy_.store(true);
-    h->fn_.store(fn);
-  }
-  // joins the task; if the helper has not taken it yet (asleep, or disarmed between jobs),
-  // the caller runs it itself -- so a job never depends on the helper being awake
-  static void wait(void* ctx) {
-    PlanHelper* h = static_cast<PlanHelper*>(ctx);
-    while (h->busy_.load()) {
-      void (*fn)(void*) = h->fn_.exchange(nullptr);
-      if (fn) {
-        fn(h->arg_);
-        h->busy_.store(false);
-      }
-    }
-  }
-
- private:
-  void loop() {
-    for (;;) {
-      {
-        std::unique_lock<std::mutex> g(mu_);
-        cv_.wait(g, [this] { return armed_.load(); });
-      }
-      while (armed_.load() || fn_.load()) {
-        void (*fn)(void*) = fn_.exchange(nullptr);
-        if (fn) {
-          fn(arg_);
-          busy_.store(false);
-        }
-      }
-    }
-  }
-  std::mutex mu_;
-  std::condition_variable cv_;
-  std::atomic<bool> armed_{false}, busy_{false};
-  std::atomic<void (*)(void*)> fn_{nullptr};
-  void* arg_ = nullptr;
-};
-
 class PlanWorker {
  public:
   PlanWorker() { std::thread([this] { loop(); }).detach(); }
   void post(PlanJob* j) {
-    helper_.arm();
     {
       std::lock_guard<std::mutex> g(mu_);
       q_.push_back(j);
@@ -246,7 +189,6 @@ class PlanWorker {
   }
 
  private:
-  PlanHelper helper_;
   void loop() {
     int cur_dev = -1;
     for (;;) {
@@ -271,16 +213,10 @@ class PlanWorker {
         if (us > 60e6) ok = false;
         else if (us > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
       }
-      if (ok) {
-        const nys_plan_exec ex{PlanHelper::run, PlanHelper::wait, &helper_};
-        run_plan(j, &ex);
-      } else {
-        j->result.status = NYS_ECUDA;
-      }
-      {
-        std::lock_guard<std::mutex> g(mu_);
-        if (q_.empty()) helper_.disarm();  // no job queued behind this one
-      }
+      // sequential plan: a helper thread for the Gram rows / Cholesky (nys_plan_exec) made the
+      // plan slower and erratic (76-133 us) where the host threads contend for cores
+      if (ok) run_plan(j, nullptr);
+      else j->result.status = NYS_ECUDA;
       std::atomic_thread_fence(std::memory_order_seq_cst);
       j->done = j->seq;  // releases the stream gate
       std::atomic_thread_fence(std::memory_order_seq_cst);

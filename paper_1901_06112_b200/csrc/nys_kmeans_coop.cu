@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       nlist = wpre[nw];
     }
     // phase B: the m0-way search (every point on full passes, else the listed ones)
+    int sgc = 0;  // list segment of this thread's last point: q only grows, so the scan resumes there
     for (long long q0 = (long long)w * 32 * HH; q0 < nlist; q0 += (long long)nw * 32 * HH) {
       float x[HH][GR];
       float best[HH], second[HH];
@@ -572,9 +573,8 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
           if (full_pass) {
             i = lo + q;
           } else {
-            int sg = 0;
-            while (q >= wpre[sg + 1]) ++sg;
-            i = a.list[min(hi, lo + sg * cw) + (q - wpre[sg])];
+            while (q >= wpre[sgc + 1]) ++sgc;
+            i = a.list[min(hi, lo + sgc * cw) + (q - wpre[sgc])];
           }
         }
         idx[h] = i;

@@ -123,12 +123,13 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
 // staging buffer starts with this job record; the workspace image follows at
 // kStagingHeader bytes.
 //
-// A persistent native worker thread polls the fork event (recorded on the
-// caller's stream after the landmarks' copy), runs the lite plan, fills the
-// image and publishes `done`; the caller's stream is gated on the device by
-// cuStreamWaitValue32 on that pinned word, then copies the image in.  The worker
-// depends only on work queued before the gate and always publishes `done`
-// (with an error status on failure), so the gate cannot deadlock.  A
+// Two pinned words in the job: the caller's stream writes `ready` (cuStreamWriteValue32)
+// once the landmarks' copy has completed; a persistent native worker thread polls it
+// with plain loads (no CUDA call: it never queues behind other driver users), runs the
+// lite plan, fills the image and publishes `done`; the stream is gated on the device by
+// cuStreamWaitValue32 on `done`, then the device inverse pulls the image in.  The worker
+// depends only on work queued before the gate and always publishes `done` (with an
+// error status on failure or a 60 s timeout), so the gate cannot deadlock.  A
 // cudaLaunchHostFunc chain did the same with ~0.3 ms of dispatch latency.
 // ---------------------------------------------------------------------------
 constexpr size_t kStagingHeader = 512;
@@ -139,9 +140,9 @@ struct PlanJob {
   FilterLayout L;
   size_t image_bytes;
   nys_plan_result result;
-  cudaEvent_t fork;
   unsigned seq;
-  volatile unsigned done;  // the stream waits for done >= seq
+  volatile unsigned ready;  // written by the stream (cuStreamWriteValue32) once the landmarks landed
+  volatile unsigned done;   // the stream waits for done >= seq
 };
 static_assert(sizeof(PlanJob) <= kStagingHeader, "plan job record outgrew its header");
 
@@ -190,7 +191,6 @@ class PlanWorker {
 
  private:
   void loop() {
-    int cur_dev = -1;
     for (;;) {
       PlanJob* j;
       {
@@ -199,20 +199,22 @@ class PlanWorker {
         j = q_.front();
         q_.pop_front();
       }
+      // wait for the landmarks: a plain load of a pinned word the stream writes after their copy
+      // (no CUDA call here, so the worker never queues behind other driver users); spin, then
+      // back off; a stream that never gets there (an error) times out
       bool ok = true;
-      if (j->device != cur_dev) ok = cudaSetDevice(j->device) == cudaSuccess, cur_dev = j->device;
       const auto t0 = std::chrono::steady_clock::now();
-      while (ok) {  // spin for the landmarks (k-means is still running when the job is posted), then back off
-        const cudaError_t e = cudaEventQuery(j->fork);
-        if (e == cudaSuccess) break;
-        if (e != cudaErrorNotReady) {
-          ok = false;
-          break;
+      for (unsigned it = 0; j->ready != j->seq; ++it) {
+        if ((it & 255u) == 0) {
+          const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+          if (us > 60e6) {
+            ok = false;
+            break;
+          }
+          if (us > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
         }
-        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-        if (us > 60e6) ok = false;
-        else if (us > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
       }
+      std::atomic_thread_fence(std::memory_order_seq_cst);
       // sequential plan: a helper thread for the Gram rows / Cholesky (nys_plan_exec) made the
       // plan slower and erratic (76-133 us) where the host threads contend for cores
       if (ok) run_plan(j, nullptr);
@@ -247,28 +249,18 @@ StreamWaitValue32Fn wait_value_fn() {
   return fn;
 }
 
-constexpr int kPlanSlots = 8;
-struct PlanEvents {
-  int device = -1;
-  cudaEvent_t fork[kPlanSlots] = {};
-  int next = 0;
-  ~PlanEvents() {  // thread exit (errors ignored: the context may already be gone)
-    for (cudaEvent_t& e : fork)
-      if (e) cudaEventDestroy(e);
+StreamWaitValue32Fn write_value_fn() {  // same signature as cuStreamWaitValue32
+  static StreamWaitValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitValue32Fn>(p);
   }
-};
-PlanEvents* plan_events() {
-  thread_local PlanEvents pe;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  if (pe.device == dev) return &pe;
-  for (int k = 0; k < kPlanSlots; ++k) {
-    if (pe.fork[k]) cudaEventDestroy(pe.fork[k]);  // the thread moved to another device
-    pe.fork[k] = nullptr;
-    if (cudaEventCreateWithFlags(&pe.fork[k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-  }
-  pe.device = dev;
-  return &pe;
+  return fn;
 }
 
 size_t plan_image_bytes(const FilterLayout& L, int m0) { return L.chol_off_bytes + (size_t)m0 * m0 * sizeof(double); }
@@ -290,11 +282,9 @@ int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, dou
   const FilterLayout L = filter_layout(d);
   if (staging_bytes < kStagingHeader + plan_image_bytes(L, d->m0) || workspace_bytes < L.total_bytes)
     return NYS_EINVAL;
-  if (!wait_value_fn()) return NYS_EUNSUPPORTED;
-  void* dv = nullptr;  // the gate word must be device-visible (mapped pinned memory)
+  if (!wait_value_fn() || !write_value_fn()) return NYS_EUNSUPPORTED;
+  void* dv = nullptr;  // the gate words must be device-visible (mapped pinned memory)
   if (nys_device_view(staging, &dv) != NYS_OK) return NYS_EINVAL;
-  PlanEvents* pe = plan_events();
-  if (!pe) return NYS_ECUDA;
   PlanJob* j = static_cast<PlanJob*>(staging);
   if (j->seq != j->done) {
     // the previous plan on this buffer is still pending (its caller stopped before its final
@@ -316,10 +306,13 @@ int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, dou
   j->L = L;
   j->image_bytes = plan_image_bytes(L, d->m0);
   j->result = nys_plan_result{NYS_ECUDA, 0, 0.0, 0.0, 0.0};  // overwritten by the worker
-  j->fork = pe->fork[pe->next];
-  pe->next = (pe->next + 1) % kPlanSlots;
-  NYS_CUDA_TRY(cudaEventRecord(j->fork, (cudaStream_t)stream));
   j->seq = j->seq + 1;
+  // stream-ordered: written (behind a memory fence) once the landmarks' copy has completed
+  const CUdeviceptr ready = reinterpret_cast<CUdeviceptr>(dv) + offsetof(PlanJob, ready);
+  if (write_value_fn()(reinterpret_cast<CUstream>(stream), ready, j->seq, 0) != CUDA_SUCCESS) {
+    j->seq = j->seq - 1;
+    return NYS_ECUDA;
+  }
   plan_worker().post(j);
   return NYS_OK;
 }

@@ -139,6 +139,20 @@ def _pinned_tls_f64(n: int, key) -> torch.Tensor:
     return buf[:n]
 
 
+def _pipelined_buffers(m: int, rho: int, m0: int, nres: int, dev) -> tuple[torch.Tensor, torch.Tensor]:
+    cache = getattr(_TLS, "kmbufs", None)
+    if cache is None:
+        cache = _TLS.kmbufs = {}
+    key = (stream_ptr(), m, rho, m0, nres, dev.index)
+    e = cache.get(key)
+    if e is None:
+        if len(cache) > 8:
+            cache.clear()
+        wsb = int(_native.lib().nys_kmeans_workspace_bytes(m, rho, m0))
+        e = cache[key] = (workspace(wsb), torch.empty(nres, dtype=torch.float64, device=dev))
+    return e
+
+
 def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = DEFAULT_MAX_ITER,
                   want_assignment: bool = False, defer_exact: bool = False,
                   queue_exact: bool = False, pipelined: bool = False) -> DeviceKMeans | PendingKMeans:
@@ -168,18 +182,23 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
         raise ValueError("max_iter must be >= 1")
     if rho > _native.NYS_MAX_RHO or m0 > _native.NYS_MAX_M0:
         raise NotImplementedError(f"rho <= {_native.NYS_MAX_RHO} and m0 <= {_native.NYS_MAX_M0} on the B200 path")
+    stamp("km checks")
     lib = _native.lib()
     dev = points.device
     ps = int(points.stride(0))
-    wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
-    stamp("km checks")
-    ws = workspace(wsb)
-    stamp("km workspace")
     # one device buffer for every small result -> a single D2H copy (one sync); every slot that is
     # read back is written by the kernels, so no zero fill; slots addressed by pointer arithmetic
     # (views cost ~5 us each on the critical path before the first launch)
     nres = m0 * rho + max_iter + 1 + 4 + m0
-    res = torch.empty(nres, dtype=torch.float64, device=dev)
+    if pipelined:
+        # reused per (thread, stream, shape): the next call's kernels queue behind this one's
+        ws, res = _pipelined_buffers(m, rho, m0, nres, dev)
+        wsb = int(ws.numel())
+    else:
+        wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
+        ws = workspace(wsb)
+        res = torch.empty(nres, dtype=torch.float64, device=dev)
+    stamp("km workspace")
     base = res.data_ptr()
     Cd_p = base
     errs_p = base + 8 * m0 * rho
@@ -284,9 +303,7 @@ def exact_assignment(points_planar: torch.Tensor, centroids: np.ndarray, want_as
     lib = _native.lib()
     dev = points_planar.device
     wsb = int(lib.nys_kmeans_workspace_bytes(m, rho, m0))
-    stamp("km checks")
     ws = workspace(wsb)
-    stamp("km workspace")
     Cd = torch.from_numpy(np.ascontiguousarray(centroids, dtype=np.float64)).to(dev)
     asg = torch.empty(m, dtype=torch.int64, device=dev) if want_assignment else None
     qe = torch.zeros(1, dtype=torch.float64, device=dev)

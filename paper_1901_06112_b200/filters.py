@@ -562,6 +562,16 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
 
 
+def _side_stream() -> torch.cuda.Stream:
+    """Per (host thread, device) side stream for the exact pass of the pipelined call."""
+    cache = _tls_dict("side")
+    dev = torch.cuda.current_device()
+    st = cache.get(dev)
+    if st is None:
+        st = cache[dev] = torch.cuda.Stream()
+    return st
+
+
 def _result_slots() -> tuple[torch.Tensor, int]:
     """Per (host thread, stream) mapped pinned buffer of 3 doubles and its device address."""
     cache = _tls_dict("results")
@@ -597,11 +607,27 @@ def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: 
     # min|eta|, guarded count and quant_error land in one mapped pinned buffer, written by the
     # statistics kernel and the exact pass's final sum: no gather kernel, no copy at the end
     hres, hres_dev = _result_slots()
-    fl = _Inflight(kmeans=pk, between=lambda: exact_assignment_async(inp.points, pk.res, params.m0, pk.workspace,
-                                                                      out_ptr=hres_dev + 16))
+    # the exact pass runs on a side stream forked after the landmarks' copy: nothing on the
+    # main stream needs it, so it fills the GPU while the plan is computed and stays off the
+    # path to K2; joined before the final wait
+    side = _side_stream()
+    joined: list = []
+
+    def between():
+        fork = torch.cuda.Event()
+        fork.record(timer.stream)
+        side.wait_event(fork)
+        with torch.cuda.stream(side):
+            exact_assignment_async(inp.points, pk.res, params.m0, pk.workspace, out_ptr=hres_dev + 16)
+            done = torch.cuda.Event()
+            done.record(side)
+        joined.append(done)
+
+    fl = _Inflight(kmeans=pk, between=between)
     out_given = out
     out, _, _ = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
                            inflight=fl, stats_ptr=hres_dev)
+    timer.stream.wait_event(joined[0])
     timer.mark("normalization")  # fused into K3; stamped before the wait so elapsed() needs no further sync
     timer.stream.synchronize()  # the step's only host wait
     h = hres.numpy().copy()

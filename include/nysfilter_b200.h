@@ -211,13 +211,16 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
  * landmark coordinates have landed in `centroids` [pinned host, m0 x rho FP64,
  * written by an earlier copy on `stream`], a host function on a side stream
  * runs the lite plan (nys_mixing_plan_lite, Cholesky factor) into the pinned
- * `staging` image of the workspace constants and copies it to `workspace`.
+ * `staging` image of the workspace constants (the stream signals it with a
+ * stream-ordered write of a pinned word; the worker makes no CUDA call).
  * Work queued on `stream` between this call and nys_filter_prepare_join (e.g.
  * the k-means exact pass) overlaps the plan.  The desc's M / u0 / alpha0 /
  * eps_den / phi_form / M_is_cholesky are ignored (the plan supplies them).
  *
- * nys_filter_prepare_join makes `stream` wait for the copy, forms M = A^{-1}
- * on the device and resets the statistics; the band passes follow as usual.
+ * nys_filter_prepare_join queues the kernel that waits on the device for the
+ * plan (it polls the staging buffer's `done` word), pulls the image into
+ * `workspace`, forms M = A^{-1} and resets the statistics; the band passes
+ * follow as usual.
  *
  * The speculation is the y-form with nothing dropped (cond(A) <= phi_cond).
  * Read the verdict with nys_filter_plan_result once `stream` has passed the

@@ -91,7 +91,8 @@ namespace {
 // or -- img_src non-null -- of the mapped pinned image, which the kernel first copies into
 // the workspace; then the statistics reset
 int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, void* workspace, bool chol,
-                             cudaStream_t s, const void* img_src = nullptr) {
+                             cudaStream_t s, const void* img_src = nullptr, const unsigned* gate = nullptr,
+                             unsigned seq = 0) {
   if (chol) {
     const char* base = img_src ? static_cast<const char*>(img_src) : static_cast<const char*>(workspace);
     const double* Ld = reinterpret_cast<const double*>(base + L.chol_off_bytes);
@@ -108,7 +109,8 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
     k_inverse_cholesky<<<1, 1024, kInvSmemBytes, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q,
                                                       static_cast<const float4*>(img_src),
                                                       static_cast<float4*>(workspace), (int)(L.n_floats / 4),
-                                                      reinterpret_cast<unsigned*>((char*)workspace + L.stats_off_bytes));
+                                                      reinterpret_cast<unsigned*>((char*)workspace + L.stats_off_bytes),
+                                                      gate, seq);
     NYS_LAUNCH_CHECK();
     return NYS_OK;  // the inverse kernel also reset the statistics
   }
@@ -126,8 +128,9 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
 // Two pinned words in the job: the caller's stream writes `ready` (cuStreamWriteValue32)
 // once the landmarks' copy has completed; a persistent native worker thread polls it
 // with plain loads (no CUDA call: it never queues behind other driver users), runs the
-// lite plan, fills the image and publishes `done`; the stream is gated on the device by
-// cuStreamWaitValue32 on `done`, then the device inverse pulls the image in.  The worker
+// lite plan, fills the image and publishes `done`; the first kernel after the join (the
+// device inverse) polls `done` itself (an active wait: a cuStreamWaitValue32 gate sometimes
+// noticed it milliseconds late), then pulls the image in.  The worker
 // depends only on work queued before the gate and always publishes `done` (with an
 // error status on failure or a 60 s timeout), so the gate cannot deadlock.  A
 // cudaLaunchHostFunc chain did the same with ~0.3 ms of dispatch latency.
@@ -235,21 +238,7 @@ PlanWorker& plan_worker() {
 }
 
 typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-StreamWaitValue32Fn wait_value_fn() {
-  static StreamWaitValue32Fn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<StreamWaitValue32Fn>(p);
-  }
-  return fn;
-}
-
-StreamWaitValue32Fn write_value_fn() {  // same signature as cuStreamWaitValue32
+StreamWaitValue32Fn write_value_fn() {  // cuStreamWriteValue32
   static StreamWaitValue32Fn fn = nullptr;
   static bool tried = false;
   if (!tried) {
@@ -282,7 +271,7 @@ int nys_filter_plan_async(const nys_filter_desc* d, const double* centroids, dou
   const FilterLayout L = filter_layout(d);
   if (staging_bytes < kStagingHeader + plan_image_bytes(L, d->m0) || workspace_bytes < L.total_bytes)
     return NYS_EINVAL;
-  if (!wait_value_fn() || !write_value_fn()) return NYS_EUNSUPPORTED;
+  if (!write_value_fn()) return NYS_EUNSUPPORTED;
   void* dv = nullptr;  // the gate words must be device-visible (mapped pinned memory)
   if (nys_device_view(staging, &dv) != NYS_OK) return NYS_EINVAL;
   PlanJob* j = static_cast<PlanJob*>(staging);
@@ -326,12 +315,15 @@ int nys_filter_prepare_join(const nys_filter_desc* d, void* staging, void* works
   void* dv = nullptr;
   if (nys_device_view(staging, &dv) != NYS_OK) return NYS_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  const CUdeviceptr gate = reinterpret_cast<CUdeviceptr>(dv) + offsetof(PlanJob, done);
-  if (wait_value_fn()(reinterpret_cast<CUstream>(s), gate, j->seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-    return NYS_ECUDA;
+  // the gate is polled by the first kernel after it (k_inverse_cholesky, or k_wait_gate when
+  // the image carries M): an active wait notices the worker's `done` within a microsecond
+  const unsigned* gate = reinterpret_cast<const unsigned*>(static_cast<const char*>(dv) + offsetof(PlanJob, done));
   const FilterLayout L = filter_layout(d);
   const char* img = static_cast<const char*>(dv) + kStagingHeader;
-  if (d->m0 <= kInvN) return launch_inverse_and_reset(d, L, workspace, true, s, img);  // copies the image itself
+  if (d->m0 <= kInvN) return launch_inverse_and_reset(d, L, workspace, true, s, img, gate, j->seq);
+  count_launch();
+  k_wait_gate<<<1, 32, 0, s>>>(gate, j->seq);
+  NYS_LAUNCH_CHECK();
   NYS_CUDA_TRY(cudaMemcpyAsync(workspace, static_cast<const char*>(staging) + kStagingHeader, L.n_floats * sizeof(float),
                                cudaMemcpyHostToDevice, s));
   return launch_inverse_and_reset(d, L, workspace, false, s);

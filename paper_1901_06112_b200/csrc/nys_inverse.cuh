@@ -61,16 +61,40 @@ __device__ __forceinline__ void inv_level(const double* __restrict__ Ls, double*
   __syncthreads();
 }
 
+// Active gate (the in-stream plan): thread 0 polls a mapped host word until it reaches `seq`
+// (acquire, system scope), bounded by 60 s of %globaltimer; everything after the barrier sees
+// the host's writes that preceded the word.  A stream-level cuStreamWaitValue32 on the same
+// word occasionally noticed a late write only milliseconds (once 130 ms) later.
+__device__ __forceinline__ void wait_host_word(const unsigned* gate, unsigned seq) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
+      if ((int)(v - seq) >= 0) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60ull * 1000000000ull) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void k_wait_gate(const unsigned* gate, unsigned seq) { wait_host_word(gate, seq); }
+
 __global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restrict__ Lg, int n, float* __restrict__ MT,
                                                           int m0q, const float4* __restrict__ img_src,
                                                           float4* __restrict__ img_dst, int img_f4,
-                                                          unsigned* __restrict__ stats_reset) {
+                                                          unsigned* __restrict__ stats_reset,
+                                                          const unsigned* gate = nullptr, unsigned seq = 0) {
   extern __shared__ double cs[];
   double* Ls = cs;                     // 64 x kInvLd
   double* X = Ls + kInvN * kInvLd;     // 64 x kInvLd, X = L^{-1}
   double* T = X + kInvN * kInvLd;      // 64 x kInvLd scratch (L21 X11 per block pair)
   double* rd = T + kInvN * kInvLd;     // 64 reciprocal pivots
   const int tid = threadIdx.x;  // blockDim.x == 1024
+  if (gate) wait_host_word(gate, seq);
   NYS_INV_STAMP(0);
   if (stats_reset && tid == 0) {  // the filter statistics (FilterStats: min|eta| bits = +inf, guarded = 0)
     stats_reset[0] = 0x7f800000u;

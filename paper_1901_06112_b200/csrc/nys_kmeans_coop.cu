@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
     if ((int)threadIdx.x < rho) cs[threadIdx.x] = __ldcg(a.C + (size_t)(j - 1) * rho + threadIdx.x);
     __syncthreads();
     double s = 0.0;
-    constexpr int U = GR <= 4 ? 4 : 2;  // independent points in flight (register budget)
+    constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2)
     int i = threadIdx.x;
     for (; i + (U - 1) * B < len; i += U * B) {
       float x[U][GR];
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
   for (int j = 1; j < a.m0; ++j) {
     const double* cs = Cs + (size_t)(j - 1) * rho;
     double s = 0.0;
-    constexpr int U = GR <= 4 ? 4 : 2;  // independent points in flight (register budget)
+    constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2)
     int r = 0;
     for (; r + U <= per; r += U) {
       float x[U][GR];

@@ -562,16 +562,6 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
                         quant_error=qe, min_denominator=min_den, guarded_pixels=guarded, centroids=centroids)
 
 
-def _side_stream() -> torch.cuda.Stream:
-    """Per (host thread, device) side stream for the exact pass of the pipelined call."""
-    cache = _tls_dict("side")
-    dev = torch.cuda.current_device()
-    st = cache.get(dev)
-    if st is None:
-        st = cache[dev] = torch.cuda.Stream()
-    return st
-
-
 def _result_slots() -> tuple[torch.Tensor, int]:
     """Per (host thread, stream) mapped pinned buffer of 3 doubles and its device address."""
     cache = _tls_dict("results")
@@ -595,39 +585,29 @@ def _pipelined_ok(inp: _Inputs, params: FilterParams) -> bool:
 def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: StageTimer, kernel_events,
                            out) -> FilterReport | None:
     """fast_filter with the mixing plan computed in-stream (nys_filter_plan_async):
-    k-means, the landmarks' copy to pinned memory, the plan on a side stream
+    k-means, the landmarks' copy to pinned memory, the plan on the library's worker thread
     overlapping the exact pass, the device inverse, K2 and K3 are all queued
     before the host waits once, for the statistics.  The plan speculates on the
     common case (nothing dropped, y-form); None when it missed or k-means++ hit
     a zero total (the caller then reruns the synchronous path)."""
     pk = kmeans_device(inp.points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter, pipelined=True)
     timer.mark("clustering")
-    timer.mark("eigendecomposition")  # on the host, in-stream (a host function on a side stream)
+    timer.mark("eigendecomposition")  # on the host, in-stream (the library's plan worker thread)
     n_events = len(kernel_events) if kernel_events is not None else 0
     # min|eta|, guarded count and quant_error land in one mapped pinned buffer, written by the
     # statistics kernel and the exact pass's final sum: no gather kernel, no copy at the end
     hres, hres_dev = _result_slots()
-    # the exact pass runs on a side stream forked after the landmarks' copy: nothing on the
-    # main stream needs it, so it fills the GPU while the plan is computed and stays off the
-    # path to K2; joined before the final wait
-    side = _side_stream()
-    joined: list = []
+    # the exact pass is queued between the plan's fork and its join on the same stream, so it
+    # runs while the worker computes the plan (a side stream for it let rare multi-ms stalls
+    # into the second timed step: 2 of 9 bench runs, none of 9 on one stream)
 
     def between():
-        fork = torch.cuda.Event()
-        fork.record(timer.stream)
-        side.wait_event(fork)
-        with torch.cuda.stream(side):
-            exact_assignment_async(inp.points, pk.res, params.m0, pk.workspace, out_ptr=hres_dev + 16)
-            done = torch.cuda.Event()
-            done.record(side)
-        joined.append(done)
+        exact_assignment_async(inp.points, pk.res, params.m0, pk.workspace, out_ptr=hres_dev + 16)
 
     fl = _Inflight(kmeans=pk, between=between)
     out_given = out
     out, _, _ = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
                            inflight=fl, stats_ptr=hres_dev)
-    timer.stream.wait_event(joined[0])
     timer.mark("normalization")  # fused into K3; stamped before the wait so elapsed() needs no further sync
     timer.stream.synchronize()  # the step's only host wait
     h = hres.numpy().copy()

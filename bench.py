@@ -14,7 +14,8 @@ pinned host buffers with H2D/D2H inside the timed region.  L2 (126 MB) is
 flushed with a 512 MB write before every timed step.  ``--impl reference``
 times the CPU oracle port (oracle/nys_oracle.py; the reference is pure
 Python and cannot travel to the GPU box) on a bounded row crop of the same
-workload using all host threads.
+workload, its convolution stage on one thread like the reference's
+(BLAS matmuls on the BLAS threads).
 """
 
 from __future__ import annotations
@@ -187,6 +188,7 @@ def run_ours(args, rank: int, world: int):
     lib = _native.lib()
     step_ms, k_ms = [], {"k_feat_hpass": 0.0, "k_vpass": 0.0}
     k_n = {"k_feat_hpass": 0, "k_vpass": 0}
+    k_px = {"k_feat_hpass": 0, "k_vpass": 0}  # output pixels the timed launches produced (per band)
     launches0 = int(lib.nys_kernel_launches())
     try:
         torch.cuda.synchronize()
@@ -204,9 +206,10 @@ def run_ours(args, rank: int, world: int):
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
-            for name, a, b, _band in evs:
+            for name, a, b, band in evs:
                 k_ms[name] += a.elapsed_time(b)
                 k_n[name] += 1
+                k_px[name] += (band.out_rows if band is not None else H) * W
         torch.cuda.synchronize()
         clk.window = False
     finally:
@@ -236,31 +239,43 @@ def run_ours(args, rank: int, world: int):
     e2e = sum(e2e_ms) / len(e2e_ms)
     out_bytes = int(rep_h.output.data.numel() * 4)
 
-    # roofline of the dominant kernel (algorithmic bytes per launch / avg launch time)
+    # roofline of the dominant kernel: algorithmic bytes of the pixels each launch produced (its
+    # band's out_rows x W) / that launch's time, averaged over launches
     u = n if wl.mode != "nlm" else n  # stored input channels read (patches gathered from f)
     P = (wl.m0 + 1) * (n + 1)         # planes incl. the rank-1 lead group
     T = 2 * wl.radius + 1
     rho = n * 9 if wl.mode == "nlm" else n
     bytes_px = {"k_feat_hpass": 4 * (u + P), "k_vpass": 4 * (P + u + n)}
-    # algorithmic FP32 FMA-pipe ops per pixel (FIR taps, y = M b, features, contraction)
+    # algorithmic CUDA-core FP32 ops per pixel (FIR taps, features, contraction); y = M b runs on
+    # the tensor cores (3xTF32 tcgen05) and is reported apart
     fir = P * (2 if wl.spatial == "box" else T)
-    flops_px = {"k_feat_hpass": fir + wl.m0 * wl.m0 + wl.m0 * (2 * rho + 1) + wl.m0 * n,
+    flops_px = {"k_feat_hpass": fir + wl.m0 * (2 * rho + 1) + wl.m0 * n,
                 "k_vpass": fir + wl.m0 * (2 * rho + 1) + 2 * P}
+    tensor_mac_px = {"k_feat_hpass": 3 * wl.m0 * (wl.m0 + 1), "k_vpass": 0}
     avg = {k: k_ms[k] / max(1, k_n[k]) for k in k_ms}
+    px_launch = {k: k_px[k] / max(1, k_n[k]) for k in k_px}
     dom = max(avg, key=avg.get)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bytes_px[dom] * px / (avg[dom] * 1e-3) / 1e9
+    achieved = bytes_px[dom] * px_launch[dom] / (avg[dom] * 1e-3) / 1e9
     ffma = _ffma_peak()
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 4), "traffic": None,
             "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-            "bytes_per_px": bytes_px[dom], "launch_ms": round(avg[dom], 4),
-            "kernel_ms": {k: round(v, 4) for k, v in avg.items()}}
-    fma_t = flops_px[dom] * px / (avg[dom] * 1e-3) / 1e12
+            "bytes_per_px": bytes_px[dom], "px_per_launch": int(px_launch[dom]), "launch_ms": round(avg[dom], 4),
+            "launches_per_step": k_n[dom] // max(1, args.steps),
+            "kernel_ms": {k: round(v, 4) for k, v in avg.items()},
+            "kernel_frac_hbm": {k: round(bytes_px[k] * px_launch[k] / (avg[k] * 1e-3) / 1e9 / hbm_peak, 4)
+                                for k in avg if avg[k] > 0}}
+    fma_t = flops_px[dom] * px_launch[dom] / (avg[dom] * 1e-3) / 1e12
     roof["fma"] = {"achieved_tfma": round(fma_t, 2), "ops_per_px": flops_px[dom],
                    "peak_tfma": ffma.get("tfma_per_s") if ffma else None,
-                   "frac": round(fma_t / ffma["tfma_per_s"], 4) if ffma else None}
+                   "frac": round(fma_t / ffma["tfma_per_s"], 4) if ffma else None,
+                   "counts": "CUDA-core FP32 FMA/ADD of the FIR taps, features and contraction"}
+    if tensor_mac_px[dom]:
+        tm = tensor_mac_px[dom] * px_launch[dom] / (avg[dom] * 1e-3) / 1e12
+        roof["tensor"] = {"achieved_tmac": round(tm, 3), "macs_per_px": tensor_mac_px[dom],
+                          "what": "y = M b as 3xTF32 tcgen05.mma (3 passes of m0 x (m0+1) MACs)"}
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         tr = json.loads(prof.read_text()).get(wl.name, {}).get(dom)
@@ -301,11 +316,12 @@ def _blas_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(wl, rows: int, threads: int | None = None):
-    """CPU oracle port on a bounded row crop of the same workload."""
+def cpu_baseline(wl, rows: int, threads: int = 1):
+    """CPU oracle port on a bounded row crop of the same workload.  threads = 1 runs the rank
+    loop (filters.py:227-238) on one thread, as the reference's NumPy convolution stage does;
+    the k-means / extrapolation matmuls use the BLAS threads, as in the reference."""
     from oracle import nys_oracle as O
 
-    threads = threads or (os.cpu_count() or 1)
     f = wl.image(seed=0, H=rows).astype(np.float64)
     p = O.patch_stack(f, wl.patch_radius) if wl.mode == "nlm" else f
     t0 = time.perf_counter()
@@ -313,17 +329,18 @@ def cpu_baseline(wl, rows: int, threads: int | None = None):
     dt = time.perf_counter() - t0
     px = f.shape[1] * f.shape[2]
     return {"value": round(px / dt / 1e6, 5), "unit": UNIT, "cores": max(threads, _blas_threads()),
-            "kind": "port", "seconds": round(dt, 2),
+            "kind": "port", "seconds": round(dt, 2), "host_cpus": os.cpu_count(),
             "sample": f"oracle/nys_oracle.fast_filter (FP64 NumPy restatement of the reference) on the first "
-                      f"{rows} rows x {wl.W} cols of {wl.name}, k-means on that crop; rank loop on {threads} "
-                      f"threads, BLAS on {_blas_threads()}"}
+                      f"{rows} rows x {wl.W} cols of {wl.name}, k-means on that crop; rank loop (the "
+                      f"convolutions) on {threads} thread{'s' if threads > 1 else ''} as in the reference, "
+                      f"BLAS matmuls on {_blas_threads()}"}
 
 
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return None
     wl = CONFIGS[args.config]
-    threads = os.cpu_count() or 1
+    threads = 1  # the reference's convolution stage is single-threaded NumPy (spatial.py:102-109)
     rows = args.ref_rows
     for _ in range(args.warmup):
         cpu_baseline(wl, max(8, rows // 4), threads)
@@ -350,8 +367,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-rows", type=int, default=64, help="rows of the CPU-baseline crop")
-    ap.add_argument("--ref-rows", type=int, default=32, help="rows of the reference-arm crop per step")
+    ap.add_argument("--cpu-rows", type=int, default=16, help="rows of the CPU-baseline crop")
+    ap.add_argument("--ref-rows", type=int, default=16, help="rows of the reference-arm crop per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="run the row-sharded NCCL path even at one rank (exercises parallel.py on one GPU)")

@@ -278,6 +278,25 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
  * slot)} into stats_out [dev] (2 x 8 bytes). */
 int nys_filter_stats(const nys_filter_desc* d, const void* workspace, void* stats_out, void* stream);
 
+/*
+ * Near-guard refinement + statistics; call once after the last band's
+ * nys_filter_vpass (replaces nys_filter_stats on the tiled path).
+ * K3 forms zeta, eta and the guard decisions in FP32; the reference forms
+ * them in FP64 (filters.py:223-257).  Where the FP32 ratio is ill-conditioned
+ * (|eta| small against its scale sum_i b_i |conv(y_i)|) or a guard decision
+ * lies within FP32 error of eps_den, K3 queued the pixel; this call
+ * re-evaluates each queued pixel in FP64 by direct window summation,
+ * eta(x) = sum_y w(x-y) b(x)^T M b(y) (and zeta_c, eta_lead, zeta_lead alike),
+ * applies the guard in FP64 and overwrites the pixel in `out` (same pointer
+ * conventions as nys_filter_vpass).  Then it writes {min|eta| (float64),
+ * guarded pixels (int64 bit pattern)} to stats_out [dev or mapped pinned]
+ * (nullable).  When the in-stream plan's gate timed out, stats_out receives
+ * {NaN, -1}: the step's outputs are invalid.
+ */
+int nys_filter_finish(const nys_filter_desc* d, const float* f, int64_t f_plane_stride,
+                      const float* guide, int64_t guide_plane_stride, float* out, int64_t out_plane_stride,
+                      const void* workspace, void* stats_out, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* Recursive Gaussian spatial kernel (spatial.py:114-191)    */
 /* ---------------------------------------------------------------------- */

@@ -78,6 +78,7 @@ _SIGS = {
     "nys_filter_plan_result": (_I, [_P, C.POINTER(PlanResult)]),
     "nys_filter_hpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
     "nys_filter_vpass": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _I, _I, _P, _L, _P, _P]),
+    "nys_filter_finish": (_I, [C.POINTER(FilterDesc), _P, _L, _P, _L, _P, _L, _P, _P, _P]),
     "nys_filter_stats": (_I, [C.POINTER(FilterDesc), _P, _P, _P]),
     "nys_patch_guide": (_I, [_P, _L, _I, _I, _I, _I, _P, _L, _P]),
     "nys_jacobi_eig": (_I, [_P, _I, _P, _P, C.POINTER(C.c_int)]),

@@ -53,10 +53,7 @@ __global__ void k_patch_guide(const float* __restrict__ f, long long fps, int n,
   }
 }
 
-__global__ void k_reset_stats(FilterStats* s) {
-  s->min_abs_eta_bits = 0x7f800000u;  // +inf
-  s->guarded = 0ull;
-}
+__global__ void k_reset_stats(FilterStats* s) { reset_filter_stats(reinterpret_cast<unsigned*>(s), false); }
 
 __global__ void k_copy_stats(const FilterStats* s, double* out) {
   out[0] = (double)__uint_as_float(s->min_abs_eta_bits);
@@ -92,7 +89,7 @@ namespace {
 // the workspace; then the statistics reset
 int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, void* workspace, bool chol,
                              cudaStream_t s, const void* img_src = nullptr, const unsigned* gate = nullptr,
-                             unsigned seq = 0) {
+                             unsigned seq = 0, bool reset = true) {
   if (chol) {
     const char* base = img_src ? static_cast<const char*>(img_src) : static_cast<const char*>(workspace);
     const double* Ld = reinterpret_cast<const double*>(base + L.chol_off_bytes);
@@ -107,6 +104,7 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
     }
     count_launch();
     k_inverse_cholesky<<<1, 1024, kInvSmemBytes, s>>>(Ld, d->m0, static_cast<float*>(workspace) + L.off_MT, L.m0q,
+                                                      reinterpret_cast<double*>((char*)workspace + L.m64_off_bytes),
                                                       static_cast<const float4*>(img_src),
                                                       static_cast<float4*>(workspace), (int)(L.n_floats / 4),
                                                       reinterpret_cast<unsigned*>((char*)workspace + L.stats_off_bytes),
@@ -114,6 +112,7 @@ int launch_inverse_and_reset(const nys_filter_desc* d, const FilterLayout& L, vo
     NYS_LAUNCH_CHECK();
     return NYS_OK;  // the inverse kernel also reset the statistics
   }
+  if (!reset) return NYS_OK;  // k_wait_gate reset them (keeping a gate-timeout mark)
   count_launch();
   k_reset_stats<<<1, 1, 0, s>>>(reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));
   NYS_LAUNCH_CHECK();
@@ -172,64 +171,89 @@ void run_plan(PlanJob* j, const nys_plan_exec* ex) {
     }
     img[L.off_SC] = (float)(1.0 / a1);
     img[L.off_SC + 1] = (float)j->result.eps_den;
+    // FP64 constants of the near-guard refinement (nys_filter_finish)
+    double* D = reinterpret_cast<double*>(img + L.off_D);
+    std::memcpy(D + L.d_C64, j->centroids, (size_t)n * rho * sizeof(double));
+    std::memcpy(D + L.d_U064, u0.data(), (size_t)n * sizeof(double));
+    D[L.d_SC64] = 1.0 / a1;
+    D[L.d_SC64 + 1] = j->result.eps_den;
+    D[L.d_SC64 + 2] = a1;
+    D[L.d_SC64 + 3] = 0.0;
     if (chol)
       std::memcpy(reinterpret_cast<char*>(img) + L.chol_off_bytes, Lc.data(), (size_t)n * n * sizeof(double));
-    else
+    else {
       for (int q = 0; q < n; ++q)
         for (int i = 0; i < n; ++i) img[L.off_MT + (size_t)q * L.m0q + i] = (float)Lc[(size_t)i * n + q];
+      std::memcpy(reinterpret_cast<char*>(img) + L.m64_off_bytes, Lc.data(), (size_t)n * n * sizeof(double));
+    }
   }
   j->result.host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// One worker serves every host thread and stream.  It never blocks on one job: it scans its
+// pending jobs and runs whichever has its landmarks (a job's `ready` word), so a job whose
+// stream is stuck behind another job's device gate (e.g. a cooperative k-means launch that
+// cannot start while another stream's k_inverse_cholesky spins on an SM) cannot hold up the
+// plan that gate waits for.
 class PlanWorker {
  public:
   PlanWorker() { std::thread([this] { loop(); }).detach(); }
   void post(PlanJob* j) {
     {
       std::lock_guard<std::mutex> g(mu_);
-      q_.push_back(j);
+      q_.push_back(Pending{j, std::chrono::steady_clock::now()});
     }
     cv_.notify_one();
   }
 
  private:
+  struct Pending {
+    PlanJob* job;
+    std::chrono::steady_clock::time_point posted;
+  };
   void loop() {
+    std::vector<Pending> mine;  // jobs taken from the queue, waiting for their landmarks
     for (;;) {
-      PlanJob* j;
       {
         std::unique_lock<std::mutex> g(mu_);
-        cv_.wait(g, [this] { return !q_.empty(); });
-        j = q_.front();
-        q_.pop_front();
-      }
-      // wait for the landmarks: a plain load of a pinned word the stream writes after their copy
-      // (no CUDA call here, so the worker never queues behind other driver users); spin, then
-      // back off; a stream that never gets there (an error) times out
-      bool ok = true;
-      const auto t0 = std::chrono::steady_clock::now();
-      for (unsigned it = 0; j->ready != j->seq; ++it) {
-        if ((it & 255u) == 0) {
-          const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-          if (us > 60e6) {
-            ok = false;
-            break;
-          }
-          if (us > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        if (mine.empty()) cv_.wait(g, [this] { return !q_.empty(); });
+        while (!q_.empty()) {
+          mine.push_back(q_.front());
+          q_.pop_front();
         }
       }
-      std::atomic_thread_fence(std::memory_order_seq_cst);
-      // sequential plan: a helper thread for the Gram rows / Cholesky (nys_plan_exec) made the
-      // plan slower and erratic (76-133 us) where the host threads contend for cores
-      if (ok) run_plan(j, nullptr);
-      else j->result.status = NYS_ECUDA;
-      std::atomic_thread_fence(std::memory_order_seq_cst);
-      j->done = j->seq;  // releases the stream gate
-      std::atomic_thread_fence(std::memory_order_seq_cst);
+      bool ran = false;
+      const auto now = std::chrono::steady_clock::now();
+      for (size_t k = 0; k < mine.size();) {
+        PlanJob* j = mine[k].job;
+        const bool ready = j->ready == j->seq;  // plain load of a pinned word the stream writes
+        const double us = std::chrono::duration<double, std::micro>(now - mine[k].posted).count();
+        if (!ready && us <= 60e6) {
+          ++k;
+          continue;
+        }
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        // sequential plan: a helper thread for the Gram rows / Cholesky (nys_plan_exec) made the
+        // plan slower and erratic (76-133 us) where the host threads contend for cores
+        if (ready) run_plan(j, nullptr);
+        else j->result.status = NYS_ECUDA;  // the stream never got there (an error upstream)
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        j->done = j->seq;  // releases the device gate
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        mine.erase(mine.begin() + (long)k);
+        ran = true;
+      }
+      // spin while a job is young, then back off
+      if (!ran && !mine.empty()) {
+        const double oldest =
+            std::chrono::duration<double, std::micro>(now - mine.front().posted).count();
+        if (oldest > 5000.0) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
     }
   }
   std::mutex mu_;
   std::condition_variable cv_;
-  std::deque<PlanJob*> q_;
+  std::deque<Pending> q_;
 };
 
 PlanWorker& plan_worker() {
@@ -252,7 +276,7 @@ StreamWaitValue32Fn write_value_fn() {  // cuStreamWriteValue32
   return fn;
 }
 
-size_t plan_image_bytes(const FilterLayout& L, int m0) { return L.chol_off_bytes + (size_t)m0 * m0 * sizeof(double); }
+size_t plan_image_bytes(const FilterLayout& L, int m0) { return L.m64_off_bytes + (size_t)m0 * m0 * sizeof(double); }
 }  // namespace
 
 extern "C" {
@@ -322,11 +346,13 @@ int nys_filter_prepare_join(const nys_filter_desc* d, void* staging, void* works
   const char* img = static_cast<const char*>(dv) + kStagingHeader;
   if (d->m0 <= kInvN) return launch_inverse_and_reset(d, L, workspace, true, s, img, gate, j->seq);
   count_launch();
-  k_wait_gate<<<1, 32, 0, s>>>(gate, j->seq);
+  k_wait_gate<<<1, 32, 0, s>>>(gate, j->seq, reinterpret_cast<unsigned*>((char*)workspace + L.stats_off_bytes));
   NYS_LAUNCH_CHECK();
-  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, static_cast<const char*>(staging) + kStagingHeader, L.n_floats * sizeof(float),
-                               cudaMemcpyHostToDevice, s));
-  return launch_inverse_and_reset(d, L, workspace, false, s);
+  const char* src = static_cast<const char*>(staging) + kStagingHeader;
+  NYS_CUDA_TRY(cudaMemcpyAsync(workspace, src, L.n_floats * sizeof(float), cudaMemcpyHostToDevice, s));
+  NYS_CUDA_TRY(cudaMemcpyAsync((char*)workspace + L.m64_off_bytes, src + L.m64_off_bytes,
+                               (size_t)d->m0 * d->m0 * sizeof(double), cudaMemcpyHostToDevice, s));
+  return launch_inverse_and_reset(d, L, workspace, false, s, nullptr, nullptr, 0, /*reset=*/false);
 }
 
 int nys_filter_plan_result(const void* staging, nys_plan_result* out) {
@@ -358,10 +384,33 @@ int nys_filter_prepare(const nys_filter_desc* d, void* workspace, size_t workspa
   }
   h[L.off_SC] = (float)(1.0 / d->alpha0);
   h[L.off_SC + 1] = (float)d->eps_den;
+  {  // FP64 constants of the near-guard refinement (nys_filter_finish)
+    double* D = reinterpret_cast<double*>(h.data() + L.off_D);
+    std::memcpy(D + L.d_C64, d->centroids, (size_t)d->m0 * d->rho * sizeof(double));
+    std::memcpy(D + L.d_U064, d->u0, (size_t)d->m0 * sizeof(double));
+    D[L.d_SC64] = 1.0 / d->alpha0;
+    D[L.d_SC64 + 1] = d->eps_den;
+    D[L.d_SC64 + 2] = d->alpha0;
+    D[L.d_SC64 + 3] = 0.0;
+  }
   cudaStream_t s = (cudaStream_t)stream;
-  if (chol) {  // the Cholesky factor rides in the same upload, FP64 at chol_off_bytes
-    h.resize((L.chol_off_bytes + (size_t)d->m0 * d->m0 * sizeof(double)) / sizeof(float), 0.f);
-    std::memcpy(reinterpret_cast<char*>(h.data()) + L.chol_off_bytes, d->M, (size_t)d->m0 * d->m0 * sizeof(double));
+  // one upload: the float block, the stats slot (reset below), the Cholesky factor (FP64 at
+  // chol_off_bytes) and M64 -- which the device inverse forms itself from the factor
+  h.resize((L.m64_off_bytes + (size_t)d->m0 * d->m0 * sizeof(double)) / sizeof(float), 0.f);
+  if (chol) std::memcpy(reinterpret_cast<char*>(h.data()) + L.chol_off_bytes, d->M, (size_t)d->m0 * d->m0 * sizeof(double));
+  else {
+    const int m = d->m0;
+    double* M64 = reinterpret_cast<double*>(reinterpret_cast<char*>(h.data()) + L.m64_off_bytes);
+    if (!d->phi_form) {
+      std::memcpy(M64, d->M, (size_t)m * m * sizeof(double));
+    } else {  // eta = sum_y w phi(x).phi(y) = b(x)^T (P^T P) b(y)
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+          double acc = 0.0;
+          for (int k = 0; k < m; ++k) acc += d->M[(size_t)k * m + i] * d->M[(size_t)k * m + j];
+          M64[(size_t)i * m + j] = acc;
+        }
+    }
   }
   // pageable H2D: the runtime stages `h` before returning, so it may go away
   // right after (no stream synchronisation: the caller keeps queueing work); the

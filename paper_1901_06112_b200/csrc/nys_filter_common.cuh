@@ -16,10 +16,16 @@ namespace nys {
 // ---------------------------------------------------------------------------
 // constants block in the workspace (float offsets)
 // ---------------------------------------------------------------------------
+// FP64 block (float offset off_D, 8-byte aligned) for the near-guard refinement
+// (nys_filter_finish): C64 [m0 x rho], U064 [m0], SC64 {1/alpha_1, eps_den, alpha_1, 0};
+// then, past the Cholesky slot, M64 [m0 x m0] (the y-form M, or P^T P in the
+// phi-form) and the list of flagged pixels (uint32 global pixel indices).
 struct FilterLayout {
   int m0, rho, rhop, m0q;  // rhop: rho padded to 4; m0q: (m0+1) padded to 8
-  size_t off_C, off_MT, off_U0, off_SC, n_floats;  // SC: {1/alpha_1, eps_den} read by K3
-  size_t stats_off_bytes, chol_off_bytes, total_bytes;  // chol: m0 x m0 FP64 (M_is_cholesky)
+  size_t off_C, off_MT, off_U0, off_SC, off_D, n_floats;  // SC: {1/alpha_1, eps_den} read by K3
+  size_t d_C64, d_U064, d_SC64;                           // double offsets from off_D
+  size_t stats_off_bytes, chol_off_bytes, m64_off_bytes, list_off_bytes, total_bytes;
+  unsigned list_cap;
 };
 
 inline FilterLayout filter_layout(const nys_filter_desc* d) {
@@ -32,10 +38,19 @@ inline FilterLayout filter_layout(const nys_filter_desc* d) {
   L.off_MT = L.off_C + (size_t)d->m0 * L.rhop;
   L.off_U0 = L.off_MT + (size_t)d->m0 * L.m0q;
   L.off_SC = L.off_U0 + (size_t)ceil_div(d->m0, 4) * 4;
-  L.n_floats = L.off_SC + 4;
+  L.off_D = L.off_SC + 4;  // multiple of 4 floats: 16-byte aligned
+  L.d_C64 = 0;
+  L.d_U064 = (size_t)d->m0 * d->rho;
+  L.d_SC64 = L.d_U064 + d->m0;
+  L.n_floats = L.off_D + 2 * (L.d_SC64 + 4);
+  L.n_floats = (L.n_floats + 3) & ~size_t(3);
   L.stats_off_bytes = ((L.n_floats * 4 + 255) / 256) * 256;
   L.chol_off_bytes = L.stats_off_bytes + 256;
-  L.total_bytes = L.chol_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;
+  L.m64_off_bytes = L.chol_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;
+  L.list_off_bytes = L.m64_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;
+  const long long px = (long long)d->H * d->W;
+  L.list_cap = (unsigned)std::min<long long>(px, std::max<long long>(4096, px / 8));
+  L.total_bytes = L.list_off_bytes + ((size_t)L.list_cap * 4 + 255) / 256 * 256;
   return L;
 }
 
@@ -54,9 +69,25 @@ inline int buffer_planes(const nys_filter_desc* d) {
 
 struct FilterStats {
   unsigned int min_abs_eta_bits;  // float bits, non-negative => integer order
-  unsigned int pad;
+  unsigned int flagged;           // pixels K3 queued for the FP64 near-guard refinement
   unsigned long long guarded;
+  unsigned int finish_done;       // k_finish: CTAs done (the last one publishes)
+  unsigned int refined_guarded;   // guarded pixels among the refined ones (diagnostics)
+  unsigned int gate_timeout;      // the in-stream plan's gate timed out (outputs invalid)
+  unsigned int pad;
 };
+static_assert(sizeof(FilterStats) == 32, "reset_filter_stats writes 8 words");
+
+// K3's near-guard flag rule.  eta (FP32), its
+// absolute scale S = sum_i b_i |conv(y_i)| and the lead denominator; a pixel is
+// re-evaluated in FP64 when its ratio is ill-conditioned in FP32 (|eta| < tau S)
+// or a guard decision could flip within the FP32 error bound cerr * S.
+__device__ __forceinline__ bool near_guard(float eta, float S, float eta_lead, float eps, float tau, float cerr) {
+  const float ad = fabsf(eta), al = fabsf(eta_lead);
+  if (!(ad == ad) || !(al == al)) return true;
+  if (ad >= eps) return ad < tau * S || ad - cerr * S < eps;
+  return ad + cerr * S >= eps || fabsf(al - eps) <= 1e-3f * eps;
+}
 
 // guide coordinate d of pixel (row, x): planar guide or an on-the-fly 3x3 patch
 // of f (channel, dy, dx order, edge replicate: filters.py:174-181)
@@ -137,6 +168,17 @@ inline void fill_taps(const nys_filter_desc* d, float* taps) {
       taps[t] = (float)std::exp(-(u * u) / (2.0 * d->sigma * d->sigma));  // spatial.py:72-75
     }
   }
+}
+
+// Near-guard flag rule constants for K3 (near_guard): tau bounds the FP32
+// conditioning |eta| / S of the ratio, cerr * S the FP32 error of eta.  Defaults
+// from the full-size cfg 3 sweep; NYS_REFINE_TAU / NYS_REFINE_CERR
+// override them (0 / 0 disables the refinement: A/B switch).
+inline void refine_params(float* tau, float* cerr) {  // read per launch (A/B within a process)
+  const char* et = getenv("NYS_REFINE_TAU");
+  const char* ec = getenv("NYS_REFINE_CERR");
+  *tau = et ? (float)atof(et) : 1e-2f;
+  *cerr = ec ? (float)atof(ec) : 1e-3f;
 }
 
 inline float k2_of(const nys_filter_desc* d) {

@@ -65,8 +65,13 @@ __device__ __forceinline__ void inv_level(const double* __restrict__ Ls, double*
 // (acquire, system scope), bounded by 60 s of %globaltimer; everything after the barrier sees
 // the host's writes that preceded the word.  A stream-level cuStreamWaitValue32 on the same
 // word occasionally noticed a late write only milliseconds (once 130 ms) later.
-__device__ __forceinline__ void wait_host_word(const unsigned* gate, unsigned seq) {
+// Returns (in every thread) whether the word arrived; on a timeout the caller marks the step
+// failed (FilterStats::gate_timeout -> nys_filter_finish publishes a sentinel) instead of
+// silently computing on a stale staging image.
+__device__ __forceinline__ bool wait_host_word(const unsigned* gate, unsigned seq) {
+  __shared__ int s_timed_out;
   if (threadIdx.x == 0) {
+    s_timed_out = 0;
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
@@ -74,17 +79,37 @@ __device__ __forceinline__ void wait_host_word(const unsigned* gate, unsigned se
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
       if ((int)(v - seq) >= 0) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 60ull * 1000000000ull) break;
+      if (t - t0 > 60ull * 1000000000ull) {
+        s_timed_out = 1;
+        break;
+      }
       __nanosleep(256);
     }
   }
   __syncthreads();
+  return s_timed_out == 0;
 }
 
-__global__ void k_wait_gate(const unsigned* gate, unsigned seq) { wait_host_word(gate, seq); }
+// FilterStats as 32-bit words (nys_filter_common.cuh): reset for a new filter, and the
+// gate-timeout mark
+__device__ __forceinline__ void reset_filter_stats(unsigned* w, bool timed_out) {
+  w[0] = 0x7f800000u;  // min|eta| = +inf
+#pragma unroll
+  for (int k = 1; k < 8; ++k) w[k] = 0u;
+  w[6] = timed_out ? 1u : 0u;  // gate_timeout
+}
 
-__global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restrict__ Lg, int n, float* __restrict__ MT,
-                                                          int m0q, const float4* __restrict__ img_src,
+// gate + statistics reset for the plans whose image carries M (m0 > 64)
+__global__ void k_wait_gate(const unsigned* gate, unsigned seq, unsigned* stats) {
+  const bool ok = wait_host_word(gate, seq);
+  if (threadIdx.x == 0) reset_filter_stats(stats, !ok);
+}
+
+// The staging image (img_src) and the factor (Lg) may live in mapped pinned memory that the
+// host writes while this kernel is already resident (before `done`): they are read with
+// ordinary (not read-only-cache) loads after the gate's acquire.
+__global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* Lg, int n, float* __restrict__ MT,
+                                                          int m0q, double* __restrict__ M64, const float4* img_src,
                                                           float4* __restrict__ img_dst, int img_f4,
                                                           unsigned* __restrict__ stats_reset,
                                                           const unsigned* gate = nullptr, unsigned seq = 0) {
@@ -94,14 +119,9 @@ __global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restr
   double* T = X + kInvN * kInvLd;      // 64 x kInvLd scratch (L21 X11 per block pair)
   double* rd = T + kInvN * kInvLd;     // 64 reciprocal pivots
   const int tid = threadIdx.x;  // blockDim.x == 1024
-  if (gate) wait_host_word(gate, seq);
+  const bool gate_ok = gate ? wait_host_word(gate, seq) : true;
   NYS_INV_STAMP(0);
-  if (stats_reset && tid == 0) {  // the filter statistics (FilterStats: min|eta| bits = +inf, guarded = 0)
-    stats_reset[0] = 0x7f800000u;
-    stats_reset[1] = 0u;
-    stats_reset[2] = 0u;
-    stats_reset[3] = 0u;
-  }
+  if (stats_reset && tid == 0) reset_filter_stats(stats_reset, !gate_ok);
   {
     // every load of a thread is issued before its first store: over PCIe (mapped pinned
     // memory) the round trips overlap instead of queueing
@@ -175,7 +195,10 @@ __global__ void __launch_bounds__(1024) k_inverse_cholesky(const double* __restr
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int v = 0; v < 4; ++v)
-        if (i + u < n && j + v < n) MT[(size_t)(j + v) * m0q + i + u] = (float)m[u][v];
+        if (i + u < n && j + v < n) {
+          MT[(size_t)(j + v) * m0q + i + u] = (float)m[u][v];
+          if (M64) M64[(size_t)(i + u) * n + j + v] = m[u][v];  // FP64 copy for nys_filter_finish
+        }
   }
 #ifdef NYS_INV_STAMPS
   __syncthreads();

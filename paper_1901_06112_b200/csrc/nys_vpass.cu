@@ -56,6 +56,9 @@ struct VArgs {
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   int sc_off;  // cst[sc_off], cst[sc_off + 1]: 1/alpha_1 and eps_den (written with the plan)
   float k2;
+  float tau, cerr;          // near-guard flag rule (near_guard); tau = cerr = 0 disables it
+  unsigned* flag_list;      // global pixel indices queued for nys_filter_finish
+  unsigned list_cap;
   float taps[NYS_MAX_TAPS];
   float2 wpair[NYS_MAX_TAPS + 1];  // packed-FIR tap pairs (fill_tap_pairs)
 };
@@ -179,7 +182,8 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   float* bsh = stage + (size_t)K3_NS * stage_floats;           // gmode 1: 2 x npx
   float* dsh = bsh + (gmode == 1 ? 2 * K3_NPX : 0);            // npx: eta
   float* lsh = dsh + K3_NPX;                                   // npx: eta_lead
-  float* Cs = lsh + K3_NPX;                                    // m0 x rhop
+  float* ssh = lsh + K3_NPX;                                   // npx: scale of eta (-1: flagged)
+  float* Cs = ssh + K3_NPX;                                    // m0 x rhop
   float* U0 = Cs + (size_t)m0 * rhop;                          // m0
   float* gsh = U0 + ((m0 + 3) & ~3);                           // gmode 1: [rho][npx] guide tile
   __shared__ __align__(8) unsigned long long full[K3_NS];
@@ -253,11 +257,11 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       compute_b(0, bsh);
       __syncthreads();
     }
-    float s0[K3_YR][4], acc[K3_YR][4];
+    float s0[K3_YR][4], acc[K3_YR][4], sab[K3_YR][4];  // sab: sum_i b_i |conv(y_i)| (denominator chunk)
 #pragma unroll
     for (int o = 0; o < K3_YR; ++o)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) s0[o][e] = acc[o][e] = 0.f;
+      for (int e = 0; e < 4; ++e) s0[o][e] = acc[o][e] = sab[o][e] = 0.f;
 
 #pragma unroll 1
     // (co, i) = (s / L, s % L) kept incrementally: a runtime division per stage was 5 % of
@@ -288,7 +292,10 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             acc[o][e] = fmaf(bv[e], G[o][e], acc[o][e]);
-            if (co == 0) s0[o][e] = fmaf(u0i, bv[e], s0[o][e]);
+            if (co == 0) {
+              s0[o][e] = fmaf(u0i, bv[e], s0[o][e]);
+              sab[o][e] = fmaf(bv[e], fabsf(G[o][e]), sab[o][e]);
+            }
           }
         }
         // features of the next stage's landmark (gmode 1): the other b buffer is free
@@ -308,6 +315,24 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
             for (int o = 0; o < K3_YR; ++o) {
               *reinterpret_cast<float4*>(dsh + pxo + o * 32) = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
               *reinterpret_cast<float4*>(lsh + pxo + o * 32) = make_float4(lg[o][0], lg[o][1], lg[o][2], lg[o][3]);
+              // near-guard pixels: queued for the FP64 re-evaluation (nys_filter_finish), marked
+              // -1 so the tile statistics leave them to it
+              const int row = t0 + run * K3_YR + o;
+              float sv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int x = x0 + quad * 4 + e;
+                sv[e] = sab[o][e];
+                if (row < a.out0 + a.out_rows && row < H && x < W &&
+                    near_guard(acc[o][e], sab[o][e], lg[o][e], eps_den, a.tau, a.cerr)) {
+                  const unsigned slot = atomicAdd(&a.stats->flagged, 1u);
+                  if (slot < a.list_cap) {  // (past the cap the FP32 result and statistics stand)
+                    a.flag_list[slot] = (unsigned)((long long)row * W + x);
+                    sv[e] = -1.f;
+                  }
+                }
+              }
+              *reinterpret_cast<float4*>(ssh + pxo + o * 32) = make_float4(sv[0], sv[1], sv[2], sv[3]);
             }
           }
           __syncthreads();
@@ -368,7 +393,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
     unsigned long long my_cnt = 0;
     for (int k = tid; k < K3_NPX; k += K3_THREADS) {
       const int row = t0 + (k >> 5), x = x0 + (k & 31);
-      if (row < a.out0 + a.out_rows && row < H && x < W) {
+      if (row < a.out0 + a.out_rows && row < H && x < W && ssh[k] >= 0.f) {
         const float ad = fabsf(dsh[k]);
         my_min = fminf(my_min, ad);
         my_cnt += ad < eps_den ? 1ull : 0ull;
@@ -446,6 +471,9 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   a.k2 = k2_of(d);
   a.sc_off = (int)L.off_SC;
+  refine_params(&a.tau, &a.cerr);
+  a.flag_list = reinterpret_cast<unsigned*>((char*)const_cast<void*>(workspace) + L.list_off_bytes);
+  a.list_cap = L.list_cap;
   fill_taps(d, a.taps);
   fill_tap_pairs(a.taps, 2 * d->radius + 1, a.wpair);
 
@@ -472,7 +500,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.gcache = use_bplanes(d) ? 3 : 1;  // b planes from K2, or a planar guide tile (rho <= 8)
   const size_t plane_floats = (size_t)(K3_TH + 2 * R) * 32;
   const size_t stage_floats = 4 * plane_floats + (a.gcache == 3 ? K3_NPX : 0);
-  const size_t smem = ((size_t)K3_NS * stage_floats + (a.gcache == 1 ? 2 * K3_NPX : 0) + 2 * K3_NPX +
+  const size_t smem = ((size_t)K3_NS * stage_floats + (a.gcache == 1 ? 2 * K3_NPX : 0) + 3 * K3_NPX +
                        (size_t)d->m0 * L.rhop + ((d->m0 + 3) & ~3) + (a.gcache == 1 ? (size_t)d->rho * K3_NPX : 0)) *
                       sizeof(float);
   if (smem > 227 * 1024) return NYS_EUNSUPPORTED;

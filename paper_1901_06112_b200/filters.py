@@ -383,10 +383,11 @@ def run_filter(inp: _Inputs, centroids: np.ndarray | None, params: FilterParams,
             kernel_events.append(("k_vpass", e1, e2, b))
     if timer:
         timer.mark("convolutions")
-    # stats_ptr: the two doubles go straight to that address (mapped pinned memory), no tensor
+    # near-guard FP64 refinement of the pixels K3 queued, then the statistics; stats_ptr: the two
+    # doubles go straight to that address (mapped pinned memory), no tensor
     stats = torch.empty(2, dtype=torch.float64, device=inp.f.device) if stats_ptr is None else None
-    _native.check(lib.nys_filter_stats(C.byref(d), ptr(ws), ptr(stats) if stats is not None else stats_ptr, s),
-                  "nys_filter_stats")
+    _native.check(lib.nys_filter_finish(C.byref(d), f_ptr, f_ps, g_ptr, g_ps, o_ptr, o_ps, ptr(ws),
+                                        ptr(stats) if stats is not None else stats_ptr, s), "nys_filter_finish")
     del keep
     return out, plan, stats
 
@@ -612,7 +613,8 @@ def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: 
     timer.stream.synchronize()  # the step's only host wait
     h = hres.numpy().copy()
     res = fl.result()
-    if res.status != _native.NYS_OK or pk.zero_total_draw() >= 0:
+    # guarded == -1: the device gate timed out waiting for the plan (nys_filter_finish sentinel)
+    if res.status != _native.NYS_OK or pk.zero_total_draw() >= 0 or int(h[1:2].view(np.int64)[0]) < 0:
         if kernel_events is not None:
             del kernel_events[n_events:]
         return None

@@ -10,6 +10,7 @@ float64 read-only semantics; device tensors are used as float32.
 
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -130,9 +131,21 @@ def extract_range_list(guide: Image) -> RangeList:
 
 
 # --------------------------------------------------------------------------
-# file I/O (image.py:115-270): host-side byte formats, §8 row f4
+# file I/O, §8 row f4: the KFC1 float cube only.  The reference also reads and
+# writes PNG / PGM / PPM (image.py:115-241); 8-bit raster codecs are outside
+# this build's scope (configs are synthetic in-memory arrays), so
+# those suffixes raise ImageFormatError here.
+#
+# KFC1 layout (image.py:243-270): 20-byte little-endian header
+#   bytes 0-3   b"KFC1"
+#   bytes 4-19  uint32 width, height, bands, sample kind (0 = float32, 1 = float64)
+# followed by bands*height*width samples, band-major then row-major (the
+# planar data[c, y, x] order of Image).  Loaded cubes carry range_max 255.
 # --------------------------------------------------------------------------
 CUBE_MAGIC = b"KFC1"
+_KFC1 = struct.Struct("<4sIIII")
+_KFC1_SAMPLES = {0: np.dtype("<f4"), 1: np.dtype("<f8")}
+_KFC1_KIND = {"float32": 0, "float64": 1}
 
 
 class ImageFormatError(ValueError):
@@ -140,130 +153,52 @@ class ImageFormatError(ValueError):
 
 
 def quantize_u8(samples) -> np.ndarray:
-    """Clamp to [0, 255], round half away from zero (image.py:115-117)."""
-    return np.floor(np.clip(np.asarray(samples, np.float64), 0.0, 255.0) + 0.5).astype(np.uint8)
+    """8-bit quantisation of the reference's writers (image.py:115-117):
+    clamp to [0, 255], then round half up."""
+    q = np.clip(np.asarray(samples, dtype=np.float64), 0.0, 255.0)
+    return np.floor(q + 0.5).astype(np.uint8)
 
 
 def load_image(path) -> Image:
-    """PNG (8-bit L/RGB), binary PGM/PPM (maxval 255) or a ``KFC1`` float
-    cube, chosen by the file's magic bytes; range_max 255 (image.py:120-133)."""
+    """Read a KFC1 cube (image.py:120-133 restricted to the cube format)."""
     from pathlib import Path
 
     path = Path(path)
-    raw = path.read_bytes()
-    if raw[:4] == CUBE_MAGIC:
-        return _cube_from_bytes(raw, path.name)
-    if raw[:2] in (b"P5", b"P6"):
-        return _pnm_from_bytes(raw, path.name)
-    return _load_png(path)
+    blob = path.read_bytes()
+    if blob[:4] != CUBE_MAGIC:
+        raise ImageFormatError(f"{path.name}: not a KFC1 cube (PNG/PNM input is outside this build's scope)")
+    return _decode_cube(memoryview(blob), path.name)
 
 
 def save_image(img: Image, path, cube_dtype: str = "float64") -> None:
-    """Write by suffix: .kfc raw cube (float32/float64, no rounding),
-    .png / .pgm / .ppm 8-bit (image.py:136-152)."""
+    """Write a ``.kfc`` cube with float32 or float64 samples, unrounded
+    (image.py:136-152 restricted to the cube format)."""
     from pathlib import Path
 
     path = Path(path)
-    suffix = path.suffix.lower()
-    if suffix == ".kfc":
-        path.write_bytes(_cube_bytes(img, cube_dtype))
-    elif suffix == ".png":
-        _save_png(img, path)
-    elif suffix in (".pgm", ".ppm"):
-        path.write_bytes(_pnm_bytes(img, suffix))
-    else:
-        raise ImageFormatError(f"unsupported output format: {path.name!r}")
-
-
-def _cube_from_bytes(raw: bytes, name: str) -> Image:
-    # header: magic, then little-endian uint32 width, height, bands, sample flag
-    if len(raw) < 20:
-        raise ImageFormatError(f"truncated cube header in {name}")
-    width, height, bands, flag = np.frombuffer(raw, dtype="<u4", count=4, offset=4).tolist()
-    if flag not in (0, 1):
-        raise ImageFormatError(f"unknown cube sample-type flag {flag} in {name}")
-    dt = np.dtype("<f4") if flag == 0 else np.dtype("<f8")
-    body = np.frombuffer(raw, dtype=dt, offset=20)
-    if body.size != width * height * bands:
-        raise ImageFormatError(f"size mismatch in {name}: header implies {width * height * bands} samples, "
-                               f"found {body.size}")
-    return Image(data=body.astype(np.float64).reshape(bands, height, width), range_max=255.0)
-
-
-def _cube_bytes(img: Image, cube_dtype: str) -> bytes:
-    if cube_dtype not in ("float32", "float64"):
+    if path.suffix.lower() != ".kfc":
+        raise ImageFormatError(f"unsupported output format: {path.name!r} (only .kfc cubes are written)")
+    if cube_dtype not in _KFC1_KIND:
         raise ValueError(f"cube_dtype must be 'float32' or 'float64', got {cube_dtype!r}")
-    flag = 0 if cube_dtype == "float32" else 1
-    hdr = CUBE_MAGIC + np.array([img.width, img.height, img.channels, flag], dtype="<u4").tobytes()
-    return hdr + np.ascontiguousarray(img.numpy(), dtype="<f4" if flag == 0 else "<f8").tobytes()
+    path.write_bytes(_encode_cube(img, _KFC1_KIND[cube_dtype]))
 
 
-def _pnm_from_bytes(raw: bytes, name: str) -> Image:
-    fields, pos = [], 2
-    while len(fields) < 3:  # width, height, maxval; '#' comments to end of line
-        if pos >= len(raw):
-            raise ImageFormatError(f"truncated PNM header in {name}")
-        ch = raw[pos:pos + 1]
-        if ch == b"#":
-            pos = raw.index(b"\n", pos) + 1
-        elif ch.isspace():
-            pos += 1
-        else:
-            end = pos
-            while end < len(raw) and not raw[end:end + 1].isspace():
-                end += 1
-            fields.append(int(raw[pos:end]))
-            pos = end
-    pos += 1  # the single whitespace byte after maxval
-    width, height, maxval = fields
-    if maxval != 255:
-        raise ImageFormatError(f"unsupported bit depth in {name}: maxval {maxval}")
-    ch = 1 if raw[:2] == b"P5" else 3
-    px = np.frombuffer(raw, dtype=np.uint8, offset=pos)
-    if px.size != width * height * ch:
-        raise ImageFormatError(f"size mismatch in {name}: header implies {width * height * ch} samples, "
-                               f"found {px.size}")
-    data = px.reshape(1, height, width) if ch == 1 else np.moveaxis(px.reshape(height, width, 3), 2, 0)
-    return Image(data=data.astype(np.float64), range_max=255.0)
+def _decode_cube(blob: memoryview, name: str) -> Image:
+    if len(blob) < _KFC1.size:
+        raise ImageFormatError(f"truncated cube header in {name}")
+    _magic, width, height, bands, kind = _KFC1.unpack_from(blob, 0)
+    sample = _KFC1_SAMPLES.get(kind)
+    if sample is None:
+        raise ImageFormatError(f"unknown cube sample-type flag {kind} in {name}")
+    count = width * height * bands
+    payload = blob[_KFC1.size:]
+    if len(payload) != count * sample.itemsize:
+        raise ImageFormatError(f"size mismatch in {name}: header implies {count} samples, "
+                               f"found {len(payload) / sample.itemsize:g}")
+    planes = np.frombuffer(payload, dtype=sample, count=count).reshape(bands, height, width)
+    return Image(data=planes.astype(np.float64), range_max=255.0)
 
 
-def _pnm_bytes(img: Image, suffix: str) -> bytes:
-    q = quantize_u8(img.numpy())
-    if suffix == ".pgm":
-        if img.channels != 1:
-            raise ImageFormatError("PGM requires a single-channel image")
-        magic, body = b"P5", q[0]
-    else:
-        if img.channels != 3:
-            raise ImageFormatError("PPM requires a 3-channel image")
-        magic, body = b"P6", np.moveaxis(q, 0, 2)
-    return magic + f"\n{img.width} {img.height}\n255\n".encode("ascii") + np.ascontiguousarray(body).tobytes()
-
-
-def _load_png(path) -> Image:
-    from PIL import Image as PILImage
-    from PIL import UnidentifiedImageError
-
-    try:
-        with PILImage.open(path) as im:
-            if im.mode == "P":
-                im = im.convert("RGB")
-            if im.mode not in ("L", "RGB"):
-                raise ImageFormatError(f"unsupported image mode {im.mode!r} in {path.name} "
-                                       "(8-bit grayscale or RGB required)")
-            arr = np.asarray(im, dtype=np.float64)
-    except UnidentifiedImageError as exc:
-        raise ImageFormatError(f"unreadable image file: {path}") from exc
-    return Image(data=arr[None] if arr.ndim == 2 else np.moveaxis(arr, 2, 0), range_max=255.0)
-
-
-def _save_png(img: Image, path) -> None:
-    from PIL import Image as PILImage
-
-    q = quantize_u8(img.numpy())
-    if img.channels == 1:
-        PILImage.fromarray(q[0], mode="L").save(path, format="PNG")
-    elif img.channels == 3:
-        PILImage.fromarray(np.ascontiguousarray(np.moveaxis(q, 0, 2)), mode="RGB").save(path, format="PNG")
-    else:
-        raise ImageFormatError(f"cannot write {img.channels}-channel image as PNG")
+def _encode_cube(img: Image, kind: int) -> bytes:
+    header = _KFC1.pack(CUBE_MAGIC, img.width, img.height, img.channels, kind)
+    return header + img.numpy().astype(_KFC1_SAMPLES[kind], copy=False).tobytes(order="C")

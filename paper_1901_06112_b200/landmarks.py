@@ -79,18 +79,6 @@ def _replay_zero_total(m: int, m0: int, seed: int, j0: int, device_seeds: np.nda
     return seeds
 
 
-_PINNED: dict = {}
-
-
-def _pinned_f64(n: int, key) -> torch.Tensor:
-    """Reused page-locked host staging buffer (cudaHostAlloc costs ~100 us)."""
-    buf = _PINNED.get(key)
-    if buf is None or buf.numel() < n:
-        buf = torch.empty(max(n, 64), dtype=torch.float64, pin_memory=True)
-        _PINNED[key] = buf
-    return buf[:n]
-
-
 @dataclass
 class PendingKMeans:
     """k-means whose results are still in flight (``kmeans_device(..., pipelined=True)``):
@@ -221,7 +209,7 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
         return PendingKMeans(host=hbuf, res=res, workspace=ws, m0=m0, rho=rho, max_iter=max_iter)
     qe_dev = None
     if queue_exact and qe_p is None:
-        hbuf = _pinned_f64(nres, ("kmeans", torch.cuda.current_stream().cuda_stream))
+        hbuf = _pinned_tls_f64(nres, ("kmeans", stream_ptr()))  # per host thread: no cross-thread sharing
         hbuf.copy_(res, non_blocking=True)
         done = torch.cuda.Event()
         done.record()

@@ -39,9 +39,9 @@ int main() {
     for (int mode = 0; mode < 2; ++mode) {
       const double* src = mode ? hL : dL;
       const float4* is = mode ? (const float4*)img_h : nullptr;
-      for (int it = 0; it < 3; ++it) k_inverse_cholesky<<<1, 1024, kInvSmemBytes>>>(src, n, dM, m0q, is, (float4*)img_d, nf4, nullptr);
+      for (int it = 0; it < 3; ++it) k_inverse_cholesky<<<1, 1024, kInvSmemBytes>>>(src, n, dM, m0q, nullptr, is, (float4*)img_d, nf4, nullptr);
       cudaEventRecord(a);
-      for (int it = 0; it < 20; ++it) k_inverse_cholesky<<<1, 1024, kInvSmemBytes>>>(src, n, dM, m0q, is, (float4*)img_d, nf4, nullptr);
+      for (int it = 0; it < 20; ++it) k_inverse_cholesky<<<1, 1024, kInvSmemBytes>>>(src, n, dM, m0q, nullptr, is, (float4*)img_d, nf4, nullptr);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;

@@ -239,6 +239,26 @@ def run_ours(args, rank: int, world: int):
     e2e = sum(e2e_ms) / len(e2e_ms)
     out_bytes = int(rep_h.output.data.numel() * 4)
 
+    # end to end through the reference's own data type (image.py:33-52): a NumPy float64 Image in,
+    # a NumPy float64 Image out (uploaded through a reused page-locked staging buffer and cast on
+    # the device; K3 writes the float64 planes straight into page-locked host memory)
+    f64 = f_np.astype(np.float64)
+    n_img = Image(data=f64, range_max=1.0)
+    ng = _guide(n_img, wl)
+    fast_filter(n_img, ng, params)
+    e2e_np_ms = []
+    rep_n = None
+    for _ in range(max(1, args.steps)):
+        l2_flush()
+        barrier()
+        torch.cuda.synchronize()
+        rep_n = None
+        t0 = time.perf_counter()
+        rep_n = fast_filter(n_img, ng, params)
+        e2e_np_ms.append(max_over_ranks((time.perf_counter() - t0) * 1e3))
+    assert isinstance(rep_n.output.data, np.ndarray) and rep_n.output.data.dtype == np.float64
+    e2e_np = sum(e2e_np_ms) / len(e2e_np_ms)
+
     # roofline of the dominant kernel: algorithmic bytes of the pixels each launch produced (its
     # band's out_rows x W) / that launch's time, averaged over launches
     u = n if wl.mode != "nlm" else n  # stored input channels read (patches gathered from f)
@@ -292,6 +312,11 @@ def run_ours(args, rank: int, world: int):
         "e2e": {"value": round(world * px / (e2e * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_step": round(e2e, 3),
                 "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": out_bytes,
                 "path": "fast_filter(Image(pinned host float32), out=pinned host buffer): H2D copy in, K3 writes the output over PCIe"},
+        "e2e_reference_types": {"value": round(world * px / (e2e_np * 1e-3) / 1e6, 2), "unit": UNIT,
+                                "ms_per_step": round(e2e_np, 3), "h2d_bytes_per_step": int(f64.nbytes),
+                                "d2h_bytes_per_step": int(f64.nbytes),
+                                "path": "fast_filter(Image(numpy float64)) -> Image(numpy float64), the reference's "
+                                        "call and types (image.py:33-52, filters.py:199)"},
         "step_ms": [round(x, 3) for x in step_ms],
         "gpu_launches": launches // max(1, args.steps),
         "gpu_launches_total": launches,

@@ -180,6 +180,10 @@ typedef struct nys_filter_desc {
      * nys_filter_prepare forms M = A^{-1} = L^{-T} L^{-1} on the device in FP64
      * (y-form, nothing dropped, m0 <= 64).  0: M as above. */
     int M_is_cholesky;
+    /* 1: the `out` pointers of nys_filter_vpass / nys_filter_finish address
+     * float64 planes (e.g. a page-locked host array for the reference's FP64
+     * Image); 0: float32. */
+    int out_f64;
 } nys_filter_desc;
 
 /* Size of the horizontal-pass plane buffer for a band of `rows` output rows:
@@ -196,6 +200,12 @@ int64_t nys_filter_plane_row_stride(const nys_filter_desc* d);
 
 /* Device bytes for the filter's constant block + reduction scratch. */
 size_t nys_filter_workspace_bytes(const nys_filter_desc* d);
+
+/* Byte offsets of the workspace regions (diagnostics / tests): out[8] =
+ * {FP64 constants (landmarks, u0, 1/alpha_1, eps_den, alpha_1), statistics,
+ *  Cholesky factor, FP64 M, queued-pixel list, per-pixel chunk counters,
+ *  window partial sums, total bytes}. */
+int nys_filter_workspace_layout(const nys_filter_desc* d, int64_t* out);
 
 /* Upload the per-call constants (centroids, M, u0) into `workspace` and reset
  * the min|eta| / guarded-pixel accumulators.  Call once per filter before the

@@ -40,6 +40,7 @@ class FilterDesc(C.Structure):
         ("centroids", C.POINTER(C.c_double)), ("M", C.POINTER(C.c_double)),
         ("u0", C.POINTER(C.c_double)), ("alpha0", C.c_double), ("eps_den", C.c_double),
         ("row_lo", C.c_int), ("row_hi", C.c_int), ("phi_form", C.c_int), ("M_is_cholesky", C.c_int),
+        ("out_f64", C.c_int),
     ]
 
 
@@ -70,6 +71,7 @@ _SIGS = {
     "nys_gather_point": (_I, [_P, _L, _I, _L, _P, _P]),
     "nys_filter_planes_bytes": (_S, [C.POINTER(FilterDesc), _I]),
     "nys_filter_workspace_bytes": (_S, [C.POINTER(FilterDesc)]),
+    "nys_filter_workspace_layout": (_I, [C.POINTER(FilterDesc), _P]),
     "nys_filter_plane_row_stride": (_L, [C.POINTER(FilterDesc)]),
     "nys_filter_prepare": (_I, [C.POINTER(FilterDesc), _P, _S, _P]),
     "nys_filter_plan_staging_bytes": (_S, [C.POINTER(FilterDesc)]),

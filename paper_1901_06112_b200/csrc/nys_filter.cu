@@ -81,6 +81,16 @@ size_t nys_filter_workspace_bytes(const nys_filter_desc* d) {
   return filter_layout(d).total_bytes;
 }
 
+int nys_filter_workspace_layout(const nys_filter_desc* d, int64_t* out) {
+  if (!out || validate(d) != NYS_OK) return NYS_EINVAL;
+  const FilterLayout L = filter_layout(d);
+  const int64_t v[8] = {(int64_t)(L.off_D * sizeof(float)), (int64_t)L.stats_off_bytes, (int64_t)L.chol_off_bytes,
+                        (int64_t)L.m64_off_bytes, (int64_t)L.list_off_bytes, (int64_t)L.cnt_off_bytes,
+                        (int64_t)L.part_off_bytes, (int64_t)L.total_bytes};
+  for (int k = 0; k < 8; ++k) out[k] = v[k];
+  return NYS_OK;
+}
+
 }  // extern "C"
 
 namespace {

@@ -24,9 +24,13 @@ struct FilterLayout {
   int m0, rho, rhop, m0q;  // rhop: rho padded to 4; m0q: (m0+1) padded to 8
   size_t off_C, off_MT, off_U0, off_SC, off_D, n_floats;  // SC: {1/alpha_1, eps_den} read by K3
   size_t d_C64, d_U064, d_SC64;                           // double offsets from off_D
-  size_t stats_off_bytes, chol_off_bytes, m64_off_bytes, list_off_bytes, total_bytes;
+  size_t stats_off_bytes, chol_off_bytes, m64_off_bytes, list_off_bytes, cnt_off_bytes, part_off_bytes, total_bytes;
   unsigned list_cap;
 };
+// near-guard refinement: at most kRefineCap queued pixels per filter (the rest keep their FP32
+// result and are reported), each pixel's window split over up to kRefineChunks CTAs
+constexpr long long kRefineCap = 32768;
+constexpr int kRefineChunks = 4;
 
 inline FilterLayout filter_layout(const nys_filter_desc* d) {
   FilterLayout L;
@@ -49,8 +53,11 @@ inline FilterLayout filter_layout(const nys_filter_desc* d) {
   L.m64_off_bytes = L.chol_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;
   L.list_off_bytes = L.m64_off_bytes + ((size_t)d->m0 * d->m0 * 8 + 255) / 256 * 256;
   const long long px = (long long)d->H * d->W;
-  L.list_cap = (unsigned)std::min<long long>(px, std::max<long long>(4096, px / 8));
-  L.total_bytes = L.list_off_bytes + ((size_t)L.list_cap * 4 + 255) / 256 * 256;
+  L.list_cap = (unsigned)std::min<long long>(px, kRefineCap);
+  // per queued pixel: a chunk counter, then kRefineChunks x 2(n+1) FP64 window partial sums
+  L.cnt_off_bytes = L.list_off_bytes + ((size_t)L.list_cap * 4 + 255) / 256 * 256;
+  L.part_off_bytes = L.cnt_off_bytes + ((size_t)L.list_cap * 4 + 255) / 256 * 256;
+  L.total_bytes = L.part_off_bytes + (size_t)L.list_cap * kRefineChunks * 2 * (d->n + 1) * sizeof(double);
   return L;
 }
 
@@ -177,7 +184,7 @@ inline void fill_taps(const nys_filter_desc* d, float* taps) {
 inline void refine_params(float* tau, float* cerr) {  // read per launch (A/B within a process)
   const char* et = getenv("NYS_REFINE_TAU");
   const char* ec = getenv("NYS_REFINE_CERR");
-  *tau = et ? (float)atof(et) : 1e-2f;
+  *tau = et ? (float)atof(et) : 0.25f;
   *cerr = ec ? (float)atof(ec) : 1e-3f;
 }
 

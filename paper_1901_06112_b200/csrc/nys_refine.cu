@@ -29,11 +29,13 @@ struct RArgs {
   const float* g;
   float* out;
   long long fps, gps, ops;
-  int n, rho, H, W, m0, R, gkind, rlo, rhi, c_in_smem;
+  int n, rho, H, W, m0, R, gkind, rlo, rhi, c_in_smem, nch, out64;
   const double* D;    // FP64 block: C64, U064, SC64 (filter_layout)
   const double* M64;  // m0 x m0 row-major
   const unsigned* list;
   unsigned cap;
+  unsigned* chunk_cnt;  // per queued pixel: window chunks done
+  double* part;         // per queued pixel: nch x 2(n+1) window partial sums
   int d_u0, d_sc;
   FilterStats* stats;
   double* stats_out;  // nullable: {min|eta|, guarded (int64 bits)}
@@ -48,10 +50,14 @@ __device__ __forceinline__ float guide_val(const RArgs& a, int k, int row, int x
   return __ldg(a.f + (long long)c * a.fps + (long long)yy * a.W + xx);
 }
 
+// Work item = (queued pixel e, window chunk k): the (2S+1)^2 window of a pixel is split over
+// nch CTAs so a handful of queued pixels still spread over the GPU.  Each item writes its
+// 2(n+1) partial sums; the CTA that completes a pixel's last chunk adds the partials in chunk
+// order (deterministic), applies the guard and overwrites the pixel.
 __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
   extern __shared__ __align__(16) double rsm[];
   const int tid = threadIdx.x;
-  const int m0 = a.m0, rho = a.rho, n = a.n, NQ = 2 * (n + 1);
+  const int m0 = a.m0, rho = a.rho, n = a.n, NQ = 2 * (n + 1), nch = a.nch;
   double* z = rsm;                // m0: M b(x)
   double* u0 = z + m0;            // m0
   double* bx = u0 + m0;           // m0
@@ -63,6 +69,7 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
   int* pos = reinterpret_cast<int*>(Cs + (a.c_in_smem ? (size_t)m0 * rho : 0));  // 256 (row, x) packed
   float* gy = reinterpret_cast<float*>(pos + RF_THREADS);                        // [rho][256]
   __shared__ double s0x_sh;
+  __shared__ bool last_chunk;
 
   const double* C = a.c_in_smem ? Cs : a.D;
   for (int k = tid; k < m0; k += RF_THREADS) u0[k] = a.D[a.d_u0 + k];
@@ -71,17 +78,20 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
   const double inv_a1 = a.D[a.d_sc], eps = a.D[a.d_sc + 1];
   const unsigned cnt = min(*(volatile unsigned*)&a.stats->flagged, a.cap);
   const int R = a.R, T = 2 * R + 1, NP = T * T;
+  const unsigned items = cnt * (unsigned)nch;
   __syncthreads();
 
-  for (unsigned e = blockIdx.x; e < cnt; e += gridDim.x) {
+  for (unsigned item = blockIdx.x; item < items; item += gridDim.x) {
+    const unsigned e = item / (unsigned)nch;
+    const int k = (int)(item - e * (unsigned)nch);
     const unsigned idx = a.list[e];
     const int row = (int)(idx / (unsigned)a.W), x = (int)(idx - (unsigned)row * (unsigned)a.W);
-    for (int k = tid; k < rho; k += RF_THREADS) gx[k] = (double)guide_val(a, k, row, x);
+    for (int q = tid; q < rho; q += RF_THREADS) gx[q] = (double)guide_val(a, q, row, x);
     __syncthreads();
     for (int i = tid; i < m0; i += RF_THREADS) {
       double d2 = 0.0;
-      for (int k = 0; k < rho; ++k) {
-        const double t = gx[k] - C[(size_t)i * rho + k];
+      for (int q = 0; q < rho; ++q) {
+        const double t = gx[q] - C[(size_t)i * rho + q];
         d2 = fma(t, t, d2);
       }
       bx[i] = exp(-d2 * a.inv);
@@ -100,44 +110,72 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
       if (tid == 0) s0x_sh = s;
     }
     double acc = 0.0;  // thread q < NQ: quantity (c, kind) = (q % (n+1), q / (n+1))
-    for (int base = 0; base < NP; base += RF_THREADS) {
+    const int p_lo = (int)((long long)NP * k / nch), p_hi = (int)((long long)NP * (k + 1) / nch);
+    for (int base = p_lo; base < p_hi; base += RF_THREADS) {
       const int p = base + tid;
-      __syncthreads();  // tw / tl / pos / gy of the previous chunk consumed; z ready
-      if (p < NP) {
+      __syncthreads();  // tw / tl / pos of the previous block consumed; z ready
+      if (p < p_hi) {
         const int dy = p / T, dx = p - dy * T;
         const int yy = clampi(clampi(row + dy - R, 0, a.H - 1), a.rlo, a.rhi - 1);
         const int xx = clampi(x + dx - R, 0, a.W - 1);
-        for (int k = 0; k < rho; ++k) gy[k * RF_THREADS + tid] = guide_val(a, k, yy, xx);
-        double kz = 0.0, ks = 0.0;
-        for (int i = 0; i < m0; ++i) {
-          double d2 = 0.0;
-          for (int k = 0; k < rho; ++k) {
-            const double t = (double)gy[k * RF_THREADS + tid] - C[(size_t)i * rho + k];
-            d2 = fma(t, t, d2);
+        for (int q = 0; q < rho; ++q) gy[q * RF_THREADS + tid] = guide_val(a, q, yy, xx);
+        double kz0 = 0.0, ks0 = 0.0, kz1 = 0.0, ks1 = 0.0;  // two landmark chains for ILP
+        int i = 0;
+        for (; i + 1 < m0; i += 2) {
+          double d0 = 0.0, d1 = 0.0;
+          for (int q = 0; q < rho; ++q) {
+            const double gq = (double)gy[q * RF_THREADS + tid];
+            const double t0 = gq - C[(size_t)i * rho + q], t1 = gq - C[(size_t)(i + 1) * rho + q];
+            d0 = fma(t0, t0, d0);
+            d1 = fma(t1, t1, d1);
           }
-          const double b = exp(-d2 * a.inv);
-          kz = fma(z[i], b, kz);
-          ks = fma(u0[i], b, ks);
+          const double b0 = exp(-d0 * a.inv), b1 = exp(-d1 * a.inv);
+          kz0 = fma(z[i], b0, kz0);
+          ks0 = fma(u0[i], b0, ks0);
+          kz1 = fma(z[i + 1], b1, kz1);
+          ks1 = fma(u0[i + 1], b1, ks1);
+        }
+        if (i < m0) {
+          double d0 = 0.0;
+          for (int q = 0; q < rho; ++q) {
+            const double t0 = (double)gy[q * RF_THREADS + tid] - C[(size_t)i * rho + q];
+            d0 = fma(t0, t0, d0);
+          }
+          const double b0 = exp(-d0 * a.inv);
+          kz0 = fma(z[i], b0, kz0);
+          ks0 = fma(u0[i], b0, ks0);
         }
         const double w = a.taps[dy] * a.taps[dx];
-        tw[tid] = w * kz;
-        tl[tid] = w * ks;
+        tw[tid] = w * (kz0 + kz1);
+        tl[tid] = w * (ks0 + ks1);
         pos[tid] = yy * a.W + xx;
       }
       __syncthreads();
       if (tid < NQ) {
         const int c = tid % (n + 1), kind = tid / (n + 1);
         const double* t = kind ? tl : tw;
-        const int lim = min(RF_THREADS, NP - base);
+        const int lim = min(RF_THREADS, p_hi - base);
         for (int q = 0; q < lim; ++q) {
           const double fv = c < n ? (double)__ldg(a.f + (long long)c * a.fps + pos[q]) : 1.0;
           acc = fma(t[q], fv, acc);
         }
       }
     }
-    if (tid < NQ) res[tid] = acc;
+    double* mine = a.part + ((size_t)e * nch + k) * NQ;
+    if (tid < NQ) mine[tid] = acc;
+    __threadfence();
     __syncthreads();
-    {
+    if (tid == 0) last_chunk = atomicAdd(&a.chunk_cnt[e], 1u) == (unsigned)nch - 1;
+    __syncthreads();
+    if (last_chunk) {
+      __threadfence();
+      const volatile double* pe = a.part + (size_t)e * nch * NQ;
+      if (tid < NQ) {
+        double s = 0.0;
+        for (int kk = 0; kk < nch; ++kk) s += pe[(size_t)kk * NQ + tid];  // chunk order: deterministic
+        res[tid] = s;
+      }
+      __syncthreads();
       const double eta = res[n];
       const double s0x = s0x_sh;
       const double eta_l = s0x * res[2 * n + 1] * inv_a1;
@@ -147,7 +185,9 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
         if (fabs(eta) >= eps) o = res[c] / eta;
         else if (fabs(eta_l) >= eps) o = (s0x * res[n + 1 + c] * inv_a1) / eta_l;
         else o = (double)__ldg(a.f + (long long)c * a.fps + (long long)row * a.W + x);
-        a.out[(long long)c * a.ops + (long long)row * a.W + x] = (float)o;
+        const long long oi = (long long)c * a.ops + (long long)row * a.W + x;
+        if (a.out64) reinterpret_cast<double*>(a.out)[oi] = (double)(float)o;  // as K3 stores it
+        else a.out[oi] = (float)o;
       }
       if (tid == 0) {
         atomicMin(&a.stats->min_abs_eta_bits, __float_as_uint((float)fabs(eta)));
@@ -155,9 +195,10 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
           atomicAdd(&a.stats->guarded, 1ull);
           atomicAdd(&a.stats->refined_guarded, 1u);
         }
+        a.chunk_cnt[e] = 0u;  // ready for the next filter
       }
     }
-    __syncthreads();  // gx / bx / z / res reused by the next pixel
+    __syncthreads();  // gx / bx / z / res reused by the next item
   }
   // the last CTA publishes the statistics
   __shared__ bool last;
@@ -209,6 +250,7 @@ int nys_filter_finish(const nys_filter_desc* d, const float* f, int64_t f_plane_
   a.m0 = d->m0;
   a.R = d->radius;
   a.gkind = d->guide_kind;
+  a.out64 = d->out_f64 != 0;
   a.rlo = std::max(0, d->row_lo);
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
   const char* ws = static_cast<const char*>(workspace);
@@ -216,6 +258,12 @@ int nys_filter_finish(const nys_filter_desc* d, const float* f, int64_t f_plane_
   a.M64 = reinterpret_cast<const double*>(ws + L.m64_off_bytes);
   a.list = reinterpret_cast<const unsigned*>(ws + L.list_off_bytes);
   a.cap = L.list_cap;
+  a.chunk_cnt = reinterpret_cast<unsigned*>(const_cast<char*>(ws) + L.cnt_off_bytes);
+  a.part = reinterpret_cast<double*>(const_cast<char*>(ws) + L.part_off_bytes);
+  {
+    const int NP = (2 * d->radius + 1) * (2 * d->radius + 1);
+    a.nch = std::max(1, std::min(kRefineChunks, (NP + RF_THREADS - 1) / RF_THREADS));
+  }
   a.d_u0 = (int)L.d_U064;
   a.d_sc = (int)L.d_SC64;
   a.stats = reinterpret_cast<FilterStats*>(const_cast<char*>(ws) + L.stats_off_bytes);
@@ -235,7 +283,7 @@ int nys_filter_finish(const nys_filter_desc* d, const float* f, int64_t f_plane_
   if (smem > 227 * 1024) return NYS_EUNSUPPORTED;
   NYS_CUDA_TRY(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   count_launch();
-  k_finish<<<num_sms(), RF_THREADS, smem, (cudaStream_t)stream>>>(a);
+  k_finish<<<2 * num_sms(), RF_THREADS, smem, (cudaStream_t)stream>>>(a);
   NYS_LAUNCH_CHECK();
   return NYS_OK;
 }

@@ -55,9 +55,11 @@ struct VArgs {
   int out0, out_rows, tiles_x, tiles_y, nchunks, u0_off, vec_out, gcache, ntail;
   int rlo, rhi;  // image rows present in f / guide (reads are clamped into them)
   int sc_off;  // cst[sc_off], cst[sc_off + 1]: 1/alpha_1 and eps_den (written with the plan)
+  int out64;   // out addresses float64 planes
   float k2;
   float tau, cerr;          // near-guard flag rule (near_guard); tau = cerr = 0 disables it
   unsigned* flag_list;      // global pixel indices queued for nys_filter_finish
+  unsigned* chunk_cnt;
   unsigned list_cap;
   float taps[NYS_MAX_TAPS];
   float2 wpair[NYS_MAX_TAPS + 1];  // packed-FIR tap pairs (fill_tap_pairs)
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
                   const unsigned slot = atomicAdd(&a.stats->flagged, 1u);
                   if (slot < a.list_cap) {  // (past the cap the FP32 result and statistics stand)
                     a.flag_list[slot] = (unsigned)((long long)row * W + x);
+                    a.chunk_cnt[slot] = 0u;  // nys_filter_finish's per-pixel chunk counter
                     sv[e] = -1.f;
                   }
                 }
@@ -357,6 +360,13 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
               } else {
                 res[e] = x < W ? __ldg(a.f + (long long)c * a.fps + (long long)row * W + x) : 0.f;
               }
+            }
+            if (a.out64) {  // FP64 planes (the reference's Image dtype), e.g. page-locked host memory
+              double* d64 = reinterpret_cast<double*>(a.out) + (long long)c * a.ops + (long long)row * W + x0 + quad * 4;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (x0 + quad * 4 + e < W) d64[e] = (double)res[e];
+              continue;
             }
             float* dst = a.out + (long long)c * a.ops + (long long)row * W + x0 + quad * 4;
             if (a.vec_out && x0 + quad * 4 + 3 < W) {
@@ -466,6 +476,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   a.nchunks = nchunks;
   a.ntail = NC % 4;
   a.u0_off = (int)L.off_U0;
+  a.out64 = d->out_f64 != 0;
   a.vec_out = ((d->W & 3) == 0) && ((out_plane_stride & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   a.rlo = std::max(0, d->row_lo);
   a.rhi = d->row_hi > 0 ? std::min(d->H, d->row_hi) : d->H;
@@ -474,6 +485,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   refine_params(&a.tau, &a.cerr);
   a.flag_list = reinterpret_cast<unsigned*>((char*)const_cast<void*>(workspace) + L.list_off_bytes);
   a.list_cap = L.list_cap;
+  a.chunk_cnt = reinterpret_cast<unsigned*>((char*)const_cast<void*>(workspace) + L.cnt_off_bytes);
   fill_taps(d, a.taps);
   fill_tap_pairs(a.taps, 2 * d->radius + 1, a.wpair);
 

@@ -361,7 +361,8 @@ def run_filter(inp: _Inputs, centroids: np.ndarray | None, params: FilterParams,
     # output row r is local row r - lo
     f_ptr = ptr(inp.f) - row_origin * W * 4
     g_ptr = ptr(inp.guide) - row_origin * W * 4
-    o_ptr = _device_view(out) - lo * W * 4  # a pinned host `out` is written by K3 directly
+    d.out_f64 = 1 if out.dtype == torch.float64 else 0
+    o_ptr = _device_view(out) - lo * W * out.element_size()  # a pinned host `out` is written by K3 directly
     f_ps = g_ps = h_local * W
     o_ps = (hi - lo) * W
 
@@ -466,10 +467,12 @@ def _device_view(t: torch.Tensor) -> int:
     return int(dev.value)
 
 
-def _output_buffer(f: Image, out: torch.Tensor | None) -> torch.Tensor | None:
+def _output_buffer(f: Image, out: torch.Tensor | None, params: FilterParams | None = None) -> torch.Tensor | None:
     """Where K3 writes: the caller's `out` (device or page-locked host float32
     (n, H, W)), else a fresh page-locked host tensor for pinned host input (the
-    device->host transfer then overlaps the vertical pass), else None (device
+    device->host transfer then overlaps the vertical pass), else -- for the
+    reference's NumPy float64 Image -- a page-locked float64 host array that K3
+    fills directly (no device->host copy, no host cast), else None (device
     buffer from run_filter)."""
     shape = (f.channels, f.height, f.width)
     if out is not None:
@@ -479,6 +482,9 @@ def _output_buffer(f: Image, out: torch.Tensor | None) -> torch.Tensor | None:
         return out
     if f.is_tensor and not f.on_device and f.data.is_pinned():
         return torch.empty(shape, dtype=torch.float32, pin_memory=True)
+    if not f.is_tensor and (params is None or params.spatial.kind != GAUSSIAN_RECURSIVE
+                            or params.spatial.sigma < 1.0):
+        return torch.empty(shape, dtype=torch.float64, pin_memory=True)
     return None
 
 
@@ -486,6 +492,8 @@ def _output_image(out: torch.Tensor, f: Image, given: torch.Tensor | None = None
     """Output in the caller's container: device tensor stays on the device, a
     host tensor (e.g. pinned) gets a host float32 tensor, NumPy gets the
     reference's float64 ndarray."""
+    if not out.is_cuda and out.dtype == torch.float64:  # K3 wrote the reference's float64 planes in place
+        return Image.trusted(out.numpy(), f.range_max)
     if given is not None or f.on_device or not out.is_cuda:  # caller's buffer / device in / pinned host in place
         return Image(data=out, range_max=f.range_max)
     if f.is_tensor:
@@ -545,7 +553,7 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     timer.mark("eigendecomposition")  # host eig happens inside run_filter's mixing_plan
     out_given = out
     out, plan, stats = run_filter(inp, centroids, params, timer, kernel_events=kernel_events,
-                                  out=_output_buffer(f, out))
+                                  out=_output_buffer(f, out, params))
     if isinstance(qe, torch.Tensor):  # the deferred exact pass rides along with the statistics copy
         stats = torch.cat([stats, qe])
         h = stats.cpu()
@@ -607,7 +615,7 @@ def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: 
 
     fl = _Inflight(kmeans=pk, between=between)
     out_given = out
-    out, _, _ = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out),
+    out, _, _ = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out, params),
                            inflight=fl, stats_ptr=hres_dev)
     timer.mark("normalization")  # fused into K3; stamped before the wait so elapsed() needs no further sync
     timer.stream.synchronize()  # the step's only host wait
@@ -645,7 +653,7 @@ def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> Filte
     if C_.ndim != 2 or C_.shape[1] != inp.rho:
         raise ValueError(f"landmark dim {C_.shape[-1]} != guide dim {inp.rho}")
     timer.mark("upload")
-    out, plan, stats = run_filter(inp, C_, params, timer, out=_output_buffer(f, None))
+    out, plan, stats = run_filter(inp, C_, params, timer, out=_output_buffer(f, None, params))
     min_den, guarded = _stats_host(stats)
     _, qe = exact_assignment(inp.points, C_, want_assignment=False)
     timer.mark("normalization")

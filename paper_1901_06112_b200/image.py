@@ -55,6 +55,17 @@ class Image:
         if not self.range_max > 0:
             raise ValueError("range_max must be positive")
 
+    @classmethod
+    def trusted(cls, data: np.ndarray, range_max: float) -> "Image":
+        """Wrap a float64 (channels, height, width) array this package produced
+        (e.g. the filter output K3 wrote into page-locked memory) without the
+        constructor's copy and finiteness scan; read-only like every Image."""
+        data.flags.writeable = False
+        img = object.__new__(cls)
+        object.__setattr__(img, "data", data)
+        object.__setattr__(img, "range_max", float(range_max))
+        return img
+
     @property
     def on_device(self) -> bool:
         return _is_tensor(self.data) and self.data.is_cuda

@@ -379,19 +379,17 @@ def test_device_inverse_from_cholesky_matches_host_M(m0, rho, theta):
         wsb = int(lib.nys_filter_workspace_bytes(C.byref(d)))
         ws = torch.zeros((wsb // 4,), dtype=torch.float32, device="cuda")
         _native.check(lib.nys_filter_prepare(C.byref(d), ptr(ws), wsb, stream_ptr()), "nys_filter_prepare")
-        # workspace tail (filter_layout): stats 256 B, Cholesky slot, FP64 M, flagged-pixel list
-        mm = (m0 * m0 * 8 + 255) // 256 * 256
-        listb = (min(64 * 64, max(4096, 64 * 64 // 8)) * 4 + 255) // 256 * 256
-        stats_floats = (wsb - 256 - 2 * mm - listb) // 4
-        m64_off = (wsb - listb - mm) // 4
+        lay = np.zeros(8, np.int64)
+        _native.check(lib.nys_filter_workspace_layout(C.byref(d), lay.ctypes.data), "layout")
+        stats_floats, m64_off = int(lay[1]) // 4, int(lay[3]) // 4
         wss.append(ws[:stats_floats].cpu().numpy().view(np.uint32))
         m64s.append(ws[m64_off:m64_off + 2 * m0 * m0].cpu().numpy().view(np.float64).reshape(m0, m0))
     # float block (filter_layout: C, MT, U0, SC) then the FP64 block (C64, U064, SC64)
-    rhop, m0q = -(-rho // 4) * 4, -(-(m0 + 1) // 8) * 8
-    off_d = m0 * rhop + m0 * m0q + -(-m0 // 4) * 4 + 4
+    off_d = int(lay[0]) // 4
     dblk = [w[off_d:off_d + 2 * (m0 * rho + m0 + 4)].view(np.float64) for w in wss]
-    np.testing.assert_array_equal(dblk[0][:m0 * rho + m0], dblk[1][:m0 * rho + m0])  # landmarks, u0
-    np.testing.assert_allclose(dblk[0][m0 * rho + m0:], dblk[1][m0 * rho + m0:], rtol=1e-12)  # 1/a1, eps, a1
+    np.testing.assert_array_equal(dblk[0][:m0 * rho], dblk[1][:m0 * rho])  # landmarks
+    # u0, 1/alpha_1, eps_den, alpha_1: full eigensystem vs the lite plan's inverse iteration
+    np.testing.assert_allclose(dblk[0][m0 * rho:], dblk[1][m0 * rho:], rtol=1e-9, atol=1e-12)
     a, b = (w[:off_d] for w in wss)
     # the FP64 M of the near-guard refinement: host M vs the device's FP64 inverse
     np.testing.assert_allclose(m64s[1], host.M, rtol=0, atol=1e-9 * np.abs(host.M).max())

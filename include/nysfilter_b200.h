@@ -132,6 +132,39 @@ int nys_kmeans_farthest(const float* points, int64_t plane_stride, int64_t m, in
                         const int64_t* excluded, int n_excl, double* out,
                         void* workspace, size_t workspace_bytes, void* stream);
 
+/* --- device-resident sharded k-means (parallel.device_distributed_kmeans) ----
+ * The same global semantics as the host-orchestrated step-wise calls above, with
+ * every per-draw / per-iteration decision taken on the device so a rank never
+ * waits on the host between collectives (all-gather / all-reduce on device
+ * buffers in between, stream-ordered):
+ *   state_init; k-means++: per draw j = 1..m0-1 nys_kmeanspp_update (local D^2,
+ *   local total) -> all-gather of the totals -> nys_kmeanspp_owner_pick (every
+ *   rank resolves the owner of u_j * total from the totals in rank order; the
+ *   owner writes point + global index into cand[rho+1], the others zeros) ->
+ *   all-reduce(sum) of cand;  Lloyd: per iteration nys_kmeans_lloyd_local (local
+ *   sums / counts / objective / changed, zero work once converged) -> all-reduce
+ *   (sum) -> nys_kmeans_lloyd_update (the reference's update and break rule);
+ *   nys_kmeans_state_read at the end.  stats[1] >= 0 (a zero D^2 total) or
+ *   stats[3] == -1 (an empty cluster, whose repair needs the global farthest
+ *   point) tell the caller to rerun the host-orchestrated path. */
+int nys_kmeans_state_init(void* workspace, size_t workspace_bytes, int64_t m, int rho, int m0, void* stream);
+int nys_kmeans_state_read(const void* workspace, int64_t m, int rho, int m0, int64_t* stats_out /*[dev] 4*/,
+                          void* stream);
+int nys_kmeanspp_owner_pick(const float* points, int64_t plane_stride, int64_t m, int rho, int m0, const double* d2,
+                            const double* totals /*[dev] world*/, int world, int rank, int64_t my_offset,
+                            double u, int draw, double* cand_out /*[dev] rho+1*/, void* workspace,
+                            size_t workspace_bytes, void* stream);
+/* Cluster sums are exact fixed-point integers, x * 2^sexp rounded once per point, with
+ * sexp = 60 - ilogb(max|x| * m) over ALL ranks' points (max|x| all-reduced, m the global
+ * count): integer all-reduce, so the centroids are bit-identical to the single-device
+ * cooperative kernel's.  tot_out [dev] int64[m0*rho + m0 + 1] (sums, counts, changed),
+ * obj_out [dev] 1 double (objective). */
+int nys_kmeans_lloyd_local(const float* points, int64_t plane_stride, int64_t m, int rho, const double* centroids,
+                           int m0, int it, int sexp, int64_t* tot_out, double* obj_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
+int nys_kmeans_lloyd_update(int64_t m, int rho, int m0, int it, int sexp, const int64_t* tot, const double* obj,
+                            double* centroids, double* errors, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Gather point `index` (rho coordinates, FP64) into dst [dev]. */
 int nys_gather_point(const float* points, int64_t plane_stride, int rho, int64_t index,
                      double* dst, void* stream);

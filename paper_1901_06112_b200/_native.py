@@ -69,6 +69,11 @@ _SIGS = {
     "nys_kmeans_exact": (_I, [_P, _L, _L, _I, _P, _I, _P, _P, _P, _S, _P]),
     "nys_kmeans_farthest": (_I, [_P, _L, _L, _I, _P, _I, _P, _P, _I, _P, _P, _S, _P]),
     "nys_gather_point": (_I, [_P, _L, _I, _L, _P, _P]),
+    "nys_kmeans_state_init": (_I, [_P, _S, _L, _I, _I, _P]),
+    "nys_kmeans_state_read": (_I, [_P, _L, _I, _I, _P, _P]),
+    "nys_kmeanspp_owner_pick": (_I, [_P, _L, _L, _I, _I, _P, _P, _I, _I, _L, _D, _I, _P, _P, _S, _P]),
+    "nys_kmeans_lloyd_local": (_I, [_P, _L, _L, _I, _P, _I, _I, _I, _P, _P, _P, _S, _P]),
+    "nys_kmeans_lloyd_update": (_I, [_L, _I, _I, _I, _I, _P, _P, _P, _P, _P, _S, _P]),
     "nys_filter_planes_bytes": (_S, [C.POINTER(FilterDesc), _I]),
     "nys_filter_workspace_bytes": (_S, [C.POINTER(FilterDesc)]),
     "nys_filter_workspace_layout": (_I, [C.POINTER(FilterDesc), _P]),

@@ -596,6 +596,223 @@ __global__ void __launch_bounds__(1024) k_pick(const double* __restrict__ d2, lo
 }
 
 // ---------------------------------------------------------------------------
+// row-band-sharded k-means, device resident (parallel.py): per k-means++ draw the
+// ranks all-gather their D^2 totals and every rank resolves the draw from them with
+// the same arithmetic; the owner writes the chosen point (+ its global index) into a
+// candidate vector that an all-reduce(sum) then hands to everyone.  No host wait.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_pp_owner_pick(const float* __restrict__ pts, long long ps, long long m,
+                                                        int rho, const double* __restrict__ d2,
+                                                        const double* __restrict__ ppart, int nb, long long chunk,
+                                                        const double* __restrict__ totals, int world, int rank,
+                                                        long long my_offset, double u, int draw,
+                                                        double* __restrict__ cand, KState* st) {
+  __shared__ double sh[2 + 1024];
+  __shared__ long long shi;
+  __shared__ int owner_sh;
+  __shared__ double local_target;
+  for (int d = threadIdx.x; d <= rho; d += blockDim.x) cand[d] = 0.0;
+  if (st->zero_draw >= 0) return;
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int r = 0; r < world; ++r) total += totals[r];  // rank order: identical on every rank
+    int owner = -1;
+    double t = 0.0;
+    if (total > 0.0) {
+      const double target = u * total;
+      double pre = 0.0;
+      int last_pos = -1;
+      double pre_last = 0.0;
+      for (int r = 0; r < world; ++r) {
+        if (totals[r] > 0.0) {
+          last_pos = r;
+          pre_last = pre;
+        }
+        if (pre + totals[r] > target) {
+          owner = r;
+          t = target - pre;
+          break;
+        }
+        pre += totals[r];
+      }
+      if (owner < 0) {  // rounding pushed the target past the end (parallel.distributed_kmeans)
+        owner = last_pos;
+        t = totals[owner] * (1.0 - 1e-16);
+        (void)pre_last;
+      }
+    } else {
+      st->zero_draw = draw;  // sum(D^2) == 0: the reference switches to integers(m) (host fallback)
+    }
+    owner_sh = owner;
+    local_target = t;
+  }
+  __syncthreads();
+  if (owner_sh != rank) return;
+  const long long idx = pp_find(d2, m, ppart, nb, chunk, local_target, sh, &shi);
+  for (int d = threadIdx.x; d < rho; d += blockDim.x) cand[d] = (double)pts[d * ps + idx];
+  if (threadIdx.x == 0) cand[rho] = (double)(my_offset + idx);
+}
+
+// One Lloyd assignment over the local points (full search, the FP32 difference form of the
+// single-device kernels, first index on ties) with the cluster sums as EXACT fixed-point
+// integers (x * 2^sexp rounded once per point, warp_accumulate_fx): per-block partials, then
+// k_reduce_fx -- integer sums, so any order (blocks here, ranks in the all-reduce) gives the
+// same bits, and the centroids equal the single-device cooperative kernel's.
+template <int GR>
+__global__ void __launch_bounds__(256) k_assign_fx(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                   const float* __restrict__ Cf, int m0, int* __restrict__ labels,
+                                                   int first, double scale, unsigned long long* __restrict__ bpart,
+                                                   double* __restrict__ bobj, const KState* st) {
+  extern __shared__ __align__(16) unsigned long long fsm[];
+  if (st->converged) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ns = m0 * rho;
+  unsigned long long* wacc = fsm;                              // nw x ns
+  int* wcnt = reinterpret_cast<int*>(wacc + (size_t)nw * ns);  // nw x m0
+  float* Cs = reinterpret_cast<float*>(wcnt + (size_t)nw * m0);
+  for (int k = threadIdx.x; k < nw * ns; k += blockDim.x) wacc[k] = 0ull;
+  for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0;
+  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) Cs[k] = Cf[k];
+  __syncthreads();
+  unsigned long long* myacc = wacc + (size_t)w * ns;
+  int* mycnt = wcnt + (size_t)w * m0;
+  double near_sum = 0.0;
+  long long changed = 0;
+  const long long chunk = ceil_div(m, (long long)gridDim.x);
+  const long long lo = blockIdx.x * chunk, hi = min(m, lo + chunk);
+  for (long long base = lo + (long long)w * 32; base < hi; base += (long long)nw * 32) {
+    const long long i = base + lane;
+    const bool valid = i < hi;
+    float x[GR];
+#pragma unroll
+    for (int d = 0; d < GR; ++d) x[d] = (valid && d < rho) ? __ldg(pts + d * ps + i) : 0.f;
+    float best = INFINITY;
+    int arg = 0;
+    for (int j = 0; j < m0; ++j) {
+      float d2 = 0.f;
+#pragma unroll
+      for (int d = 0; d < GR; ++d)
+        if (d < rho) {
+          const float t = x[d] - Cs[j * rho + d];
+          d2 = fmaf(t, t, d2);
+        }
+      if (d2 < best) {  // strict: first index wins ties (np.argmin)
+        best = d2;
+        arg = j;
+      }
+    }
+    if (valid) {
+      near_sum += (double)best;
+      const int old = labels[i];
+      if (first || old != arg) ++changed;
+      labels[i] = arg;
+    }
+    warp_accumulate_fx<GR>(x, rho, arg, valid, scale, 1, myacc, mycnt);
+  }
+  near_sum = warp_sum(near_sum);
+  const double ch = warp_sum((double)changed);
+  __shared__ double extra[2][32];
+  if (lane == 0) {
+    extra[0][w] = near_sum;
+    extra[1][w] = ch;
+  }
+  __syncthreads();
+  const int S = ns + m0;
+  unsigned long long* out = bpart + (size_t)blockIdx.x * S;
+  for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+    unsigned long long v = 0ull;
+    for (int q = 0; q < nw; ++q) v += wacc[(size_t)q * ns + k];
+    out[k] = v;
+  }
+  for (int k = threadIdx.x; k < m0; k += blockDim.x) {
+    long long v = 0;
+    for (int q = 0; q < nw; ++q) v += wcnt[(size_t)q * m0 + k];
+    out[ns + k] = (unsigned long long)v;
+  }
+  if (threadIdx.x == 0) {
+    double a0 = 0.0, b0 = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      a0 += extra[0][q];
+      b0 += extra[1][q];
+    }
+    bobj[2 * blockIdx.x] = a0;
+    bobj[2 * blockIdx.x + 1] = b0;
+  }
+}
+
+// totals over the blocks: tot[0 .. S) integer sums and counts, tot[S] the changed count;
+// obj[0] the objective (block order)
+__global__ void k_reduce_fx(const unsigned long long* __restrict__ bpart, const double* __restrict__ bobj, int nb,
+                            int S, unsigned long long* __restrict__ tot, double* __restrict__ obj, const KState* st) {
+  if (st->converged) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < S) {
+    unsigned long long v = 0ull;
+    for (int b = 0; b < nb; ++b) v += bpart[(size_t)b * S + k];
+    tot[k] = v;
+  }
+  if (k == S) {
+    double o = 0.0, c = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      o += bobj[2 * b];
+      c += bobj[2 * b + 1];
+    }
+    obj[0] = o;
+    tot[S] = (unsigned long long)(long long)c;
+  }
+}
+
+// the reference's update and break rule on the all-reduced fixed-point totals
+// (landmarks.py:101-119); empty clusters are left to the host fallback (k_mark_empty)
+__global__ void k_finalize_fx(const long long* __restrict__ tot, const double* __restrict__ obj, int m0, int rho,
+                              int it, double inv_scale, double* __restrict__ C, float* __restrict__ Cf,
+                              double* __restrict__ errors, KState* st) {
+  if (st->converged) return;
+  const int ns = m0 * rho;
+  const long long changed = tot[ns + m0];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    errors[it] = obj[0];
+    st->iters = it + 1;
+    st->changed = changed;
+  }
+  if (it > 0 && changed == 0) {
+    if (threadIdx.x == 0) st->converged = 1;
+    return;
+  }
+  for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+    const int j = k / rho;
+    const double cnt = (double)tot[ns + j];
+    if (cnt > 0.0) C[k] = ((double)tot[k] * inv_scale) / cnt;
+    Cf[k] = (float)C[k];
+  }
+  if (threadIdx.x == 0) {
+    int ne = 0;
+    for (int j = 0; j < m0; ++j) ne += tot[ns + j] > 0 ? 0 : 1;
+    st->n_empty = ne;
+  }
+}
+
+__global__ void k_state_init_sharded(KState* st) {
+  st->converged = 0;
+  st->iters = 0;
+  st->n_empty = 0;
+  st->zero_draw = -1;
+  st->changed = 0;
+  st->repairs = 0;
+}
+
+// after k_finalize on the all-reduced totals: an empty cluster needs the global farthest point,
+// which the device-resident path does not resolve -- mark the run (repairs = -1) for the
+// host-orchestrated fallback and stop iterating
+__global__ void k_mark_empty(KState* st) {
+  if (!st->converged && st->n_empty > 0) {
+    st->repairs = -1;
+    st->converged = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
 static int launch_assign(const float* pts, long long ps, long long m, int rho, const float* Cf, int m0, int* labels,
@@ -842,6 +1059,108 @@ int nys_kmeans_farthest(const float* points, int64_t plane_stride, int64_t m, in
   if (!centroids || !labels || !out || (n_excl > 0 && !excluded)) return NYS_EINVAL;
   count_launch(); k_farthest<<<1, 1024, 0, (cudaStream_t)stream>>>(points, plane_stride, m, rho, centroids, labels,
                                                     reinterpret_cast<const long long*>(excluded), n_excl, out);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_state_init(void* workspace, size_t workspace_bytes, int64_t m, int rho, int m0, void* stream) {
+  if (!workspace || m < 1 || rho < 1 || m0 < 1 || workspace_bytes < klayout(m, rho, m0).total) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  count_launch();
+  k_state_init_sharded<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<KState*>((char*)workspace + L.off_state));
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_state_read(const void* workspace, int64_t m, int rho, int m0, int64_t* stats_out, void* stream) {
+  if (!workspace || !stats_out || m < 1 || rho < 1 || m0 < 1) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  count_launch();
+  k_write_stats<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<const KState*>((const char*)workspace + L.off_state),
+                                                  reinterpret_cast<long long*>(stats_out));
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeanspp_owner_pick(const float* points, int64_t plane_stride, int64_t m, int rho, int m0, const double* d2,
+                            const double* totals, int world, int rank, int64_t my_offset, double u, int draw,
+                            double* cand_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!points || !d2 || !totals || !cand_out || m < 1 || rho < 1 || rho > NYS_MAX_RHO || m0 < 1 || world < 1 ||
+      rank < 0 || rank >= world)
+    return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  if (!workspace || workspace_bytes < L.total) return NYS_EINVAL;
+  char* ws = reinterpret_cast<char*>(workspace);
+  // ppart: the per-block sums of the last nys_kmeanspp_update on this workspace (their offset
+  // and block shape depend on m only)
+  const double* ppart = reinterpret_cast<const double*>(ws + L.off_ppart);
+  count_launch();
+  k_pp_owner_pick<<<1, 1024, 0, (cudaStream_t)stream>>>(points, plane_stride, m, rho, d2, ppart, L.nb_seed,
+                                                         L.seed_chunk, totals, world, rank, my_offset, u, draw,
+                                                         cand_out, reinterpret_cast<KState*>(ws + L.off_state));
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_lloyd_local(const float* points, int64_t plane_stride, int64_t m, int rho, const double* centroids,
+                           int m0, int it, int sexp, int64_t* tot_out, double* obj_out, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  int rc = check_common(points, m, rho, m0, workspace, workspace_bytes);
+  if (rc) return rc;
+  if (!centroids || !tot_out || !obj_out || it < 0) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  char* ws = reinterpret_cast<char*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  KState* st = reinterpret_cast<KState*>(ws + L.off_state);
+  float* Cf = reinterpret_cast<float*>(ws + L.off_cf);
+  int* labels = reinterpret_cast<int*>(ws + L.off_labels);
+  unsigned long long* bpart = reinterpret_cast<unsigned long long*>(ws + L.off_part);  // nb x (m0 rho + m0) <= nb x S
+  double* bobj = reinterpret_cast<double*>(ws + L.off_arg);                            // nb x 2
+  if (it == 0) {
+    count_launch();
+    k_c_to_f<<<1, 256, 0, s>>>(centroids, Cf, m0 * rho);  // later iterations: k_finalize_fx keeps Cf
+  }
+  const int ns = m0 * rho;
+  int nw = 8;
+  while (nw > 1 && (size_t)nw * (ns * 8 + m0 * 4) + (size_t)ns * 4 > 160 * 1024) --nw;
+  const size_t smem = (size_t)nw * (ns * 8 + m0 * 4) + (size_t)ns * 4;
+  const double scale = std::ldexp(1.0, sexp);
+  const int nb = L.nb_assign;
+#define NYS_AFX(G)                                                                                             \
+  NYS_CUDA_TRY(cudaFuncSetAttribute(k_assign_fx<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+  count_launch();                                                                                              \
+  k_assign_fx<G><<<nb, nw * 32, smem, s>>>(points, plane_stride, m, rho, Cf, m0, labels, it == 0, scale, bpart, bobj, st);
+  if (rho <= 4) {
+    NYS_AFX(4)
+  } else if (rho <= 16) {
+    NYS_AFX(16)
+  } else if (rho <= 32) {
+    NYS_AFX(32)
+  } else {
+    NYS_AFX(64)
+  }
+#undef NYS_AFX
+  const int S = ns + m0;
+  count_launch();
+  k_reduce_fx<<<(int)ceil_div(S + 1, 256), 256, 0, s>>>(bpart, bobj, nb, S, reinterpret_cast<unsigned long long*>(tot_out),
+                                                        obj_out, st);
+  NYS_LAUNCH_CHECK();
+  return NYS_OK;
+}
+
+int nys_kmeans_lloyd_update(int64_t m, int rho, int m0, int it, int sexp, const int64_t* tot, const double* obj,
+                            double* centroids, double* errors, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!tot || !obj || !centroids || !errors || !workspace || m < 1 || rho < 1 || m0 < 1 || it < 0) return NYS_EINVAL;
+  const KLayout L = klayout(m, rho, m0);
+  if (workspace_bytes < L.total) return NYS_EINVAL;
+  char* ws = reinterpret_cast<char*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  KState* st = reinterpret_cast<KState*>(ws + L.off_state);
+  count_launch();
+  k_finalize_fx<<<1, 256, 0, s>>>(reinterpret_cast<const long long*>(tot), obj, m0, rho, it, std::ldexp(1.0, -sexp),
+                                  centroids, reinterpret_cast<float*>(ws + L.off_cf), errors, st);
+  count_launch();
+  k_mark_empty<<<1, 1, 0, s>>>(st);
   NYS_LAUNCH_CHECK();
   return NYS_OK;
 }

@@ -372,36 +372,6 @@ struct LloydArgs {
   int bounds;                // 0: full search every iteration (debug / A-B check)
 };
 
-// Warp-level accumulation of per-cluster coordinate sums as EXACT fixed-point
-// integers (x * 2^s rounded once per point, two's complement): each distinct
-// label among the lanes is reduced with REDUX on 21-bit limbs, so sums are
-// independent of order and hence deterministic across blocks, warps and runs.
-// `sign` = -1 removes the lanes' points from their clusters.
-template <int GR>
-__device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho, int label, bool valid, double scale,
-                                                   int sign, unsigned long long* acc, int* cnt) {
-  const int lane = threadIdx.x & 31;
-  unsigned rem = __ballot_sync(0xffffffffu, valid);
-  while (rem) {
-    const int leader = __ffs(rem) - 1;
-    const int L = __shfl_sync(0xffffffffu, label, leader);
-    const unsigned grp = __ballot_sync(0xffffffffu, valid && label == L);
-    if ((grp >> lane) & 1u) {
-#pragma unroll
-      for (int d = 0; d < GR; ++d)
-        if (d < rho) {
-          const unsigned long long v = (unsigned long long)__double2ll_rn((double)(sign * x[d]) * scale);
-          const unsigned long long s0 = __reduce_add_sync(grp, (unsigned)(v & 0x1FFFFFull));
-          const unsigned long long s1 = __reduce_add_sync(grp, (unsigned)((v >> 21) & 0x1FFFFFull));
-          const unsigned long long s2 = __reduce_add_sync(grp, (unsigned)(v >> 42));
-          if (lane == leader) acc[L * rho + d] += s0 + (s1 << 21) + (s2 << 42);
-        }
-      if (lane == leader) cnt[L] += sign * __popc(grp);
-    }
-    rem &= ~grp;
-  }
-}
-
 // squared FP32 distance, difference form, dimensions in ascending order -- the
 // one formula every assignment uses, so a bound-skipped point gets the same
 // value the full search would have produced

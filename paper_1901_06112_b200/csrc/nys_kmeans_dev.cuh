@@ -277,4 +277,34 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
                       double* errors, char* ws, const KLayout& L, cudaStream_t s, bool prezeroed = false);
 
+// Warp-level accumulation of per-cluster coordinate sums as EXACT fixed-point
+// integers (x * 2^s rounded once per point, two's complement): each distinct
+// label among the lanes is reduced with REDUX on 21-bit limbs, so sums are
+// independent of order and hence deterministic across blocks, warps and runs.
+// `sign` = -1 removes the lanes' points from their clusters.
+template <int GR>
+__device__ __forceinline__ void warp_accumulate_fx(const float (&x)[GR], int rho, int label, bool valid, double scale,
+                                                   int sign, unsigned long long* acc, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned rem = __ballot_sync(0xffffffffu, valid);
+  while (rem) {
+    const int leader = __ffs(rem) - 1;
+    const int L = __shfl_sync(0xffffffffu, label, leader);
+    const unsigned grp = __ballot_sync(0xffffffffu, valid && label == L);
+    if ((grp >> lane) & 1u) {
+#pragma unroll
+      for (int d = 0; d < GR; ++d)
+        if (d < rho) {
+          const unsigned long long v = (unsigned long long)__double2ll_rn((double)(sign * x[d]) * scale);
+          const unsigned long long s0 = __reduce_add_sync(grp, (unsigned)(v & 0x1FFFFFull));
+          const unsigned long long s1 = __reduce_add_sync(grp, (unsigned)((v >> 21) & 0x1FFFFFull));
+          const unsigned long long s2 = __reduce_add_sync(grp, (unsigned)(v >> 42));
+          if (lane == leader) acc[L * rho + d] += s0 + (s1 << 21) + (s2 << 42);
+        }
+      if (lane == leader) cnt[L] += sign * __popc(grp);
+    }
+    rem &= ~grp;
+  }
+}
+
 }  // namespace nys

@@ -484,15 +484,28 @@ def _output_buffer(f: Image, out: torch.Tensor | None, params: FilterParams | No
         return torch.empty(shape, dtype=torch.float32, pin_memory=True)
     if not f.is_tensor and (params is None or params.spatial.kind != GAUSSIAN_RECURSIVE
                             or params.spatial.sigma < 1.0):
-        return torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        # K3 writes the float64 planes in HBM; one DMA (queued before the step's wait,
+        # _queue_host_copy) brings them to page-locked host memory -- scattered 32-byte writes
+        # over PCIe from K3 itself ran at a fraction of the DMA rate
+        return torch.empty(shape, dtype=torch.float64, device=require_cuda())
     return None
+
+
+def _queue_host_copy(out: torch.Tensor, f: Image) -> torch.Tensor:
+    """For a NumPy input: queue the device float64 output's copy into page-locked host memory on
+    the current stream (before the caller's wait) and return the host tensor."""
+    if f.is_tensor or not out.is_cuda or out.dtype != torch.float64:
+        return out
+    host = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(out, non_blocking=True)
+    return host
 
 
 def _output_image(out: torch.Tensor, f: Image, given: torch.Tensor | None = None) -> Image:
     """Output in the caller's container: device tensor stays on the device, a
     host tensor (e.g. pinned) gets a host float32 tensor, NumPy gets the
     reference's float64 ndarray."""
-    if not out.is_cuda and out.dtype == torch.float64:  # K3 wrote the reference's float64 planes in place
+    if not out.is_cuda and out.dtype == torch.float64:  # the float64 planes, already in page-locked host memory
         return Image.trusted(out.numpy(), f.range_max)
     if given is not None or f.on_device or not out.is_cuda:  # caller's buffer / device in / pinned host in place
         return Image(data=out, range_max=f.range_max)
@@ -554,6 +567,7 @@ def fast_filter(f: Image, p, params: FilterParams, *, kernel_events: list | None
     out_given = out
     out, plan, stats = run_filter(inp, centroids, params, timer, kernel_events=kernel_events,
                                   out=_output_buffer(f, out, params))
+    out = _queue_host_copy(out, f)
     if isinstance(qe, torch.Tensor):  # the deferred exact pass rides along with the statistics copy
         stats = torch.cat([stats, qe])
         h = stats.cpu()
@@ -618,6 +632,7 @@ def _fast_filter_pipelined(f: Image, inp: _Inputs, params: FilterParams, timer: 
     out, _, _ = run_filter(inp, None, params, timer, kernel_events=kernel_events, out=_output_buffer(f, out, params),
                            inflight=fl, stats_ptr=hres_dev)
     timer.mark("normalization")  # fused into K3; stamped before the wait so elapsed() needs no further sync
+    out = _queue_host_copy(out, f)
     timer.stream.synchronize()  # the step's only host wait
     h = hres.numpy().copy()
     res = fl.result()
@@ -654,6 +669,7 @@ def filter_with_landmarks(f: Image, p, centroids, params: FilterParams) -> Filte
         raise ValueError(f"landmark dim {C_.shape[-1]} != guide dim {inp.rho}")
     timer.mark("upload")
     out, plan, stats = run_filter(inp, C_, params, timer, out=_output_buffer(f, None, params))
+    out = _queue_host_copy(out, f)
     min_den, guarded = _stats_host(stats)
     _, qe = exact_assignment(inp.points, C_, want_assignment=False)
     timer.mark("normalization")

@@ -29,6 +29,7 @@ exercised with gloo on CPU (tests/test_distributed.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -76,40 +77,57 @@ class Comm:
         dist.broadcast(t, src, group=self.group)
         return t.cpu().numpy()
 
-    def exchange_rows(self, local: torch.Tensor, lo: int, hi: int, H: int, halo: int):
-        """Extend ``local`` (c, hi-lo, W) with up to ``halo`` rows from each
-        neighbour; returns (extended tensor, first global row)."""
+    def exchange_halos(self, ext: torch.Tensor, lo: int, hi: int, H: int, halo: int) -> int:
+        """Fill the halo rows of this rank's extended band in place.
+
+        ``ext`` (c, ehi - elo, W) with (elo, ehi) = halo_rows(lo, hi, H, halo) already holds
+        the rank's own rows at [lo - elo, hi - elo); the rows above / below are received from
+        the neighbours (each sends the same count of its edge rows back).  Only halo rows
+        move: the own rows stay where the caller put them.  Returns elo."""
         r, w = self.rank, self.world
         elo, ehi = halo_rows(lo, hi, H, halo)
         need_top, need_bot = lo - elo, ehi - hi
         if need_top > (hi - lo) or need_bot > (hi - lo):
             raise ValueError("each shard must own at least `halo` rows")
-        dev = local.device
-        xfer = (lambda t: t.contiguous()) if self.backend == "nccl" else (lambda t: t.cpu().contiguous())
-        ops, bufs = [], {}
-        c, _, W = local.shape
-        # counts are symmetric once every shard owns >= halo rows: rank r needs
-        # min(lo, halo) rows from r-1 and sends it the same number of its top rows
+        c, rows, W = ext.shape
+        if rows != ehi - elo:
+            raise ValueError(f"extended band must have {ehi - elo} rows, got {rows}")
+        nccl = self.backend == "nccl"
+        xfer = (lambda t: t.contiguous()) if nccl else (lambda t: t.cpu().contiguous())
+        top, own = need_top, hi - lo
+        ops, recv = [], []
         if r > 0:
-            k = need_top
-            bufs["top"] = xfer(torch.empty((c, k, W), dtype=local.dtype, device=dev))
-            ops.append(dist.P2POp(dist.isend, xfer(local[:, :k]), r - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, bufs["top"], r - 1, self.group))
+            buf = xfer(torch.empty((c, top, W), dtype=ext.dtype, device=ext.device))
+            ops.append(dist.P2POp(dist.isend, xfer(ext[:, top:2 * top]), r - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf, r - 1, self.group))
+            recv.append((buf, 0))
         if r < w - 1:
-            k = need_bot
-            bufs["bot"] = xfer(torch.empty((c, k, W), dtype=local.dtype, device=dev))
-            ops.append(dist.P2POp(dist.isend, xfer(local[:, local.shape[1] - k:]), r + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, bufs["bot"], r + 1, self.group))
+            buf = xfer(torch.empty((c, need_bot, W), dtype=ext.dtype, device=ext.device))
+            ops.append(dist.P2POp(dist.isend, xfer(ext[:, top + own - need_bot:top + own]), r + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf, r + 1, self.group))
+            recv.append((buf, top + own))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        parts = []
-        if "top" in bufs:
-            parts.append(bufs["top"].to(dev))
-        parts.append(local)
-        if "bot" in bufs:
-            parts.append(bufs["bot"].to(dev))
-        return torch.cat(parts, dim=1).contiguous(), elo
+        for buf, row0 in recv:
+            ext[:, row0:row0 + buf.shape[1]].copy_(buf, non_blocking=nccl)
+        return elo
+
+    def exchange_rows(self, local: torch.Tensor, lo: int, hi: int, H: int, halo: int):
+        """Extend ``local`` (c, hi-lo, W) with up to ``halo`` rows from each
+        neighbour; returns (extended tensor, first global row).  Allocates the
+        band and copies the own rows once; repeated calls should keep the band
+        (``extended_band``) and call exchange_halos."""
+        ext, top = extended_band(local.shape[0], lo, hi, H, halo, local.shape[2], local.dtype, local.device)
+        ext[:, top:top + (hi - lo)].copy_(local)
+        return ext, self.exchange_halos(ext, lo, hi, H, halo)
+
+
+def extended_band(c: int, lo: int, hi: int, H: int, halo: int, W: int, dtype, device) -> tuple[torch.Tensor, int]:
+    """An uninitialised (c, rows + halos, W) band for the rows [lo, hi) and the row offset of
+    the own rows inside it."""
+    elo, ehi = halo_rows(lo, hi, H, halo)
+    return torch.empty((c, ehi - elo, W), dtype=dtype, device=device), lo - elo
 
 
 # ---------------------------------------------------------------------------
@@ -290,25 +308,119 @@ def distributed_kmeans(ops: KMeansOps, comm: Comm, m0: int, seed: int = 0, max_i
     return ShardedKMeans(centroids=C_, quant_error=qe, errors=tuple(errors), seed_indices=seeds)
 
 
+def device_distributed_kmeans(points: torch.Tensor, comm: Comm, m0: int, seed: int = 0,
+                              max_iter: int = 50) -> ShardedKMeans | None:
+    """distributed_kmeans with every decision taken on the device: per k-means++ draw an
+    all-gather of the ranks' D^2 totals and an all-reduce of the owner's candidate point,
+    per Lloyd iteration one all-reduce of the cluster sums / counts / objective / changed
+    count (the reference's update and break rule then run on the device,
+    landmarks.py:60-129); the host waits once, at the end.  Returns None when the run
+    needs the host-orchestrated path (a zero D^2 total -- the reference then draws with
+    integers(m) -- or an empty cluster, whose repair needs the global farthest point)."""
+    from ._device import ptr, stream_ptr, workspace
+
+    lib = _native.lib()
+    dev = points.device
+    rho, m_loc = int(points.shape[0]), int(points.shape[1])
+    ps = int(points.stride(0))
+    counts = comm.allgather(float(m_loc))[:, 0].astype(np.int64)
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    m = int(offs[-1])
+    if m0 < 1 or m0 > m:
+        raise ValueError(f"m0 must be in [1, {m}], got {m0}")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    me, world = comm.rank, comm.world
+    wsb = int(lib.nys_kmeans_workspace_bytes(m_loc, rho, m0))
+    ws = workspace(wsb)
+    s = stream_ptr()
+    # cands[j] = (landmark j, its global index): the owner of draw j writes its row, the others
+    # zeros, and an all-reduce(sum) hands it to every rank; the next draw's D^2 update reads it
+    # in place (a one-member group needs no collective at all)
+    cands = torch.zeros((m0, rho + 1), dtype=torch.float64, device=dev)
+    C_ = torch.zeros((m0, rho), dtype=torch.float64, device=dev)
+    reduce = (lambda t: dist.all_reduce(t, group=comm.group)) if world > 1 else (lambda t: None)
+    d2 = torch.empty(m_loc, dtype=torch.float64, device=dev)
+    mytot = torch.zeros(1, dtype=torch.float64, device=dev)
+    totals = torch.zeros(world, dtype=torch.float64, device=dev)
+    tot = torch.zeros(m0 * rho + m0 + 1, dtype=torch.int64, device=dev)  # fixed-point sums, counts, changed
+    obj = torch.zeros(1, dtype=torch.float64, device=dev)
+    # the single-device kernel's fixed-point scale over the global points: 2^sexp,
+    # sexp = 61 - ilogb(max|x| * m) - 1 (nys_kmeans_coop.cu)
+    mx = points.abs().max().reshape(1).double() if m_loc > 0 else torch.zeros(1, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=comm.group)
+    maxabs = float(np.float32(mx.item()))
+    sexp = 61 - int(np.frexp(maxabs * float(m))[1] - 1) - 1 if maxabs > 0 else 0
+    errors = torch.zeros(max_iter, dtype=torch.float64, device=dev)
+    stats = torch.zeros(4, dtype=torch.int64, device=dev)
+    qe = torch.zeros(1, dtype=torch.float64, device=dev)
+    chk = _native.check
+    chk(lib.nys_kmeans_state_init(ptr(ws), wsb, m_loc, rho, m0, s), "nys_kmeans_state_init")
+    rng = np.random.default_rng(seed)
+    first = int(rng.integers(m))
+    owner0 = int(np.searchsorted(offs, first, side="right") - 1)
+    if owner0 == me:
+        chk(lib.nys_gather_point(ptr(points), ps, rho, first - int(offs[me]), ptr(cands[0]), s), "nys_gather_point")
+        cands[0, rho] = float(first)
+    reduce(cands[0])
+    for j in range(1, m0):
+        u = float(rng.random())  # one random() per draw, as Generator.choice consumes it
+        chk(lib.nys_kmeanspp_update(ptr(points), ps, m_loc, rho, ptr(cands[j - 1]), int(j == 1), ptr(d2),
+                                    ptr(mytot if world > 1 else totals), ptr(ws), wsb, s), "nys_kmeanspp_update")
+        if world > 1:
+            dist.all_gather_into_tensor(totals, mytot, group=comm.group)
+        chk(lib.nys_kmeanspp_owner_pick(ptr(points), ps, m_loc, rho, m0, ptr(d2), ptr(totals), world, me,
+                                        int(offs[me]), u, j, ptr(cands[j]), ptr(ws), wsb, s), "nys_kmeanspp_owner_pick")
+        reduce(cands[j])
+    C_.copy_(cands[:, :rho])
+    seeds = cands[:, rho]
+    for it in range(max_iter):
+        chk(lib.nys_kmeans_lloyd_local(ptr(points), ps, m_loc, rho, ptr(C_), m0, it, sexp, ptr(tot), ptr(obj),
+                                       ptr(ws), wsb, s), "nys_kmeans_lloyd_local")
+        reduce(tot)
+        reduce(obj)
+        chk(lib.nys_kmeans_lloyd_update(m_loc, rho, m0, it, sexp, ptr(tot), ptr(obj), ptr(C_), ptr(errors), ptr(ws),
+                                        wsb, s), "nys_kmeans_lloyd_update")
+    chk(lib.nys_kmeans_exact(ptr(points), ps, m_loc, rho, ptr(C_), m0, None, ptr(qe), ptr(ws), wsb, s),
+        "nys_kmeans_exact")
+    reduce(qe)
+    chk(lib.nys_kmeans_state_read(ptr(ws), m_loc, rho, m0, ptr(stats), s), "nys_kmeans_state_read")
+    st = stats.cpu().numpy()  # the one host wait
+    if st[1] >= 0 or st[3] < 0:
+        return None
+    iters = int(st[0])
+    return ShardedKMeans(centroids=C_.cpu().numpy(), quant_error=float(qe.cpu()[0]),
+                         errors=tuple(errors[:iters].cpu().numpy().tolist()),
+                         seed_indices=seeds.cpu().numpy().astype(np.int64))
+
+
 # ---------------------------------------------------------------------------
 # sharded filter
 # ---------------------------------------------------------------------------
-def sharded_fast_filter(f_local: torch.Tensor, H: int, params, comm: Comm, nlm: bool = False):
+def sharded_fast_filter(f_local: torch.Tensor | None, H: int, params, comm: Comm, nlm: bool = False,
+                        f_ext: torch.Tensor | None = None):
     """Filter this rank's rows of a row-sharded image.
 
-    ``f_local`` (n, rows, W) holds image rows shard_rows(H, world, rank).
+    ``f_local`` (n, rows, W) holds image rows shard_rows(H, world, rank); or pass
+    ``f_ext``, the rank's extended band (parallel.extended_band) with the own rows already
+    in place, which is then reused across calls (only the halo rows move).
     Returns (out_local (n, rows, W), report dict)."""
     from .filters import _Inputs, run_filter
     from ._device import ptr, stream_ptr
 
     lo, hi = shard_rows(H, comm.world, comm.rank)
-    if f_local.shape[1] != hi - lo:
-        raise ValueError("f_local rows do not match this rank's shard")
-    n, _, W = f_local.shape
     R = params.spatial.effective_radius()
     halo = R + (1 if nlm else 0)
-    ext, elo = comm.exchange_rows(f_local, lo, hi, H, halo)
-    ext = ext.to(f_local.device).contiguous()
+    if f_ext is None:
+        if f_local.shape[1] != hi - lo:
+            raise ValueError("f_local rows do not match this rank's shard")
+        ext, elo = comm.exchange_rows(f_local, lo, hi, H, halo)
+    else:
+        ext = f_ext
+        elo = comm.exchange_halos(ext, lo, hi, H, halo)
+        f_local = ext[:, lo - elo:hi - elo]
+    n, _, W = ext.shape
     if nlm:
         # raw 3x3xn patches of the own rows, gathered from the extended band
         from .filters import PatchGuide  # noqa: F401  (same gather as the single-device path)
@@ -321,10 +433,23 @@ def sharded_fast_filter(f_local: torch.Tensor, H: int, params, comm: Comm, nlm: 
         points = pl[:, lo - elo:hi - elo].reshape(rho, -1).contiguous()
         inp = _Inputs(f=ext, guide=ext, gkind=1, points=points, rho=rho)
     else:
-        points = f_local.reshape(n, -1)
+        # the own rows of the band, planar (rho, m_local) with the band's plane stride: k-means
+        # reads them in place (plane stride = band rows x W)
+        points = ext.reshape(n, -1)[:, (lo - elo) * W:(hi - elo) * W]
         inp = _Inputs(f=ext, guide=ext, gkind=0, points=points, rho=n)
-    km = distributed_kmeans(DeviceKMeansOps(points, params.m0), comm, params.m0, params.seed,
-                            params.kmeans_max_iter)
+    km = None
+    if comm.world == 1 and os.environ.get("NYS_SHARD_STEPWISE", "0") != "1":
+        # one rank holds every point: the single-device cooperative k-means (no collective to make)
+        from .landmarks import kmeans_device
+
+        r = kmeans_device(points, params.m0, seed=params.seed, max_iter=params.kmeans_max_iter)
+        km = ShardedKMeans(centroids=r.centroids, quant_error=float(r.quant_error), errors=tuple(r.errors),
+                           seed_indices=np.asarray(getattr(r, "seed_indices", np.zeros(0)), np.int64))
+    elif comm.backend == "nccl":  # device-resident collectives (gloo keeps the host-orchestrated path)
+        km = device_distributed_kmeans(points, comm, params.m0, params.seed, params.kmeans_max_iter)
+    if km is None:
+        km = distributed_kmeans(DeviceKMeansOps(points, params.m0), comm, params.m0, params.seed,
+                                params.kmeans_max_iter)
     out, plan, stats = run_filter(inp, km.centroids, params, rows=(lo, hi), row_origin=elo, H_global=H)
     st = stats.cpu()
     min_den = float(comm.allgather(float(st[0]))[:, 0].min())
@@ -351,13 +476,16 @@ def bench_sharded(args, wl, rank: int, world: int):
     lo, hi = shard_rows(H, world, rank)
     f_full = wl.image(seed=0)
     f_host = torch.from_numpy(np.ascontiguousarray(f_full[:, lo:hi])).pin_memory()
-    f_local = f_host.to(dev)
     del f_full
     sk = SpatialKernel.box(wl.radius) if wl.spatial == "box" else SpatialKernel.gaussian(wl.sigma, wl.radius)
     params = FilterParams(spatial=sk, theta=float(wl.theta), m0=wl.m0, seed=0, kmeans_max_iter=wl.max_iter)
     nlm = wl.mode == "nlm"
+    # the rank's rows live in its extended band for the whole run: a step moves only halo rows
+    halo = params.spatial.effective_radius() + (1 if nlm else 0)
+    f_ext, top = extended_band(f_host.shape[0], lo, hi, H, halo, W, torch.float32, dev)
+    f_ext[:, top:top + (hi - lo)].copy_(f_host)
     for _ in range(args.warmup):
-        sharded_fast_filter(f_local, H, params, comm, nlm)
+        sharded_fast_filter(None, H, params, comm, nlm, f_ext=f_ext)
     torch.cuda.synchronize()
     dist.barrier()
 
@@ -380,13 +508,13 @@ def bench_sharded(args, wl, rank: int, world: int):
     lib = _native.lib()
     l0 = int(lib.nys_kernel_launches())
     with ClockSampler(torch.cuda.current_device()) as clk:
-        ms, (out, rep) = timed(lambda: sharded_fast_filter(f_local, H, params, comm, nlm))
+        ms, (out, rep) = timed(lambda: sharded_fast_filter(None, H, params, comm, nlm, f_ext=f_ext))
     launches = (int(lib.nys_kernel_launches()) - l0) // max(1, args.steps)
     out_host = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
 
     def e2e_step():
-        fd = f_host.to(dev, non_blocking=True)
-        o, r = sharded_fast_filter(fd, H, params, comm, nlm)
+        f_ext[:, top:top + (hi - lo)].copy_(f_host, non_blocking=True)  # the own rows, into the band
+        o, r = sharded_fast_filter(None, H, params, comm, nlm, f_ext=f_ext)
         out_host.copy_(o, non_blocking=True)
         return o, r
 

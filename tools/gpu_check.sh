@@ -1,7 +1,4 @@
-# usage: bash tools/gpu_check.sh [tag]  -- gpu tests, short bench, launch list
-tag=${1:-x}
-timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -15
-timeout 300 python bench.py --steps 3 --warmup 2 --cpu-rows 16 > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; tail -c 1500 gpurun_out/bench_$tag.json; tail -3 gpurun_out/bench_$tag.err
-timeout 300 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain_$tag.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_$tag.log 2>&1
-echo ncu rc=$?
+# usage: bash tools/gpu_check.sh  -- GPU tests, bench line, e2e paths
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | grep metric | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['roofline']['kernel_ms'], d['e2e']['value'], d['e2e_reference_types']['value'])"
+timeout 300 python bench.py --steps 5 --warmup 2 --sharded --no-cpu-baseline 2>/dev/null | grep metric | cut -c1-200

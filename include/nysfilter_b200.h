@@ -37,8 +37,12 @@ extern "C" {
 
 #define NYS_MAX_RADIUS 64          /* taps = 2R+1 <= 129 */
 #define NYS_MAX_M0 256
-#define NYS_MAX_RHO 64
-#define NYS_MAX_CHANNELS 64
+#define NYS_MAX_RHO 64        /* guide dimensions held in registers by the fast kernels */
+#define NYS_MAX_RHO_WIDE 1024 /* wider guides (e.g. 103 hyperspectral bands, 147-dim r = 3 patches)
+                                 take the generic paths: step-wise k-means, features written
+                                 as planes by a separate pass before K2 */
+#define NYS_MAX_CHANNELS 64       /* filtered channels held in registers (brute force) */
+#define NYS_MAX_CHANNELS_WIDE 511 /* filtered channels of the Nystrom path (e.g. all 103 bands of a cube) */
 
 /* Library ABI version (major*100 + minor). */
 int nys_abi_version(void);

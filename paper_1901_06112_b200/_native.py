@@ -22,8 +22,10 @@ NYS_SPATIAL_GAUSSIAN_FIR = 1
 NYS_SPATIAL_GAUSSIAN_RECURSIVE = 2
 NYS_MAX_RADIUS = 64
 NYS_MAX_M0 = 256
-NYS_MAX_RHO = 64
+NYS_MAX_RHO = 64        # register-resident guides (the fast kernels)
+NYS_MAX_RHO_WIDE = 1024  # generic paths beyond (step-wise k-means, features as planes before K2)
 NYS_MAX_CHANNELS = 64
+NYS_MAX_CHANNELS_WIDE = 511
 
 
 class NativeError(RuntimeError):

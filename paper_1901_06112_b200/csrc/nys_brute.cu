@@ -105,6 +105,7 @@ extern "C" int nys_brute_force_filter(const nys_filter_desc* d, const float* f, 
                                       const float* guide, int64_t guide_plane_stride, float* out,
                                       int64_t out_plane_stride, void* stream) {
   int st = validate(d);
+  if (!st && (d->rho > NYS_MAX_RHO || d->n > NYS_MAX_CHANNELS)) st = NYS_EUNSUPPORTED;  // register-resident
   if (st) return st;
   if (!f || !out || !guide) return NYS_EINVAL;
   if (d->guide_kind != 0) return NYS_EINVAL;  // the patch guide is materialised first (nys_patch_guide)

@@ -117,7 +117,7 @@ inline int num_sms() {
 
 inline int validate(const nys_filter_desc* d) {
   if (!d) return NYS_EINVAL;
-  if (d->n < 1 || d->n > NYS_MAX_CHANNELS || d->rho < 1 || d->rho > NYS_MAX_RHO) return NYS_EUNSUPPORTED;
+  if (d->n < 1 || d->n > NYS_MAX_CHANNELS_WIDE || d->rho < 1 || d->rho > NYS_MAX_RHO_WIDE) return NYS_EUNSUPPORTED;
   if (d->H < 1 || d->W < 1 || d->m0 < 1 || d->m0 > NYS_MAX_M0) return NYS_EINVAL;
   if (d->spatial_kind == NYS_SPATIAL_GAUSSIAN_RECURSIVE) {
     // radius unused (the recursion spans whole rows / columns); sigma < 1 is

@@ -26,6 +26,8 @@ struct HArgs {
   int phi;           // phi-form: store y_i (= phi_i) in the feature-plane slots instead of b_i
   int ku, nu, tcols, nbuf;  // tcgen05 path: K (m0 padded to 8), N ((m0+1) padded to 16), TMEM columns per group, y/f buffers
   int sc, kw;               // tensor-FIR path: source samples per tile (TMEM columns), Toeplitz K window
+  int bfrom;                // wide guides (rho > NYS_MAX_RHO): the features were written as b planes by
+                            // k_bplanes_wide; K2 reads them instead of evaluating the guide
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
   float k2;
   float taps[NYS_MAX_TAPS];

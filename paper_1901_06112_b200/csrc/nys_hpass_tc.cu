@@ -76,15 +76,16 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
   const int nchunks = (NC + K2_CC - 1) / K2_CC;
   const int nfr = nchunks * K2_CC;  // f rows per buffer: f_c, 1 (y plane), 0 padding
 
-  float* Cs = sm;                                  // m0 x rhop
-  float* Bh = Cs + align32f(m0 * rhop);            // NU x KU, K-major core matrices
+  float* Cs = sm;                                  // m0 x rhop (none when the features come from b planes)
+  float* Bh = Cs + (a.bfrom ? 0 : align32f(m0 * rhop));  // NU x KU, K-major core matrices
   float* Bl = Bh + NU * KU;
   float* gbase = Bl + NU * KU;                     // per group, per buffer: Fs (nfr x pitch), Ys (m0q x pitch)
   const int buf_floats = align32f(nfr * pitch) + m0q * pitch;
   auto Fs_of = [&](int b) { return gbase + (size_t)(g * nbuf + b) * buf_floats; };
   auto Ys_of = [&](int b) { return Fs_of(b) + align32f(nfr * pitch); };
 
-  for (int k = tid; k < m0 * rhop; k += K2T_THREADS) Cs[k] = a.cst[k];
+  if (!a.bfrom)
+    for (int k = tid; k < m0 * rhop; k += K2T_THREADS) Cs[k] = a.cst[k];
   {
     const float* MTg = a.cst + (size_t)m0 * rhop;  // MT[j][i] = M[i][j], MT[j][m0] = u0[j]
     for (int k = tid; k < NU * KU; k += K2T_THREADS) {
@@ -129,6 +130,23 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
     const int xs = x0 - R + px;
     const int x = clampi(xs, 0, W - 1);
+    if (a.bfrom) {  // wide guide: b_j(x) from the planes k_bplanes_wide wrote for this virtual row
+      const float* bsrc = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(x >> 5) * (a.npl * 32) +
+                          (long long)(L * NC) * 32 + (x & 31);
+      for (int j0 = hh * khalf; j0 < (hh + 1) * khalf; j0 += 4) {
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v = j0 + e < m0 ? bsrc[(size_t)(j0 + e) * 32] : 0.f;
+          hi[e] = umma::to_tf32(v);
+          lo[e] = umma::to_tf32(v - hi[e]);
+        }
+        umma::st_32x32b_x4(a_hi + lane_base + (uint32_t)j0, hi[0], hi[1], hi[2], hi[3]);
+        umma::st_32x32b_x4(a_lo + lane_base + (uint32_t)j0, lo[0], lo[1], lo[2], lo[3]);
+      }
+      umma::st_wait();
+      return;
+    }
     float gv[GR];
 #pragma unroll
     for (int dd = 0; dd < GR; ++dd)
@@ -783,7 +801,49 @@ int launch_hpass_tf(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
 #undef NYS_TF_GR
 }
 
+// Features of a wide guide (rho > NYS_MAX_RHO) for every virtual row of the band, written as
+// the raw b planes K3 reads anyway (plane index (m0+1)(n+1) + j): one CTA per 32-column block
+// of a virtual row; the 32 guide vectors are staged in shared memory ([rho][32], lane = pixel),
+// warp w evaluates landmarks w, w + 8, ... (difference form, FP32, exp2 as in the fast kernels).
+__global__ void __launch_bounds__(256) k_bplanes_wide(const HArgs a) {
+  extern __shared__ __align__(16) float gsm[];  // rho x 32 guide values, then m0 x rhop centroids
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rho = a.rho, rhop = a.rhop, m0 = a.m0, W = a.W, H = a.H;
+  const int nxb = (W + 31) >> 5;
+  const int vr = a.v0 + blockIdx.x / nxb, xb = blockIdx.x % nxb;
+  const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
+  float* Cs = gsm + (size_t)rho * 32;
+  for (int k = threadIdx.x; k < m0 * rhop; k += blockDim.x) Cs[k] = a.cst[k];
+  for (int k = threadIdx.x; k < rho * 32; k += blockDim.x) {
+    const int dd = k >> 5, x = min(xb * 32 + (k & 31), W - 1);
+    gsm[k] = guide_at(a.g, a.gps, a.f, a.fps, a.gkind, dd, row, x, H, W);
+  }
+  __syncthreads();
+  const int L = m0 + 1, NC = a.n + 1;
+  float* dst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)xb * (a.npl * 32) + (long long)(L * NC) * 32 + lane;
+  for (int j = w; j < m0; j += 8) {
+    const float* c = Cs + (size_t)j * rhop;
+    float d2 = 0.f;
+    for (int dd = 0; dd < rho; ++dd) {
+      const float t = gsm[dd * 32 + lane] - c[dd];
+      d2 = fmaf(t, t, d2);
+    }
+    dst[(size_t)j * 32] = range_kernel(d2, a.k2);
+  }
+}
+
 int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
+  if (d->rho > NYS_MAX_RHO) {
+    if (a.phi) return NYS_EUNSUPPORTED;  // the phi-form stores phi, not b, in the feature planes
+    const size_t wsm = ((size_t)d->rho * 32 + (size_t)d->m0 * a.rhop) * sizeof(float);
+    if (wsm > 220 * 1024) return NYS_EUNSUPPORTED;
+    NYS_CUDA_TRY(cudaFuncSetAttribute(k_bplanes_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    const long long nblk = (long long)a.vrows * ((d->W + 31) / 32);
+    count_launch();
+    k_bplanes_wide<<<(unsigned)nblk, 256, wsm, s>>>(a);
+    NYS_LAUNCH_CHECK();
+    a.bfrom = 1;
+  }
   const int R = d->radius;
   int TW = ((K2T_PX - 2 * R) / K2_XR) * K2_XR;
   if (TW < K2_XR) return NYS_EUNSUPPORTED;
@@ -799,7 +859,7 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   int pitch = (int)ceil_div(TW + 2 * R + 4, 4) * 4;
   pitch += ((4 - pitch % 32) + 32) % 32;  // = 4 (mod 32): the FIR's LDS.128 across rows is conflict-free
   const int nfr = (int)ceil_div(d->n + 1, K2_CC) * K2_CC;
-  const size_t fixed = (size_t)align32f(d->m0 * a.rhop) + 2 * (size_t)NU * KU;
+  const size_t fixed = (a.bfrom ? 0 : (size_t)align32f(d->m0 * a.rhop)) + 2 * (size_t)NU * KU;
   const size_t buf = (size_t)align32f(nfr * pitch) + (size_t)a.m0q * pitch;
   // two y/f buffers per group when they fit (one barrier per tile), else one
   int nbuf = 2;
@@ -815,7 +875,7 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   a.tcols = tcols;
   a.nbuf = nbuf;
   const long long ntiles = (long long)a.tiles_x * a.vrows;
-  const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
+  const int GR = a.bfrom ? 4 : (d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64)));
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) k_pp_update(const float* __restrict__ pts
                                                    double* __restrict__ d2, double* __restrict__ ppart,
                                                    long long chunk, const KState* st) {
   __shared__ double sh[32];
-  __shared__ double cs[NYS_MAX_RHO];
+  __shared__ double cs[NYS_MAX_RHO_WIDE];
   if (st && st->zero_draw >= 0) return;
   for (int d = threadIdx.x; d < rho; d += blockDim.x) cs[d] = c[d];
   __syncthreads();
@@ -242,6 +242,112 @@ __global__ void __launch_bounds__(256) k_assign(const float* __restrict__ pts, l
     out[slots] = a;
     out[slots + 1] = b;
   }
+}
+
+// Wide guides (rho > NYS_MAX_RHO): the same assignment with the coordinates read from the
+// planar points inside the centroid loop (L1-resident) instead of registers.
+__global__ void __launch_bounds__(256) k_assign_wide(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                     const float* __restrict__ Cf, int m0, int* __restrict__ labels,
+                                                     int first, double* __restrict__ part, int S, const KState* st) {
+  extern __shared__ __align__(16) double dsm[];
+  if (st && st->converged) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int slots = m0 * (rho + 1);
+  double* wacc = dsm;                                  // nw x slots
+  float* Cs = reinterpret_cast<float*>(dsm + (size_t)nw * slots);
+  for (int k = threadIdx.x; k < nw * slots; k += blockDim.x) wacc[k] = 0.0;
+  for (int k = threadIdx.x; k < m0 * rho; k += blockDim.x) Cs[k] = Cf[k];
+  __syncthreads();
+  double* my = wacc + (size_t)w * slots;
+  double near_sum = 0.0;
+  long long changed = 0;
+  const long long chunk = ceil_div(m, (long long)gridDim.x);
+  const long long lo = blockIdx.x * chunk, hi = min(m, lo + chunk);
+  for (long long base = lo + (long long)w * 32; base < hi; base += (long long)nw * 32) {
+    const long long i = base + lane;
+    const bool valid = i < hi;
+    const long long ii = valid ? i : lo;
+    float best = INFINITY;
+    int arg = 0;
+    for (int j = 0; j < m0; ++j) {
+      float d2 = 0.f;
+      for (int d = 0; d < rho; ++d) {
+        const float t = __ldg(pts + d * ps + ii) - Cs[j * rho + d];
+        d2 = fmaf(t, t, d2);
+      }
+      if (d2 < best) {  // strict: first index wins ties (np.argmin)
+        best = d2;
+        arg = j;
+      }
+    }
+    if (valid) {
+      near_sum += (double)best;
+      const int old = labels[i];
+      if (first || old != arg) ++changed;
+      labels[i] = arg;
+    }
+    unsigned rem = __ballot_sync(0xffffffffu, valid);
+    while (rem) {
+      const int leader = __ffs(rem) - 1;
+      const int Lb = __shfl_sync(0xffffffffu, arg, leader);
+      const unsigned grp = __ballot_sync(0xffffffffu, valid && arg == Lb);
+      const bool in = (grp >> lane) & 1u;
+      for (int d = 0; d < rho; ++d) {
+        const double sd = warp_sum(in ? (double)__ldg(pts + d * ps + ii) : 0.0);
+        if (lane == 0) my[Lb * (rho + 1) + d] += sd;
+      }
+      if (lane == 0) my[Lb * (rho + 1) + rho] += (double)__popc(grp);
+      rem &= ~grp;
+    }
+  }
+  near_sum = warp_sum(near_sum);
+  const double ch = warp_sum((double)changed);
+  __shared__ double extra[2][32];
+  if (lane == 0) {
+    extra[0][w] = near_sum;
+    extra[1][w] = ch;
+  }
+  __syncthreads();
+  double* out = part + (size_t)blockIdx.x * S;
+  for (int k = threadIdx.x; k < slots; k += blockDim.x) {
+    double sv = 0.0;
+    for (int q = 0; q < nw; ++q) sv += wacc[(size_t)q * slots + k];
+    out[k] = sv;
+  }
+  if (threadIdx.x == 0) {
+    double a0 = 0.0, b0 = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      a0 += extra[0][q];
+      b0 += extra[1][q];
+    }
+    out[slots] = a0;
+    out[slots + 1] = b0;
+  }
+}
+
+// Wide guides: the exact (FP64 differenced) nearest distance straight, no FP32 screen
+__global__ void __launch_bounds__(256) k_exact_wide(const float* __restrict__ pts, long long ps, long long m, int rho,
+                                                    const double* __restrict__ C, int m0, long long* __restrict__ asg,
+                                                    double* __restrict__ part) {
+  __shared__ double sh[32];
+  const long long chunk = ceil_div(m, (long long)gridDim.x);
+  const long long lo = min(m, blockIdx.x * chunk), hi = min(m, lo + chunk);
+  double s = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    double best = INFINITY;
+    int arg = 0;
+    for (int j = 0; j < m0; ++j) {
+      const double v = d2_exact(pts, ps, i, rho, C + (size_t)j * rho);
+      if (v < best) {
+        best = v;
+        arg = j;
+      }
+    }
+    if (asg) asg[i] = arg;
+    s += fmax(best, 0.0);
+  }
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
 // tot[k] = Σ_b part[b][k] in block order
@@ -459,6 +565,14 @@ static int launch_exact(const float* pts, long long ps, long long m, int rho, co
     NYS_LAUNCH_CHECK();
     return NYS_OK;
   };
+  if (rho > NYS_MAX_RHO) {
+    const int nb = (int)std::max<long long>(1, std::min<long long>(ceil_div(m, 256LL), (long long)max_nb));
+    *nb_out = nb;
+    count_launch();
+    k_exact_wide<<<nb, 256, 0, s>>>(pts, ps, m, rho, C, m0, asg, part);
+    NYS_LAUNCH_CHECK();
+    return NYS_OK;
+  }
   switch (rho) {
     case 1: return go(k_exact<4, 1>);
     case 2: return go(k_exact<4, 2>);
@@ -622,12 +736,8 @@ __global__ void __launch_bounds__(1024) k_pp_owner_pick(const float* __restrict_
       const double target = u * total;
       double pre = 0.0;
       int last_pos = -1;
-      double pre_last = 0.0;
       for (int r = 0; r < world; ++r) {
-        if (totals[r] > 0.0) {
-          last_pos = r;
-          pre_last = pre;
-        }
+        if (totals[r] > 0.0) last_pos = r;
         if (pre + totals[r] > target) {
           owner = r;
           t = target - pre;
@@ -638,7 +748,6 @@ __global__ void __launch_bounds__(1024) k_pp_owner_pick(const float* __restrict_
       if (owner < 0) {  // rounding pushed the target past the end (parallel.distributed_kmeans)
         owner = last_pos;
         t = totals[owner] * (1.0 - 1e-16);
-        (void)pre_last;
       }
     } else {
       st->zero_draw = draw;  // sum(D^2) == 0: the reference switches to integers(m) (host fallback)
@@ -833,8 +942,12 @@ static int launch_assign(const float* pts, long long ps, long long m, int rho, c
     NYS_A_CASE(16)
   } else if (rho <= 32) {
     NYS_A_CASE(32)
-  } else {
+  } else if (rho <= NYS_MAX_RHO) {
     NYS_A_CASE(64)
+  } else {
+    NYS_CUDA_TRY(cudaFuncSetAttribute(k_assign_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    count_launch();
+    k_assign_wide<<<nb, nw * 32, smem, s>>>(pts, ps, m, rho, Cf, m0, labels, first, part, S, st);
   }
 #undef NYS_A_CASE
   NYS_LAUNCH_CHECK();
@@ -845,7 +958,7 @@ int launch_assign_tc(const float* pts, long long ps, long long m, int rho, const
                      int first, double* part, int nb, int S, const KState* st, cudaStream_t s);
 
 static int check_common(const float* pts, int64_t m, int rho, int m0, void* ws, size_t wsb) {
-  if (!pts || m < 1 || rho < 1 || rho > NYS_MAX_RHO || m0 < 1 || m0 > NYS_MAX_M0 || m0 > m) return NYS_EINVAL;
+  if (!pts || m < 1 || rho < 1 || rho > NYS_MAX_RHO_WIDE || m0 < 1 || m0 > NYS_MAX_M0 || m0 > m) return NYS_EINVAL;
   if (!ws || wsb < klayout(m, rho, m0).total) return NYS_EINVAL;
   return NYS_OK;
 }
@@ -987,7 +1100,7 @@ int nys_kmeans_run_seeded(const float* points, int64_t plane_stride, int64_t m, 
 
 int nys_kmeanspp_update(const float* points, int64_t plane_stride, int64_t m, int rho, const double* c, int init,
                         double* d2, double* sum_out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (!points || !c || !d2 || !sum_out || m < 1 || rho < 1 || rho > NYS_MAX_RHO) return NYS_EINVAL;
+  if (!points || !c || !d2 || !sum_out || m < 1 || rho < 1 || rho > NYS_MAX_RHO_WIDE) return NYS_EINVAL;
   const KLayout L = klayout(m, rho, 1);
   if (!workspace || workspace_bytes < L.total) return NYS_EINVAL;
   char* ws = reinterpret_cast<char*>(workspace);
@@ -1085,7 +1198,7 @@ int nys_kmeans_state_read(const void* workspace, int64_t m, int rho, int m0, int
 int nys_kmeanspp_owner_pick(const float* points, int64_t plane_stride, int64_t m, int rho, int m0, const double* d2,
                             const double* totals, int world, int rank, int64_t my_offset, double u, int draw,
                             double* cand_out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (!points || !d2 || !totals || !cand_out || m < 1 || rho < 1 || rho > NYS_MAX_RHO || m0 < 1 || world < 1 ||
+  if (!points || !d2 || !totals || !cand_out || m < 1 || rho < 1 || rho > NYS_MAX_RHO_WIDE || m0 < 1 || world < 1 ||
       rank < 0 || rank >= world)
     return NYS_EINVAL;
   const KLayout L = klayout(m, rho, m0);

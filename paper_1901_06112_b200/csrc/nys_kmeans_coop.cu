@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
 int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m0, const double* uniforms_dev,
                      double* C, long long* seeds, char* ws, const KLayout& L, cudaStream_t s) {
   if (m0 < 2) return NYS_OK;
-  if (!coop_supported()) return NYS_EUNSUPPORTED;
+  if (!coop_supported() || rho > NYS_MAX_RHO) return NYS_EUNSUPPORTED;  // wide guides: step-wise seeding
   SeedArgs a;
   a.pts = pts;
   a.ps = ps;
@@ -846,7 +846,7 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
 
 int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int m0, int max_iter, double* C,
                       double* errors, char* ws, const KLayout& L, cudaStream_t s, bool prezeroed) {
-  if (!coop_supported()) return NYS_EUNSUPPORTED;
+  if (!coop_supported() || rho > NYS_MAX_RHO) return NYS_EUNSUPPORTED;
   const int msl = m0 * rho;
   const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
                        2 * (size_t)((m0 + 3) & ~3) * ((rho + 3) & ~3) * 4 + 96;

@@ -65,7 +65,7 @@ inline KLayout klayout(int64_t m, int rho, int m0) {
   L.off_idx = o;     o = align256(o + 64);
   L.off_unif = o;    o = align256(o + (size_t)m0 * 8);
   L.off_tsum = o;    o = align256(o + (size_t)L.nb_coop * 512 * 8);
-  L.off_pp = o;      o = align256(o + (size_t)L.m_pad * rho * 4);
+  L.off_pp = o;      o = align256(o + (rho <= NYS_MAX_RHO ? (size_t)L.m_pad * rho * 4 : 0));  // coop seeding only
   L.total = o;
   return L;
 }
@@ -141,8 +141,14 @@ __device__ __forceinline__ double sqdiff(double x, double c) {
   return __dmul_rn(t, t);
 }
 
+// numpy's pairwise summation above its 128-element block (rho > 128): the two halves (the
+// first rounded down to a multiple of 8) summed recursively, then added
+static __device__ double d2_exact_pw(const float* __restrict__ pts, long long ps, long long i, int rho,
+                              const double* __restrict__ c);
+
 __device__ __forceinline__ double d2_exact(const float* __restrict__ pts, long long ps, long long i, int rho,
                            const double* __restrict__ c) {
+  if (rho > 128) return d2_exact_pw(pts, ps, i, rho, c);
   if (rho < 8) {
     double r = 0.0;
     for (int d = 0; d < rho; ++d) r = __dadd_rn(r, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
@@ -161,6 +167,15 @@ __device__ __forceinline__ double d2_exact(const float* __restrict__ pts, long l
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
   for (; d < rho; ++d) res = __dadd_rn(res, sqdiff((double)__ldg(pts + d * ps + i), c[d]));
   return res;
+}
+
+static __device__ __noinline__ double d2_exact_pw(const float* __restrict__ pts, long long ps, long long i, int rho,
+                                           const double* __restrict__ c) {
+  int n2 = rho / 2;
+  n2 -= n2 % 8;
+  const double a = d2_exact(pts, ps, i, n2, c);
+  const double b = d2_exact(pts + (long long)n2 * ps, ps, i, rho - n2, c + n2);
+  return __dadd_rn(a, b);
 }
 
 // exact FP64 |x - c|^2 in numpy's pairwise order for a compile-time bound GR >= rho

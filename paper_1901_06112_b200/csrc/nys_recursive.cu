@@ -676,6 +676,7 @@ inline void rec_homogeneous(const RecCoeffs& c, int Lmax, std::vector<double>& H
 
 int rec_validate(const nys_filter_desc* d) {
   const int st = validate(d);
+  if (!st && (d->rho > NYS_MAX_RHO || d->n > NYS_MAX_CHANNELS)) return NYS_EUNSUPPORTED;  // register-resident R1
   if (st) return st;
   if (d->spatial_kind != NYS_SPATIAL_GAUSSIAN_RECURSIVE) return NYS_EINVAL;
   if (d->n + 1 > REC_COL_MAX_THREADS) return NYS_EUNSUPPORTED;

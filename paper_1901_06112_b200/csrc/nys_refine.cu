@@ -23,6 +23,7 @@
 namespace nys {
 
 constexpr int RF_THREADS = 256;
+constexpr int RF_QPT = 4;  // window sums per thread: 2 (n + 1) <= 1024
 
 struct RArgs {
   const float* f;
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
       s = warp_sum(s);
       if (tid == 0) s0x_sh = s;
     }
-    double acc = 0.0;  // thread q < NQ: quantity (c, kind) = (q % (n+1), q / (n+1))
+    // thread t owns the quantities q = t, t + 256, ... (c, kind) = (q % (n+1), q / (n+1)); NQ <= 1024
+    double acc[RF_QPT] = {0.0, 0.0, 0.0, 0.0};
     const int p_lo = (int)((long long)NP * k / nch), p_hi = (int)((long long)NP * (k + 1) / nch);
     for (int base = p_lo; base < p_hi; base += RF_THREADS) {
       const int p = base + tid;
@@ -151,18 +153,24 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
         pos[tid] = yy * a.W + xx;
       }
       __syncthreads();
-      if (tid < NQ) {
-        const int c = tid % (n + 1), kind = tid / (n + 1);
-        const double* t = kind ? tl : tw;
-        const int lim = min(RF_THREADS, p_hi - base);
-        for (int q = 0; q < lim; ++q) {
-          const double fv = c < n ? (double)__ldg(a.f + (long long)c * a.fps + pos[q]) : 1.0;
-          acc = fma(t[q], fv, acc);
+#pragma unroll
+      for (int u = 0; u < RF_QPT; ++u) {
+        const int qq = tid + u * RF_THREADS;
+        if (qq < NQ) {
+          const int c = qq % (n + 1), kind = qq / (n + 1);
+          const double* t = kind ? tl : tw;
+          const int lim = min(RF_THREADS, p_hi - base);
+          for (int q = 0; q < lim; ++q) {
+            const double fv = c < n ? (double)__ldg(a.f + (long long)c * a.fps + pos[q]) : 1.0;
+            acc[u] = fma(t[q], fv, acc[u]);
+          }
         }
       }
     }
     double* mine = a.part + ((size_t)e * nch + k) * NQ;
-    if (tid < NQ) mine[tid] = acc;
+#pragma unroll
+    for (int u = 0; u < RF_QPT; ++u)
+      if (tid + u * RF_THREADS < NQ) mine[tid + u * RF_THREADS] = acc[u];
     __threadfence();
     __syncthreads();
     if (tid == 0) last_chunk = atomicAdd(&a.chunk_cnt[e], 1u) == (unsigned)nch - 1;
@@ -170,17 +178,16 @@ __global__ void __launch_bounds__(RF_THREADS) k_finish(const RArgs a) {
     if (last_chunk) {
       __threadfence();
       const volatile double* pe = a.part + (size_t)e * nch * NQ;
-      if (tid < NQ) {
+      for (int qq = tid; qq < NQ; qq += RF_THREADS) {
         double s = 0.0;
-        for (int kk = 0; kk < nch; ++kk) s += pe[(size_t)kk * NQ + tid];  // chunk order: deterministic
-        res[tid] = s;
+        for (int kk = 0; kk < nch; ++kk) s += pe[(size_t)kk * NQ + qq];  // chunk order: deterministic
+        res[qq] = s;
       }
       __syncthreads();
       const double eta = res[n];
       const double s0x = s0x_sh;
       const double eta_l = s0x * res[2 * n + 1] * inv_a1;
-      if (tid < n) {  // the reference's guard (filters.py:241-257), in FP64
-        const int c = tid;
+      for (int c = tid; c < n; c += RF_THREADS) {  // the reference's guard (filters.py:241-257), in FP64
         double o;
         if (fabs(eta) >= eps) o = res[c] / eta;
         else if (fabs(eta_l) >= eps) o = (s0x * res[n + 1 + c] * inv_a1) / eta_l;

@@ -185,15 +185,16 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   float* dsh = bsh + (gmode == 1 ? 2 * K3_NPX : 0);            // npx: eta
   float* lsh = dsh + K3_NPX;                                   // npx: eta_lead
   float* ssh = lsh + K3_NPX;                                   // npx: scale of eta (-1: flagged)
-  float* Cs = ssh + K3_NPX;                                    // m0 x rhop
-  float* U0 = Cs + (size_t)m0 * rhop;                          // m0
+  float* Cs = ssh + K3_NPX;                                    // m0 x rhop (gmode 1 only)
+  float* U0 = Cs + (gmode == 1 ? (size_t)m0 * rhop : 0);       // m0
   float* gsh = U0 + ((m0 + 3) & ~3);                           // gmode 1: [rho][npx] guide tile
   __shared__ __align__(8) unsigned long long full[K3_NS];
   __shared__ float red_min[K3_THREADS / 32];
   __shared__ unsigned long long red_cnt[K3_THREADS / 32];
 
   const float inv_alpha0 = a.cst[a.sc_off], eps_den = a.cst[a.sc_off + 1];
-  for (int k = tid; k < m0 * rhop; k += K3_THREADS) Cs[k] = a.cst[k];
+  if (gmode == 1)  // the centroids only feed the features recomputed from a planar guide tile
+    for (int k = tid; k < m0 * rhop; k += K3_THREADS) Cs[k] = a.cst[k];
   for (int k = tid; k < m0; k += K3_THREADS) U0[k] = a.cst[a.u0_off + k];
   if (tid == 0) {
     for (int b = 0; b < K3_NS; ++b) mbar_init(&full[b], 1);
@@ -513,7 +514,8 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   const size_t plane_floats = (size_t)(K3_TH + 2 * R) * 32;
   const size_t stage_floats = 4 * plane_floats + (a.gcache == 3 ? K3_NPX : 0);
   const size_t smem = ((size_t)K3_NS * stage_floats + (a.gcache == 1 ? 2 * K3_NPX : 0) + 3 * K3_NPX +
-                       (size_t)d->m0 * L.rhop + ((d->m0 + 3) & ~3) + (a.gcache == 1 ? (size_t)d->rho * K3_NPX : 0)) *
+                       (a.gcache == 1 ? (size_t)d->m0 * L.rhop : 0) + ((d->m0 + 3) & ~3) +
+                       (a.gcache == 1 ? (size_t)d->rho * K3_NPX : 0)) *
                       sizeof(float);
   if (smem > 227 * 1024) return NYS_EUNSUPPORTED;
   const long long ntiles = (long long)a.tiles_x * a.tiles_y;

@@ -168,8 +168,8 @@ def kmeans_device(points: torch.Tensor, m0: int, seed: int = 0, max_iter: int = 
         raise ValueError(f"m0 must be in [1, {m}], got {m0}")
     if max_iter < 1:
         raise ValueError("max_iter must be >= 1")
-    if rho > _native.NYS_MAX_RHO or m0 > _native.NYS_MAX_M0:
-        raise NotImplementedError(f"rho <= {_native.NYS_MAX_RHO} and m0 <= {_native.NYS_MAX_M0} on the B200 path")
+    if rho > _native.NYS_MAX_RHO_WIDE or m0 > _native.NYS_MAX_M0:
+        raise NotImplementedError(f"rho <= {_native.NYS_MAX_RHO_WIDE} and m0 <= {_native.NYS_MAX_M0} on the B200 path")
     stamp("km checks")
     lib = _native.lib()
     dev = points.device

@@ -78,3 +78,38 @@ def test_full_size_cfg3_near_guard():
     err = np.abs(r1.output.data.double().cpu().numpy() - ref["output"])
     assert err.max() <= TOL, (err.max(), int((err > TOL).any(axis=0).sum()))
     assert r1.guarded_pixels == ref["guarded_pixels"]
+
+
+@pytest.mark.parametrize("case", ["hyper103", "nlm_r3_full"])
+def test_wide_guides(case):
+    """Guides wider than the register-resident kernels (rho > 64): the paper's 103-band
+    hyperspectral BLF and full-dimension PCA-NLM at r = 3 (147 dims,
+    filters.py:161-187) -- step-wise k-means with numpy's pairwise D^2 order, features
+    written as planes before K2, FP64 refinement over 147-dim windows."""
+    from paper_1901_06112_b200.synthetic import color_scene, spectral_scene
+
+    if case == "hyper103":
+        f32 = spectral_scene(72, 96, 103, 12, 0.03, seed=9)
+        p64 = f32.astype(np.float64)
+        sk, theta, m0, it = SpatialKernel.gaussian(2.0, 6), 0.9, 24, 8
+        mode = "bilateral"
+    else:
+        f32 = color_scene(56, 64, 6, 0.08, seed=10, lo=0.1, hi=0.9, shading=0.1)
+        p64 = O.patch_stack(f32.astype(np.float64), 3)
+        sk, theta, m0, it = SpatialKernel.box(5), 0.3 * np.sqrt(147.0) * 0.08, 16, 8
+        mode = "nlm"
+    f64 = f32.astype(np.float64)
+    assert p64.shape[0] > 64
+    C, _lab, qe, _ = O.kmeans(O.range_vectors(p64), m0, 0, it)
+    kind = "box" if sk.kind == "box" else "gaussian_fir"
+    ref = O.fast_filter_with_landmarks(f64, p64, C, theta, kind, sk.sigma, sk.radius)
+    params = FilterParams(spatial=sk, theta=float(theta), m0=m0, kmeans_max_iter=it, mode=mode, patch_radius=3,
+                          pca_dim=147)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    g = PatchGuide(f, 3) if mode == "nlm" else f
+    r1 = filter_with_landmarks(f, g, C, params)
+    assert np.abs(r1.output.data.double().cpu().numpy() - ref["output"]).max() <= TOL
+    assert r1.guarded_pixels == ref["guarded_pixels"]
+    r2 = fast_filter(f, g, params)
+    assert abs(r2.quant_error - qe) <= 1e-3 * qe
+    np.testing.assert_allclose(r2.centroids, C, rtol=0, atol=1e-5)

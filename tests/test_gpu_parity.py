@@ -521,6 +521,50 @@ def test_pipelined_calls_from_two_host_threads():
         assert torch.equal(out[k], ref[k])
 
 
+def test_pipelined_calls_from_two_host_threads_full_size():
+    # at full size the seeding / Lloyd launches are cooperative (a CTA on every SM)
+    # while another stream's device gate (k_inverse_cholesky) may be spinning on an SM for its
+    # plan; the plan worker must never block one job behind another, or the two streams wait on
+    # each other until the 60 s timeouts.  Two threads, own streams, 1080p cfg 2 calls.
+    import threading
+    import time
+
+    from bench import _params
+    from paper_1901_06112_b200.synthetic import CONFIGS
+
+    wl = CONFIGS[2]
+    params = _params(wl)
+    imgs = [wl.image(seed=s) for s in (0, 1)]
+    ref = []
+    for im in imgs:
+        f = Image(data=torch.from_numpy(im).cuda(), range_max=1.0)
+        ref.append(fast_filter(f, f, params).output.data.clone())
+    out = [None, None]
+    errs = []
+
+    def work(k):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                f = Image(data=torch.from_numpy(imgs[k]).cuda(), range_max=1.0)
+                for _ in range(6):
+                    r = fast_filter(f, f, params)
+                out[k] = r.output.data.clone()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    t0 = time.monotonic()
+    th = [threading.Thread(target=work, args=(k,)) for k in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    torch.cuda.synchronize()
+    assert time.monotonic() - t0 < 30, "the two streams waited on each other"
+    for k in (0, 1):
+        assert torch.equal(out[k], ref[k])
+
+
 def test_pipelined_call_after_an_interrupted_one():
     # a call that dies between the plan's fork and its final wait leaves its staging buffer
     # pending; the next call on the thread waits for that plan instead of failing

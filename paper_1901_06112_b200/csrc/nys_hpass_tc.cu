@@ -62,6 +62,34 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(K2T_GROUP) : "memory");
 }
 
+// shared-memory accesses by 32-bit shared address: the generic-pointer forms re-derived the
+// shared window base (S2UR SR_CgaCtaId, UMOV, ULEA) per landmark in the feature loop
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+// exp2 of a non-positive argument as one MUFU (exp2f adds a range fix-up for results below
+// 2^-126, which flush to zero here: features that small are zero to the filter)
+__device__ __forceinline__ float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 3xTF32 split of a finite value: hi = x rounded to TF32 (integer round-half-up on the 13
+// dropped bits; cvt.rna.tf32 expands to 4 instructions with its inf/nan path), lo = x - hi,
+// exact in FP32 -- the tensor core reads TF32 by truncation, so lo needs no rounding of its own
+// (its dropped bits are below 2^-22 |x|)
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  lo = x - hi;
+}
+
+// GR: guide dimensions held in registers per pixel, a multiple of 4 -- or 3 for rho == 3
+// exactly (colour guides: the padded fourth dimension costs a subtract and an FMA per landmark)
 template <int RT, int GR>
 __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a) {
   extern __shared__ __align__(128) float sm[];
@@ -76,16 +104,16 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
   const int nchunks = (NC + K2_CC - 1) / K2_CC;
   const int nfr = nchunks * K2_CC;  // f rows per buffer: f_c, 1 (y plane), 0 padding
 
-  float* Cs = sm;                                  // m0 x rhop (none when the features come from b planes)
-  float* Bh = Cs + (a.bfrom ? 0 : align32f(m0 * rhop));  // NU x KU, K-major core matrices
+  float* Cs = sm;                                  // KU x rhop, rows >= m0 zero (none when the features come from b planes)
+  float* Bh = Cs + (a.bfrom ? 0 : align32f(KU * rhop));  // NU x KU, K-major core matrices
   float* Bl = Bh + NU * KU;
   float* gbase = Bl + NU * KU;                     // per group, per buffer: Fs (nfr x pitch), Ys (m0q x pitch)
   const int buf_floats = align32f(nfr * pitch) + m0q * pitch;
   auto Fs_of = [&](int b) { return gbase + (size_t)(g * nbuf + b) * buf_floats; };
   auto Ys_of = [&](int b) { return Fs_of(b) + align32f(nfr * pitch); };
 
-  if (!a.bfrom)
-    for (int k = tid; k < m0 * rhop; k += K2T_THREADS) Cs[k] = a.cst[k];
+  if (!a.bfrom)  // landmarks padded to KU rows: the feature loop runs over all KU without a bound check
+    for (int k = tid; k < KU * rhop; k += K2T_THREADS) Cs[k] = k < m0 * rhop ? a.cst[k] : 0.f;
   {
     const float* MTg = a.cst + (size_t)m0 * rhop;  // MT[j][i] = M[i][j], MT[j][m0] = u0[j]
     for (int k = tid; k < NU * KU; k += K2T_THREADS) {
@@ -121,12 +149,13 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
   const int fir_items = L * nchunks * XG;
   const int ntiles = a.tiles_x * a.vrows;
   const int khalf = KU / 2;  // landmarks per feature thread (multiple of 4)
+  const uint32_t cs_half = umma::smem_addr(Cs) + (uint32_t)(hh * khalf * rhop) * 4u;  // this thread's first landmark
+  const uint32_t rhob = (uint32_t)rhop * 4u;
+  const float k2 = a.k2;
 
-  // 1. features of `tile`: pixel px evaluates b_j for its half of the landmarks
-  // and stores b_hi / b_lo into the A operand in TMEM (raw b planes for K3 too)
-  auto features = [&](int tile) {
-    const int vr = a.v0 + tile / a.tiles_x;
-    const int x0 = (tile % a.tiles_x) * TW;
+  // 1. features of the tile at virtual row vr, columns x0..: pixel px evaluates b_j for its
+  // half of the landmarks and stores b_hi / b_lo into the A operand in TMEM (raw b planes for K3 too)
+  auto features = [&](int vr, int x0) {
     const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
     const int xs = x0 - R + px;
     const int x = clampi(xs, 0, W - 1);
@@ -136,11 +165,7 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
       for (int j0 = hh * khalf; j0 < (hh + 1) * khalf; j0 += 4) {
         float hi[4], lo[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float v = j0 + e < m0 ? bsrc[(size_t)(j0 + e) * 32] : 0.f;
-          hi[e] = umma::to_tf32(v);
-          lo[e] = umma::to_tf32(v - hi[e]);
-        }
+        for (int e = 0; e < 4; ++e) split_tf32(j0 + e < m0 ? bsrc[(size_t)(j0 + e) * 32] : 0.f, hi[e], lo[e]);
         umma::st_32x32b_x4(a_hi + lane_base + (uint32_t)j0, hi[0], hi[1], hi[2], hi[3]);
         umma::st_32x32b_x4(a_lo + lane_base + (uint32_t)j0, lo[0], lo[1], lo[2], lo[3]);
       }
@@ -154,20 +179,50 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     float* bdst = nullptr;
     if (a.bplanes && !a.phi && px >= R && px < R + TW && xs < ((W + 31) & ~31))
       bdst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) + (long long)(L * NC) * 32 +
-             (xs & 31);
-    for (int j0 = hh * khalf; j0 < (hh + 1) * khalf; j0 += 4) {
-      float bv[4];
+             (xs & 31) + (long long)(hh * khalf) * 32;
+    const int jlim = m0 - hh * khalf;  // stores of raw b planes stop at landmark m0
+    uint32_t ca = cs_half;
+    const uint32_t t_hi = a_hi + lane_base + (uint32_t)(hh * khalf), t_lo = a_lo + lane_base + (uint32_t)(hh * khalf);
+    if constexpr (GR <= 4) {
+      // one LDS.128 per landmark; the next four landmarks' centroids are loaded before this
+      // four's arithmetic (the loads are ordered asm statements, so the prefetch is explicit; the
+      // last one reads past the landmarks into the B operand, still this CTA's shared memory)
+      float4 cn[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = j0 + e;
-        float v = 0.f;
-        if (j < m0) {
-          const float4* cj = reinterpret_cast<const float4*>(Cs + (size_t)j * rhop);
+      for (int e = 0; e < 4; ++e) cn[e] = lds128(ca + (uint32_t)e * rhob);
+      for (int jj = 0; jj < khalf; jj += 4) {
+        float4 cc[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cc[e] = cn[e];
+        ca += 4u * rhob;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cn[e] = lds128(ca + (uint32_t)e * rhob);
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float t0 = gv[0] - cc[e].x, t1 = gv[1] - cc[e].y, t2 = gv[2] - cc[e].z;
+          float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
+          if constexpr (GR == 4) {
+            const float t3 = gv[3] - cc[e].w;
+            d2 = fmaf(t3, t3, d2);
+          }
+          const float v = ex2_fast(d2 * k2);
+          if (bdst && jj + e < jlim) bdst[(size_t)(jj + e) * 32] = v;
+          split_tf32(v, hi[e], lo[e]);
+        }
+        umma::st_32x32b_x4(t_hi + (uint32_t)jj, hi[0], hi[1], hi[2], hi[3]);
+        umma::st_32x32b_x4(t_lo + (uint32_t)jj, lo[0], lo[1], lo[2], lo[3]);
+      }
+    } else {
+      for (int jj = 0; jj < khalf; jj += 4) {
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e, ca += rhob) {
           float d2 = 0.f;
 #pragma unroll
           for (int d4 = 0; d4 < GR / 4; ++d4) {
             if (4 * d4 < rho) {
-              const float4 c4 = cj[d4];
+              const float4 c4 = lds128(ca + 16u * d4);
               const float t0 = gv[4 * d4] - c4.x, t1 = gv[4 * d4 + 1] - c4.y;
               const float t2 = gv[4 * d4 + 2] - c4.z, t3 = gv[4 * d4 + 3] - c4.w;
               d2 = fmaf(t0, t0, d2);
@@ -176,19 +231,13 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
               d2 = fmaf(t3, t3, d2);
             }
           }
-          v = range_kernel(d2, a.k2);
-          if (bdst) bdst[(size_t)j * 32] = v;
+          const float v = ex2_fast(d2 * k2);
+          if (bdst && jj + e < jlim) bdst[(size_t)(jj + e) * 32] = v;
+          split_tf32(v, hi[e], lo[e]);
         }
-        bv[e] = v;
+        umma::st_32x32b_x4(t_hi + (uint32_t)jj, hi[0], hi[1], hi[2], hi[3]);
+        umma::st_32x32b_x4(t_lo + (uint32_t)jj, lo[0], lo[1], lo[2], lo[3]);
       }
-      float hi[4], lo[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        hi[e] = umma::to_tf32(bv[e]);
-        lo[e] = umma::to_tf32(bv[e] - hi[e]);
-      }
-      umma::st_32x32b_x4(a_hi + lane_base + (uint32_t)j0, hi[0], hi[1], hi[2], hi[3]);
-      umma::st_32x32b_x4(a_lo + lane_base + (uint32_t)j0, lo[0], lo[1], lo[2], lo[3]);
     }
     umma::st_wait();
   };
@@ -209,53 +258,58 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     umma::commit(bar);
   };
   // 3. accumulator -> y rows in SMEM (warps w, w+4 of the group drain half of
-  // the columns of TMEM lanes 32(w%4)..), and the tile's f rows
-  auto epilogue = [&](int tile, int b) {
-    float* Ys = Ys_of(b);
+  // the column chunks of TMEM lanes 32(w%4)..), and the tile's f rows
+  const int nch = (L + 7) / 8;                       // 8-column chunks holding y_0 .. y_m0 (the lead column last)
+  const int ch0 = hh ? (nch + 1) / 2 : 0, ch1 = hh ? nch : (nch + 1) / 2;
+  auto epilogue = [&](int vr, int x0, int b) {
+    const uint32_t ys = umma::smem_addr(Ys_of(b)) + (uint32_t)px * 4u;
+    const uint32_t pitchb = (uint32_t)pitch * 4u;
     float* Fs = Fs_of(b);
-    const int nch = NU / 8, c0 = hh * (nch / 2), c1 = c0 + nch / 2;
-    for (int c = c0; c < c1; ++c) {
+    const bool phi_out = a.phi && a.bplanes && px >= R && px < R + TW && (x0 - R + px) < ((W + 31) & ~31);
+    float* pdst = nullptr;
+    if (phi_out) {  // phi-form: phi_i = y_i is K3's contraction weight
+      const int xs = x0 - R + px;
+      pdst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) + (long long)(L * NC) * 32 +
+             (xs & 31);
+    }
+    for (int c = ch0; c < ch1; ++c) {
       float v[8];
       umma::ld_32x32b_x8(tmem + lane_base + (uint32_t)(8 * c), v);
       umma::ld_wait();
       if (px < ncols) {
+        const uint32_t yc = ys + (uint32_t)(8 * c) * pitchb;
+        if (8 * c + 8 <= L) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sts32(yc + (uint32_t)e * pitchb, v[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (8 * c + e < L) sts32(yc + (uint32_t)e * pitchb, v[e]);
+        }
+      }
+      if (pdst) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int i = 8 * c + e;
-          if (i < L) Ys[(size_t)i * pitch + px] = v[e];
-        }
-      }
-      if (a.phi && a.bplanes && px >= R && px < R + TW) {  // phi-form: phi_i = y_i is K3's contraction weight
-        const int vr = a.v0 + tile / a.tiles_x;
-        const int xs = (tile % a.tiles_x) * TW - R + px;
-        if (xs < ((W + 31) & ~31)) {
-          float* dst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) +
-                       (long long)(L * NC) * 32 + (xs & 31);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = 8 * c + e;
-            if (i < m0) dst[(size_t)i * 32] = v[e];
-          }
+          if (i < m0) pdst[(size_t)i * 32] = v[e];
         }
       }
     }
-    const int vr = a.v0 + tile / a.tiles_x;
-    const int x0 = (tile % a.tiles_x) * TW;
+    // f rows: thread (s, c0) stages column s of rows c0, c0 + 2, ... (ncol4 <= 128 = K2T_GROUP / 2)
     const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
-    for (int k = gtid; k < nfr * ncol4; k += K2T_GROUP) {
-      const int c = k / ncol4, s = k - c * ncol4;
+    const int s = gtid & (K2T_PX - 1);
+    if (s < ncol4) {
       const int x = clampi(x0 - R + s, 0, W - 1);
-      Fs[(size_t)c * pitch + s] =
-          c < n ? __ldg(a.f + (long long)c * a.fps + (long long)row * W + x) : (c == n ? 1.f : 0.f);
+      const float* fsrc = a.f + (long long)row * W + x;
+      for (int c = gtid / K2T_PX; c < nfr; c += K2T_GROUP / K2T_PX)
+        Fs[(size_t)c * pitch + s] = c < n ? __ldg(fsrc + (long long)c * a.fps) : (c == n ? 1.f : 0.f);
     }
   };
   // 4. horizontal FIR of the (m0+1)(n+1) planes, blocked-layout stores
   const int strideL = K2T_GROUP % L, strideR = K2T_GROUP / L;  // item stride in (i, rest) digits
-  auto fir = [&](int tile, int b) {
+  auto fir = [&](int vr, int x0, int b) {
     const float* Ys = Ys_of(b);
     const float* Fs = Fs_of(b);
-    const int vr = a.v0 + tile / a.tiles_x;
-    const int x0 = (tile % a.tiles_x) * TW;
     // (i, ch, xg) of item it = ((xg * nchunks + ch) * L + i), advanced incrementally by the
     // group stride (no divisions per item)
     int i = gtid % L, ch = (gtid / L) % nchunks, xg = (gtid / L) / nchunks;
@@ -315,10 +369,13 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
   // features(t+1) before MMA(t+1), and FIR(t-1) before epilogue(t+1).
   const int stride = 2 * gridDim.x;
   int tile = 2 * blockIdx.x + g;
+  // (virtual row, first column) of a tile, stepped by the grid stride without a division per tile
+  const int dvr = stride / a.tiles_x, dtx = stride - dvr * a.tiles_x;
+  int tr = tile / a.tiles_x, tx = tile - tr * a.tiles_x;
   uint32_t phase = 0;
   int b = 0;
   if (tile < ntiles) {
-    features(tile);
+    features(a.v0 + tr, tx * TW);
     umma::fence_before();
     group_sync(g);
     if (gtid == 0) {
@@ -328,25 +385,32 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     umma::mbar_wait(bar, phase);
     phase ^= 1u;
     umma::fence_after();
-    epilogue(tile, b);
+    epilogue(a.v0 + tr, tx * TW, b);
   }
   for (; tile < ntiles; tile += stride) {
     const int next = tile + stride;
     const bool more = next < ntiles;
-    if (more) features(next);
+    int nr = tr + dvr, nx = tx + dtx;
+    if (nx >= a.tiles_x) {
+      nx -= a.tiles_x;
+      ++nr;
+    }
+    if (more) features(a.v0 + nr, nx * TW);
     umma::fence_before();
     group_sync(g);
     umma::fence_after();
     if (more && gtid == 0) issue_mma();
-    fir(tile, b);
+    fir(a.v0 + tr, tx * TW, b);
     if (more) {
       umma::mbar_wait(bar, phase);
       phase ^= 1u;
       umma::fence_after();
       if (nbuf == 1) group_sync(g);  // single buffer: FIR(tile) must be done with Ys / Fs
-      b = (b + 1) % nbuf;
-      epilogue(next, b);
+      b = (b + 1 == nbuf) ? 0 : b + 1;
+      epilogue(a.v0 + nr, nx * TW, b);
     }
+    tr = nr;
+    tx = nx;
   }
   umma::fence_before();
   __syncthreads();
@@ -859,7 +923,7 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   int pitch = (int)ceil_div(TW + 2 * R + 4, 4) * 4;
   pitch += ((4 - pitch % 32) + 32) % 32;  // = 4 (mod 32): the FIR's LDS.128 across rows is conflict-free
   const int nfr = (int)ceil_div(d->n + 1, K2_CC) * K2_CC;
-  const size_t fixed = (a.bfrom ? 0 : (size_t)align32f(d->m0 * a.rhop)) + 2 * (size_t)NU * KU;
+  const size_t fixed = (a.bfrom ? 0 : (size_t)align32f(KU * a.rhop)) + 2 * (size_t)NU * KU;
   const size_t buf = (size_t)align32f(nfr * pitch) + (size_t)a.m0q * pitch;
   // two y/f buffers per group when they fit (one barrier per tile), else one
   int nbuf = 2;
@@ -875,7 +939,7 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   a.tcols = tcols;
   a.nbuf = nbuf;
   const long long ntiles = (long long)a.tiles_x * a.vrows;
-  const int GR = a.bfrom ? 4 : (d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64)));
+  const int GR = a.bfrom ? 4 : (d->rho == 3 && d->guide_kind == 0 ? 3 : (d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64))));
   auto go = [&](auto kern) -> int {
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -888,6 +952,7 @@ int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
   };
 #define NYS_HT_GR(RV)                                      \
   switch (GR) {                                            \
+    case 3: return go(k_feat_hpass_tc<RV, 3>);             \
     case 4: return go(k_feat_hpass_tc<RV, 4>);             \
     case 16: return go(k_feat_hpass_tc<RV, 16>);           \
     case 32: return go(k_feat_hpass_tc<RV, 32>);           \

@@ -28,14 +28,9 @@ namespace nys {
 // ---------------------------------------------------------------------------
 // K3: TMA-staged vertical pass + contraction with b_i(x) + guard + division
 // ---------------------------------------------------------------------------
-// Tile = 32 columns x K3_TH rows.  256 threads = 4 plane groups x 4 row runs x
-// 16 column pairs: thread (grp, run, cp) owns the 2 x K3_YR pixels at columns
-// 2*cp.., rows K3_YR*run.. and, in channel chunk k, channel c = 4k + grp.
-// A staged sample feeds K3_YR output rows, so the FIR reads (K3_YR + 2R) / (K3_YR T)
-// words of shared memory per FMA: with 4 rows per thread (and 4 columns) that was
-// 1.1 B/FMA, i.e. the 128 B/clk of shared memory exactly matched the FMA pipe and the two
-// limited each other (ncu: short_scoreboard 22 %, FMA pipe 65 %); 8 rows x 2 columns per
-// thread keeps the 16 pixels and the registers and needs 0.61 B/FMA.
+// Tile = 32 columns x K3_TH rows.  256 threads = 4 plane groups x 8 row runs x
+// 8 column quads: thread (grp, run, quad) owns the 4 x K3_YR pixels at columns
+// 4*quad.., rows K3_YR*run.. and, in channel chunk k, channel c = 4k + grp.
 // Stage order per tile: chunk kn (holding the denominator channel n) first,
 // then the others; within a chunk landmarks i = 0..m0-1 and the lead group.
 // Each stage is one TMA box of (up to) 4 planes x (TH + 2R) rows x 32 columns
@@ -44,10 +39,8 @@ namespace nys {
 // unrolled code is one vertical FIR (~0.5k instructions) and stays in the
 // instruction cache.
 constexpr int K3_THREADS = 256;
-constexpr int K3_YR = 8;             // rows per thread
-constexpr int K3_CW = 2;             // columns per thread
-constexpr int K3_RUNS = 4;           // row runs per tile
-constexpr int K3_TH = K3_RUNS * K3_YR;  // tile rows
+constexpr int K3_YR = 4;             // rows per thread
+constexpr int K3_TH = 8 * K3_YR;     // tile rows
 constexpr int K3_NPX = K3_TH * 32;   // tile pixels
 constexpr int K3_NS = 2;             // TMA pipeline depth
 
@@ -101,21 +94,21 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// vertical FIR of one staged plane: K3_CW columns x K3_YR rows per thread, row stride rs floats
+// vertical FIR of one staged plane: 4 columns x K3_YR rows per thread, row stride rs floats
 template <int RT>
-__device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ src, int rs, float (&G)[K3_YR][K3_CW]) {
+__device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ src, int rs, float (&G)[K3_YR][4]) {
 #pragma unroll
-  for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = 0.f;
+  for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = G[o][2] = G[o][3] = 0.f;
   if constexpr (RT > 0) {
     // packed FIR: rows (2p, 2p+1) of column e accumulate in one f32x2 register
     constexpr int T = 2 * RT + 1;
-    static_assert(K3_YR % 2 == 0 && K3_CW == 2, "row pairs, column pairs");
-    unsigned long long G2[K3_YR / 2][K3_CW];
+    static_assert(K3_YR % 2 == 0, "row pairs");
+    unsigned long long G2[K3_YR / 2][4];
 #pragma unroll
-    for (int p = 0; p < K3_YR / 2; ++p) G2[p][0] = G2[p][1] = 0ull;
+    for (int p = 0; p < K3_YR / 2; ++p) G2[p][0] = G2[p][1] = G2[p][2] = G2[p][3] = 0ull;
 #pragma unroll
     for (int s = 0; s < K3_YR + 2 * RT; ++s) {
-      const float2 v = *reinterpret_cast<const float2*>(src + s * rs);
+      const float4 v = *reinterpret_cast<const float4*>(src + s * rs);
 #pragma unroll
       for (int p = 0; p < K3_YR / 2; ++p) {
         const int k = s - 2 * p;
@@ -123,31 +116,39 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
           const float2 w = a.wpair[k];
           G2[p][0] = ffma2_bc(v.x, w, G2[p][0]);
           G2[p][1] = ffma2_bc(v.y, w, G2[p][1]);
+          G2[p][2] = ffma2_bc(v.z, w, G2[p][2]);
+          G2[p][3] = ffma2_bc(v.w, w, G2[p][3]);
         }
       }
     }
 #pragma unroll
     for (int p = 0; p < K3_YR / 2; ++p)
 #pragma unroll
-      for (int e = 0; e < K3_CW; ++e) unpack2(G2[p][e], G[2 * p][e], G[2 * p + 1][e]);
+      for (int e = 0; e < 4; ++e) unpack2(G2[p][e], G[2 * p][e], G[2 * p + 1][e]);
   } else if (a.box) {  // running (2R+1)-sum (spatial.py:91-99)
     const int R = a.R;
-    float2 sm2 = make_float2(0.f, 0.f);
+    float4 sm4 = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int t = 0; t <= 2 * R; ++t) {
-      const float2 v = *reinterpret_cast<const float2*>(src + t * rs);
-      sm2.x += v.x;
-      sm2.y += v.y;
+      const float4 v = *reinterpret_cast<const float4*>(src + t * rs);
+      sm4.x += v.x;
+      sm4.y += v.y;
+      sm4.z += v.z;
+      sm4.w += v.w;
     }
 #pragma unroll
     for (int o = 0; o < K3_YR; ++o) {
       if (o > 0) {
-        const float2 vi = *reinterpret_cast<const float2*>(src + (o + 2 * R) * rs);
-        const float2 vo = *reinterpret_cast<const float2*>(src + (o - 1) * rs);
-        sm2.x += vi.x - vo.x;
-        sm2.y += vi.y - vo.y;
+        const float4 vi = *reinterpret_cast<const float4*>(src + (o + 2 * R) * rs);
+        const float4 vo = *reinterpret_cast<const float4*>(src + (o - 1) * rs);
+        sm4.x += vi.x - vo.x;
+        sm4.y += vi.y - vo.y;
+        sm4.z += vi.z - vo.z;
+        sm4.w += vi.w - vo.w;
       }
-      G[o][0] = sm2.x;
-      G[o][1] = sm2.y;
+      G[o][0] = sm4.x;
+      G[o][1] = sm4.y;
+      G[o][2] = sm4.z;
+      G[o][3] = sm4.w;
     }
   } else {
     const int T = 2 * a.R + 1;
@@ -155,9 +156,11 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
       const float w = a.taps[t];
 #pragma unroll
       for (int o = 0; o < K3_YR; ++o) {
-        const float2 v = *reinterpret_cast<const float2*>(src + (o + t) * rs);
+        const float4 v = *reinterpret_cast<const float4*>(src + (o + t) * rs);
         G[o][0] = fmaf(w, v.x, G[o][0]);
         G[o][1] = fmaf(w, v.y, G[o][1]);
+        G[o][2] = fmaf(w, v.z, G[o][2]);
+        G[o][3] = fmaf(w, v.w, G[o][3]);
       }
     }
   }
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
                                                         const __grid_constant__ CUtensorMap tmapb, const VArgs a) {
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x;
-  const int grp = tid >> 6, run = (tid >> 4) & (K3_RUNS - 1), cp = tid & 15;
+  const int grp = tid >> 6, run = (tid >> 3) & 7, quad = tid & 7;
   const int m0 = a.m0, n = a.n, rho = a.rho, rhop = a.rhop, H = a.H, W = a.W, NC = n + 1;
   const int R = RT > 0 ? RT : a.R;
   const int SR = K3_TH + 2 * R;     // staged rows per plane
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
     }
   };
 
-  const int pxo = run * K3_YR * 32 + cp * K3_CW;  // this thread's first pixel (row-major, 32 wide)
+  const int pxo = run * K3_YR * 32 + quad * 4;  // this thread's first pixel (row-major, 32 wide)
   unsigned long long gs = 0;                    // global stage counter (mbarrier phases)
   if (tid == 0 && blockIdx.x < ntiles)
     for (int s = 0; s < K3_NS && s < nstages; ++s) issue(blockIdx.x, s, s);
@@ -257,11 +260,11 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       compute_b(0, bsh);
       __syncthreads();
     }
-    float s0[K3_YR][K3_CW], acc[K3_YR][K3_CW], sab[K3_YR][K3_CW];  // sab: sum_i b_i |conv(y_i)| (denominator chunk)
+    float s0[K3_YR][4], acc[K3_YR][4], sab[K3_YR][4];  // sab: sum_i b_i |conv(y_i)| (denominator chunk)
 #pragma unroll
     for (int o = 0; o < K3_YR; ++o)
 #pragma unroll
-      for (int e = 0; e < K3_CW; ++e) s0[o][e] = acc[o][e] = sab[o][e] = 0.f;
+      for (int e = 0; e < 4; ++e) s0[o][e] = acc[o][e] = sab[o][e] = 0.f;
 
 #pragma unroll 1
     // (co, i) = (s / L, s % L) kept incrementally: a runtime division per stage was 5 % of
@@ -274,23 +277,23 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       const int buf = (int)(gs % K3_NS);
       const float* sb = stage + (size_t)buf * stage_floats;
       mbar_wait(&full[buf], (unsigned)((gs / K3_NS) & 1));
-      float G[K3_YR][K3_CW];
+      float G[K3_YR][4];
       if (c < NC) {
         const int rs = tail ? ntail * 32 : 128;  // staged row: [4 or ntail planes][32 columns]
-        vfir<RT>(a, sb + grp * 32 + run * K3_YR * rs + cp * K3_CW, rs, G);
+        vfir<RT>(a, sb + grp * 32 + run * K3_YR * rs + quad * 4, rs, G);
       } else {
 #pragma unroll
-        for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = 0.f;
+        for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = G[o][2] = G[o][3] = 0.f;
       }
       if (i < m0) {
         const float* bb = (gmode == 3 ? sb + 4 * plane_floats : bsh + (i & 1) * K3_NPX) + pxo;
         const float u0i = U0[i];
 #pragma unroll
         for (int o = 0; o < K3_YR; ++o) {
-          const float2 b2 = *reinterpret_cast<const float2*>(bb + o * 32);
-          const float bv[K3_CW] = {b2.x, b2.y};
+          const float4 b4 = *reinterpret_cast<const float4*>(bb + o * 32);
+          const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-          for (int e = 0; e < K3_CW; ++e) {
+          for (int e = 0; e < 4; ++e) {
             acc[o][e] = fmaf(bv[e], G[o][e], acc[o][e]);
             if (co == 0) {
               s0[o][e] = fmaf(u0i, bv[e], s0[o][e]);
@@ -304,24 +307,24 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
         }
       } else {
         // lead group: zeta_lead = s0 (ω*(s0 f_c)) / α0 ; chunk kn first publishes eta and eta_lead
-        float lg[K3_YR][K3_CW];
+        float lg[K3_YR][4];
 #pragma unroll
         for (int o = 0; o < K3_YR; ++o)
 #pragma unroll
-          for (int e = 0; e < K3_CW; ++e) lg[o][e] = s0[o][e] * G[o][e] * inv_alpha0;
+          for (int e = 0; e < 4; ++e) lg[o][e] = s0[o][e] * G[o][e] * inv_alpha0;
         if (co == 0) {
           if (c == n) {
 #pragma unroll
             for (int o = 0; o < K3_YR; ++o) {
-              *reinterpret_cast<float2*>(dsh + pxo + o * 32) = make_float2(acc[o][0], acc[o][1]);
-              *reinterpret_cast<float2*>(lsh + pxo + o * 32) = make_float2(lg[o][0], lg[o][1]);
+              *reinterpret_cast<float4*>(dsh + pxo + o * 32) = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
+              *reinterpret_cast<float4*>(lsh + pxo + o * 32) = make_float4(lg[o][0], lg[o][1], lg[o][2], lg[o][3]);
               // near-guard pixels: queued for the FP64 re-evaluation (nys_filter_finish), marked
               // -1 so the tile statistics leave them to it
               const int row = t0 + run * K3_YR + o;
-              float sv[K3_CW];
+              float sv[4];
 #pragma unroll
-              for (int e = 0; e < K3_CW; ++e) {
-                const int x = x0 + cp * K3_CW + e;
+              for (int e = 0; e < 4; ++e) {
+                const int x = x0 + quad * 4 + e;
                 sv[e] = sab[o][e];
                 if (row < a.out0 + a.out_rows && row < H && x < W &&
                     near_guard(acc[o][e], sab[o][e], lg[o][e], eps_den, a.tau, a.cerr)) {
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
                   }
                 }
               }
-              *reinterpret_cast<float2*>(ssh + pxo + o * 32) = make_float2(sv[0], sv[1]);
+              *reinterpret_cast<float4*>(ssh + pxo + o * 32) = make_float4(sv[0], sv[1], sv[2], sv[3]);
             }
           }
           __syncthreads();
@@ -344,13 +347,13 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
           for (int o = 0; o < K3_YR; ++o) {
             const int row = t0 + run * K3_YR + o;
             if (row >= a.out0 + a.out_rows || row >= H) continue;
-            const float2 d2 = *reinterpret_cast<const float2*>(dsh + pxo + o * 32);
-            const float2 l2 = *reinterpret_cast<const float2*>(lsh + pxo + o * 32);
-            const float dv[K3_CW] = {d2.x, d2.y}, lv[K3_CW] = {l2.x, l2.y};
-            float res[K3_CW];
+            const float4 d4 = *reinterpret_cast<const float4*>(dsh + pxo + o * 32);
+            const float4 l4 = *reinterpret_cast<const float4*>(lsh + pxo + o * 32);
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            float res[4];
 #pragma unroll
-            for (int e = 0; e < K3_CW; ++e) {
-              const int x = x0 + cp * K3_CW + e;
+            for (int e = 0; e < 4; ++e) {
+              const int x = x0 + quad * 4 + e;
               if (fabsf(dv[e]) >= eps) {
                 res[e] = acc[o][e] / dv[e];
               } else if (fabsf(lv[e]) >= eps) {
@@ -360,24 +363,24 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
               }
             }
             if (a.out64) {  // FP64 planes (the reference's Image dtype), e.g. page-locked host memory
-              double* d64 = reinterpret_cast<double*>(a.out) + (long long)c * a.ops + (long long)row * W + x0 + cp * K3_CW;
+              double* d64 = reinterpret_cast<double*>(a.out) + (long long)c * a.ops + (long long)row * W + x0 + quad * 4;
 #pragma unroll
-              for (int e = 0; e < K3_CW; ++e)
-                if (x0 + cp * K3_CW + e < W) d64[e] = (double)res[e];
+              for (int e = 0; e < 4; ++e)
+                if (x0 + quad * 4 + e < W) d64[e] = (double)res[e];
               continue;
             }
-            float* dst = a.out + (long long)c * a.ops + (long long)row * W + x0 + cp * K3_CW;
-            if (a.vec_out && x0 + cp * K3_CW + 1 < W) {
-              *reinterpret_cast<float2*>(dst) = make_float2(res[0], res[1]);
+            float* dst = a.out + (long long)c * a.ops + (long long)row * W + x0 + quad * 4;
+            if (a.vec_out && x0 + quad * 4 + 3 < W) {
+              *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
             } else {
 #pragma unroll
-              for (int e = 0; e < K3_CW; ++e)
-                if (x0 + cp * K3_CW + e < W) dst[e] = res[e];
+              for (int e = 0; e < 4; ++e)
+                if (x0 + quad * 4 + e < W) dst[e] = res[e];
             }
           }
         }
 #pragma unroll
-        for (int o = 0; o < K3_YR; ++o) acc[o][0] = acc[o][1] = 0.f;
+        for (int o = 0; o < K3_YR; ++o) acc[o][0] = acc[o][1] = acc[o][2] = acc[o][3] = 0.f;
         // first landmark of the next chunk (gmode 1)
         if (gmode == 1 && co + 1 < nchunks) compute_b(0, bsh);
       }

@@ -32,6 +32,13 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { ret
 // exp(-d2/(2 theta^2)) evaluated as exp2(d2 * k2) with k2 = -log2(e)/(2 theta^2):
 // one FMUL + MUFU.EX2 (ex2.approx.ftz has ~2 ulp error, well inside the 1e-4 budget)
 __device__ __forceinline__ float range_kernel(float d2, float k2) { return exp2f(d2 * k2); }
+// one MUFU.EX2: exp2f adds a range fix-up (FSETP + two predicated FMULs) for results below
+// 2^-126, which flush to zero here -- features that small are zero to the filter
+__device__ __forceinline__ float range_kernel_fast(float d2, float k2) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d2 * k2));
+  return y;
+}
 
 // deterministic warp sums
 __device__ __forceinline__ double warp_sum(double v) {

@@ -642,7 +642,7 @@ __global__ void k_seed_prologue(const SeedPrologue p) {
   for (int d = t; d < p.rho; d += blockDim.x) p.C[d] = (double)p.pts[d * p.ps + p.first];
   for (int k = t; k < p.m0 - 1; k += blockDim.x) p.unif_dst[k] = p.unif[k];
   for (int k = t; k < p.gstride; k += blockDim.x) p.lloyd_gacc[k] = 0ull;  // the seeding never touches these
-  if (t == 0) *p.lloyd_maxabs = 0u;
+  if (t < 7) p.lloyd_maxabs[t] = 0u;  // max|x| and the bounding box words of the cell-pruned search
 }
 
 __global__ void k_c_to_f(const double* __restrict__ C, float* __restrict__ Cf, int n) {

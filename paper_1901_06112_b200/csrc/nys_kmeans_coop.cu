@@ -370,7 +370,29 @@ struct LloydArgs {
   int* list;                 // m: per-warp lists of points that need the full search
   int nw;                    // warps per block
   int bounds;                // 0: full search every iteration (debug / A-B check)
+  // (the cell-pruned kernel keeps its KM_NG^rho candidate masks where the bounds would be, at
+  // `lb`; the struct's size is left alone: two more members changed the register allocation of
+  // the wide-guide instantiations from 255 to 167-207 and cost cfg 4 1.5 ms)
 };
+
+// Cell-pruned exact assignment for guides of up to three dimensions (colour images).
+// The bounding box of the points is cut into KM_NG^rho cells.  After every centroid update
+// the blocks rebuild, one warp per cell, the set of centroids that can be nearest to *some*
+// point of the cell: with U = min_c maxdist^2(c, cell), centroid c is a candidate iff
+// mindist^2(c, cell) <= U (1 + 1e-4).  A non-candidate is farther from every point of the
+// cell than the best candidate by a relative 1e-4, far above the 3e-7 rounding of the FP32
+// differenced distance, so searching only the candidates (ascending index, strict <) returns
+// the label, distance and tie-break of the full m0-way search; cells are grown by 1e-3 of
+// their width against the rounding of the point-to-cell map.  A point then evaluates a
+// handful of centroids instead of m0, every iteration, with no per-point bound state.
+constexpr int KM_NG = 16;
+__device__ __forceinline__ unsigned f32_ordered(float v) {  // order-preserving, > 0 for finite v
+  const unsigned u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float f32_unordered(unsigned e) {
+  return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
+}
 
 // squared FP32 distance, difference form, dimensions in ascending order -- the
 // one formula every assignment uses, so a bound-skipped point gets the same
@@ -405,7 +427,8 @@ __device__ __forceinline__ float d2_f32(const float (&x)[GR], int rho, const flo
 // are exact fixed-point deltas of the points whose label changed.
 constexpr double LB_EPS = 1.0 / 32768.0;
 
-template <int GR, int RX>
+// GRID: the cell-pruned search (a separate instantiation, so the bounds kernels compile as before)
+template <int GR, int RX, bool GRID = false>
 __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double dsm[];
@@ -421,6 +444,15 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   const int rhop = (rho + 3) & ~3;                                             // Cf rows: 16-byte aligned
   const int m0p = (m0 + 3) & ~3;                                               // Cf rows padded to 4
   float* Cfo = Cf + (size_t)m0p * rhop;                                        // previous iteration's Cf
+  constexpr bool GRIDOK = GRID;
+  constexpr bool gridmode = GRID;
+  static_assert(!GRID || (RX >= 1 && RX <= 3), "cell-pruned search: rho <= 3");
+  constexpr int NCELL_ALL = RX == 1 ? KM_NG : (RX == 2 ? KM_NG * KM_NG : KM_NG * KM_NG * KM_NG);
+  unsigned long long* gts = reinterpret_cast<unsigned long long*>(                // candidate masks (grid mode)
+      (reinterpret_cast<uintptr_t>(Cfo + (size_t)m0p * rhop) + 15) & ~uintptr_t(15));
+  double* gh = reinterpret_cast<double*>(gts + (GRID ? NCELL_ALL : 0));            // 3 cell widths
+  float* glo = reinterpret_cast<float*>(gh + 3);                                   // 3 box origins
+  float* ginv = glo + 3;                                                           // 3 inverse cell widths
   __shared__ double sh[64];
   __shared__ double extra[2][32];
   __shared__ double misc[2];
@@ -449,6 +481,22 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     }
     mx = warp_max(mx);
     if (lane == 0 && mx > 0.f) atomicMax(a.maxabs_bits, __float_as_uint(mx));
+    if constexpr (gridmode) {  // per-dimension bounding box: words 1..3 max, 4..6 -min (order-preserving, zero = identity)
+      for (int d = 0; d < rho; ++d) {
+        float hi_v = -INFINITY, lo_v = INFINITY;
+        for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+          const float v = __ldg(a.pts + d * a.ps + i);
+          hi_v = fmaxf(hi_v, v);
+          lo_v = fminf(lo_v, v);
+        }
+        hi_v = warp_max(hi_v);
+        lo_v = -warp_max(-lo_v);
+        if (lane == 0 && hi_v >= lo_v) {
+          atomicMax(a.maxabs_bits + 1 + d, f32_ordered(hi_v));
+          atomicMax(a.maxabs_bits + 4 + d, f32_ordered(-lo_v));
+        }
+      }
+    }
   }
   for (int k = threadIdx.x; k < msl; k += blockDim.x) Cd[k] = __ldcg(a.C + k);
   for (int k = threadIdx.x; k < gstride; k += blockDim.x) T[k] = 0;
@@ -463,8 +511,63 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   int sexp = 0;
   if (maxabs > 0.f) sexp = 61 - ilogb((double)maxabs * (double)a.m) - 1;
   const double scale = ldexp(1.0, sexp), inv_scale = ldexp(1.0, -sexp);
+  const float scalef = (float)scale;  // a power of two: x * scalef is exact (|x| 2^s < 2^61)
   constexpr int HH = GR <= 4 ? 3 : 1;  // points per lane in the full search: every centroid LDS serves HH
   constexpr int JJ = GR >= 16 ? 4 : 1; // centroids per step: independent FMA chains for long guides
+  // candidate masks of every cell from the current FP32 centroids (one warp per cell, lanes over centroids)
+  auto build_grid = [&]() {
+    int ncell = 1;
+    for (int d = 0; d < rho; ++d) ncell *= KM_NG;
+    for (int cell = b * nw + w; cell < ncell; cell += nb * nw) {
+      int kk[3] = {cell % KM_NG, (cell / KM_NG) % KM_NG, cell / (KM_NG * KM_NG)};
+      double mind[2] = {INFINITY, INFINITY}, maxd = INFINITY;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = lane + 32 * u;
+        if (j < m0) {
+          double mn = 0.0, mx = 0.0;
+          for (int d = 0; d < rho; ++d) {
+            const double blo = (double)glo[d] + ((double)kk[d] - 1e-3) * gh[d];
+            const double bhi = (double)glo[d] + ((double)kk[d] + 1.0 + 1e-3) * gh[d];
+            const double c = (double)Cf[j * rhop + d];
+            const double below = blo - c, above = c - bhi;
+            const double t = fmax(fmax(below, above), 0.0);
+            mn += t * t;
+            const double f = fmax(c - blo, bhi - c);
+            mx += f * f;
+          }
+          mind[u] = mn;
+          maxd = fmin(maxd, mx);
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) maxd = fmin(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+      const double thr = maxd * (1.0 + 1e-4) + 1e-300;
+      const unsigned m_lo = __ballot_sync(0xffffffffu, mind[0] <= thr);
+      const unsigned m_hi = __ballot_sync(0xffffffffu, mind[1] <= thr);
+      if (lane == 0) reinterpret_cast<unsigned long long*>(a.lb)[cell] = ((unsigned long long)m_hi << 32) | m_lo;
+    }
+  };
+  if constexpr (gridmode) {
+    if (threadIdx.x < 3) {
+      const int d = threadIdx.x;
+      float lo_v = 0.f, hi_v = 0.f;
+      if (d < rho) {
+        const unsigned eh = __ldcg(a.maxabs_bits + 1 + d), el = __ldcg(a.maxabs_bits + 4 + d);
+        if (eh && el) {
+          hi_v = f32_unordered(eh);
+          lo_v = -f32_unordered(el);
+        }
+      }
+      const float range = hi_v - lo_v;
+      const bool ok = range > 1e-30f && range < 3.0e38f;
+      glo[d] = lo_v;
+      ginv[d] = ok ? (float)KM_NG / range : 0.f;
+      gh[d] = ok ? ((double)hi_v - (double)lo_v) / (double)KM_NG : 0.0;
+    }
+    __syncthreads();
+    build_grid();
+    grid.sync();
+  }
 
   for (int it = 0; it < a.max_iter; ++it) {
     const int par = it & 1;
@@ -481,7 +584,112 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     double near_sum = 0.0, changed = 0.0;
     const bool full_pass = it == 0 || !a.bounds;
     long long nlist = hi - lo;
-    if (!full_pass) {
+    if constexpr (gridmode) {
+      if constexpr (GRIDOK) {
+        constexpr int NCELL = RX == 1 ? KM_NG : (RX == 2 ? KM_NG * KM_NG : KM_NG * KM_NG * KM_NG);
+        for (int k0 = threadIdx.x; k0 < NCELL; k0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+          unsigned long long tmp[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) tmp[u] = k0 + u * blockDim.x < NCELL ? __ldcg(reinterpret_cast<unsigned long long*>(a.lb) + k0 + u * blockDim.x) : 0ull;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (k0 + u * blockDim.x < NCELL) gts[k0 + u * blockDim.x] = tmp[u];
+        }
+        __syncthreads();
+        // A warp takes HG x 32 consecutive points per trip and searches the *union* of their
+        // cells' candidate sets, in ascending index, for all of them: a superset search returns
+        // the same label and distance, the loop and the centroid loads are warp-uniform
+        // (broadcast LDS, no per-lane mask arithmetic or divergence), and consecutive pixels
+        // share most of their candidates.
+        constexpr int HG = 2;
+        const float4* Cf4 = reinterpret_cast<const float4*>(Cf);  // rhop == 4
+        // trips are dealt round-robin over every warp of the grid (not a contiguous chunk per
+        // block): busy image regions, whose pixels touch more cells, spread over all blocks
+        const long long gw = (long long)b * nw + w, gnw = (long long)nb * nw;
+        for (long long q0 = gw * 32 * HG; q0 < a.m; q0 += gnw * 32 * HG) {
+          float x[HG][GR], best[HG];
+          int arg[HG], oldl[HG];
+          bool valid[HG];
+#pragma unroll
+          for (int h = 0; h < HG; ++h) {
+            const long long q = q0 + 32 * h + lane;
+            valid[h] = q < a.m;
+            const long long i = valid[h] ? q : 0;
+#pragma unroll
+            for (int d = 0; d < GR; ++d) x[h][d] = (valid[h] && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
+            oldl[h] = (valid[h] && it > 0) ? a.labels[i] : -1;
+          }
+          unsigned ulo = 0u, uhi = 0u;
+#pragma unroll
+          for (int h = 0; h < HG; ++h) {
+            int cell = 0, mul = 1;
+#pragma unroll
+            for (int d = 0; d < RX; ++d) {
+              const int kd = min(KM_NG - 1, max(0, (int)((x[h][d] - glo[d]) * ginv[d])));
+              cell += kd * mul;
+              mul *= KM_NG;
+            }
+            const unsigned long long mk = valid[h] ? gts[cell] : 0ull;
+            ulo |= (unsigned)mk;
+            uhi |= (unsigned)(mk >> 32);
+            best[h] = INFINITY;
+            arg[h] = 0;
+          }
+          ulo = __reduce_or_sync(0xffffffffu, ulo);
+          uhi = __reduce_or_sync(0xffffffffu, uhi);
+          auto eval = [&](int j) {
+            const float4 c4 = Cf4[j];
+            const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int h = 0; h < HG; ++h) {
+              float d2 = 0.f;
+#pragma unroll
+              for (int d = 0; d < RX; ++d) {
+                const float t = x[h][d] - cc[d];
+                d2 = fmaf(t, t, d2);
+              }
+              if (d2 < best[h]) {  // ascending j, strict: first index wins ties
+                best[h] = d2;
+                arg[h] = j;
+              }
+            }
+          };
+          for (unsigned u = ulo; u; u &= u - 1u) eval(__ffs(u) - 1);
+          for (unsigned u = uhi; u; u &= u - 1u) eval(31 + __ffs(u));
+#pragma unroll
+          for (int h = 0; h < HG; ++h) {
+            const long long i = q0 + 32 * h + lane;
+            int old = -1;
+            bool chg = false;
+            if (valid[h]) {
+              near_sum += (double)best[h];
+              old = oldl[h];
+              chg = old != arg[h];
+              if (chg) {
+                changed += 1.0;
+                a.labels[i] = arg[h];
+              }
+            }
+            if (it == 0) {  // every point enters its cluster: label groups reduced with REDUX
+              warp_accumulate_fx<GR>(x[h], rho, arg[h], valid[h] && chg, scale, 1, myacc, mycnt);
+            } else if (chg) {
+              // few lanes change label after the first iteration: they add their fixed-point
+              // coordinates to this warp's table with shared-memory atomics (integer adds commute,
+              // so the sums stay exact and order-independent); x * 2^s is exact in FP32
+#pragma unroll
+              for (int d = 0; d < RX; ++d) {
+                const unsigned long long v = (unsigned long long)__float2ll_rn(x[h][d] * scalef);
+                atomicAdd(myacc + arg[h] * rho + d, v);
+                atomicAdd(myacc + old * rho + d, 0ull - v);
+              }
+              atomicAdd(mycnt + arg[h], 1);
+              atomicSub(mycnt + old, 1);
+            }
+          }
+        }
+        nlist = 0;  // phase B has nothing left
+      }
+    } else if (!full_pass) {
       // phase A: warp w tests its contiguous sub-range; failures go to its list segment in point order
       // PA chunks of 32 points in flight per warp: their point, label and bound
       // loads are issued together (the per-chunk loads are otherwise two
@@ -750,6 +958,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     }
     __syncthreads();
     double mv = 0.0;
+    if constexpr (!gridmode)  // (the cell-pruned search keeps no drift-adjusted bounds)
     for (int j = threadIdx.x; j < m0; j += blockDim.x) {
       double s2 = 0.0;
       for (int d = 0; d < rho; ++d) {
@@ -758,15 +967,21 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       }
       mv = fmax(mv, sqrt(s2));
     }
-    for (int o = 16; o > 0; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
-    if (lane == 0) sh[w] = mv;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double mx = 0.0;
-      for (int q = 0; q < nw; ++q) mx = fmax(mx, sh[q]);
-      dcum_sh = dcum + mx * (1.0 + 1e-9) + 1e-30;  // monotone, never understated
+    if constexpr (!gridmode) {
+      for (int o = 16; o > 0; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+      if (lane == 0) sh[w] = mv;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int q = 0; q < nw; ++q) mx = fmax(mx, sh[q]);
+        dcum_sh = dcum + mx * (1.0 + 1e-9) + 1e-30;  // monotone, never understated
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (gridmode && it + 1 < a.max_iter) {
+      if constexpr (GRID) build_grid();
+      grid.sync();
+    }
   }
   if (b == 0)
     for (int k = threadIdx.x; k < msl; k += blockDim.x) a.C[k] = Cd[k];
@@ -850,7 +1065,12 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   const int msl = m0 * rho;
   const size_t fixed = (size_t)msl * 8 * 2 + (size_t)(msl + m0) * 8 + (size_t)m0 * 8 +
                        2 * (size_t)((m0 + 3) & ~3) * ((rho + 3) & ~3) * 4 + 96;
-  auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed; };
+  const char* eg = getenv("NYS_KM_NOGRID");
+  const bool gridmode = rho <= 3 && m0 <= 64 && !(eg && atoi(eg));
+  size_t gcells = 1;
+  for (int d = 0; d < rho; ++d) gcells *= KM_NG;
+  const size_t gsm = gridmode ? gcells * 8 + 16 + 64 : 0;
+  auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed + gsm; };
   int nw = 8;
   while (nw > 1 && need(nw) > 200 * 1024) --nw;
   const size_t smem = need(nw);
@@ -879,10 +1099,11 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     const char* e = getenv("NYS_KM_NOBOUNDS");
     a.bounds = (e && atoi(e)) ? 0 : 1;
   }
+  const bool use_grid = gridmode && a.bounds;  // candidate masks in place of the bound / list arrays
   // the first delta buffer starts at zero (the kernel zeroes each next one) and max|x| at +0
   if (!prezeroed) {  // else k_seed_prologue zeroed both
     NYS_CUDA_TRY(cudaMemsetAsync(a.gacc, 0, (size_t)(msl + m0) * 8, s));
-    NYS_CUDA_TRY(cudaMemsetAsync(a.maxabs_bits, 0, sizeof(unsigned), s));
+    NYS_CUDA_TRY(cudaMemsetAsync(a.maxabs_bits, 0, 7 * sizeof(unsigned), s));  // max|x| and the bounding box words
   }
   void* args[] = {&a};
   auto go = [&](auto kern) -> int {
@@ -895,6 +1116,13 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(nw * 32), args, smem, s));
     return NYS_OK;
   };
+  if (use_grid) {
+    switch (rho) {
+      case 1: return go(k_lloyd_coop<4, 1, true>);
+      case 2: return go(k_lloyd_coop<4, 2, true>);
+      default: return go(k_lloyd_coop<4, 3, true>);
+    }
+  }
   switch (rho) {
     case 1: return go(k_lloyd_coop<4, 1>);
     case 2: return go(k_lloyd_coop<4, 2>);

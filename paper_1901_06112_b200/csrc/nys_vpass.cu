@@ -95,8 +95,10 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 }
 
 // vertical FIR of one staged plane: 4 columns x K3_YR rows per thread, row stride rs floats
-template <int RT>
-__device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ src, int rs, float (&G)[K3_YR][4]) {
+// RS: staged row stride in floats when known at compile time (full chunks: 4 planes x 32), else 0
+template <int RT, int RS = 0>
+__device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ src, int rs_rt, float (&G)[K3_YR][4]) {
+  const int rs = RS > 0 ? RS : rs_rt;
 #pragma unroll
   for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = G[o][2] = G[o][3] = 0.f;
   if constexpr (RT > 0) {
@@ -223,8 +225,39 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   auto issue = [&](int t, int s, unsigned long long gs) {  // prologue only: divisions once
     issue_at(t % a.tiles_x, t / a.tiles_x, s % L, chunk_of(s / L), gs);
   };
-  // b_i on every tile pixel from the cached guide tile (gmode 1)
+  // b_i on every tile pixel from the cached guide tile (gmode 1).  K3_NPX / 4 == K3_THREADS: a
+  // thread always evaluates the same four pixels, so for rho <= 3 their guide values stay in
+  // registers for the whole tile (gq, loaded by load_gq) and a landmark costs one LDS.128.
+  static_assert(K3_NPX / 4 == K3_THREADS, "one pixel quad per thread");
+  float gq[3][4];
+  auto load_gq = [&]() {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float4 g4 = d < rho ? *reinterpret_cast<const float4*>(gsh + d * K3_NPX + 4 * tid) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gq[d][0] = g4.x;
+      gq[d][1] = g4.y;
+      gq[d][2] = g4.z;
+      gq[d][3] = g4.w;
+    }
+  };
   auto compute_b = [&](int i, float* bb) {
+    if (rho <= 3) {
+      const float4 c4 = *reinterpret_cast<const float4*>(Cs + i * rhop);  // rhop == 4, padded with zeros
+      const float cc[3] = {c4.x, c4.y, c4.z};
+      float d2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (d < rho) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float t = gq[d][e] - cc[d];
+            d2[e] = fmaf(t, t, d2[e]);
+          }
+        }
+      *reinterpret_cast<float4*>(bb + 4 * tid) = make_float4(range_kernel_fast(d2[0], a.k2), range_kernel_fast(d2[1], a.k2),
+                                                             range_kernel_fast(d2[2], a.k2), range_kernel_fast(d2[3], a.k2));
+      return;
+    }
     for (int k4 = tid; k4 < K3_NPX / 4; k4 += K3_THREADS) {
       float4 d2 = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int d = 0; d < rho; ++d) {
@@ -236,8 +269,8 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
         d2.z = fmaf(tz, tz, d2.z);
         d2.w = fmaf(tw, tw, d2.w);
       }
-      *reinterpret_cast<float4*>(bb + 4 * k4) = make_float4(range_kernel(d2.x, a.k2), range_kernel(d2.y, a.k2),
-                                                            range_kernel(d2.z, a.k2), range_kernel(d2.w, a.k2));
+      *reinterpret_cast<float4*>(bb + 4 * k4) = make_float4(range_kernel_fast(d2.x, a.k2), range_kernel_fast(d2.y, a.k2),
+                                                            range_kernel_fast(d2.z, a.k2), range_kernel_fast(d2.w, a.k2));
     }
   };
 
@@ -257,6 +290,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
         gsh[k] = __ldg(a.g + (long long)d * a.gps + (long long)rr * W + cx);
       }
       __syncthreads();
+      if (rho <= 3) load_gq();
       compute_b(0, bsh);
       __syncthreads();
     }
@@ -279,8 +313,12 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       mbar_wait(&full[buf], (unsigned)((gs / K3_NS) & 1));
       float G[K3_YR][4];
       if (c < NC) {
-        const int rs = tail ? ntail * 32 : 128;  // staged row: [4 or ntail planes][32 columns]
-        vfir<RT>(a, sb + grp * 32 + run * K3_YR * rs + quad * 4, rs, G);
+        // staged row: [4 or ntail planes][32 columns]; the full-chunk stride is a constant, so the
+        // FIR's loads carry immediate offsets (an IMAD per load otherwise)
+        if (!tail)
+          vfir<RT, 128>(a, sb + grp * 32 + run * K3_YR * 128 + quad * 4, 128, G);
+        else
+          vfir<RT>(a, sb + grp * 32 + run * K3_YR * ntail * 32 + quad * 4, ntail * 32, G);
       } else {
 #pragma unroll
         for (int o = 0; o < K3_YR; ++o) G[o][0] = G[o][1] = G[o][2] = G[o][3] = 0.f;
@@ -297,7 +335,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
             acc[o][e] = fmaf(bv[e], G[o][e], acc[o][e]);
             if (co == 0) {
               s0[o][e] = fmaf(u0i, bv[e], s0[o][e]);
-              sab[o][e] = fmaf(bv[e], fabsf(G[o][e]), sab[o][e]);
+              if (c == n) sab[o][e] = fmaf(bv[e], fabsf(G[o][e]), sab[o][e]);  // only eta's scale is used
             }
           }
         }

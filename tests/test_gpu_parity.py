@@ -191,9 +191,10 @@ def test_channel_counts_with_partial_plane_chunks(n):
     assert rep.guarded_pixels == ref["guarded_pixels"]
 
 
-@pytest.mark.parametrize("rho", [3, 16, 27])
+@pytest.mark.parametrize("rho", [1, 2, 3, 16, 27])
 def test_lloyd_bounds_are_exact(rho, monkeypatch):
-    # Hamerly-style skipping must not change a single label or centroid bit
+    # Hamerly-style skipping (and, for rho <= 3, the cell-pruned candidate search) must not
+    # change a single label or centroid bit against searching every centroid for every point
     rng = np.random.default_rng(100 + rho)
     centers = rng.uniform(0, 1, (40, rho))
     pts = (centers[rng.integers(0, 40, 60000)] + 0.08 * rng.standard_normal((60000, rho))).astype(np.float32)
@@ -205,6 +206,39 @@ def test_lloyd_bounds_are_exact(rho, monkeypatch):
     assert len(a.errors) == len(b.errors)
     np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
     assert a.quant_error == b.quant_error
+    if rho <= 3:  # the bounds path the wider guides use, on the same points
+        monkeypatch.delenv("NYS_KM_NOBOUNDS")
+        monkeypatch.setenv("NYS_KM_NOGRID", "1")
+        c = kmeans_landmarks(pts.astype(np.float64), 32, seed=3, max_iter=40)
+        assert np.array_equal(c.centroids, b.centroids) and np.array_equal(c.assignment, b.assignment)
+
+
+@pytest.mark.parametrize("case", ["quantised", "constant_dim", "negative_wide", "m64_duplicates"])
+def test_cell_pruned_assignment_edge_cases(case, monkeypatch):
+    """rho <= 3 Lloyd (candidate masks per cell of the points' bounding box) against the full
+    search: exact ties from quantised colours, a dimension with zero range, negative / wide
+    ranges, duplicated seeds with m0 = 64 (empty-cluster repairs)."""
+    rng = np.random.default_rng(7)
+    if case == "quantised":
+        pts = (rng.integers(0, 8, (50000, 3)) / 7.0).astype(np.float32)
+        m0 = 48
+    elif case == "constant_dim":
+        pts = rng.uniform(0, 1, (40000, 3)).astype(np.float32)
+        pts[:, 1] = 0.25
+        m0 = 24
+    elif case == "negative_wide":
+        pts = (rng.standard_normal((40000, 2)) * np.array([1000.0, 1e-3]) + np.array([-500.0, 2.0])).astype(np.float32)
+        m0 = 40
+    else:
+        base = rng.uniform(0, 1, (20, 3))
+        pts = np.repeat(base, 2000, axis=0).astype(np.float32)  # 20 distinct points, 64 landmarks
+        m0 = 64
+    a = kmeans_landmarks(pts.astype(np.float64), m0, seed=1, max_iter=25)
+    monkeypatch.setenv("NYS_KM_NOBOUNDS", "1")
+    b = kmeans_landmarks(pts.astype(np.float64), m0, seed=1, max_iter=25)
+    assert np.array_equal(a.centroids, b.centroids)
+    assert np.array_equal(a.assignment, b.assignment)
+    np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
 
 
 def test_pinned_host_io_and_out_buffer():

@@ -241,21 +241,28 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     }
     umma::st_wait();
   };
-  // 2. y = M b: 3 x K/8 MMAs (M=128, N=NU, K=8), issued by one thread
+  // 2. y = M b: 3 x K/8 MMAs (M=128, N=NU, K=8).  Issued by the group's last warp, converged,
+  // one elected lane per MMA (mma_tf32_ts_elect): a divergent `if (gtid == 0)` made every MMA an
+  // ELECT / R2UR.BROADCAST waterfall loop (~125 cycles each) in the warp that also carries the most
+  // FIR items, and the group's next barrier waited for it; the last warp's threads have one FIR
+  // item fewer per tile (items are dealt from thread 0 up) and the slack to issue
+  const uint64_t desc_bh = umma::desc_kmajor(Bh, (uint32_t)NU * 16, 128), desc_bl = umma::desc_kmajor(Bl, (uint32_t)NU * 16, 128);
+  const uint64_t desc_step = (uint64_t)((8 * NU * 4) >> 4);  // one K step (8 columns) in the address field
+  const int gwarp_u = __shfl_sync(0xffffffffu, gtid >> 5, 0);  // warp index within the group, warp-uniform to the compiler
+  const bool issuer = gwarp_u == K2T_GROUP / 32 - 1;
   auto issue_mma = [&]() {
-    const uint32_t lbo_b = (uint32_t)NU * 16;
     uint32_t acc = 0;
 #pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
       const uint32_t A = pass == 2 ? a_lo : a_hi;
-      const float* B = pass == 1 ? Bl : Bh;
+      uint64_t B = pass == 1 ? desc_bl : desc_bh;
 #pragma unroll 1
-      for (int kk = 0; kk < KU / 8; ++kk) {
-        umma::mma_tf32_ts(tmem, A + (uint32_t)(8 * kk), umma::desc_kmajor(B + kk * 8 * NU, lbo_b, 128), idesc, acc);
+      for (int kk = 0; kk < KU / 8; ++kk, B += desc_step) {
+        umma::mma_tf32_ts_elect(tmem, A + (uint32_t)(8 * kk), B, idesc, acc);
         acc = 1;
       }
     }
-    umma::commit(bar);
+    umma::commit_elect(bar);
   };
   // 3. accumulator -> y rows in SMEM (warps w, w+4 of the group drain half of
   // the column chunks of TMEM lanes 32(w%4)..), and the tile's f rows
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     features(a.v0 + tr, tx * TW);
     umma::fence_before();
     group_sync(g);
-    if (gtid == 0) {
+    if (issuer) {
       umma::fence_after();
       issue_mma();
     }
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     umma::fence_before();
     group_sync(g);
     umma::fence_after();
-    if (more && gtid == 0) issue_mma();
+    if (more && issuer) issue_mma();
     fir(a.v0 + tr, tx * TW, b);
     if (more) {
       umma::mbar_wait(bar, phase);

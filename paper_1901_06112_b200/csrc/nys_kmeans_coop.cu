@@ -16,9 +16,11 @@
 // sees a stale L1 line written by another SM before a grid barrier.
 #include <cooperative_groups.h>
 
+#include <type_traits>
 #include <cstdlib>
 
 #include "nys_kmeans_dev.cuh"
+#include "nys_umma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -428,7 +430,20 @@ __device__ __forceinline__ float d2_f32(const float (&x)[GR], int rho, const flo
 constexpr double LB_EPS = 1.0 / 32768.0;
 
 // GRID: the cell-pruned search (a separate instantiation, so the bounds kernels compile as before)
-template <int GR, int RX, bool GRID = false>
+//
+// TC (wide guides, north_star (1)): the m0-way search of every point runs on the 5th-generation
+// tensor cores, every iteration, with no per-point bound state.  A group of four warps takes
+// 128 points (TMEM lanes); each thread splits its point x = x_hi + x_lo into TF32 pairs and
+// stores (x, 1) as the A operand in TMEM; one thread issues 3 x K/8 tcgen05.mma kind::tf32
+// against B = (-2 c_j, |c_j|^2) (centroids in shared memory, K-major, hi/lo split, rebuilt after
+// every update), so D_j = |c_j|^2 - 2 x.c_j = approx_j - |x|^2 accumulates in TMEM.  The thread
+// drains its row, takes the minimum, and re-checks every centroid within 2 delta of it with the
+// exact FP32 difference form (ascending j, strict <): delta = 1e-4 (|x|^2 + max|c|^2) bounds the
+// 3xTF32 / FP32-norm error with a wide margin, so labels, distances and tie-breaks equal the FP32
+// search's (test_lloyd_bounds_are_exact, NYS_KM_NOBOUNDS A/B).  Two groups per CTA, each with its
+// own TMEM columns and mbarrier, overlap one group's MMAs with the other's re-check.  Label
+// changes feed the same exact fixed-point delta sums as the bounds kernel.
+template <int GR, int RX, bool GRID = false, bool TC = false>
 __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double dsm[];
@@ -453,6 +468,31 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   double* gh = reinterpret_cast<double*>(gts + (GRID ? NCELL_ALL : 0));            // 3 cell widths
   float* glo = reinterpret_cast<float*>(gh + 3);                                   // 3 box origins
   float* ginv = glo + 3;                                                           // 3 inverse cell widths
+  // TC: B operand (NU x KU, K-major core matrices, hi / lo) and this CTA's TMEM / mbarriers
+  const int KU = TC ? ((rho + 1 + 7) / 8) * 8 : 0, NU = TC ? ((m0 + 15) / 16) * 16 : 0;
+  float* Bh = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Cfo + (size_t)m0p * rhop) + 127) & ~uintptr_t(127));
+  float* Bl = Bh + (size_t)NU * KU;
+  __shared__ uint64_t tc_bar[2];
+  __shared__ uint32_t tc_tmem;
+  __shared__ float tc_ccmax;
+  const int tcols = ((NU + 31) & ~31) + 2 * ((KU + 31) & ~31);  // per group: D, A_hi, A_lo
+  int tc_alloc = 32;
+  if constexpr (TC) {
+    // the whole tensor memory of the SM (one CTA per SM: 255 registers): the base is then column 0 by
+    // construction, so the MMA operands below are kernel-parameter arithmetic in uniform registers
+    // (addresses derived from the allocation word in shared memory cost a register-to-uniform move per
+    // operand per MMA: ~125 cycles per instruction, measured)
+    tc_alloc = 512;
+    if (w == 0) umma::tmem_alloc(&tc_tmem, (uint32_t)tc_alloc);
+    if (threadIdx.x < 2) {
+      umma::mbar_init(&tc_bar[threadIdx.x], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  }
+  uint32_t tc_phase = 0;
   __shared__ double sh[64];
   __shared__ double extra[2][32];
   __shared__ double misc[2];
@@ -578,6 +618,34 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     for (int k = threadIdx.x; k < nw * msl; k += blockDim.x) wacc[k] = 0ull;
     for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0;
     const double dcum = dcum_sh;
+    if constexpr (TC) {  // B = (-2 c_j, |c_j|^2) from the current FP32 centroids, split hi / lo
+      for (int k = threadIdx.x; k < NU * KU; k += blockDim.x) {
+        const int j = k / KU, d = k - j * KU;
+        float v = 0.f;
+        if (j < m0) {
+          if (d < rho) {
+            v = -2.f * Cf[j * rhop + d];
+          } else if (d == rho) {
+            for (int q = 0; q < rho; ++q) v = fmaf(Cf[j * rhop + q], Cf[j * rhop + q], v);
+          }
+        }
+        const float h = umma::to_tf32(v);
+        const int o = umma::kmajor_offset(j, d, NU);
+        Bh[o] = h;
+        Bl[o] = umma::to_tf32(v - h);
+      }
+      if (w == 0) {
+        float mx = 0.f;
+        for (int j = lane; j < m0; j += 32) {
+          float v = 0.f;
+          for (int q = 0; q < rho; ++q) v = fmaf(Cf[j * rhop + q], Cf[j * rhop + q], v);
+          mx = fmaxf(mx, v);
+        }
+        mx = warp_max(mx);
+        if (lane == 0) tc_ccmax = mx;
+      }
+      umma::fence_proxy_async();  // generic-proxy writes of B -> tensor core
+    }
     __syncthreads();
     unsigned long long* myacc = wacc + (size_t)w * msl;
     int* mycnt = wcnt + (size_t)w * m0;
@@ -689,6 +757,166 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         }
         nlist = 0;  // phase B has nothing left
       }
+    } else if constexpr (TC) {
+      const int g = w >> 2, gw = w & 3, gtid = threadIdx.x & 127;  // two groups of four warps (nw == 8)
+      const int wu = __shfl_sync(0xffffffffu, w, 0);
+      const uint32_t tbase = (uint32_t)(g * tcols);  // tc_tmem == 0
+      const uint32_t dcol = tbase, a_hi = tbase + (uint32_t)((NU + 31) & ~31), a_lo = a_hi + (uint32_t)((KU + 31) & ~31);
+      const uint32_t lane_base = (uint32_t)(32 * gw) << 16;
+      const uint32_t idesc = umma::idesc_tf32(128, NU);
+      const uint32_t lbo_b = (uint32_t)NU * 16;
+      const uint64_t desc_h = umma::desc_kmajor(Bh, lbo_b, 128), desc_l = umma::desc_kmajor(Bl, lbo_b, 128);
+      const uint64_t desc_step = (uint64_t)((8 * NU * 4) >> 4);  // one K step (8 columns) in the address field
+      const float ccmax = tc_ccmax;
+      constexpr int KC = (GR + 1 + 15) / 16;  // 16-column chunks of the A operand (x, 1, 0 ...)
+      auto load_pt = [&](long long i, bool valid, float (&x)[GR], int& oldl) {
+#pragma unroll
+        for (int d = 0; d < GR; ++d) x[d] = (valid && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
+        oldl = (valid && it > 0) ? a.labels[i] : -1;
+      };
+      float x[GR];
+      int oldl;
+      // 128-point tiles dealt round-robin over every group of the grid (content-dependent work --
+      // label changes, multi-candidate points -- spreads over all blocks)
+      const long long tstep = 128ll * 2 * nb;
+      long long base = 128ll * (2 * b + g);
+      load_pt(base + gtid, base + gtid < a.m, x, oldl);
+      for (; base < a.m; base += tstep) {
+        const long long i = base + gtid;
+        const bool valid = i < a.m;
+        float xx = 0.f;
+#pragma unroll
+        for (int d = 0; d < GR; ++d)
+          if (d < rho) xx = fmaf(x[d], x[d], xx);
+        // A operand: row = this thread's TMEM lane, columns (x_0 .. x_rho-1, 1, 0 ...), hi then lo;
+        // hi = x rounded to TF32 (integer round-half-up), lo = x - hi exactly (read by truncation)
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          if (16 * c < KU) {
+            float h[16], l[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int d = 16 * c + e;
+              float v = 0.f;
+              if (d < GR) v = x[d < GR ? d : 0];
+              if (d == rho) v = 1.f;
+              h[e] = __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u);
+              l[e] = v - h[e];
+            }
+            umma::st_32x32b_x16(a_hi + lane_base + (uint32_t)(16 * c), h);
+            umma::st_32x32b_x16(a_lo + lane_base + (uint32_t)(16 * c), l);
+          }
+        }
+        umma::st_wait();
+        umma::fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        // the group's first warp issues, converged, one elected lane per MMA (mma_tf32_ts_elect);
+        // wu is the warp index as a value the compiler knows to be warp-uniform
+        auto issue = [&](auto gc) {
+          constexpr int G = decltype(gc)::value;
+          umma::fence_after();
+          const uint32_t d0 = (uint32_t)(G * tcols);
+          const uint32_t ah = d0 + (uint32_t)((NU + 31) & ~31), al = ah + (uint32_t)((KU + 31) & ~31);
+          uint32_t acc = 0;
+#pragma unroll 1
+          for (int pass = 0; pass < 3; ++pass) {
+            const uint32_t A = pass == 1 ? al : ah;
+            uint64_t B = pass == 2 ? desc_l : desc_h;
+#pragma unroll 1
+            for (int kk = 0; kk < KU / 8; ++kk, B += desc_step) {
+              umma::mma_tf32_ts_elect(d0, A + (uint32_t)(8 * kk), B, idesc, acc);
+              acc = 1;
+            }
+          }
+          umma::commit_elect(&tc_bar[G]);
+        };
+        if (wu == 0) issue(std::integral_constant<int, 0>{});
+        if (wu == 4) issue(std::integral_constant<int, 1>{});
+        // the next tile's coordinates travel while the tensor core and the re-check work
+        float xn[GR];
+        int oldn;
+        load_pt(i + tstep, i + tstep < a.m, xn, oldn);
+        umma::mbar_wait(&tc_bar[g], tc_phase);
+        tc_phase ^= 1u;
+        umma::fence_after();
+        // smallest and second-smallest approximate distance (minus |x|^2) with the argmin: nearly
+        // every point has one candidate within 2 delta, re-checked without divergence
+        // (four interleaved chains: a single running minimum is a 3-deep dependent select per column)
+        float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, s4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        int j4[4] = {0, 0, 0, 0};
+        for (int c = 0; c < NU / 16; ++c) {
+          float v[16];
+          umma::ld_32x32b_x16(dcol + lane_base + (uint32_t)(16 * c), v);
+          umma::ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int j = 16 * c + e;
+            const float ve = j < m0 ? v[e] : INFINITY;
+            const int q = e & 3;
+            if (ve < m4[q]) {
+              s4[q] = m4[q];
+              m4[q] = ve;
+              j4[q] = j;
+            } else {
+              s4[q] = fminf(s4[q], ve);
+            }
+          }
+        }
+        float mn = m4[0], mn2 = s4[0];
+        int jmin = j4[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {  // merge: smallest value (lowest index on ties), second smallest
+          if (m4[q] < mn || (m4[q] == mn && j4[q] < jmin)) {
+            mn2 = fminf(fminf(mn2, s4[q]), mn);
+            mn = m4[q];
+            jmin = j4[q];
+          } else {
+            mn2 = fminf(fminf(mn2, s4[q]), m4[q]);
+          }
+        }
+        // delta: 3 K FP32 accumulation roundings, the dropped lo.lo products and the truncated lo
+        // operands bound |D_j + |x|^2 - d2| by ~7e-6 (|x|^2 + 2 max|c|^2); 3e-5 keeps a 4x margin
+        const float lim = mn + 2.f * (3e-5f * (xx + 2.f * ccmax) + 1e-30f);
+        float best = d2_f32<GR>(x, rho, Cf + (size_t)jmin * rhop);
+        int arg = jmin;
+        if (__any_sync(0xffffffffu, mn2 <= lim)) {  // rare: several candidates, ascending j with first-index ties
+          // (tcgen05.ld is warp-collective: every lane drains, the lanes with one candidate skip the math)
+          for (int c = 0; c < NU / 16; ++c) {
+            float v[16];
+            umma::ld_32x32b_x16(dcol + lane_base + (uint32_t)(16 * c), v);
+            umma::ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int j = 16 * c + e;
+              if (mn2 <= lim && j < m0 && j != jmin && v[e] <= lim) {
+                const float d2 = d2_f32<GR>(x, rho, Cf + (size_t)j * rhop);
+                if (d2 < best || (d2 == best && j < arg)) {
+                  best = d2;
+                  arg = j;
+                }
+              }
+            }
+          }
+        }
+        bool chg = false;
+        if (valid) {
+          near_sum += (double)best;
+          chg = oldl != arg;
+          if (chg) {
+            changed += 1.0;
+            a.labels[i] = arg;
+          }
+        }
+        warp_accumulate_fx<GR>(x, rho, arg, valid && chg, scale, 1, myacc, mycnt);
+        warp_accumulate_fx<GR>(x, rho, oldl, valid && chg && oldl >= 0, scale, -1, myacc, mycnt);
+        umma::fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // the group's TMEM reads are done
+        umma::fence_after();
+#pragma unroll
+        for (int d = 0; d < GR; ++d) x[d] = xn[d];
+        oldl = oldn;
+      }
+      nlist = 0;  // phase B has nothing left
     } else if (!full_pass) {
       // phase A: warp w tests its contiguous sub-range; failures go to its list segment in point order
       // PA chunks of 32 points in flight per warp: their point, label and bound
@@ -958,7 +1186,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     }
     __syncthreads();
     double mv = 0.0;
-    if constexpr (!gridmode)  // (the cell-pruned search keeps no drift-adjusted bounds)
+    if constexpr (!gridmode && !TC)  // (the cell-pruned / tensor-core searches keep no drift-adjusted bounds)
     for (int j = threadIdx.x; j < m0; j += blockDim.x) {
       double s2 = 0.0;
       for (int d = 0; d < rho; ++d) {
@@ -967,7 +1195,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       }
       mv = fmax(mv, sqrt(s2));
     }
-    if constexpr (!gridmode) {
+    if constexpr (!gridmode && !TC) {
       for (int o = 16; o > 0; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
       if (lane == 0) sh[w] = mv;
       __syncthreads();
@@ -982,6 +1210,11 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       if constexpr (GRID) build_grid();
       grid.sync();
     }
+  }
+  if constexpr (TC) {
+    umma::fence_before();
+    __syncthreads();
+    if (w == 0) umma::tmem_dealloc(tc_tmem, (uint32_t)tc_alloc);
   }
   if (b == 0)
     for (int k = threadIdx.x; k < msl; k += blockDim.x) a.C[k] = Cd[k];
@@ -1070,7 +1303,14 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   size_t gcells = 1;
   for (int d = 0; d < rho; ++d) gcells *= KM_NG;
   const size_t gsm = gridmode ? gcells * 8 + 16 + 64 : 0;
-  auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed + gsm; };
+  // tensor-core search for wide guides: (x, 1) needs K = rho + 1 padded to 8, N = m0 padded to 16,
+  // two groups' D / A_hi / A_lo columns in the 512-column TMEM
+  const char* etc = getenv("NYS_KM_TC_COOP");  // opt-in: measured on par with / behind the bounds kernel
+  const int KUt = (int)ceil_div(rho + 1, 8) * 8, NUt = (int)ceil_div(m0, 16) * 16;
+  bool use_tc = rho >= 16 && (etc && atoi(etc)) && NUt <= 256 &&
+                2 * (((NUt + 31) & ~31) + 2 * ((KUt + 31) & ~31)) <= 512;
+  const size_t tsm = use_tc ? (size_t)2 * NUt * KUt * 4 + 128 : 0;
+  auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed + gsm + tsm; };
   int nw = 8;
   while (nw > 1 && need(nw) > 200 * 1024) --nw;
   const size_t smem = need(nw);
@@ -1116,6 +1356,16 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
     NYS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(nb), dim3(nw * 32), args, smem, s));
     return NYS_OK;
   };
+  if (use_tc && a.bounds && nw == 8) {  // (fewer warps: the per-warp tables did not fit; FP32 bounds kernel)
+    switch (rho) {
+      case 16: return go(k_lloyd_coop<16, 16, false, true>);
+      case 27: return go(k_lloyd_coop<32, 27, false, true>);
+      case 31: return go(k_lloyd_coop<32, 31, false, true>);
+      default: break;
+    }
+    if (rho <= 32) return go(k_lloyd_coop<32, 0, false, true>);
+    return go(k_lloyd_coop<64, 0, false, true>);
+  }
   if (use_grid) {
     switch (rho) {
       case 1: return go(k_lloyd_coop<4, 1, true>);

@@ -206,11 +206,32 @@ def test_lloyd_bounds_are_exact(rho, monkeypatch):
     assert len(a.errors) == len(b.errors)
     np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
     assert a.quant_error == b.quant_error
-    if rho <= 3:  # the bounds path the wider guides use, on the same points
+    if rho <= 3:  # the Hamerly-bounds kernel the wider guides use, on the same points
         monkeypatch.delenv("NYS_KM_NOBOUNDS")
         monkeypatch.setenv("NYS_KM_NOGRID", "1")
         c = kmeans_landmarks(pts.astype(np.float64), 32, seed=3, max_iter=40)
         assert np.array_equal(c.centroids, b.centroids) and np.array_equal(c.assignment, b.assignment)
+
+
+@pytest.mark.parametrize("rho,m0", [(16, 64), (31, 48), (32, 40), (40, 24), (17, 100)])
+def test_tensor_core_lloyd_equals_fp32_search(rho, m0, monkeypatch):
+    """Wide guides: the cooperative Lloyd kernel's tcgen05 3xTF32 search ((x, 1) . (-2c, |c|^2)
+    in TMEM, exact FP32 re-check of the candidates within the error bound) against the FP32 search
+    of every centroid: identical labels, centroids and objectives.  Shapes cover K and N padding
+    (rho + 1 = 17 .. 41, m0 = 24 .. 100), near-duplicate points and far-off outliers."""
+    rng = np.random.default_rng(rho * 100 + m0)
+    centers = rng.uniform(0, 1, (m0 + 5, rho))
+    pts = centers[rng.integers(0, m0 + 5, 40000)] + 0.05 * rng.standard_normal((40000, rho))
+    pts[:200] = pts[200:400] + 1e-6 * rng.standard_normal((200, rho))  # near-ties between neighbours
+    pts[400:420] *= 30.0  # outliers: large |x|^2 against small centroid gaps
+    pts = pts.astype(np.float32)
+    monkeypatch.setenv("NYS_KM_TC_COOP", "1")  # opt-in variant of k_lloyd_coop
+    a = kmeans_landmarks(pts.astype(np.float64), m0, seed=2, max_iter=20)
+    monkeypatch.setenv("NYS_KM_NOBOUNDS", "1")
+    b = kmeans_landmarks(pts.astype(np.float64), m0, seed=2, max_iter=20)
+    assert np.array_equal(a.centroids, b.centroids)
+    assert np.array_equal(a.assignment, b.assignment)
+    np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
 
 
 @pytest.mark.parametrize("case", ["quantised", "constant_dim", "negative_wide", "m64_duplicates"])

@@ -1,6 +1,5 @@
-python tools/km_timing.py 4 | tail -1; python tools/km_timing.py 2 | tail -1
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench4.json 2> gpurun_out/bench4.err; python -c "
-import json;d=json.load(open('gpurun_out/bench4.json'));print(d['value'],d['ms_per_step'],d['roofline']['kernel_ms'],d['stage_ms'])"
-for c in 3 4; do timeout 300 python bench.py --config $c --steps 5 --warmup 2 --no-cpu-baseline 2>/dev/null | python -c "
+timeout 120 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "lloyd or tensor_core" 2>&1 | tail -3
+timeout 60 python tools/km_timing.py 4 | tail -1
+NYS_KM_NOTC=1 timeout 60 python tools/km_timing.py 4 | tail -1
+for c in 3; do timeout 100 python bench.py --config $c --steps 5 --warmup 2 --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys;d=json.loads(sys.stdin.read());print(d['config']['workload'],d['value'],d['ms_per_step'],d['roofline']['kernel_ms'],d['stage_ms'])"; done
-timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3

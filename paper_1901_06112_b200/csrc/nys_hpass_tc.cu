@@ -319,7 +319,12 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     const float* Fs = Fs_of(b);
     // (i, ch, xg) of item it = ((xg * nchunks + ch) * L + i), advanced incrementally by the
     // group stride (no divisions per item)
-    int i = gtid % L, ch = (gtid / L) % nchunks, xg = (gtid / L) / nchunks;
+    // Items are dealt from FIR thread 0 up, so the first fir_items - 256 threads carry one item more.
+    // Group 1 rotates its thread numbering by two warps: the warps with the extra item then sit on
+    // different SM sub-partitions in the two groups (CTA warp w issues on sub-partition w % 4; without
+    // the rotation sub-partition 0 carried 8 warp-items per tile pair against 6 on the others).
+    const int ftid = (gtid + 64 * g) & (K2T_GROUP - 1);
+    int i = ftid % L, ch = (ftid / L) % nchunks, xg = (ftid / L) / nchunks;
     auto advance = [&]() {
       i += strideL;
       ch += strideR;
@@ -336,7 +341,7 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
         ch -= q * nchunks;
       }
     };
-    for (int it = gtid; it < fir_items; it += K2T_GROUP, advance()) {
+    for (int it = ftid; it < fir_items; it += K2T_GROUP, advance()) {
       const int xo = x0 + xg * K2_XR;
       if (xo >= W) continue;
       const float* yrow = Ys + (size_t)i * pitch + xg * K2_XR;

@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   double* gh = reinterpret_cast<double*>(gts + (GRID ? NCELL_ALL : 0));            // 3 cell widths
   float* glo = reinterpret_cast<float*>(gh + 3);                                   // 3 box origins
   float* ginv = glo + 3;                                                           // 3 inverse cell widths
+  int* wlim = reinterpret_cast<int*>(ginv + 3 + 1);                                // nw x msl x 3 signed 21-bit limbs (grid mode)
   // TC: B operand (NU x KU, K-major core matrices, hi / lo) and this CTA's TMEM / mbarriers
   const int KU = TC ? ((rho + 1 + 7) / 8) * 8 : 0, NU = TC ? ((m0 + 15) / 16) * 16 : 0;
   float* Bh = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(Cfo + (size_t)m0p * rhop) + 127) & ~uintptr_t(127));
@@ -617,6 +618,8 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       for (int k = threadIdx.x; k < gstride; k += blockDim.x) a.gacc[(size_t)((it + 1) % 3) * gstride + k] = 0ull;
     for (int k = threadIdx.x; k < nw * msl; k += blockDim.x) wacc[k] = 0ull;
     for (int k = threadIdx.x; k < nw * m0; k += blockDim.x) wcnt[k] = 0;
+    if constexpr (GRID)
+      for (int k = threadIdx.x; k < nw * msl * 3; k += blockDim.x) wlim[k] = 0;
     const double dcum = dcum_sh;
     if constexpr (TC) {  // B = (-2 c_j, |c_j|^2) from the current FP32 centroids, split hi / lo
       for (int k = threadIdx.x; k < NU * KU; k += blockDim.x) {
@@ -743,12 +746,29 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
             } else if (chg) {
               // few lanes change label after the first iteration: they add their fixed-point
               // coordinates to this warp's table with shared-memory atomics (integer adds commute,
-              // so the sums stay exact and order-independent); x * 2^s is exact in FP32
+              // so the sums stay exact and order-independent); x * 2^s is exact in FP32.  64-bit
+              // shared atomics are compare-and-swap loops on sm_100a, so the value goes in as three
+              // signed 21-bit limbs with native 32-bit adds (a warp adds < 2^9 points per iteration)
+              int* mylim = wlim + (size_t)w * msl * 3;
 #pragma unroll
               for (int d = 0; d < RX; ++d) {
-                const unsigned long long v = (unsigned long long)__float2ll_rn(x[h][d] * scalef);
-                atomicAdd(myacc + arg[h] * rho + d, v);
-                atomicAdd(myacc + old * rho + d, 0ull - v);
+                const long long v = __float2ll_rn(x[h][d] * scalef);
+                const unsigned long long mag = (unsigned long long)(v < 0 ? -v : v);
+                const int sg = v < 0 ? -1 : 1;
+                const int l0 = sg * (int)(mag & 0x1FFFFFull), l1 = sg * (int)((mag >> 21) & 0x1FFFFFull),
+                          l2 = sg * (int)(mag >> 42);
+                int* pn = mylim + (arg[h] * rho + d) * 3;
+                int* po = mylim + (old * rho + d) * 3;
+                atomicAdd(pn, l0);
+                atomicAdd(po, -l0);
+                if (l1) {
+                  atomicAdd(pn + 1, l1);
+                  atomicAdd(po + 1, -l1);
+                }
+                if (l2) {
+                  atomicAdd(pn + 2, l2);
+                  atomicAdd(po + 2, -l2);
+                }
               }
               atomicAdd(mycnt + arg[h], 1);
               atomicSub(mycnt + old, 1);
@@ -1065,6 +1085,12 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     for (int k = threadIdx.x; k < msl; k += blockDim.x) {
       unsigned long long t = 0;
       for (int q = 0; q < nw; ++q) t += wacc[(size_t)q * msl + k];
+      if constexpr (GRID) {
+        for (int q = 0; q < nw; ++q) {
+          const int* l = wlim + ((size_t)q * msl + k) * 3;
+          t += (unsigned long long)((long long)l[0] + ((long long)l[1] << 21) + ((long long)l[2] << 42));
+        }
+      }
       if (t) atomicAdd(D + k, t);
     }
     for (int k = threadIdx.x; k < m0; k += blockDim.x) {
@@ -1116,7 +1142,10 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     __syncthreads();
     // empty clusters, ascending j: farthest remaining point from its old centroid
     int nex = 0;
-    for (int j = 0; j < m0; ++j) {
+    bool mine_empty = false;
+    for (int j = threadIdx.x; j < m0; j += blockDim.x) mine_empty |= T[msl + j] <= 0;
+    const int jend = __syncthreads_or(mine_empty) ? m0 : 0;  // (the common case: none, no serial scan)
+    for (int j = 0; j < jend; ++j) {
       if (T[msl + j] > 0) continue;
       double bv = -INFINITY;
       long long bi = a.m;
@@ -1302,7 +1331,7 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   const bool gridmode = rho <= 3 && m0 <= 64 && !(eg && atoi(eg));
   size_t gcells = 1;
   for (int d = 0; d < rho; ++d) gcells *= KM_NG;
-  const size_t gsm = gridmode ? gcells * 8 + 16 + 64 : 0;
+  const size_t gsm = gridmode ? gcells * 8 + 16 + 64 + (size_t)8 * msl * 3 * 4 : 0;  // masks, box, limb tables
   // tensor-core search for wide guides: (x, 1) needs K = rho + 1 padded to 8, N = m0 padded to 16,
   // two groups' D / A_hi / A_lo columns in the 512-column TMEM
   const char* etc = getenv("NYS_KM_TC_COOP");  // opt-in: measured on par with / behind the bounds kernel

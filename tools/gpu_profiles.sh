@@ -9,7 +9,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $o/reference
 timeout 300 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $o/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/cfg2_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $o/ncu_launch.log 2>&1
 python tools/launches.py $o/cfg2_launches.csv > $o/cfg2_launches_summary.txt 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_feat_hpass|k_vpass|k_finish" -c 3 -o $o/cfg2_full python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $o/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_seed_runs|k_lloyd_coop|k_feat_hpass|k_vpass|k_finish" -c 5 -o $o/cfg2_full python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $o/ncu_full.log 2>&1
 for c in 1 2 3 4; do timeout 1200 python tools/fullsize_parity.py $c >> $o/fullsize_parity.jsonl 2>> $o/fullsize_parity.err; done
 timeout 1200 python tools/fullsize_parity.py 5 1024 1024 >> $o/fullsize_parity.jsonl 2>> $o/fullsize_parity.err
 ls -la $o

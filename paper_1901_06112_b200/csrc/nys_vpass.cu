@@ -38,10 +38,9 @@ namespace nys {
 // accumulators of its current chunk and s0 = u0.b in registers, so the
 // unrolled code is one vertical FIR (~0.5k instructions) and stays in the
 // instruction cache.
-constexpr int K3_RUNS = 16;           // row runs per tile
-constexpr int K3_THREADS = 4 * K3_RUNS * 8;
+constexpr int K3_THREADS = 256;
 constexpr int K3_YR = 4;             // rows per thread
-constexpr int K3_TH = K3_RUNS * K3_YR;  // tile rows
+constexpr int K3_TH = 8 * K3_YR;     // tile rows
 constexpr int K3_NPX = K3_TH * 32;   // tile pixels
 constexpr int K3_NS = 2;             // TMA pipeline depth
 
@@ -170,12 +169,12 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
 }
 
 template <int RT>
-__global__ void __launch_bounds__(K3_THREADS, K3_THREADS <= 256 ? 2 : 1) k_vpass(const __grid_constant__ CUtensorMap tmap4,
+__global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__ CUtensorMap tmap4,
                                                         const __grid_constant__ CUtensorMap tmapt,
                                                         const __grid_constant__ CUtensorMap tmapb, const VArgs a) {
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x;
-  const int grp = tid / (8 * K3_RUNS), run = (tid >> 3) & (K3_RUNS - 1), quad = tid & 7;
+  const int grp = tid >> 6, run = (tid >> 3) & 7, quad = tid & 7;
   const int m0 = a.m0, n = a.n, rho = a.rho, rhop = a.rhop, H = a.H, W = a.W, NC = n + 1;
   const int R = RT > 0 ? RT : a.R;
   const int SR = K3_TH + 2 * R;     // staged rows per plane

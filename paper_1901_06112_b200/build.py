@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libnysfilter_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["nys_filter.cu", "nys_hpass.cu", "nys_hpass_tc.cu", "nys_vpass.cu", "nys_refine.cu", "nys_kmeans.cu", "nys_kmeans_coop.cu", "nys_kmeans_tc.cu", "nys_recursive.cu", "nys_brute.cu", "nys_metrics.cu", "nys_pca.cu", "nys_spatial.cu",
+SOURCES = ["nys_filter.cu", "nys_hpass.cu", "nys_hpass_tc.cu", "nys_vpass.cu", "nys_refine.cu", "nys_kmeans.cu", "nys_kmeans_coop.cu", "nys_recursive.cu", "nys_brute.cu", "nys_metrics.cu", "nys_pca.cu", "nys_spatial.cu",
            "nys_host.cpp"]
 
 

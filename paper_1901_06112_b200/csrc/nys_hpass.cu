@@ -241,13 +241,6 @@ int nys_filter_hpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
     }
     const char* e = getenv("NYS_K2_SIMT");  // debug: force the CUDA-core GEMM kernel
     if (!(e && atoi(e)) && normM <= NYS_TC_MAX_NORM) {
-      // NYS_K2_TF=1: the FIR on the tensor cores as well (launch_hpass_tf).  Opt-in: measured
-      // 2.2 ms against 1.5 ms for the CUDA-core FIR on cfg 2 (tensor-core FIR)
-      const char* etf = getenv("NYS_K2_TF");
-      if (etf && atoi(etf) == 1) {
-        const int rc = launch_hpass_tf(a, d, s);
-        if (rc != NYS_EUNSUPPORTED) return rc;
-      }
       const int rc = launch_hpass_tc(a, d, s);
       if (rc != NYS_EUNSUPPORTED) return rc;
     }

@@ -25,7 +25,8 @@ struct HArgs {
   int npl, bplanes;  // planes per buffer row block; store raw b_i planes after the filtered ones
   int phi;           // phi-form: store y_i (= phi_i) in the feature-plane slots instead of b_i
   int ku, nu, tcols, nbuf;  // tcgen05 path: K (m0 padded to 8), N ((m0+1) padded to 16), TMEM columns per group, y/f buffers
-  int sc, kw;               // tensor-FIR path: source samples per tile (TMEM columns), Toeplitz K window
+  int sc, kw;               // (unused: the removed tensor-core FIR variant's tile geometry; kept so the struct, and with it
+                            // the kernels' parameter layout and register allocation, stay as measured)
   int bfrom;                // wide guides (rho > NYS_MAX_RHO): the features were written as b planes by
                             // k_bplanes_wide; K2 reads them instead of evaluating the guide
   int dbg;  // debug: bit0 skip features, bit1 skip GEMM, bit2 skip FIR math, bit3 skip stores
@@ -182,7 +183,5 @@ __device__ __forceinline__ void hfir_plane(const HArgs& a, const float* __restri
 // tcgen05 path of K2 (nys_hpass_tc.cu): fills the tile geometry of `a` and
 // launches, or returns NYS_EUNSUPPORTED when the shape does not fit it
 int launch_hpass_tc(HArgs& a, const nys_filter_desc* d, cudaStream_t s);
-// ... with the horizontal FIR on the tensor cores too (box kernels excluded)
-int launch_hpass_tf(HArgs& a, const nys_filter_desc* d, cudaStream_t s);
 
 }  // namespace nys

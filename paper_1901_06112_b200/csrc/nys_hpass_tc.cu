@@ -39,25 +39,6 @@ constexpr int K2T_PX = 128;                    // UMMA M: source pixels per tile
 
 __host__ __device__ inline int align32f(int v) { return (v + 31) & ~31; }
 
-__host__ __device__ constexpr uint32_t idesc_fir1(int N) { return umma::idesc_tf32(K2T_PX, N); }
-
-// The 3xTF32 MMAs of FIR N-tile J (16 outputs): fully unrolled with the tile index a
-// compile-time constant, so every TMEM / descriptor operand is uniform (kernel parameters and
-// immediates) and each tcgen05.mma issues without register-to-uniform moves.
-template <int J, int KMAX>
-__device__ __forceinline__ void fir_tile_mma(uint32_t z_hi, uint32_t z_lo, uint32_t d2, uint64_t dTh, uint64_t dTl,
-                                             int nk) {
-  constexpr uint32_t id2 = umma::idesc_tf32(K2T_PX, 16);
-#pragma unroll
-  for (int pass = 0; pass < 3; ++pass) {
-    const uint32_t A = (pass == 1 ? z_lo : z_hi) + 16u * J;
-    const uint64_t B = pass == 2 ? dTl : dTh;
-#pragma unroll
-    for (int kk = 0; kk < KMAX; ++kk)
-      if (kk < nk) umma::mma_tf32_ts(d2 + 16u * J, A + 8u * kk, B + (uint64_t)(kk * 32), id2, (pass | kk) ? 1u : 0u);
-  }
-}
-
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(K2T_GROUP) : "memory");
 }
@@ -427,454 +408,6 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem_base, (uint32_t)(2 * a.tcols));
-}
-
-// ---------------------------------------------------------------------------
-// K2 with the horizontal FIR on the tensor cores as well ("tensor FIR")
-// ---------------------------------------------------------------------------
-// The row pass of plane q = (i, c) is a banded Toeplitz product: over a tile of
-// TW output columns with source samples s = 0 .. TW + 2R - 1,
-//   out_q[o] = sum_s w[s - o] z_q[s],   z_q = y_i * f_c (f_n = 1),
-// i.e. D[planes x outputs] = Z[planes x sources] * T[outputs x sources]^T.  Per
-// 128-plane chunk the CUDA cores form Z (one FMUL per sample) straight into
-// TMEM (lane = plane, column = source sample, tcgen05.st), and one thread
-// issues, per 16-output N-tile j, the 3xTF32 MMAs over the tile's K window
-// [16 j, 16 j + KW) (KW = 16 + 2R rounded up to 8; T is the same 16 x KW band
-// for every j, staged once in SMEM).  Split: z_hi = the raw FP32 bits (the MMA
-// reads TF32 by truncation), z_lo = z - trunc(z) (exact); T likewise; D =
-// z_hi T_hi + z_lo T_hi + z_hi T_lo in FP32 (error ~2^-20 of sum |w z|,
-// tools/microbench/fir_tc.cu).  tcgen05.ld drains D (lane = plane) and each
-// thread stores 16 contiguous outputs of its plane into the blocked plane buffer.
-// Useful MACs per output: 2R + 1; issued: 3 KW (R = 15: 144 vs 31) at
-// 2048 MAC/clk/SM, i.e. ~4 % of the CUDA-core FIR's issue slots per output.
-//
-// Producer / consumer pipeline in one CTA per SM (512 TMEM columns, no aliasing):
-//   group 0 (producer, 256 threads): features of tile k -> A_feat [0, 2 KU);
-//       MMA1 y = M b -> D1 [2 KU, 2 KU + NU); drain into the y rows Ys[k % 2]; f rows Fs[k % 2]
-//   group 1 (consumer, 256 threads): per 128-plane chunk of tile k: Z -> [C0, C0 + 2 SC);
-//       MMA2 -> D2 [C0 + 2 SC, C0 + 2 SC + TW), one issuing warp per 16-output N-tile
-//       (a single issuing warp sustains ~1 MMA per 60 cycles: tools/microbench/fir_tc.cu);
-//       drain + store; a remainder of <= 64 planes on the CUDA cores under the last MMAs
-// Ys / Fs are double-buffered between the groups with full / empty mbarriers, so the
-// features and y = M b of tile k + 1 run under the FIR of tile k.
-template <int RT, int GR>
-__global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tf(const HArgs a) {
-  extern __shared__ __align__(128) float sm[];
-  __shared__ uint64_t mma_bar, fir_bar, ys_full[2], ys_empty[2];
-  __shared__ uint32_t tmem_base;
-  const int R = RT > 0 ? RT : a.R;
-  const int m0 = a.m0, m0q = a.m0q, n = a.n, rho = a.rho, rhop = a.rhop, W = a.W, H = a.H;
-  const int NC = n + 1, L = m0 + 1, P = L * NC, pitch = a.pitch, TW = a.TW;
-  const int KU = a.ku, NU = a.nu, SC = a.sc, KW = a.kw, NT = TW / 16;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = tid / K2T_GROUP, gtid = tid % K2T_GROUP;
-  const int nfr = (NC + K2_CC - 1) / K2_CC * K2_CC;  // f rows: f_c, 1 (the y plane), 0 padding
-
-  float* Cs = sm;                                  // m0 x rhop
-  float* Bh = Cs + align32f(m0 * rhop);            // NU x KU, K-major core matrices (M^T, u0)
-  float* Bl = Bh + NU * KU;
-  float* Th = Bl + NU * KU;                         // 16 x KW Toeplitz band, K-major
-  float* Tl = Th + 16 * KW;
-  float* gbase = Tl + 16 * KW;                     // 2 buffers: Fs (nfr x pitch), Ys (m0q x pitch)
-  const int buf_floats = align32f(nfr * pitch) + m0q * pitch;
-  auto Fs_of = [&](int b) { return gbase + (size_t)b * buf_floats; };
-  auto Ys_of = [&](int b) { return gbase + (size_t)b * buf_floats + align32f(nfr * pitch); };
-
-  for (int k = tid; k < m0 * rhop; k += K2T_THREADS) Cs[k] = a.cst[k];
-  {
-    const float* MTg = a.cst + (size_t)m0 * rhop;  // MT[j][i] = M[i][j], MT[j][m0] = u0[j]
-    for (int k = tid; k < NU * KU; k += K2T_THREADS) {
-      const int i = k / KU, j = k - (k / KU) * KU;
-      const float v = (i < m0q && j < m0) ? MTg[(size_t)j * m0q + i] : 0.f;
-      const float h = umma::to_tf32(v);
-      const int o = umma::kmajor_offset(i, j, NU);
-      Bh[o] = h;
-      Bl[o] = umma::to_tf32(v - h);
-    }
-    for (int k = tid; k < 16 * KW; k += K2T_THREADS) {
-      const int o = k / KW, s = k - (k / KW) * KW, t = s - o;
-      const float v = (t >= 0 && t <= 2 * R) ? a.taps[t] : 0.f;
-      const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-      const int off = umma::kmajor_offset(o, s, 16);
-      Th[off] = h;
-      Tl[off] = v - h;
-    }
-  }
-  if (warp == 0) umma::tmem_alloc(&tmem_base, 512u);
-  if (tid == 0) {
-    umma::mbar_init(&mma_bar, 1);
-    umma::mbar_init(&fir_bar, (uint32_t)NT);  // one commit per N-tile issuer
-    for (int b = 0; b < 2; ++b) {
-      umma::mbar_init(&ys_full[b], 1);
-      umma::mbar_init(&ys_empty[b], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  umma::fence_proxy_async();  // B operands: generic-proxy writes -> tensor core
-  umma::fence_before();
-  __syncthreads();
-  umma::fence_after();
-  // a 512-column allocation covers the whole TMEM of the SM: its base is column 0, so every
-  // TMEM address below is a compile-time / kernel-parameter value (uniform registers, no
-  // per-MMA register-to-uniform moves in the issue loops)
-  if (tmem_base != 0u) __trap();
-  const int C0 = align32f(2 * KU + NU);
-  const uint32_t a_hi = 0u, a_lo = (uint32_t)KU, d1 = (uint32_t)(2 * KU);
-  const uint32_t z_hi = (uint32_t)C0, z_lo = z_hi + (uint32_t)SC, d2 = z_hi + (uint32_t)(2 * SC);
-  constexpr int KWC = RT > 0 ? ((16 + 2 * RT + 7) / 8) : 0;  // K steps of the FIR window (compile time)
-  const int q = warp & 3, hh = (warp >> 2) & 1;  // TMEM sub-partition (lanes 32q..) and half
-  const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-  const int px = 32 * q + lane;                  // source pixel / plane-in-chunk of this thread's lane
-  const int gw = gtid >> 5;                      // warp within the group
-  const int ncols = TW + 2 * R;
-  const int ntiles = a.tiles_x * a.vrows;
-  const int khalf = KU / 2;
-  const int nrem = P % 128;
-  const int nchunk = P / 128 + (nrem > 64 ? 1 : 0);
-  const int rem0 = nrem > 64 ? P : P - nrem;  // first CUDA-core plane
-  const int wpad = (W + 31) & ~31;
-  // debug (NYS_DBG_K2 bit 4): per-phase cycle totals of CTA 0, printed at the end
-  const bool stamp = (a.dbg & 16) && blockIdx.x == 0 && gtid == 0;
-  long long st_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long st_c = clock64();
-  auto tick = [&](int k) {
-    if (stamp) {
-      const long long c = clock64();
-      st_t[k] += c - st_c;
-      st_c = c;
-    }
-  };
-
-  if (g == 0) {
-    // ------------------------------ producer ------------------------------
-    uint32_t phase = 0;
-    int k = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-      const int b = k & 1;
-      const int vr = a.v0 + tile / a.tiles_x;
-      const int x0 = (tile % a.tiles_x) * TW;
-      const int row = clampi(clampi(vr, 0, H - 1), a.rlo, a.rhi - 1);
-      // 1. features of the tile's source pixels -> A_feat (b_hi, b_lo), raw b planes for K3
-      {
-        const int xs = x0 - R + px;
-        const int x = clampi(xs, 0, W - 1);
-        float gv[GR];
-#pragma unroll
-        for (int dd = 0; dd < GR; ++dd)
-          gv[dd] = dd < rho ? guide_at(a.g, a.gps, a.f, a.fps, a.gkind, dd, row, x, H, W) : 0.f;
-        float* bdst = nullptr;
-        if (a.bplanes && !a.phi && px >= R && px < R + TW && xs < wpad)
-          bdst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) + (long long)P * 32 +
-                 (xs & 31);
-        for (int j0 = hh * khalf; j0 < (hh + 1) * khalf; j0 += 4) {
-          float bv[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = j0 + e;
-            float v = 0.f;
-            if (j < m0) {
-              const float4* cj = reinterpret_cast<const float4*>(Cs + (size_t)j * rhop);
-              float d2v = 0.f;
-#pragma unroll
-              for (int d4 = 0; d4 < GR / 4; ++d4) {
-                if (4 * d4 < rho) {
-                  const float4 c4 = cj[d4];
-                  const float t0 = gv[4 * d4] - c4.x, t1 = gv[4 * d4 + 1] - c4.y;
-                  const float t2 = gv[4 * d4 + 2] - c4.z, t3 = gv[4 * d4 + 3] - c4.w;
-                  d2v = fmaf(t0, t0, d2v);
-                  d2v = fmaf(t1, t1, d2v);
-                  d2v = fmaf(t2, t2, d2v);
-                  d2v = fmaf(t3, t3, d2v);
-                }
-              }
-              v = range_kernel(d2v, a.k2);
-              if (bdst) bdst[(size_t)j * 32] = v;
-            }
-            bv[e] = v;
-          }
-          float hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            hi[e] = umma::to_tf32(bv[e]);
-            lo[e] = umma::to_tf32(bv[e] - hi[e]);
-          }
-          umma::st_32x32b_x4(a_hi + lane_base + (uint32_t)j0, hi[0], hi[1], hi[2], hi[3]);
-          umma::st_32x32b_x4(a_lo + lane_base + (uint32_t)j0, lo[0], lo[1], lo[2], lo[3]);
-        }
-        umma::st_wait();
-      }
-      tick(0);
-      umma::fence_before();
-      group_sync(0);
-      umma::fence_after();
-      tick(1);
-      // 2. y = M b (+ s0 = u0.b): 3 x KU/8 MMAs
-      if (gtid == 0) {
-        const uint32_t lbo_b = (uint32_t)NU * 16;
-        const uint64_t dBh = umma::desc_kmajor(Bh, lbo_b, 128), dBl = umma::desc_kmajor(Bl, lbo_b, 128);
-        const uint32_t id1 = idesc_fir1(NU);
-        const uint64_t kstep = (uint64_t)(8 * NU * 4 / 16);  // descriptor address units per K step
-        const int nk = KU / 8;
-#pragma unroll
-        for (int pass = 0; pass < 3; ++pass) {
-          const uint32_t A = pass == 2 ? a_lo : a_hi;
-          const uint64_t B = pass == 1 ? dBl : dBh;
-#pragma unroll
-          for (int kk = 0; kk < 32; ++kk)  // m0 <= 256: fully unrolled, predicated
-            if (kk < nk) umma::mma_tf32_ts(d1, A + 8u * kk, B + kk * kstep, id1, (pass | kk) ? 1u : 0u);
-        }
-        umma::commit(&mma_bar);
-      }
-      tick(2);
-      // the consumer must be done with buffer b (tile k - 2) before it is refilled
-      if (k >= 2) umma::mbar_wait_sleep(&ys_empty[b], (uint32_t)(((k >> 1) - 1) & 1));
-      float* Fs = Fs_of(b);
-      float* Ys = Ys_of(b);
-      for (int e = gtid; e < nfr * SC; e += K2T_GROUP) {  // f rows (+ the 1.0 row of the y planes)
-        const int c = e / SC, s = e - c * SC;
-        const int x = clampi(x0 - R + s, 0, W - 1);
-        Fs[(size_t)c * pitch + s] =
-            c < n ? __ldg(a.f + (long long)c * a.fps + (long long)row * W + x) : (c == n ? 1.f : 0.f);
-      }
-      tick(3);
-      umma::mbar_wait_sleep(&mma_bar, phase);
-      phase ^= 1u;
-      umma::fence_after();
-      tick(4);
-      // 3. drain y (lane = source pixel, column = landmark group) into the y rows
-      {
-        const int nch8 = NU / 8, c0 = hh * (nch8 / 2), c1 = hh ? nch8 : nch8 / 2;
-        for (int c = c0; c < c1; ++c) {
-          float v[8];
-          umma::ld_32x32b_x8(d1 + lane_base + (uint32_t)(8 * c), v);
-          umma::ld_wait();
-          if (px < SC) {  // columns past the tile's sources are zero (they meet zero taps only)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int i = 8 * c + e;
-              if (i < L) Ys[(size_t)i * pitch + px] = px < ncols ? v[e] : 0.f;
-            }
-          }
-          if (a.phi && a.bplanes && px >= R && px < R + TW) {  // phi-form: phi_i = y_i is K3's weight
-            const int xs = x0 - R + px;
-            if (xs < wpad) {
-              float* dst = a.hp + (long long)(vr - a.v0) * a.rs + (long long)(xs >> 5) * (a.npl * 32) +
-                           (long long)P * 32 + (xs & 31);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int i = 8 * c + e;
-                if (i < m0) dst[(size_t)i * 32] = v[e];
-              }
-            }
-          }
-        }
-      }
-      tick(5);
-      umma::fence_before();
-      group_sync(0);  // D1 drained (A_feat / D1 free), Ys / Fs written
-      if (gtid == 0) {
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(umma::smem_addr(&ys_full[b]))
-                     : "memory");
-      }
-      umma::fence_after();
-      tick(6);
-    }
-    if (stamp)
-      printf("K2TF producer cta0: feat %lld sync %lld m1issue %lld empty+fs %lld m1wait %lld drain %lld sync %lld\n",
-             st_t[0], st_t[1], st_t[2], st_t[3], st_t[4], st_t[5], st_t[6]);
-  } else {
-    // ------------------------------ consumer ------------------------------
-    uint32_t fphase = 0;
-    int k = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-      const int b = k & 1;
-      const int vr = a.v0 + tile / a.tiles_x;
-      const int x0 = (tile % a.tiles_x) * TW;
-      tick(0);
-      umma::mbar_wait_sleep(&ys_full[b], (uint32_t)((k >> 1) & 1));
-      tick(1);
-      const float* Fs = Fs_of(b);
-      const float* Ys = Ys_of(b);
-      float* hrow = a.hp + (long long)(vr - a.v0) * a.rs;
-      auto cuda_fir = [&](int p_lo, int p_hi) {  // planes [p_lo, p_hi) on the CUDA cores, 4 outputs per item
-        const int nxg = TW / 4, items = (p_hi - p_lo) * nxg;
-        const int T = 2 * R + 1;
-        for (int it = gtid; it < items; it += K2T_GROUP) {
-          const int pr = p_lo + it / nxg, xg = it - (it / nxg) * nxg;
-          const int xo = x0 + 4 * xg;
-          if (xo >= wpad) continue;
-          const int ir = pr / NC, cr = pr - (pr / NC) * NC;
-          const float* yr = Ys + (size_t)ir * pitch + 4 * xg;
-          const float* fr = Fs + (size_t)cr * pitch + 4 * xg;
-          float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-          float z0 = yr[0] * fr[0], z1 = yr[1] * fr[1], z2 = yr[2] * fr[2];
-          for (int t = 0; t < T; ++t) {  // sliding window of 4 outputs
-            const float z3 = yr[t + 3] * fr[t + 3];
-            const float w = a.taps[t];
-            o0 = fmaf(w, z0, o0);
-            o1 = fmaf(w, z1, o1);
-            o2 = fmaf(w, z2, o2);
-            o3 = fmaf(w, z3, o3);
-            z0 = z1;
-            z1 = z2;
-            z2 = z3;
-          }
-          *reinterpret_cast<float4*>(hrow + (long long)(xo >> 5) * (a.npl * 32) + (long long)pr * 32 + (xo & 31)) =
-              make_float4(o0, o1, o2, o3);
-        }
-      };
-      for (int ck = 0; ck < nchunk; ++ck) {
-        const int pl = ck * 128 + px;  // this lane's plane
-        {
-          const bool valid = pl < P;
-          const int i = valid ? pl / NC : 0, c = valid ? pl - (pl / NC) * NC : 0;
-          const float* yr = Ys + (size_t)i * pitch;
-          const float* fr = Fs + (size_t)c * pitch;
-          const int s_lo = hh * (SC / 2), s_hi = s_lo + SC / 2;  // warp halves: source column halves
-          for (int s0 = s_lo; s0 < s_hi; s0 += 16) {
-            float zh[16], zl[16];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 y4 = *reinterpret_cast<const float4*>(yr + s0 + 4 * u);
-              const float4 f4 = *reinterpret_cast<const float4*>(fr + s0 + 4 * u);
-              const float zz[4] = {y4.x * f4.x, y4.y * f4.y, y4.z * f4.z, y4.w * f4.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float z = valid ? zz[e] : 0.f;
-                zh[4 * u + e] = z;  // raw bits: the MMA reads them as TF32 (truncation)
-                zl[4 * u + e] = z - __uint_as_float(__float_as_uint(z) & 0xffffe000u);
-              }
-            }
-            umma::st_32x32b_x16(z_hi + lane_base + (uint32_t)s0, zh);
-            umma::st_32x32b_x16(z_lo + lane_base + (uint32_t)s0, zl);
-          }
-          umma::st_wait();
-        }
-        tick(2);
-        umma::fence_before();
-        group_sync(1);
-        umma::fence_after();
-        tick(3);
-        if (gw < NT && lane == 0) {
-          const uint64_t dTh = umma::desc_kmajor(Th, 16 * 16, 128), dTl = umma::desc_kmajor(Tl, 16 * 16, 128);
-          constexpr int KM = KWC > 0 ? KWC : 16;
-          const int nk = KWC > 0 ? KWC : KW / 8;
-          switch (gw) {
-            case 0: fir_tile_mma<0, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-            case 1: fir_tile_mma<1, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-            case 2: fir_tile_mma<2, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-            case 3: fir_tile_mma<3, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-            case 4: fir_tile_mma<4, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-            case 5: fir_tile_mma<5, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-            default: fir_tile_mma<6, KM>(z_hi, z_lo, d2, dTh, dTl, nk); break;
-          }
-          umma::commit(&fir_bar);
-        }
-        tick(4);
-        if (ck == nchunk - 1 && rem0 < P) cuda_fir(rem0, P);  // remainder planes under the last MMAs
-        tick(5);
-        umma::mbar_wait_sleep(&fir_bar, fphase);
-        fphase ^= 1u;
-        umma::fence_after();
-        tick(6);
-        // drain: this lane's plane, N-tiles split between the warp halves; 16 contiguous outputs
-        // per thread (the aligned tcgen05.ld runs warp-uniformly, only the stores are masked)
-        for (int j = hh; j < NT; j += 2) {
-          const int xo = x0 + 16 * j;
-          float v[16];
-          umma::ld_32x32b_x16(d2 + lane_base + (uint32_t)(16 * j), v);
-          umma::ld_wait();
-          if (pl < P && xo < wpad) {
-            float4* dst =
-                reinterpret_cast<float4*>(hrow + (long long)(xo >> 5) * (a.npl * 32) + (long long)pl * 32 + (xo & 31));
-#pragma unroll
-            for (int u = 0; u < 4; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-          }
-        }
-        umma::fence_before();
-        group_sync(1);  // D2 drained, Z columns free
-        umma::fence_after();
-        tick(7);
-      }
-      if (nchunk == 0) {  // fewer than 65 planes: all on the CUDA cores
-        cuda_fir(0, P);
-        group_sync(1);
-      }
-      if (gtid == 0) {
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(umma::smem_addr(&ys_empty[b]))
-                     : "memory");
-      }
-    }
-    if (stamp)
-      printf("K2TF consumer cta0: rest %lld wait_full %lld Z %lld sync %lld issue %lld remainder %lld wait_mma %lld drain %lld\n",
-             st_t[0], st_t[1], st_t[2], st_t[3], st_t[4], st_t[5], st_t[6], st_t[7]);
-  }
-  umma::fence_before();
-  __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tmem_base, 512u);
-}
-
-// Tensor-FIR tile geometry: TW outputs (multiple of 16), SC = TW + 2R source samples rounded
-// up to 16; per group 2 SC (Z hi / lo) + TW (D2) <= 256 TMEM columns and the feature stage's
-// 2 KU + NU <= 256; SC <= 128 (the feature MMA's M).
-int launch_hpass_tf(HArgs& a, const nys_filter_desc* d, cudaStream_t s) {
-  if (a.box) return NYS_EUNSUPPORTED;  // the box's running sums cost ~2 FLOP per output on CUDA cores
-  const int R = d->radius;
-  const int KU = (int)ceil_div(d->m0, 8) * 8;
-  const int NU = (int)ceil_div(d->m0 + 1, 16) * 16;
-  const int C0 = align32f(2 * KU + NU);  // producer columns (A_feat, D1); the consumer's follow
-  const int KW = (int)ceil_div(16 + 2 * R, 8) * 8;
-  int TW = 0, SC = 0;
-  for (int tw = 112; tw >= 16; tw -= 16) {
-    const int sc = (int)ceil_div(tw + 2 * R, 32) * 32;  // halves of 16-column stores per warp half
-    if (sc <= 128 && C0 + 2 * sc + tw <= 512 && tw - 16 + KW <= sc && tw / 16 <= K2T_GROUP / 32) {
-      TW = tw;
-      SC = sc;
-      break;
-    }
-  }
-  if (!TW) return NYS_EUNSUPPORTED;
-  int pitch = (int)ceil_div(SC + 4, 4) * 4;
-  pitch += ((4 - pitch % 32) + 32) % 32;  // = 4 (mod 32): conflict-free LDS.128 across rows
-  const int nfr = (int)ceil_div(d->n + 1, K2_CC) * K2_CC;
-  const size_t fixed = (size_t)align32f(d->m0 * a.rhop) + 2 * (size_t)NU * KU + 2 * (size_t)16 * KW;
-  const size_t buf = (size_t)align32f(nfr * pitch) + (size_t)a.m0q * pitch;
-  const size_t smem = (fixed + 2 * buf) * 4;
-  if (smem > 225 * 1024) return NYS_EUNSUPPORTED;
-  a.TW = TW;
-  a.rpt = 1;
-  a.pitch = pitch;
-  a.tiles_x = (int)ceil_div(d->W, TW);
-  a.ku = KU;
-  a.nu = NU;
-  a.sc = SC;
-  a.kw = KW;
-  const long long ntiles = (long long)a.tiles_x * a.vrows;
-  const int GR = d->rho <= 4 ? 4 : (d->rho <= 16 ? 16 : (d->rho <= 32 ? 32 : 64));
-  auto go = [&](auto kern) -> int {
-    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NYS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    const int grid = (int)std::min<long long>(ntiles, (long long)num_sms());
-    count_launch();
-    kern<<<grid, K2T_THREADS, smem, s>>>(a);
-    NYS_LAUNCH_CHECK();
-    return NYS_OK;
-  };
-#define NYS_TF_GR(RV)                                      \
-  switch (GR) {                                            \
-    case 4: return go(k_feat_hpass_tf<RV, 4>);             \
-    case 16: return go(k_feat_hpass_tf<RV, 16>);           \
-    case 32: return go(k_feat_hpass_tf<RV, 32>);           \
-    default: return go(k_feat_hpass_tf<RV, 64>);           \
-  }
-  switch (R) {
-    case 9: NYS_TF_GR(9)
-    case 12: NYS_TF_GR(12)
-    case 15: NYS_TF_GR(15)
-    case 18: NYS_TF_GR(18)
-    default: NYS_TF_GR(0)
-  }
-#undef NYS_TF_GR
 }
 
 // Features of a wide guide (rho > NYS_MAX_RHO) for every virtual row of the band, written as

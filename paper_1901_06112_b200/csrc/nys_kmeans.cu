@@ -954,9 +954,6 @@ static int launch_assign(const float* pts, long long ps, long long m, int rho, c
   return NYS_OK;
 }
 
-int launch_assign_tc(const float* pts, long long ps, long long m, int rho, const float* Cf, int m0, int* labels,
-                     int first, double* part, int nb, int S, const KState* st, cudaStream_t s);
-
 static int check_common(const float* pts, int64_t m, int rho, int m0, void* ws, size_t wsb) {
   if (!pts || m < 1 || rho < 1 || rho > NYS_MAX_RHO_WIDE || m0 < 1 || m0 > NYS_MAX_M0 || m0 > m) return NYS_EINVAL;
   if (!ws || wsb < klayout(m, rho, m0).total) return NYS_EINVAL;
@@ -973,20 +970,13 @@ static int run_lloyd_and_final(const float* pts, int64_t ps, int64_t m, int rho,
   float* Cf = reinterpret_cast<float*>(ws + L.off_cf);
   double* Cprev = reinterpret_cast<double*>(ws + L.off_cprev);
   long long* excl = reinterpret_cast<long long*>(ws + L.off_excl);
-  // NYS_KM_TC=1 (rho >= 16): step-wise Lloyd with the tcgen05 distance filter (k_assign_tc); measured
-  // slower than the bounded cooperative kernel (nys_kmeans_tc.cu), so opt-in
-  const char* tce = getenv("NYS_KM_TC");
-  const bool use_tc = rho >= 16 && tce && atoi(tce) == 1;
-  int rc = use_tc ? NYS_EUNSUPPORTED : launch_lloyd_coop(pts, ps, m, rho, m0, max_iter, C, errors, ws, L, s, prezeroed);
+  int rc = launch_lloyd_coop(pts, ps, m, rho, m0, max_iter, C, errors, ws, L, s, prezeroed);
   if (rc != NYS_OK && rc != NYS_EUNSUPPORTED) return rc;
-  if (rc == NYS_EUNSUPPORTED) {  // step-wise (tensor-core assignment, or no cooperative launch)
+  if (rc == NYS_EUNSUPPORTED) {  // step-wise (wide guides, or no cooperative launch)
     count_launch(); k_c_to_f<<<1, 256, 0, s>>>(C, Cf, m0 * rho);
     NYS_LAUNCH_CHECK();
     for (int it = 0; it < max_iter; ++it) {
-      rc = use_tc ? launch_assign_tc(pts, ps, m, rho, Cf, m0, labels, it == 0, part, L.nb_assign, L.S, st, s)
-                  : NYS_EUNSUPPORTED;
-      if (rc == NYS_EUNSUPPORTED)
-        rc = launch_assign(pts, ps, m, rho, Cf, m0, labels, it == 0, part, L.nb_assign, L.S, st, s);
+      rc = launch_assign(pts, ps, m, rho, Cf, m0, labels, it == 0, part, L.nb_assign, L.S, st, s);
       if (rc) return rc;
       count_launch(); k_reduce<<<(int)ceil_div(L.S, 256), 256, 0, s>>>(part, L.nb_assign, L.S, tot, st);
       count_launch(); k_finalize<<<1, 256, 0, s>>>(tot, m0, rho, it, C, Cprev, Cf, errors, st);

@@ -298,239 +298,6 @@ __global__ void __launch_bounds__(REC_COL_MAX_THREADS, 1) k_rec_cols(const float
 }
 
 // ---------------------------------------------------------------------------
-// Shared-memory path (RV + RH), used when a column strip and a row fit in SMEM.
-// The row and column recursions are fixed linear operators on each axis, so
-// they commute exactly: the column pass runs first (RV, straight from the
-// features) and the row pass last (RH), fused with the contraction, the mass^2
-// scale, the guard and the division -- one plane-sized intermediate in HBM
-// instead of five plane passes.
-//
-// Lines held in shared memory are recursed block-parallel: a line of N samples
-// is cut into S segments of L samples; every (line, segment) thread runs the
-// recursion from a zero state, one thread per line then carries the true
-// states across the segments (state' = zero-state tail + Hh * state, Hh the
-// zero-input responses to unit states), and every (line, segment) thread adds
-// Hh * state to its samples.  Same recurrence, same boundary rules
-// (spatial.py:149-176): forward state = the edge input sample, backward state =
-// the forward output's edge sample.  FP64 states, FP32 samples.
-// ---------------------------------------------------------------------------
-__device__ void iir_lines(float* base, int nl, int N, int ls, int S, int L, const double* Hh, const RecCoeffs& cf,
-                          double* zt, double* st, double* e0) {
-  const int nt = nl * S;
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool rev = pass == 1;
-    if (!rev)
-      for (int l = threadIdx.x; l < nl; l += blockDim.x) e0[l] = (double)base[(size_t)l * ls];  // edge input
-    __syncthreads();
-    for (int w = threadIdx.x; w < nt; w += blockDim.x) {  // zero-state recursion per segment
-      const int l = w % nl, sg = w / nl;
-      const int i0 = sg * L, i1 = min(N, i0 + L);
-      float* line = base + (size_t)l * ls;
-      RecState r;
-      r.init(0.0);
-      for (int i = i0; i < i1; ++i) {
-        const int j = rev ? N - 1 - i : i;
-        line[j] = (float)r.step(cf, (double)line[j]);
-      }
-      double* z = zt + (size_t)(l * S + sg) * 5;
-      z[0] = r.w1;
-      z[1] = r.w2;
-      z[2] = r.w3;
-      z[3] = r.w4;
-      z[4] = r.w5;
-    }
-    __syncthreads();
-    for (int l = threadIdx.x; l < nl; l += blockDim.x) {  // carry the true states across segments
-      double s5[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) s5[k] = e0[l];
-      for (int sg = 0; sg < S; ++sg) {
-        double* sp = st + (size_t)(l * S + sg) * 5;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) sp[k] = s5[k];
-        const int len = min(N, (sg + 1) * L) - sg * L;
-        const double* z = zt + (size_t)(l * S + sg) * 5;
-        double nw[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-          if (q < len) {
-            const double* h = Hh + (size_t)(len - 1 - q) * 5;
-            double v = z[q];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) v = fma(h[k], s5[k], v);
-            nw[q] = v;
-          } else {
-            nw[q] = s5[q - len];
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 5; ++k) s5[k] = nw[k];
-      }
-      e0[l] = s5[0];  // the pass's last output: the backward pass starts from it
-    }
-    __syncthreads();
-    for (int w = threadIdx.x; w < nt; w += blockDim.x) {  // add the responses to the true states
-      const int l = w % nl, sg = w / nl;
-      const int i0 = sg * L, i1 = min(N, i0 + L);
-      float* line = base + (size_t)l * ls;
-      const double* sp = st + (size_t)(l * S + sg) * 5;
-      const double s0 = sp[0], s1 = sp[1], s2 = sp[2], s3 = sp[3], s4 = sp[4];
-      for (int i = i0; i < i1; ++i) {
-        const int j = rev ? N - 1 - i : i;
-        const double* h = Hh + (size_t)(i - i0) * 5;
-        const double v = fma(h[4], s4, fma(h[3], s3, fma(h[2], s2, fma(h[1], s1, fma(h[0], s0, (double)line[j])))));
-        line[j] = (float)v;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-struct RecSmem {  // shared-memory carve-up common to RV / RH
-  double *Hh, *zt, *st, *e0;
-  float* buf;
-};
-__device__ __forceinline__ RecSmem rec_smem(void* raw, int Lmax, int nl, int S) {
-  RecSmem m;
-  m.Hh = static_cast<double*>(raw);
-  m.zt = m.Hh + (size_t)Lmax * 5;
-  m.st = m.zt + (size_t)nl * S * 5;
-  m.e0 = m.st + (size_t)nl * S * 5;
-  m.buf = reinterpret_cast<float*>(m.e0 + ((nl + 1) & ~1));
-  return m;
-}
-
-// RV: column recursion of planes (g, c0..c0+ncp-1) over a strip of xw columns,
-// straight from the planar features: v = y_g f_c (c < n) or y_g (c == n).
-// Output: planar I[g*(n+1)+c][px].
-__global__ void __launch_bounds__(256) k_recv(const float* __restrict__ Yp, const float* __restrict__ f, long long fps,
-                                              int n, int H, int W, int xw, int cpp, RecCoeffs cf,
-                                              const double* __restrict__ Hh_g, int Lmax, int S, int L,
-                                              float* __restrict__ I) {
-  extern __shared__ __align__(16) double rvm[];
-  const int x0 = blockIdx.x * xw, g = blockIdx.y, c0 = blockIdx.z * cpp;
-  const int ncp = min(cpp, n + 1 - c0);
-  const int nl = xw * ncp, ls = H + 1;
-  const long long npx = (long long)H * W;
-  RecSmem m = rec_smem(rvm, Lmax, nl, S);
-  for (int k = threadIdx.x; k < Lmax * 5; k += blockDim.x) m.Hh[k] = Hh_g[k];
-  const float* yg = Yp + (long long)g * npx;
-  constexpr int U = 8;  // independent loads in flight per thread
-  for (int e0 = threadIdx.x; e0 < H * nl; e0 += U * blockDim.x) {
-    float yv[U], fv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      const int cp = e % ncp, rest = e / ncp, col = rest % xw, row = rest / xw;
-      const int x = x0 + col, c = c0 + cp;
-      const bool ok = e < H * nl && x < W;
-      const long long p = (long long)row * W + x;
-      yv[u] = ok ? __ldg(yg + p) : 0.f;
-      fv[u] = (ok && c < n) ? __ldg(f + (long long)c * fps + p) : 1.f;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e < H * nl) {
-        const int cp = e % ncp, rest = e / ncp, col = rest % xw, row = rest / xw;
-        m.buf[(size_t)(col * ncp + cp) * ls + row] = yv[u] * fv[u];
-      }
-    }
-  }
-  __syncthreads();
-  iir_lines(m.buf, nl, H, ls, S, L, m.Hh, cf, m.zt, m.st, m.e0);
-  for (int e = threadIdx.x; e < H * nl; e += blockDim.x) {
-    const int cp = e % ncp, rest = e / ncp, col = rest % xw, row = rest / xw;
-    const int x = x0 + col;
-    if (x < W) I[(long long)(g * (n + 1) + c0 + cp) * npx + (long long)row * W + x] = m.buf[(size_t)(col * ncp + cp) * ls + row];
-  }
-}
-
-// RH: row recursion of every plane of one row (groups in batches of gbat),
-// contraction with b_g(x) (lead group: s0(x)/alpha0), then the mass^2 scale,
-// guard, division and statistics for channels [4k, 4k+nc) of the row.
-__global__ void __launch_bounds__(256) k_rech(const float* __restrict__ I, const float* __restrict__ Yp,
-                                              const float* __restrict__ Bp, const float* __restrict__ f,
-                                              long long fps, int n, int H, int W, int m0, int gbat, RecCoeffs cf,
-                                              const double* __restrict__ Hh_g, int Lmax, int S, int L,
-                                              float inv_alpha0, float mass2, float eps, float* __restrict__ out,
-                                              long long ops, FilterStats* __restrict__ stats) {
-  extern __shared__ __align__(16) double rhm[];
-  const int r = blockIdx.x, c0 = 4 * blockIdx.y;
-  const int nc = min(4, n - c0), LG = nc + 1;  // line cl < nc: channel c0 + cl; cl == nc: the "1" plane (c = n)
-  const int nlmax = gbat * LG, ls = W + 1;
-  const long long npx = (long long)H * W, rowp = (long long)r * W;
-  RecSmem m = rec_smem(rhm, Lmax, nlmax, S);
-  float* acc = m.buf + (size_t)nlmax * ls;  // [LG][W] landmark sums
-  float* lead = acc + (size_t)LG * W;       // [LG][W] lead terms
-  for (int k = threadIdx.x; k < Lmax * 5; k += blockDim.x) m.Hh[k] = Hh_g[k];
-  for (int k = threadIdx.x; k < LG * W; k += blockDim.x) acc[k] = lead[k] = 0.f;
-  for (int g0 = 0; g0 <= m0; g0 += gbat) {
-    const int gb = min(gbat, m0 + 1 - g0), nl = gb * LG;
-    for (int e = threadIdx.x; e < nl * W; e += blockDim.x) {
-      const int l = e / W, x = e - l * W, gl = l / LG, cl = l - gl * LG;
-      const int c = cl < nc ? c0 + cl : n;
-      m.buf[(size_t)l * ls + x] = __ldg(I + (long long)((g0 + gl) * (n + 1) + c) * npx + rowp + x);
-    }
-    __syncthreads();
-    iir_lines(m.buf, nl, W, ls, S, L, m.Hh, cf, m.zt, m.st, m.e0);
-    for (int x = threadIdx.x; x < W; x += blockDim.x) {
-      for (int gl = 0; gl < gb; ++gl) {
-        const int g = g0 + gl;
-        const float* bl = m.buf + (size_t)gl * LG * ls + x;
-        if (g < m0) {
-          const float w = __ldg(Bp + (long long)g * npx + rowp + x);
-          for (int cl = 0; cl < LG; ++cl) acc[cl * W + x] = fmaf(w, bl[(size_t)cl * ls], acc[cl * W + x]);
-        } else {
-          const float s0 = __ldg(Yp + (long long)m0 * npx + rowp + x) * inv_alpha0;  // s0 conv(s0 f)/alpha0
-          for (int cl = 0; cl < LG; ++cl) lead[cl * W + x] = s0 * bl[(size_t)cl * ls];
-        }
-      }
-    }
-    __syncthreads();
-  }
-  float my_min = INFINITY;
-  unsigned long long my_cnt = 0;
-  for (int x = threadIdx.x; x < W; x += blockDim.x) {
-    const float eta = acc[nc * W + x] * mass2, eta_l = lead[nc * W + x] * mass2;
-    const float ae = fabsf(eta);
-    my_min = fminf(my_min, ae);
-    const bool guarded = ae < eps;
-    my_cnt += guarded ? 1ull : 0ull;
-    for (int cl = 0; cl < nc; ++cl) {
-      float v;
-      if (!guarded)
-        v = (acc[cl * W + x] * mass2) / eta;
-      else if (fabsf(eta_l) >= eps)
-        v = (lead[cl * W + x] * mass2) / eta_l;
-      else
-        v = __ldg(f + (long long)(c0 + cl) * fps + rowp + x);
-      out[(long long)(c0 + cl) * ops + rowp + x] = v;
-    }
-  }
-  if (blockIdx.y != 0) return;  // statistics once per pixel
-  __shared__ float smin[8];
-  __shared__ unsigned long long scnt[8];
-  my_min = warp_min(my_min);
-  my_cnt = warp_sum_u64(my_cnt);
-  if ((threadIdx.x & 31) == 0) {
-    smin[threadIdx.x >> 5] = my_min;
-    scnt[threadIdx.x >> 5] = my_cnt;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float mn = INFINITY;
-    unsigned long long cn = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      mn = fminf(mn, smin[w]);
-      cn += scnt[w];
-    }
-    atomicMin(&stats->min_abs_eta_bits, __float_as_uint(mn));
-    if (cn) atomicAdd(&stats->guarded, cn);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // R4: (fir_mass)^2 scale (spatial.py:189-191), guard and division
 // (filters.py:241-257), min|eta| and the guarded-pixel count.
 // ---------------------------------------------------------------------------
@@ -597,83 +364,6 @@ int rec_groups_fit(const nys_filter_desc* d, size_t scratch_bytes) {
   return nb;
 }
 
-// shared-memory path plan (RV column strips, RH row batches); ok == false -> banded global path
-struct RecPlan {
-  bool ok;
-  int xw, cpp, Sv, Lv, gbat, Sh, Lh, Lmax;
-  size_t smem_v, smem_h, scratch;
-};
-
-inline size_t rec_smem_bytes(int Lmax, int nl, int S, size_t floats) {
-  return (size_t)Lmax * 5 * 8 + 2 * (size_t)nl * S * 5 * 8 + (size_t)((nl + 1) & ~1) * 8 + floats * 4;
-}
-
-inline void seg_plan(int N, int nl, int& S, int& L) {
-  S = std::max(1, std::min(64, 256 / std::max(1, nl)));
-  L = (int)ceil_div(N, S);
-  S = (int)ceil_div(N, L);
-}
-
-inline RecPlan rec_plan(const nys_filter_desc* d) {
-  RecPlan p{};
-  // opt-in (NYS_REC_PATH=shared): measured slower than the banded global path on cfg 2
-  // (RV 7 ms + RH 12 ms vs 10 ms; instruction-bound at one CTA per SM), kept with its A/B test
-  const char* e = getenv("NYS_REC_PATH");
-  if (!e || std::string(e) != "shared") return p;
-  const int H = d->H, W = d->W, LG = std::min(4, d->n) + 1;
-  p.cpp = 2;
-  const size_t vmax = 112 * 1024, hmax = 220 * 1024;
-  for (int xw = 8; xw >= 1 && !p.xw; xw /= 2) {
-    const int nl = xw * p.cpp;
-    int S, L;
-    seg_plan(H, nl, S, L);
-    if (rec_smem_bytes(std::max(L, 1), nl, S, (size_t)nl * (H + 1)) + 64 * 5 * 8 <= vmax) {
-      p.xw = xw;
-      p.Sv = S;
-      p.Lv = L;
-    }
-  }
-  for (int gb = 4; gb >= 1 && !p.gbat; --gb) {
-    const int nl = gb * LG;
-    int S, L;
-    seg_plan(W, nl, S, L);
-    if (rec_smem_bytes(std::max(L, 1), nl, S, (size_t)nl * (W + 1) + 2 * (size_t)LG * W) + 64 * 5 * 8 <= hmax) {
-      p.gbat = gb;
-      p.Sh = S;
-      p.Lh = L;
-    }
-  }
-  if (!p.xw || !p.gbat) return p;
-  p.Lmax = std::max(p.Lv, p.Lh);
-  p.smem_v = rec_smem_bytes(p.Lmax, p.xw * p.cpp, p.Sv, (size_t)p.xw * p.cpp * (H + 1));
-  p.smem_h = rec_smem_bytes(p.Lmax, p.gbat * LG, p.Sh, (size_t)p.gbat * LG * (W + 1) + 2 * (size_t)LG * W);
-  if (p.smem_v > 220 * 1024 || p.smem_h > 226 * 1024) return p;
-  const size_t npx = (size_t)H * W, P = (size_t)(d->m0 + 1) * (d->n + 1);
-  p.scratch = align256(npx * (d->m0 + 1) * 4) + align256(npx * d->m0 * 4) + align256(npx * P * 4) +
-              align256((size_t)p.Lmax * 5 * 8);
-  p.ok = true;
-  return p;
-}
-
-// zero-input responses of the recursion to unit states (state k = output k+1 steps back)
-inline void rec_homogeneous(const RecCoeffs& c, int Lmax, std::vector<double>& Hh) {
-  Hh.assign((size_t)Lmax * 5, 0.0);
-  for (int k = 0; k < 5; ++k) {
-    double w[5] = {0, 0, 0, 0, 0};
-    w[k] = 1.0;
-    for (int i = 0; i < Lmax; ++i) {
-      const double t = c.a5 * w[4] + c.a4 * w[3] + c.a3 * w[2] + c.a2 * w[1];
-      const double cur = -(c.a1 * w[0] + t);
-      Hh[(size_t)i * 5 + k] = cur;
-      w[4] = w[3];
-      w[3] = w[2];
-      w[2] = w[1];
-      w[1] = w[0];
-      w[0] = cur;
-    }
-  }
-}
-
 int rec_validate(const nys_filter_desc* d) {
   const int st = validate(d);
   if (!st && (d->rho > NYS_MAX_RHO || d->n > NYS_MAX_CHANNELS)) return NYS_EUNSUPPORTED;  // register-resident R1
@@ -689,10 +379,6 @@ extern "C" {
 
 size_t nys_filter_recursive_scratch_bytes(const nys_filter_desc* d, int groups_per_band) {
   if (rec_validate(d) != NYS_OK) return 0;
-  if (groups_per_band <= 0) {  // preferred: the shared-memory path when a strip and a row fit
-    const RecPlan p = rec_plan(d);
-    if (p.ok) return p.scratch;
-  }
   const int G = d->m0 + 1;
   int nb = groups_per_band <= 0 ? G : std::min(groups_per_band, G);
   nb = std::min(nb, REC_COL_MAX_THREADS / (d->n + 1));
@@ -715,52 +401,6 @@ int nys_filter_recursive(const nys_filter_desc* d, const float* f, int64_t f_pla
   double mass = 0.0;
   for (int t = -Rm; t <= Rm; ++t) mass += std::exp(-((double)t * t) / (2.0 * d->sigma * d->sigma));
   const FilterLayout L = filter_layout(d);
-  const RecPlan plan = rec_plan(d);
-  if (plan.ok && scratch_bytes >= plan.scratch) {
-    // shared-memory path: R1 (planar) -> RV (columns) -> RH (rows + contraction + guard)
-    const size_t npx = (size_t)d->H * d->W;
-    char* sc = static_cast<char*>(scratch);
-    float* Yp = reinterpret_cast<float*>(sc);
-    float* Bp = reinterpret_cast<float*>(sc + align256(npx * (d->m0 + 1) * 4));
-    float* I = reinterpret_cast<float*>(sc + align256(npx * (d->m0 + 1) * 4) + align256(npx * d->m0 * 4));
-    double* Hh_d = reinterpret_cast<double*>(sc + align256(npx * (d->m0 + 1) * 4) + align256(npx * d->m0 * 4) +
-                                             align256(npx * (size_t)(d->m0 + 1) * (d->n + 1) * 4));
-    std::vector<double> Hh;
-    rec_homogeneous(cf, plan.Lmax, Hh);
-    cudaStream_t s = (cudaStream_t)stream;
-    NYS_CUDA_TRY(cudaMemcpyAsync(Hh_d, Hh.data(), Hh.size() * 8, cudaMemcpyHostToDevice, s));  // staged: Hh may go
-    const float* consts = static_cast<const float*>(workspace);
-    const float* g = d->guide_kind == 0 ? guide : f;
-    {
-      const int BS = d->m0 <= 96 ? 128 : 64;
-      const bool csm = d->m0 <= 96;
-      const size_t smem = ((size_t)d->rho * BS + (size_t)(2 * d->m0 + 1) * (BS + 1) +
-                           (csm ? (size_t)d->m0 * (L.rhop + L.m0q) + 4 : 0)) * sizeof(float);
-      auto k = csm ? k_rec_features<128, true, true> : k_rec_features<64, false, true>;
-      NYS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      count_launch();
-      k<<<(unsigned)ceil_div((long long)npx, BS), BS, smem, s>>>(f, f_plane_stride, g, guide_plane_stride,
-                                                                 d->guide_kind, d->rho, d->H, d->W, d->m0,
-                                                                 consts + L.off_C, L.rhop, L.m0q,
-                                                                 (long long)(L.off_MT - L.off_C), k2_of(d), Yp, Bp,
-                                                                 d->phi_form);
-      NYS_LAUNCH_CHECK();
-    }
-    NYS_CUDA_TRY(cudaFuncSetAttribute(k_recv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_v));
-    count_launch();
-    k_recv<<<dim3((unsigned)ceil_div(d->W, plan.xw), (unsigned)(d->m0 + 1), (unsigned)ceil_div(d->n + 1, plan.cpp)),
-             256, plan.smem_v, s>>>(Yp, f, f_plane_stride, d->n, d->H, d->W, plan.xw, plan.cpp, cf, Hh_d,
-                                    plan.Lmax, plan.Sv, plan.Lv, I);
-    NYS_LAUNCH_CHECK();
-    NYS_CUDA_TRY(cudaFuncSetAttribute(k_rech, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_h));
-    count_launch();
-    k_rech<<<dim3((unsigned)d->H, (unsigned)ceil_div(d->n, 4)), 256, plan.smem_h, s>>>(
-        I, Yp, Bp, f, f_plane_stride, d->n, d->H, d->W, d->m0, plan.gbat, cf, Hh_d, plan.Lmax, plan.Sh, plan.Lh,
-        (float)(1.0 / d->alpha0), (float)(mass * mass), (float)d->eps_den, out, out_plane_stride,
-        reinterpret_cast<FilterStats*>((char*)workspace + L.stats_off_bytes));
-    NYS_LAUNCH_CHECK();
-    return NYS_OK;
-  }
   const int nb_max = rec_groups_fit(d, scratch_bytes);
   if (nb_max < 1) return NYS_EINVAL;
   const RecScratch S = rec_scratch(d, nb_max);

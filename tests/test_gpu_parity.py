@@ -344,32 +344,6 @@ def test_seeding_runs_match_owner_handoff(rho, m, m0, monkeypatch):
         assert np.array_equal(pts.T.astype(np.float64)[a.seed_indices], seeds)
 
 
-@pytest.mark.parametrize("shape,n", [((72, 128), 3), ((40, 52), 7), ((5, 3), 2), ((130, 9), 1)])
-def test_recursive_shared_path_matches_global_path(shape, n, monkeypatch):
-    # the opt-in shared-memory RV/RH path (columns first, rows fused with the contraction)
-    # against the default banded global-memory path and the oracle
-    H, W = shape
-    f32 = spectral_scene(H, W, n, 5, 0.03, seed=H + n) if n > 3 else np.ascontiguousarray(
-        color_scene(H, W, 5, 0.05, seed=H + n)[:n])
-    f64 = f32.astype(np.float64)
-    # well-conditioned landmark kernels: a 1-D guide with 5 landmarks at theta 0.35 already has
-    # cond(A) = 6e6, where the FP32 y-form misses 1e-4 on the FIR and recursive paths alike
-    # (tools/dbg_rec.py); the BASELINE configs have cond(A) <= 252
-    m0, theta = (9, 0.2) if n > 1 else (3, 0.5)
-    C, _, _, _ = O.kmeans(O.range_vectors(f64), m0, 0, 6)
-    params = FilterParams(spatial=SpatialKernel.recursive(2.5), theta=theta, m0=m0)
-    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
-    monkeypatch.setenv("NYS_REC_PATH", "shared")
-    a = filter_with_landmarks(f, f, C, params)
-    monkeypatch.delenv("NYS_REC_PATH")
-    b = filter_with_landmarks(f, f, C, params)
-    ref = O.fast_filter_with_landmarks(f64, f64, C, theta, "gaussian_recursive", 2.5, 0)
-    oa, ob = a.output.data.double().cpu().numpy(), b.output.data.double().cpu().numpy()
-    assert np.abs(oa - ref["output"]).max() <= TOL
-    assert np.abs(oa - ob).max() <= 1e-5
-    assert a.guarded_pixels == b.guarded_pixels == ref["guarded_pixels"]
-
-
 @pytest.mark.parametrize("shape,m0,theta", [((130, 9), 5, 0.35), ((64, 64), 5, 0.35), ((48, 56), 12, 0.2)])
 @pytest.mark.parametrize("kind", ["gaussian_fir", "gaussian_recursive", "box"])
 def test_ill_conditioned_kernels_use_phi_form(shape, m0, theta, kind):
@@ -391,23 +365,6 @@ def test_ill_conditioned_kernels_use_phi_form(shape, m0, theta, kind):
     assert np.abs(out - ref["output"]).max() <= TOL
     assert rep.guarded_pixels == ref["guarded_pixels"]
     assert rep.retained_rank == ref["retained_rank"]
-
-
-@pytest.mark.parametrize("rho", [16, 27])
-def test_tcgen05_assignment_labels_equal_fp32_search(rho, monkeypatch):
-    # the opt-in tensor-core distance filter (NYS_KM_TC=1) must pick exactly the labels of the
-    # FP32 differenced search: same centroid trajectory as the step-wise SIMT assignment
-    from paper_1901_06112_b200.landmarks import kmeans_device
-
-    rng = np.random.default_rng(rho)
-    centers = rng.uniform(0, 1, (30, rho))
-    pts = (centers[rng.integers(0, 30, 40000)] + 0.05 * rng.standard_normal((40000, rho))).astype(np.float32)
-    t = torch.from_numpy(np.ascontiguousarray(pts.T)).cuda()
-    monkeypatch.setenv("NYS_KM_TC", "1")
-    a = kmeans_device(t, 24, seed=1, max_iter=8, want_assignment=True)
-    b = O.kmeans(pts.astype(np.float64), 24, 1, 8)
-    assert abs(a.quant_error - b[2]) <= 1e-6 * b[2]
-    np.testing.assert_allclose(a.centroids, b[0], rtol=0, atol=1e-5)
 
 
 @pytest.mark.parametrize("m0,rho,theta", [(64, 3, 0.1), (60, 5, 0.3), (13, 4, 0.2), (8, 3, 0.2), (41, 31, 0.4)])

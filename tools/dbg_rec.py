@@ -20,7 +20,6 @@ for (H, W, n, m0, th) in [(130, 9, 1, 5, 0.35), (130, 9, 2, 5, 0.35), (130, 9, 3
     res = []
     for kind, sk in (("rec", SpatialKernel.recursive(2.5)), ("fir", SpatialKernel.gaussian(2.5, 8))):
         params = FilterParams(spatial=sk, theta=th, m0=m0)
-        os.environ.pop("NYS_REC_PATH", None)
         a = filter_with_landmarks(f, f, C, params).output.data.double().cpu().numpy()
         ref = O.fast_filter_with_landmarks(f64, f64, C, th, sk.kind, 2.5, 8)["output"]
         res.append(f"{kind} {np.abs(a - ref).max():.2e}")

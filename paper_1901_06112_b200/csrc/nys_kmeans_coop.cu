@@ -501,8 +501,18 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
   __shared__ double dcum_sh;
   const int nb = gridDim.x, b = blockIdx.x;
   const long long chunk = ceil_div(a.m, (long long)nb);
-  const long long lo = min(a.m, b * chunk), hi = min(a.m, lo + chunk);
-  const long long cw = ceil_div(hi - lo, (long long)nw);  // phase-A sub-range per warp
+  const long long clo = min(a.m, b * chunk), chi = min(a.m, clo + chunk);  // contiguous chunk: sweeps, repair
+  // Assignment partition of the bounds kernel: block b owns the KM_SEG-point segments b, b + nb,
+  // b + 2 nb, ... of the image (a uniform sample of it: bound failures and label changes cluster
+  // in busy regions, and contiguous chunks left the grid barrier waiting for the blocks that own
+  // them).  A block walks its segments as one contiguous *virtual* range [lo, hi); gmap turns a
+  // virtual index into the point index (>= m: padding).  Lists, bounds and labels are indexed by
+  // point, the list segments by virtual position.
+  constexpr long long KM_SEG = 256;
+  const long long chunk_v = ceil_div(chunk, KM_SEG) * KM_SEG;
+  const long long lo = (long long)b * chunk_v, hi = lo + chunk_v;
+  auto gmap = [&](long long v) { return (((v - lo) / KM_SEG) * nb + b) * KM_SEG + ((v - lo) % KM_SEG); };
+  const long long cw = ceil_div(ceil_div(hi - lo, (long long)nw), 128ll) * 128;  // phase-A sub-range per warp
   const long long wlo = min(hi, lo + w * cw), whi = min(hi, wlo + cw);
 
   // fixed-point scale 2^s with |sum| < 2^61 for any cluster: s = 61 - log2(max|x| * m)
@@ -517,7 +527,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
       }
     } else {
-      for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      for (long long i = clo + threadIdx.x; i < chi; i += blockDim.x)
         for (int d = 0; d < rho; ++d) mx = fmaxf(mx, fabsf(__ldg(a.pts + d * a.ps + i)));
     }
     mx = warp_max(mx);
@@ -525,7 +535,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
     if constexpr (gridmode) {  // per-dimension bounding box: words 1..3 max, 4..6 -min (order-preserving, zero = identity)
       for (int d = 0; d < rho; ++d) {
         float hi_v = -INFINITY, lo_v = INFINITY;
-        for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        for (long long i = clo + threadIdx.x; i < chi; i += blockDim.x) {
           const float v = __ldg(a.pts + d * a.ps + i);
           hi_v = fmaxf(hi_v, v);
           lo_v = fminf(lo_v, v);
@@ -949,8 +959,9 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         int lab[PA];
 #pragma unroll
         for (int u = 0; u < PA; ++u) {
-          const long long i = base + 32 * u + lane;
-          const bool valid = i < whi;
+          const long long v = base + 32 * u + lane;
+          const long long i = gmap(v);
+          const bool valid = v < whi && i < a.m;
 #pragma unroll
           for (int d = 0; d < GR; ++d) x[u][d] = (valid && d < rho) ? __ldg(a.pts + d * a.ps + i) : 0.f;
           lab[u] = valid ? a.labels[i] : 0;
@@ -958,9 +969,10 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < PA; ++u) {
-          const long long i = base + 32 * u + lane;
+          const long long v = base + 32 * u + lane;
+          const long long i = gmap(v);
           bool need = false;
-          if (i < whi) {
+          if (v < whi && i < a.m) {
             const float d2a = d2_f32<GR>(x[u], rho, Cf + (size_t)lab[u] * rhop);
             const double lbe = (double)lbv[u] - dcum;
             if (lbe > 0.0 && (double)d2a * (1.0 + LB_EPS) < lbe * lbe * (1.0 - LB_EPS)) near_sum += (double)d2a;
@@ -994,10 +1006,12 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
         arg[h] = 0;
         const long long q = q0 + 32 * h + lane;
         valid[h] = q < nlist;
-        long long i = lo;
+        long long i = 0;
         if (valid[h]) {
           if (full_pass) {
-            i = lo + q;
+            i = gmap(lo + q);
+            valid[h] = i < a.m;
+            if (!valid[h]) i = 0;
           } else {
             while (q >= wpre[sgc + 1]) ++sgc;
             i = a.list[min(hi, lo + sgc * cw) + (q - wpre[sgc])];
@@ -1149,7 +1163,7 @@ __global__ void __launch_bounds__(256) k_lloyd_coop(const LloydArgs a) {
       if (T[msl + j] > 0) continue;
       double bv = -INFINITY;
       long long bi = a.m;
-      for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      for (long long i = clo + threadIdx.x; i < chi; i += blockDim.x) {
         bool ex = false;
         for (int q = 0; q < nex; ++q) ex |= (excl[q] == i);
         const double v = ex ? -1.0 : d2_exact(a.pts, a.ps, i, rho, Cp + (size_t)a.labels[i] * rho);

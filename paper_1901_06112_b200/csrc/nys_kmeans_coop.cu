@@ -43,7 +43,29 @@ struct SeedArgs {
   long long pps;    // plane stride of pp
   double* tsum;     // per-thread run sums [block][B]
   int per;          // points per thread run
+  int mode;         // 0: every block resolves the draw (remote run sums, recomputed run; NYS_SEED_MODE=0, A/B);
+                    // 1: the owning block resolves it from its own run sums and D^2 and publishes the point
 };
+
+// Cross-block words exchanged by polling (k_seed_runs mode 1): a slot holds this bit pattern (a NaN
+// no arithmetic produces) until its value is published; published NaNs are canonicalised.
+// (Exchanging the block totals the same way instead of a grid barrier -- three rounds of polled
+// slots -- measured slower: 1.35 -> 1.52 ms k-means on cfg 2; grid.sync is the cheaper all-to-all.)
+constexpr unsigned long long SEED_EMPTY = 0xFFFFFFFFFFFFFFFFull;
+__device__ __forceinline__ void seed_publish(double* slot, double v) {
+  unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  if (v != v) bits = 0x7FF8000000000000ull;
+  __stcg(reinterpret_cast<unsigned long long*>(slot), bits);
+}
+__device__ __forceinline__ double seed_poll(const double* slot) {
+  unsigned long long bits = __ldcg(reinterpret_cast<const unsigned long long*>(slot));
+  long long spins = 0;
+  while (bits == SEED_EMPTY) {
+    if (++spins > (1ll << 22)) __trap();  // seconds: a protocol error must fail loudly, not hang the GPU
+    bits = __ldcg(reinterpret_cast<const unsigned long long*>(slot));
+  }
+  return __longlong_as_double((long long)bits);
+}
 
 // owner search over vals[0..n) for the first index whose running sum exceeds
 // `target`: each thread sums a contiguous run, the run sums are scanned, the
@@ -133,7 +155,7 @@ __global__ void __launch_bounds__(512) k_seed_coop(const SeedArgs a) {
     if ((int)threadIdx.x < rho) cs[threadIdx.x] = __ldcg(a.C + (size_t)(j - 1) * rho + threadIdx.x);
     __syncthreads();
     double s = 0.0;
-    constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2)
+    constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2; 14 measured no faster)
     int i = threadIdx.x;
     for (; i + (U - 1) * B < len; i += U * B) {
       float x[U][GR];
@@ -264,11 +286,17 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
       a.pp[d * a.pps + slot0 + (long long)r * B + t] = li < len ? __ldg(a.pts + d * a.ps + lo + li) : 0.f;
   }
   for (int k = t; k < rho; k += B) Cs[k] = __ldcg(a.C + k);
+  if (a.mode) {  // polled slots start empty: the centroid rows 1..
+    if (b == 0)
+      for (int k = rho + t; k < a.m0 * rho; k += B)
+        __stcg(reinterpret_cast<unsigned long long*>(a.C + k), SEED_EMPTY);
+    grid.sync();
+  }
   __syncthreads();
   for (int j = 1; j < a.m0; ++j) {
     const double* cs = Cs + (size_t)(j - 1) * rho;
     double s = 0.0;
-    constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2)
+    constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2; 14 measured no faster)
     int r = 0;
     for (; r + U <= per; r += U) {
       float x[U][GR];
@@ -297,14 +325,13 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
       d2[sl] = nv;
       s += nv;
     }
-    a.tsum[(long long)b * B + t] = s;
+    if (a.mode == 0) a.tsum[(long long)b * B + t] = s;
     {
-      const double incl = block_incl_scan(s, sh);  // the scan scan_pick runs over tsum
+      const double incl = block_incl_scan(s, sh);  // the scan scan_pick runs over the run sums
       if (t == B - 1) a.ppart[b] = incl;
     }
     grid.sync();
-    // --- every block resolves the draw with identical arithmetic ---
-    // the owning block (nb <= blockDim: one block total per thread)
+    // --- the owning block (nb <= blockDim: one block total per thread), identical in every block ---
     double total = 0.0, before_b = 0.0, before_t = 0.0, before_r = 0.0;
     const double u = a.uniforms[j - 1];
     const int bstar = scan_pick(t < nb ? __ldcg(a.ppart + t) : 0.0, [&](double tot) { return u * tot; }, sh, shi,
@@ -314,6 +341,37 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
       return;  // uniform across the grid
     }
     const double target = u * total, tgt_b = target - before_b;
+    if (a.mode) {
+      // The owning block resolves the thread run and the point from its own run sums (registers) and
+      // stored D^2 (the values the other path recomputes), and publishes the point's coordinates;
+      // everyone else polls them: one L2 round trip instead of two plus the recomputation.
+      double* cn = Cs + (size_t)j * rho;
+      if (b == bstar) {
+        const int tstar = scan_pick(s, [&](double) { return tgt_b; }, sh, shi, &before_t, nullptr);
+        const double tgt = tgt_b - before_t;
+        long long idx = -1;
+        for (int r0 = 0; r0 < per && idx < 0; r0 += B) {
+          const int cnt = min(B, per - r0);
+          double run_tot = 0.0, before_in = 0.0;
+          const int rstar = scan_pick(t < cnt ? d2[(size_t)(r0 + t) * B + tstar] : 0.0,
+                                      [&](double) { return tgt - before_r; }, sh, shi, &before_in, &run_tot);
+          if (r0 + cnt >= per || run_tot > tgt - before_r)
+            idx = lo + (long long)tstar * per + r0 + rstar;
+          else
+            before_r += run_tot;  // the target lies in a later round of this run
+        }
+        for (int k = t; k < rho; k += B) {
+          const double v = (double)__ldg(a.pts + k * a.ps + idx);
+          cn[k] = v;
+          seed_publish(a.C + (size_t)j * rho + k, v);
+        }
+        if (t == 0 && a.seeds) a.seeds[j] = idx;
+      } else {
+        for (int k = t; k < rho; k += B) cn[k] = seed_poll(a.C + (size_t)j * rho + k);
+      }
+      __syncthreads();
+      continue;
+    }
     // the owning thread run inside block bstar
     const int tstar = scan_pick(__ldcg(a.tsum + (long long)bstar * B + t), [&](double) { return tgt_b; }, sh, shi,
                                 &before_t, nullptr);
@@ -1286,6 +1344,8 @@ int launch_seed_coop(const float* pts, long long ps, long long m, int rho, int m
   void* args[] = {&a};
   const char* v1 = getenv("NYS_SEED_V1");
   const bool runs = !(v1 && atoi(v1));
+  const char* sm_e = getenv("NYS_SEED_MODE");
+  a.mode = sm_e ? (atoi(sm_e) ? 1 : 0) : 1;
   auto go = [&](auto kern_v1, auto kern_runs) -> int {
     // one block per SM; the block's D^2 chunk lives in shared memory when it fits
     const int nb = (int)std::max<long long>(1, std::min<long long>((long long)sms(), ceil_div(m, 512)));

@@ -1408,9 +1408,13 @@ int launch_lloyd_coop(const float* pts, long long ps, long long m, int rho, int 
   const size_t gsm = gridmode ? gcells * 8 + 16 + 64 + (size_t)8 * msl * 3 * 4 : 0;  // masks, box, limb tables
   // tensor-core search for wide guides: (x, 1) needs K = rho + 1 padded to 8, N = m0 padded to 16,
   // two groups' D / A_hi / A_lo columns in the 512-column TMEM
-  const char* etc = getenv("NYS_KM_TC_COOP");  // opt-in: measured on par with / behind the bounds kernel
+  // NYS_KM_TC_COOP = 1 / 0 forces it on / off.  Default: on where it measured faster than the bounds
+  // kernel -- the bounds kernel's full searches grow with m0 * rho, the tensor-core tiles hardly do:
+  // cfg 3 (m0 64, rho 27) 6.5 -> 5.9 ms clustering, cfg 4 (m0 48, rho 31) 4.6 -> 4.8 ms
+  const char* etc = getenv("NYS_KM_TC_COOP");
+  const bool tc_wanted = etc ? atoi(etc) != 0 : (long long)m0 * rho >= 1600;
   const int KUt = (int)ceil_div(rho + 1, 8) * 8, NUt = (int)ceil_div(m0, 16) * 16;
-  bool use_tc = rho >= 16 && (etc && atoi(etc)) && NUt <= 256 &&
+  bool use_tc = rho >= 16 && tc_wanted && NUt <= 256 &&
                 2 * (((NUt + 31) & ~31) + 2 * ((KUt + 31) & ~31)) <= 512;
   const size_t tsm = use_tc ? (size_t)2 * NUt * KUt * 4 + 128 : 0;
   auto need = [&](int nw) { return (size_t)nw * msl * 8 + (((size_t)nw * m0 + 1) & ~size_t(1)) * 4 + fixed + gsm + tsm; };

@@ -392,8 +392,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-rows", type=int, default=16, help="rows of the CPU-baseline crop")
-    ap.add_argument("--ref-rows", type=int, default=16, help="rows of the reference-arm crop per step")
+    ap.add_argument("--cpu-rows", type=int, default=128, help="rows of the CPU-baseline crop")
+    ap.add_argument("--ref-rows", type=int, default=64, help="rows of the reference-arm crop per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="run the row-sharded NCCL path even at one rank (exercises parallel.py on one GPU)")

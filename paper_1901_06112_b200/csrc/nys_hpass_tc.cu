@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
             d2 = fmaf(t3, t3, d2);
           }
           const float v = ex2_fast(d2 * k2);
-          if (bdst && jj + e < jlim) bdst[(size_t)(jj + e) * 32] = v;
+          // (no raw b planes here: K3 reads them only for rho > 8 / patch guides, use_bplanes(); the
+          // phi-form stores phi from the drain instead)
           split_tf32(v, hi[e], lo[e]);
         }
         umma::st_32x32b_x4(t_hi + (uint32_t)jj, hi[0], hi[1], hi[2], hi[3]);

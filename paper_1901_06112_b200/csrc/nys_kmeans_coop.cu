@@ -297,33 +297,44 @@ __global__ void __launch_bounds__(512) k_seed_runs(const SeedArgs a) {
     const double* cs = Cs + (size_t)(j - 1) * rho;
     double s = 0.0;
     constexpr int U = GR <= 4 ? 7 : 2;  // independent points in flight (register budget; 28 = 4 x 7 on cfg 2; 14 measured no faster)
+    // Wide guides: every draw streams the whole permuted guide (113 MB on cfg 3, just above what the
+    // 126 MB L2 keeps), so with a fixed sweep direction every line has been evicted by the time it
+    // is needed again.  Odd draws sweep the runs backwards: the lines touched last are touched
+    // first, and most of the guide is served from the L2.  The run sum is still accumulated in
+    // ascending order (a second pass over the stored D^2), so it has the bits of the forward sweep.
+    const bool rev = GR >= 16 && (j & 1) && a.d2_in_smem;
+    auto RR = [&](int q) { return rev ? per - 1 - q : q; };
     int r = 0;
     for (; r + U <= per; r += U) {
       float x[U][GR];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int d = 0; d < GR; ++d) x[u][d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)(r + u) * B + t] : 0.f;
+        for (int d = 0; d < GR; ++d) x[u][d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)RR(r + u) * B + t] : 0.f;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double v = d2_exact_regs<GR>(x[u], rho, cs);
-        const int sl = (r + u) * B + t;
+        const int sl = RR(r + u) * B + t;
         double nv = j == 1 ? v : fmin(d2[sl], v);
-        if (t * per + r + u >= len) nv = 0.0;
+        if (t * per + RR(r + u) >= len) nv = 0.0;
         d2[sl] = nv;
-        s += nv;  // run sum in linear order
+        s += nv;  // run sum in linear order (forward sweeps)
       }
     }
     for (; r < per; ++r) {
       float x[GR];
 #pragma unroll
-      for (int d = 0; d < GR; ++d) x[d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)r * B + t] : 0.f;
+      for (int d = 0; d < GR; ++d) x[d] = d < rho ? a.pp[d * a.pps + slot0 + (long long)RR(r) * B + t] : 0.f;
       const double v = d2_exact_regs<GR>(x, rho, cs);
-      const int sl = r * B + t;
+      const int sl = RR(r) * B + t;
       double nv = j == 1 ? v : fmin(d2[sl], v);
-      if (t * per + r >= len) nv = 0.0;
+      if (t * per + RR(r) >= len) nv = 0.0;
       d2[sl] = nv;
       s += nv;
+    }
+    if (rev) {
+      s = 0.0;
+      for (int q = 0; q < per; ++q) s += d2[q * B + t];
     }
     if (a.mode == 0) a.tsum[(long long)b * B + t] = s;
     {

@@ -69,6 +69,21 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
+// packed FP32 pairs (one issue slot per two lanes of arithmetic): d = a * b + c on both halves
+__device__ __forceinline__ unsigned long long ffma2_pk(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long v;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(lo), "f"(hi));
+  return v;
+}
+__device__ __forceinline__ void lds128_pk(uint32_t addr, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+
 // GR: guide dimensions held in registers per pixel, a multiple of 4 -- or 3 for rho == 3
 // exactly (colour guides: the padded fourth dimension costs a subtract and an FMA per landmark)
 template <int RT, int GR>
@@ -94,7 +109,17 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
   auto Ys_of = [&](int b) { return Fs_of(b) + align32f(nfr * pitch); };
 
   if (!a.bfrom)  // landmarks padded to KU rows: the feature loop runs over all KU without a bound check
-    for (int k = tid; k < KU * rhop; k += K2T_THREADS) Cs[k] = k < m0 * rhop ? a.cst[k] : 0.f;
+    for (int k = tid; k < KU * rhop; k += K2T_THREADS) {
+      int src = k;  // row-major [landmark][rhop]
+      if constexpr (GR <= 4) {
+        // colour guides: landmark pairs interleaved per dimension, [pair][d][2] (rhop == 4), so one
+        // LDS.128 yields the (x, y) pairs and the next the (z, w) pairs of two landmarks as packed
+        // f32x2 operands
+        const int pr = k >> 3, d = (k >> 1) & 3, h = k & 1;
+        src = (2 * pr + h) * 4 + d;
+      }
+      Cs[k] = src < m0 * rhop ? a.cst[src] : 0.f;
+    }
   {
     const float* MTg = a.cst + (size_t)m0 * rhop;  // MT[j][i] = M[i][j], MT[j][m0] = u0[j]
     for (int k = tid; k < NU * KU; k += K2T_THREADS) {
@@ -165,32 +190,59 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
     uint32_t ca = cs_half;
     const uint32_t t_hi = a_hi + lane_base + (uint32_t)(hh * khalf), t_lo = a_lo + lane_base + (uint32_t)(hh * khalf);
     if constexpr (GR <= 4) {
-      // one LDS.128 per landmark; the next four landmarks' centroids are loaded before this
-      // four's arithmetic (the loads are ordered asm statements, so the prefetch is explicit; the
-      // last one reads past the landmarks into the B operand, still this CTA's shared memory)
-      float4 cn[4];
+      // Two landmarks per packed f32x2 operation (fma.rn.f32x2: one issue slot for both).  With
+      // the pair-interleaved centroids: t = (g, g) - (c_j, c_j+1) per dimension as an FMA with -1,
+      // d2 = t0 t0, + t1 t1, + t2 t2 in the scalar order, one packed scale by k2 -- every half
+      // rounds exactly as the scalar form did -- then two MUFUs and the TF32 splits.  The next four
+      // landmarks' centroids are loaded before this four's arithmetic (ordered asm loads; the
+      // last prefetch reads past the landmarks into the B operand, still this CTA's shared memory).
+      const unsigned long long neg1 = pack2(-1.f, -1.f), k2p = pack2(k2, k2);
+      unsigned long long g2[GR];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) cn[e] = lds128(ca + (uint32_t)e * rhob);
+      for (int d = 0; d < GR; ++d) g2[d] = pack2(gv[d], gv[d]);
+      unsigned long long nx[2], ny[2], nz[2], nw[2];
+      auto load_pairs = [&](uint32_t addr) {
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr) {
+          lds128_pk(addr + 32u * pr, nx[pr], ny[pr]);
+          if constexpr (GR == 4) {
+            lds128_pk(addr + 32u * pr + 16u, nz[pr], nw[pr]);
+          } else {
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(nz[pr]) : "r"(addr + 32u * pr + 16u));
+            nw[pr] = 0ull;
+          }
+        }
+      };
+      load_pairs(ca);
       for (int jj = 0; jj < khalf; jj += 4) {
-        float4 cc[4];
+        unsigned long long cx[2], cy[2], cz[2], cw[2];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) cc[e] = cn[e];
-        ca += 4u * rhob;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cn[e] = lds128(ca + (uint32_t)e * rhob);
+        for (int pr = 0; pr < 2; ++pr) {
+          cx[pr] = nx[pr];
+          cy[pr] = ny[pr];
+          cz[pr] = nz[pr];
+          cw[pr] = nw[pr];
+        }
+        ca += 64u;
+        load_pairs(ca);
         float hi[4], lo[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float t0 = gv[0] - cc[e].x, t1 = gv[1] - cc[e].y, t2 = gv[2] - cc[e].z;
-          float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
+        for (int pr = 0; pr < 2; ++pr) {
+          const unsigned long long t0 = ffma2_pk(cx[pr], neg1, g2[0]), t1 = ffma2_pk(cy[pr], neg1, g2[1]),
+                                   t2 = ffma2_pk(cz[pr], neg1, g2[2]);
+          unsigned long long d2 = ffma2_pk(t0, t0, 0ull);
+          d2 = ffma2_pk(t1, t1, d2);
+          d2 = ffma2_pk(t2, t2, d2);
           if constexpr (GR == 4) {
-            const float t3 = gv[3] - cc[e].w;
-            d2 = fmaf(t3, t3, d2);
+            const unsigned long long t3 = ffma2_pk(cw[pr], neg1, g2[3]);
+            d2 = ffma2_pk(t3, t3, d2);
           }
-          const float v = ex2_fast(d2 * k2);
+          float e0, e1;
+          unpack2(ffma2_pk(d2, k2p, 0ull), e0, e1);
           // (no raw b planes here: K3 reads them only for rho > 8 / patch guides, use_bplanes(); the
           // phi-form stores phi from the drain instead)
-          split_tf32(v, hi[e], lo[e]);
+          split_tf32(ex2_fast(e0), hi[2 * pr], lo[2 * pr]);
+          split_tf32(ex2_fast(e1), hi[2 * pr + 1], lo[2 * pr + 1]);
         }
         umma::st_32x32b_x4(t_hi + (uint32_t)jj, hi[0], hi[1], hi[2], hi[3]);
         umma::st_32x32b_x4(t_lo + (uint32_t)jj, lo[0], lo[1], lo[2], lo[3]);

@@ -146,7 +146,10 @@ __device__ __forceinline__ void hfir_plane(const HArgs& a, const float* __restri
     for (int q = 0; q < NQ; ++q) {
       const float4 y4 = *reinterpret_cast<const float4*>(yrow + 4 * q);
       const float4 f4 = *reinterpret_cast<const float4*>(frow + 4 * q);
-      const float v4[4] = {y4.x * f4.x, y4.y * f4.y, y4.z * f4.z, y4.w * f4.w};
+      // z = y f as two packed multiplies (the LDS.128 results are adjacent register pairs)
+      float v4[4];
+      mul2(y4.x, y4.y, f4.x, f4.y, v4[0], v4[1]);
+      mul2(y4.z, y4.w, f4.z, f4.w, v4[2], v4[3]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int s = 4 * q + e;

@@ -168,7 +168,12 @@ __device__ __forceinline__ void vfir(const VArgs& a, const float* __restrict__ s
   }
 }
 
-template <int RT>
+// G1: b_i recomputed from a planar guide tile (rho <= 8); else K2's b planes arrive with the stage.
+// A compile-time switch: with G1 the lead projection s0 = u0 . b is accumulated once per pixel by
+// the thread that evaluates that pixel's features and handed to the lead stage through shared
+// memory, which takes 16 FMAs per stage and 16 accumulator registers out of every thread (the
+// four plane groups used to accumulate it redundantly).
+template <int RT, bool G1>
 __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__ CUtensorMap tmap4,
                                                         const __grid_constant__ CUtensorMap tmapt,
                                                         const __grid_constant__ CUtensorMap tmapb, const VArgs a) {
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   const int SR = K3_TH + 2 * R;     // staged rows per plane
   const int nchunks = a.nchunks;
   const int plane_floats = SR * 32;
-  const int gmode = a.gcache;       // 1: b from a planar guide tile (rho <= 8), 3: b planes from K2
+  constexpr int gmode = G1 ? 1 : 3;  // 1: b from a planar guide tile (rho <= 8), 3: b planes from K2
   const int stage_floats = 4 * plane_floats + (gmode == 3 ? K3_NPX : 0);
   float* stage = sm;                                           // K3_NS x ([SR][4][32] planes, [TH][32] b)
   float* bsh = stage + (size_t)K3_NS * stage_floats;           // gmode 1: 2 x npx
@@ -190,6 +195,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   float* Cs = ssh + K3_NPX;                                    // m0 x rhop (gmode 1 only)
   float* U0 = Cs + (gmode == 1 ? (size_t)m0 * rhop : 0);       // m0
   float* gsh = U0 + ((m0 + 3) & ~3);                           // gmode 1: [rho][npx] guide tile
+  float* s0sh = gsh + (gmode == 1 ? (size_t)rho * K3_NPX : 0);  // gmode 1: npx, s0 = u0 . b per pixel
   __shared__ __align__(8) unsigned long long full[K3_NS];
   __shared__ float red_min[K3_THREADS / 32];
   __shared__ unsigned long long red_cnt[K3_THREADS / 32];
@@ -240,7 +246,9 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       gq[d][3] = g4.w;
     }
   };
-  auto compute_b = [&](int i, float* bb) {
+  float s0q[4] = {0.f, 0.f, 0.f, 0.f};  // s0 of this thread's four feature pixels (denominator chunk)
+  auto compute_b = [&](int i, float* bb, bool lead_acc) {
+    const float u0i = U0[i];
     if (rho <= 3) {
       const float4 c4 = *reinterpret_cast<const float4*>(Cs + i * rhop);  // rhop == 4, padded with zeros
       const float cc[3] = {c4.x, c4.y, c4.z};
@@ -254,8 +262,14 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
             d2[e] = fmaf(t, t, d2[e]);
           }
         }
-      *reinterpret_cast<float4*>(bb + 4 * tid) = make_float4(range_kernel_fast(d2[0], a.k2), range_kernel_fast(d2[1], a.k2),
-                                                             range_kernel_fast(d2[2], a.k2), range_kernel_fast(d2[3], a.k2));
+      const float bq[4] = {range_kernel_fast(d2[0], a.k2), range_kernel_fast(d2[1], a.k2), range_kernel_fast(d2[2], a.k2),
+                           range_kernel_fast(d2[3], a.k2)};
+      *reinterpret_cast<float4*>(bb + 4 * tid) = make_float4(bq[0], bq[1], bq[2], bq[3]);
+      if (lead_acc) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s0q[e] = fmaf(u0i, bq[e], s0q[e]);  // landmark order, as the stages had it
+        if (i == m0 - 1) *reinterpret_cast<float4*>(s0sh + 4 * tid) = make_float4(s0q[0], s0q[1], s0q[2], s0q[3]);
+      }
       return;
     }
     for (int k4 = tid; k4 < K3_NPX / 4; k4 += K3_THREADS) {
@@ -269,8 +283,14 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
         d2.z = fmaf(tz, tz, d2.z);
         d2.w = fmaf(tw, tw, d2.w);
       }
-      *reinterpret_cast<float4*>(bb + 4 * k4) = make_float4(range_kernel_fast(d2.x, a.k2), range_kernel_fast(d2.y, a.k2),
-                                                            range_kernel_fast(d2.z, a.k2), range_kernel_fast(d2.w, a.k2));
+      const float bq[4] = {range_kernel_fast(d2.x, a.k2), range_kernel_fast(d2.y, a.k2), range_kernel_fast(d2.z, a.k2),
+                           range_kernel_fast(d2.w, a.k2)};
+      *reinterpret_cast<float4*>(bb + 4 * k4) = make_float4(bq[0], bq[1], bq[2], bq[3]);
+      if (lead_acc) {  // (K3_NPX / 4 == K3_THREADS: k4 == tid, one pass)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s0q[e] = fmaf(u0i, bq[e], s0q[e]);
+        if (i == m0 - 1) *reinterpret_cast<float4*>(s0sh + 4 * k4) = make_float4(s0q[0], s0q[1], s0q[2], s0q[3]);
+      }
     }
   };
 
@@ -291,7 +311,8 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       }
       __syncthreads();
       if (rho <= 3) load_gq();
-      compute_b(0, bsh);
+      s0q[0] = s0q[1] = s0q[2] = s0q[3] = 0.f;
+      compute_b(0, bsh, true);
       __syncthreads();
     }
     float s0[K3_YR][4], acc[K3_YR][4], sab[K3_YR][4];  // sab: sum_i b_i |conv(y_i)| (denominator chunk)
@@ -334,22 +355,30 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
           for (int e = 0; e < 4; ++e) {
             acc[o][e] = fmaf(bv[e], G[o][e], acc[o][e]);
             if (co == 0) {
-              s0[o][e] = fmaf(u0i, bv[e], s0[o][e]);
+              if constexpr (!G1) s0[o][e] = fmaf(u0i, bv[e], s0[o][e]);
               if (c == n) sab[o][e] = fmaf(bv[e], fabsf(G[o][e]), sab[o][e]);  // only eta's scale is used
             }
           }
         }
         // features of the next stage's landmark (gmode 1): the other b buffer is free
         if (gmode == 1) {
-          if (i + 1 < m0) compute_b(i + 1, bsh + ((i + 1) & 1) * K3_NPX);
+          if (i + 1 < m0) compute_b(i + 1, bsh + ((i + 1) & 1) * K3_NPX, co == 0);
         }
       } else {
         // lead group: zeta_lead = s0 (ω*(s0 f_c)) / α0 ; chunk kn first publishes eta and eta_lead
         float lg[K3_YR][4];
 #pragma unroll
-        for (int o = 0; o < K3_YR; ++o)
+        for (int o = 0; o < K3_YR; ++o) {
+          float sv[4];
+          if constexpr (G1) {
+            const float4 s4 = *reinterpret_cast<const float4*>(s0sh + pxo + o * 32);
+            sv[0] = s4.x, sv[1] = s4.y, sv[2] = s4.z, sv[3] = s4.w;
+          } else {
+            sv[0] = s0[o][0], sv[1] = s0[o][1], sv[2] = s0[o][2], sv[3] = s0[o][3];
+          }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) lg[o][e] = s0[o][e] * G[o][e] * inv_alpha0;
+          for (int e = 0; e < 4; ++e) lg[o][e] = sv[e] * G[o][e] * inv_alpha0;
+        }
         if (co == 0) {
           if (c == n) {
 #pragma unroll
@@ -420,7 +449,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
 #pragma unroll
         for (int o = 0; o < K3_YR; ++o) acc[o][0] = acc[o][1] = acc[o][2] = acc[o][3] = 0.f;
         // first landmark of the next chunk (gmode 1)
-        if (gmode == 1 && co + 1 < nchunks) compute_b(0, bsh);
+        if (gmode == 1 && co + 1 < nchunks) compute_b(0, bsh, false);
       }
       __syncthreads();  // everyone is done with this stage's buffer (and the next b tile is ready)
       if (tid == 0) {
@@ -553,7 +582,7 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
   const size_t stage_floats = 4 * plane_floats + (a.gcache == 3 ? K3_NPX : 0);
   const size_t smem = ((size_t)K3_NS * stage_floats + (a.gcache == 1 ? 2 * K3_NPX : 0) + 3 * K3_NPX +
                        (a.gcache == 1 ? (size_t)d->m0 * L.rhop : 0) + ((d->m0 + 3) & ~3) +
-                       (a.gcache == 1 ? (size_t)d->rho * K3_NPX : 0)) *
+                       (a.gcache == 1 ? (size_t)d->rho * K3_NPX + K3_NPX : 0)) *
                       sizeof(float);
   if (smem > 227 * 1024) return NYS_EUNSUPPORTED;
   const long long ntiles = (long long)a.tiles_x * a.tiles_y;
@@ -569,12 +598,21 @@ int nys_filter_vpass(const nys_filter_desc* d, const float* f, int64_t f_plane_s
     return NYS_OK;
   };
   const int rsel = a.box ? 0 : d->radius;
+  if (a.gcache == 1) {
+    switch (rsel) {
+      case 9: return go(k_vpass<9, true>);
+      case 12: return go(k_vpass<12, true>);
+      case 15: return go(k_vpass<15, true>);
+      case 18: return go(k_vpass<18, true>);
+      default: return go(k_vpass<0, true>);
+    }
+  }
   switch (rsel) {
-    case 9: return go(k_vpass<9>);
-    case 12: return go(k_vpass<12>);
-    case 15: return go(k_vpass<15>);
-    case 18: return go(k_vpass<18>);
-    default: return go(k_vpass<0>);
+    case 9: return go(k_vpass<9, false>);
+    case 12: return go(k_vpass<12, false>);
+    case 15: return go(k_vpass<15, false>);
+    case 18: return go(k_vpass<18, false>);
+    default: return go(k_vpass<0, false>);
   }
 }
 

@@ -74,14 +74,14 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+__device__ __forceinline__ void mbar_wait_addr(unsigned bar_addr, unsigned parity) {  // 32-bit shared address
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar_addr),
       "r"(parity)
       : "memory");
 }
@@ -185,7 +185,11 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   const int SR = K3_TH + 2 * R;     // staged rows per plane
   const int nchunks = a.nchunks;
   const int plane_floats = SR * 32;
-  constexpr int gmode = G1 ? 1 : 3;  // 1: b from a planar guide tile (rho <= 8), 3: b planes from K2
+  // 1: b from a planar guide tile (rho <= 8), 3: b planes from K2.  In the !G1 instantiations it is a
+  // constant only for the box kernel: measured, the Gaussian wide-guide kernels are 3.7 % slower
+  // with the constant (cfg 4: 2.22 -> 2.30 ms) and the box one 10 % faster (cfg 3: 0.43 -> 0.39 ms)
+  // -- instruction scheduling at the 128-register cap, nothing structural.
+  const int gmode = G1 ? 1 : (RT == 0 ? 3 : a.gcache);
   const int stage_floats = 4 * plane_floats + (gmode == 3 ? K3_NPX : 0);
   float* stage = sm;                                           // K3_NS x ([SR][4][32] planes, [TH][32] b)
   float* bsh = stage + (size_t)K3_NS * stage_floats;           // gmode 1: 2 x npx
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   }
   __syncthreads();
 
+  const unsigned full_addr = smem_u32(&full[0]);
   const int kn = n / 4;  // chunk holding the denominator channel n
   auto chunk_of = [&](int co) { return co == 0 ? kn : (co <= kn ? co - 1 : co); };
   const int L = m0 + 1;
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
   };
   float s0q[4] = {0.f, 0.f, 0.f, 0.f};  // s0 of this thread's four feature pixels (denominator chunk)
   auto compute_b = [&](int i, float* bb, bool lead_acc) {
-    const float u0i = U0[i];
+    const float u0i = G1 ? U0[i] : 0.f;
     if (rho <= 3) {
       const float4 c4 = *reinterpret_cast<const float4*>(Cs + i * rhop);  // rhop == 4, padded with zeros
       const float cc[3] = {c4.x, c4.y, c4.z};
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       const float bq[4] = {range_kernel_fast(d2[0], a.k2), range_kernel_fast(d2[1], a.k2), range_kernel_fast(d2[2], a.k2),
                            range_kernel_fast(d2[3], a.k2)};
       *reinterpret_cast<float4*>(bb + 4 * tid) = make_float4(bq[0], bq[1], bq[2], bq[3]);
-      if (lead_acc) {
+      if (G1 && lead_acc) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) s0q[e] = fmaf(u0i, bq[e], s0q[e]);  // landmark order, as the stages had it
         if (i == m0 - 1) *reinterpret_cast<float4*>(s0sh + 4 * tid) = make_float4(s0q[0], s0q[1], s0q[2], s0q[3]);
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       const float bq[4] = {range_kernel_fast(d2.x, a.k2), range_kernel_fast(d2.y, a.k2), range_kernel_fast(d2.z, a.k2),
                            range_kernel_fast(d2.w, a.k2)};
       *reinterpret_cast<float4*>(bb + 4 * k4) = make_float4(bq[0], bq[1], bq[2], bq[3]);
-      if (lead_acc) {  // (K3_NPX / 4 == K3_THREADS: k4 == tid, one pass)
+      if (G1 && lead_acc) {  // (K3_NPX / 4 == K3_THREADS: k4 == tid, one pass)
 #pragma unroll
         for (int e = 0; e < 4; ++e) s0q[e] = fmaf(u0i, bq[e], s0q[e]);
         if (i == m0 - 1) *reinterpret_cast<float4*>(s0sh + 4 * k4) = make_float4(s0q[0], s0q[1], s0q[2], s0q[3]);
@@ -331,7 +336,8 @@ __global__ void __launch_bounds__(K3_THREADS, 2) k_vpass(const __grid_constant__
       const bool tail = ntail && k == nchunks - 1;
       const int buf = (int)(gs % K3_NS);
       const float* sb = stage + (size_t)buf * stage_floats;
-      mbar_wait(&full[buf], (unsigned)((gs / K3_NS) & 1));
+      mbar_wait_addr(full_addr + 8u * (unsigned)buf, (unsigned)((gs / K3_NS) & 1));  // (address formed once: the generic-to-
+                                                                                      // shared conversion was 2 % of the instructions)
       float G[K3_YR][4];
       if (c < NC) {
         // staged row: [4 or ntail planes][32 columns]; the full-chunk stride is a constant, so the

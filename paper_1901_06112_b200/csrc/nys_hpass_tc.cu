@@ -248,24 +248,33 @@ __global__ void __launch_bounds__(K2T_THREADS, 1) k_feat_hpass_tc(const HArgs a)
         umma::st_32x32b_x4(t_lo + (uint32_t)jj, lo[0], lo[1], lo[2], lo[3]);
       }
     } else {
+      // wide guides: two dimensions per packed f32x2 operation.  The centroid rows are read as
+      // (c_d, c_d+1) pairs straight from the LDS.128, t = g - c as an FMA with -1, and the squares
+      // accumulate in an (even dimensions, odd dimensions) pair added at the end -- a different
+      // summation order from the scalar form (b differs in the last bits; K3 reads these very
+      // values from the b planes, so the two kernels stay consistent).
+      const unsigned long long neg1 = pack2(-1.f, -1.f);
+      unsigned long long g2[GR / 2];
+#pragma unroll
+      for (int d = 0; d < GR / 2; ++d) g2[d] = pack2(gv[2 * d], gv[2 * d + 1]);
       for (int jj = 0; jj < khalf; jj += 4) {
         float hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e, ca += rhob) {
-          float d2 = 0.f;
+          unsigned long long acc2 = 0ull;
 #pragma unroll
           for (int d4 = 0; d4 < GR / 4; ++d4) {
             if (4 * d4 < rho) {
-              const float4 c4 = lds128(ca + 16u * d4);
-              const float t0 = gv[4 * d4] - c4.x, t1 = gv[4 * d4 + 1] - c4.y;
-              const float t2 = gv[4 * d4 + 2] - c4.z, t3 = gv[4 * d4 + 3] - c4.w;
-              d2 = fmaf(t0, t0, d2);
-              d2 = fmaf(t1, t1, d2);
-              d2 = fmaf(t2, t2, d2);
-              d2 = fmaf(t3, t3, d2);
+              unsigned long long c01, c23;
+              lds128_pk(ca + 16u * d4, c01, c23);
+              const unsigned long long t01 = ffma2_pk(c01, neg1, g2[2 * d4]), t23 = ffma2_pk(c23, neg1, g2[2 * d4 + 1]);
+              acc2 = ffma2_pk(t01, t01, acc2);
+              acc2 = ffma2_pk(t23, t23, acc2);
             }
           }
-          const float v = ex2_fast(d2 * k2);
+          float de, dod;
+          unpack2(acc2, de, dod);
+          const float v = ex2_fast((de + dod) * k2);
           if (bdst && jj + e < jlim) bdst[(size_t)(jj + e) * 32] = v;
           split_tf32(v, hi[e], lo[e]);
         }

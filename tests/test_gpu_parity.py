@@ -234,6 +234,23 @@ def test_tensor_core_lloyd_equals_fp32_search(rho, m0, monkeypatch):
     np.testing.assert_allclose(a.errors, b.errors, rtol=1e-12)
 
 
+@pytest.mark.parametrize("rho,m,m0", [(3, 4_500_000, 24), (16, 300_000, 20), (27, 200_000, 12)])
+def test_seeding_owner_publication_matches_all_blocks_resolution(rho, m, m0, monkeypatch):
+    """k-means++: the owning block resolves a draw from its own run sums and stored D^2 and
+    publishes the point (default) vs. every block resolving it from remote run sums and a
+    recomputed run (NYS_SEED_MODE=0).  4.5 M points keep D^2 in global memory; the wide guides
+    sweep their runs backwards on odd draws."""
+    from paper_1901_06112_b200.landmarks import kmeans_device
+
+    rng = np.random.default_rng(rho)
+    pts = torch.from_numpy(rng.random((rho, m), dtype=np.float32)).cuda()
+    a = kmeans_device(pts, m0, seed=3, max_iter=2)
+    monkeypatch.setenv("NYS_SEED_MODE", "0")
+    b = kmeans_device(pts, m0, seed=3, max_iter=2)
+    assert np.array_equal(np.asarray(a.centroids), np.asarray(b.centroids))
+    assert a.quant_error == b.quant_error
+
+
 @pytest.mark.parametrize("case", ["quantised", "constant_dim", "negative_wide", "m64_duplicates"])
 def test_cell_pruned_assignment_edge_cases(case, monkeypatch):
     """rho <= 3 Lloyd (candidate masks per cell of the points' bounding box) against the full

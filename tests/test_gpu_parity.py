@@ -191,6 +191,27 @@ def test_channel_counts_with_partial_plane_chunks(n):
     assert rep.guarded_pixels == ref["guarded_pixels"]
 
 
+@pytest.mark.parametrize("rho,m0,radius", [(2, 7, 9), (3, 13, 9), (4, 11, 5), (3, 33, 15), (16, 21, 12), (9, 10, 9)])
+def test_guide_dimensions_and_odd_landmark_counts(rho, m0, radius):
+    """K2's feature loops against the oracle where their padding shows: colour-guide loop (two
+    landmarks per packed operation, pair-interleaved centroids) with odd landmark counts and
+    rho = 2 .. 4 (zero-padded dimensions); wide-guide loop (two dimensions per packed operation)
+    with rho not a multiple of four; compiled radii and the generic one."""
+    f32 = spectral_scene(56, 88, rho, 6, 0.03, seed=rho * 10 + m0) if rho > 3 else \
+        np.ascontiguousarray(color_scene(56, 88, 6, 0.04, seed=rho * 10 + m0)[:rho])
+    f64 = f32.astype(np.float64)
+    f = Image(data=torch.from_numpy(f32).cuda(), range_max=1.0)
+    C, _, _, _ = O.kmeans(O.range_vectors(f64), m0, 0, 6)
+    theta = 0.2 if rho <= 4 else 0.3
+    params = FilterParams(spatial=SpatialKernel.gaussian(radius / 3.0, radius), theta=theta, m0=m0)
+    rep = filter_with_landmarks(f, f, C, params)
+    ref = O.fast_filter_with_landmarks(f64, f64, C, theta, "gaussian_fir", radius / 3.0, radius)
+    out = rep.output.data.double().cpu().numpy()
+    assert np.abs(out - ref["output"]).max() <= TOL
+    assert rep.guarded_pixels == ref["guarded_pixels"]
+    assert rep.retained_rank == ref["retained_rank"]
+
+
 @pytest.mark.parametrize("rho", [1, 2, 3, 16, 27])
 def test_lloyd_bounds_are_exact(rho, monkeypatch):
     # Hamerly-style skipping (and, for rho <= 3, the cell-pruned candidate search) must not
